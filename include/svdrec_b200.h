@@ -1,0 +1,204 @@
+/*
+ * svdrec_b200.h -- C ABI of the B200-native adaptive-PCA / CF hot path.
+ *
+ * Drop-in boundary for the reference package ``svdrec``
+ * (/root/reference/pkg/src/svdrec).  The reference is Python; its hot path
+ * calls numpy/scipy through the functions cited below.  Each entry point
+ * here replaces one of those calls with an sm_100a kernel; the Python host
+ * layer (paper_2009_02251_b200/) binds them with ctypes exactly like the
+ * stub in INTEGRATION.md and mirrors the reference's function names,
+ * argument meaning and errors.
+ *
+ * Conventions
+ *  - plain pointers + sizes, no torch types; every pointer named d_* is
+ *    DEVICE memory, every other pointer is host memory;
+ *  - dense matrices are ROW-MAJOR with an explicit leading dimension
+ *    (elements), float64 unless the name says otherwise;
+ *  - ``stream`` is a cudaStream_t passed as void*; every call is
+ *    asynchronous on that stream, nothing synchronises the device;
+ *  - return value: 0 on success, otherwise a CUDA error code (>0) or a
+ *    negative SVDREC_E* code; svdrec_last_error() gives the message;
+ *  - data-dependent failures that the reference raises as exceptions
+ *    (rank-deficient pivot, near-singular Gram, exhausted raw stream) are
+ *    reported through a device int32 status word the caller reads back
+ *    when it next synchronises (bit flags SVDREC_STATUS_*).
+ *  - scratch memory is supplied by the caller; *_workspace_bytes() sizes it.
+ */
+#ifndef SVDREC_B200_H
+#define SVDREC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVDREC_E_ARG (-1)       /* invalid argument (shape, ld, size)   */
+#define SVDREC_E_WORKSPACE (-2) /* workspace smaller than required      */
+#define SVDREC_E_UNSUPPORTED (-3)
+
+#define SVDREC_STATUS_ZERO_PIVOT 1u    /* lu: exactly singular pivot    */
+#define SVDREC_STATUS_NEAR_SINGULAR 2u /* eig: Gram eigenvalue <= floor */
+#define SVDREC_STATUS_STREAM_SHORT 4u  /* normal: raw window too short  */
+#define SVDREC_STATUS_NO_CONVERGE 8u   /* eig: Jacobi sweep cap hit     */
+
+int svdrec_abi_version(void);
+const char* svdrec_last_error(void);
+int svdrec_device_sm_count(void);
+
+/* ---------------------------------------------------------------------
+ * Gaussian stream.  Replaces GaussianStream.normal / gaussian_matrix
+ * (reference pkg/src/svdrec/linalg.py:28-51), i.e. numpy
+ * Generator(Philox(key=seed)).standard_normal((rows, cols)).  Bit-exact:
+ * Philox4x64-10 raw words parsed by numpy's 256-layer ziggurat as a
+ * 3-state transducer with a parallel chunk-composition scan.
+ *
+ * Draws ``count`` samples starting at raw-word position *d_pos (device
+ * int64, 0 for a fresh seed) and advances *d_pos past them, so successive
+ * calls continue the stream exactly as the reference's successive
+ * stream.normal() calls do.  out[e] is the e-th sample (C order of the
+ * reference's (rows, cols) draw); with ``row_perm`` non-NULL sample
+ * (i, j) of a (count/cols, cols) draw lands at out[row_perm[i]*ld + j].
+ * ------------------------------------------------------------------- */
+size_t svdrec_normal_workspace_bytes(int64_t count);
+int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_pos,
+                       int64_t count, int64_t cols, const int32_t* d_row_perm,
+                       double* d_out, int64_t ld, void* d_work, size_t work_bytes,
+                       uint32_t* d_status, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Sparse x dense.  Replaces sparse_dense_mul (linalg.py:141-158):
+ * Y = A @ X with A in CSR (int64 indptr, int32 indices, float64 values).
+ * A.T @ X is the same call on the CSR of A.T (the host keeps both).
+ * Rows are cut into segments of <= seg_max nonzeros by the host plan
+ * (svdrec_spmm_plan_*); long rows go through a deterministic fix-up, so
+ * results are bitwise reproducible run to run.
+ *   seg_row/seg_begin/seg_end : nseg segments, row-ordered
+ *   seg_slot                  : -1 = segment covers its whole row (direct
+ *                               store), else partial slot index
+ *   long_row/long_slot0/long_slot1: nlong split rows and their slot range
+ *   d_partial                 : (nslots x b) scratch
+ * ------------------------------------------------------------------- */
+int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                const int64_t* d_seg_end, const int32_t* d_seg_slot,
+                const int32_t* d_indices, const double* d_values,
+                const double* d_X, int64_t ldx, double* d_Y, int64_t ldy, int32_t b,
+                int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
+                const int32_t* d_long_slot1, double* d_partial, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Dense tall-skinny contractions (the deflation products of
+ * rsvd.py:135-142, 179-194: Q @ (B @ X), Q @ (Q.T @ X), B.T @ (Q.T @ X)
+ * and the Gram M.T @ M of eig_svd, linalg.py:127).
+ *   gemm_tn: C (p x q) = alpha * X.T @ Y + beta * C, X (r x p), Y (r x q);
+ *            deterministic split-r reduction through d_work.
+ *   gemm_nn: Y (r x q) = alpha * X @ C + beta * Y, X (r x p), C (p x q).
+ * ------------------------------------------------------------------- */
+size_t svdrec_gemm_tn_workspace_bytes(int64_t r, int64_t p, int64_t q);
+int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, const double* d_X,
+                   int64_t ldx, const double* d_Y, int64_t ldy, double beta, double* d_C,
+                   int64_t ldc, void* d_work, size_t work_bytes, void* stream);
+int svdrec_gemm_nn(int64_t r, int64_t p, int64_t q, double alpha, const double* d_X,
+                   int64_t ldx, const double* d_C, int64_t ldc, double beta, double* d_Y,
+                   int64_t ldy, void* stream);
+
+/* Sum of squares of a strided r x q block, per column (d_colsq, q values,
+ * may be NULL) and in total (d_total, 1 value, may be NULL); fixed-order.
+ * fro_norm_sq (linalg.py:161-168) and the error-indicator update
+ * ||B_i||_F^2 (rsvd.py:146, 197) / row energies (rsvd.py:209). */
+size_t svdrec_sumsq_workspace_bytes(int64_t r, int64_t q);
+int svdrec_sumsq(int64_t r, int64_t q, const double* d_X, int64_t ldx, double* d_colsq,
+                 double* d_total, void* d_work, size_t work_bytes, void* stream);
+
+/* Fixed-order sum of a float64 vector (the global mean of _global_mean,
+ * cf.py:102-105). */
+size_t svdrec_vec_sum_workspace_bytes(int64_t n);
+int svdrec_vec_sum(int64_t n, const double* d_x, double* d_out, void* d_work, size_t work_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * orthonormal_basis (linalg.py:54-81): economic Householder QR of the
+ * tall r x b block A via a TSQR tree; writes the explicit Q (r x b, may
+ * alias A) and R (b x b row-major, upper).  Orthonormal to working
+ * precision even for rank-deficient input (the reference's
+ * check_rank=False behaviour); the host applies the 1e-12 |R_ii| floor.
+ * Supports b <= 80.
+ * ------------------------------------------------------------------- */
+size_t svdrec_tsqr_workspace_bytes(int64_t r, int32_t b);
+int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q,
+                int64_t ldq, double* d_R, void* d_work, size_t work_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * lu_lower_basis (linalg.py:84-97): partial-pivoting LU of the tall
+ * r x b block, in place, returning P.L (original row order, unit
+ * diagonal on pivot rows) and U's diagonal in d_udiag (b values).
+ * Exactly zero pivot -> SVDREC_STATUS_ZERO_PIVOT.  One cooperative
+ * kernel, one grid barrier per column.
+ * ------------------------------------------------------------------- */
+size_t svdrec_lu_workspace_bytes(int64_t r, int32_t b);
+int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag,
+                    void* d_work, size_t work_bytes, uint32_t* d_status, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Symmetric eigendecomposition for eig_svd (linalg.py:108-138): the
+ * k x k Gram G (row-major, symmetric PSD) -> eigenvalues ascending in
+ * d_w and eigenvectors as columns of d_V (k x k row-major).  Parallel
+ * one-sided Jacobi in one cooperative kernel.  Flags
+ * SVDREC_STATUS_NEAR_SINGULAR when w[0] <= 0 or w[0] < 1e-14 trace(G).
+ * ------------------------------------------------------------------- */
+size_t svdrec_syev_workspace_bytes(int32_t k);
+int svdrec_syev(int32_t k, const double* d_G, int64_t ldg, double* d_w, double* d_V,
+                int64_t ldv, void* d_work, size_t work_bytes, uint32_t* d_status,
+                void* stream);
+
+/* One-sided Jacobi SVD of a tall rows x k block (rows >= k): singular
+ * values descending in d_s, left vectors d_U (rows x k), right vectors as
+ * columns of d_V (k x k).  Replaces scipy.linalg.svd(b) of basic_rsvd
+ * (rsvd.py:263), applied to b.T so no condition number is squared. */
+size_t svdrec_gesvj_workspace_bytes(int64_t rows, int32_t k);
+int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double* d_s, double* d_U,
+                 int64_t ldu, double* d_V, int64_t ldv, void* d_work, size_t work_bytes,
+                 uint32_t* d_status, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Collaborative filtering (cf.py:77-190).
+ *  svdrec_cf_factors: from Bt (n x k, = B.T) and the k x k matrix W
+ *   (eigenvectors scaled by s^-1/2, descending) form T.T = Bt @ W
+ *   (n x k), its column... item norms ``d_norm`` and the unit rows
+ *   ``d_Tn`` (zero rows for zero-norm items).  (latent_from_qb +
+ *   LatentFactors.from_matrix.)
+ *  svdrec_cf_predict: Alg. 4 (_predict, cf.py:108-143) for nsamp
+ *   (user, item) pairs grouped by user: ``d_group_start`` (ngroups+1)
+ *   offsets into the user-sorted samples.  Writes clamped value, raw
+ *   value and fallback flag per sample (in grouped order).
+ *  svdrec_abs_err_sum: fixed-order sum |pred - truth| and (pred-truth)^2.
+ * ------------------------------------------------------------------- */
+int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int64_t ldt, double* d_Tn,
+                        int64_t ldn, double* d_norm, void* stream);
+int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32_t* d_users,
+                      const int32_t* d_items, const int64_t* d_indptr,
+                      const int32_t* d_indices, const double* d_values, int32_t k,
+                      const double* d_Tn, int64_t ldn, const double* d_norm,
+                      double global_mean, double rating_min, double rating_max,
+                      double* d_value, double* d_raw, uint8_t* d_fallback, void* stream);
+size_t svdrec_err_sum_workspace_bytes(int64_t nsamp);
+int svdrec_err_sum(int64_t nsamp, const double* d_pred, const double* d_truth,
+                   double* d_out2, void* d_work, size_t work_bytes, void* stream);
+
+/* Count samples whose (user, item) is stored in the CSR (ValidationMae's
+ * disjointness check, cf.py:243-254); binary search per sample. */
+int svdrec_count_overlap(int64_t nsamp, const int32_t* d_users, const int32_t* d_items,
+                         const int64_t* d_indptr, const int32_t* d_indices,
+                         int32_t* d_count, void* stream);
+
+/* North-star extension (not in the reference): model-based prediction
+ * mu + U_k S_k V_k^T at sampled (i, j), pred[t] = mu + sum_l U[i,l] s[l] V[j,l]. */
+int svdrec_lowrank_predict(int64_t nsamp, const int32_t* d_users, const int32_t* d_items,
+                           int32_t k, const double* d_U, int64_t ldu, const double* d_s,
+                           const double* d_V, int64_t ldv, double mu, double* d_pred,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVDREC_B200_H */

@@ -1,0 +1,319 @@
+"""Item-based collaborative filtering on latent factors (Algs. 4 and 5).
+
+Mirrors ``svdrec.cf`` (reference pkg/src/svdrec/cf.py): LatentFactors,
+latent_from_qb, predict_rating, mae, evaluate_mae, ValidationMae and
+auto_latent_factors, same contracts and exceptions.  All scoring runs in
+csrc/cf.cu; held-out samples are grouped by user once (one warp per user
+builds the two k-vectors P_u, S_u and scores all of that user's samples).
+"""
+from __future__ import annotations
+
+import time
+from typing import Iterable, NamedTuple, Sequence
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from ._lib import STATUS_NEAR_SINGULAR
+from .linalg import EIG_FLOOR, GaussianStream, NearSingularError
+from .rsvd import QbState, RankExhaustedError, qb_pass_blocks
+from .sparse import SparseRatings
+
+WEIGHT_FLOOR = 1e-9  # cf.py:23
+F64 = torch.float64
+
+
+class Prediction(NamedTuple):
+    """A predicted rating: clamped value, raw pre-clamp value, fallback flag."""
+
+    value: float
+    raw: float
+    fallback: bool
+
+
+class BlockEval(NamedTuple):
+    """Validation result after one factorization block."""
+
+    k: int
+    mae: float
+    seconds: float
+
+
+class LatentFactors:
+    """Item embedding T (k x items) with cached column norms (cf.py:42-74).
+
+    Device-resident as ``Tt`` (items x k, = T.T), its unit rows ``Tn`` and
+    ``norm_device``; ``T`` / ``col_norms`` materialise numpy copies.
+    """
+
+    def __init__(self, Tt: torch.Tensor, Tn: torch.Tensor | None = None, norm: torch.Tensor | None = None):
+        if Tt.dim() != 2:
+            raise ValueError("T must be 2-d")
+        self.Tt = Tt.contiguous()
+        if Tn is None or norm is None:
+            Tn, norm = K.cf_normalize(self.Tt)
+        self.Tn = Tn
+        self.norm_device = norm
+        self._T = None
+        self._norms = None
+
+    @property
+    def k(self) -> int:
+        return int(self.Tt.shape[1])
+
+    @property
+    def n_items(self) -> int:
+        return int(self.Tt.shape[0])
+
+    @property
+    def T(self) -> np.ndarray:
+        if self._T is None:
+            self._T = np.asfortranarray(self.Tt.cpu().numpy().T)
+        return self._T
+
+    @property
+    def col_norms(self) -> np.ndarray:
+        if self._norms is None:
+            self._norms = self.norm_device.cpu().numpy()
+        return self._norms
+
+    @classmethod
+    def from_matrix(cls, T) -> "LatentFactors":
+        if isinstance(T, torch.Tensor):
+            Tt = T.to(F64).T.contiguous().cuda()
+        else:
+            T = np.asarray(T, dtype=np.float64)
+            if T.ndim != 2:
+                raise ValueError("T must be 2-d")
+            Tt = torch.from_numpy(np.ascontiguousarray(T.T)).cuda()
+        return cls(Tt)
+
+
+def _latent_device(Bt: torch.Tensor, G: torch.Tensor | None = None) -> LatentFactors:
+    """T.T = B.T V diag(s^-1/2) with eig(B B.T) descending (cf.py:77-92)."""
+    st = K.new_status(Bt.device)
+    if G is None:
+        G = K.gemm_tn(Bt, Bt)
+    w, V = K.syev(G, st)
+    if K.check_status(st) & STATUS_NEAR_SINGULAR:
+        raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
+                                f"{EIG_FLOOR * float(torch.trace(G)):.3e}")
+    Wm = V.flip(1) * torch.rsqrt(torch.sqrt(torch.clamp(w.flip(0), min=0.0)))
+    Tt = K.gemm_nn(Bt, Wm.contiguous())
+    return LatentFactors(Tt)
+
+
+def latent_from_qb(state: QbState) -> LatentFactors:
+    """Distill item factors from a QB snapshot: T = sqrt(S) U.T, rows by
+    descending singular value (cf.py:77-92)."""
+    if state.rank == 0:
+        raise ValueError("empty factorization has no latent factors")
+    return _latent_device(state.Bt_device)
+
+
+class _Samples:
+    """Held-out (user, item, rating) triples, user-grouped, on the device."""
+
+    def __init__(self, samples, device):
+        if isinstance(samples, tuple) and len(samples) == 3 and hasattr(samples[0], "__len__") and \
+                not isinstance(samples[0], (int, np.integer)):
+            u = np.asarray(samples[0], dtype=np.int64)
+            i = np.asarray(samples[1], dtype=np.int64)
+            r = np.asarray(samples[2], dtype=np.float64)
+        else:
+            arr = list(samples)
+            u = np.array([int(s[0]) for s in arr], dtype=np.int64)
+            i = np.array([int(s[1]) for s in arr], dtype=np.int64)
+            r = np.array([float(s[2]) for s in arr], dtype=np.float64)
+        self.n = int(u.size)
+        order = np.argsort(u, kind="stable")
+        self.order = order
+        us = u[order]
+        starts = np.flatnonzero(np.r_[True, us[1:] != us[:-1]]) if us.size else np.empty(0, np.int64)
+        groups = np.r_[starts, us.size].astype(np.int64)
+        self.users_np, self.items_np, self.truth_np = u, i, r
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).astype(dt)).to(device)  # noqa: E731
+        self.groups = t(groups, np.int64)
+        self.users = t(us, np.int32)
+        self.items = t(i[order], np.int32)
+        self.truth = t(r[order], np.float64)
+
+    def check_bounds(self, A: SparseRatings) -> None:
+        if self.n == 0:
+            return
+        bad = (self.users_np < 0) | (self.users_np >= A.m) | (self.items_np < 0) | (self.items_np >= A.n)
+        if bad.any():
+            j = int(np.flatnonzero(bad)[0])
+            raise ValueError(f"sample ({self.users_np[j]}, {self.items_np[j]}) outside matrix bounds")
+
+
+def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float):
+    d = A.device(factors.Tt.device)
+    return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Tn, factors.norm_device, gmean, A.rating_min,
+                        A.rating_max)
+
+
+def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: int) -> Prediction:
+    """Alg. 4: cosine-weighted average of the user's ratings, clamped;
+    user/global mean fallback (cf.py:146-164)."""
+    if not 0 <= user < A.m:
+        raise IndexError(f"user {user} out of range")
+    if not 0 <= item < A.n:
+        raise IndexError(f"item {item} out of range")
+    if factors.n_items != A.n:
+        raise ValueError("factor matrix does not cover this item set")
+    d = A.device(factors.Tt.device)
+    if A.nnz == 0:
+        raise ValueError("cannot take the mean of a matrix with no ratings")
+    s = _Samples(([user], [item], [0.0]), factors.Tt.device)
+    val, raw, fb = _predict_device(A, factors, s, d.global_mean)
+    out = torch.stack([val, raw, fb.to(F64)]).cpu().numpy()
+    return Prediction(value=float(out[0, 0]), raw=float(out[1, 0]), fallback=bool(out[2, 0]))
+
+
+def predict_many(A: SparseRatings, factors: LatentFactors, samples) -> np.ndarray:
+    """Batch Alg. 4: (n, 3) array of value, raw, fallback in input order."""
+    s = _Samples(samples, factors.Tt.device)
+    s.check_bounds(A)
+    val, raw, fb = _predict_device(A, factors, s, A.device(factors.Tt.device).global_mean)
+    out = np.empty((s.n, 3))
+    out[s.order, 0] = val.cpu().numpy()
+    out[s.order, 1] = raw.cpu().numpy()
+    out[s.order, 2] = fb.cpu().numpy()
+    return out
+
+
+def mae(predictions: Sequence[float], truths: Sequence[float]) -> float:
+    """Mean absolute error between two equally long nonempty sequences (Eq. 6)."""
+    p = np.asarray(predictions, dtype=np.float64)
+    t = np.asarray(truths, dtype=np.float64)
+    if p.shape != t.shape or p.ndim != 1:
+        raise ValueError("predictions and truths must be 1-d of equal length")
+    if p.size == 0:
+        raise ValueError("cannot average zero errors")
+    return float(np.abs(p - t).mean())
+
+
+def _errors(A, factors, s: _Samples):
+    if A.nnz == 0:
+        raise ValueError("cannot take the mean of a matrix with no ratings")
+    if s.n == 0:
+        raise ValueError("cannot average zero errors")
+    val, _, _ = _predict_device(A, factors, s, A.device(factors.Tt.device).global_mean)
+    e = K.err_sum(val, s.truth).cpu().numpy()
+    return float(e[0] / s.n), float(np.sqrt(e[1] / s.n))
+
+
+def evaluate_mae(A: SparseRatings, factors: LatentFactors, samples: Iterable) -> float:
+    """MAE of clamped predictions over held-out triples (cf.py:178-190)."""
+    s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Tt.device)
+    return _errors(A, factors, s)[0]
+
+
+def evaluate_errors(A: SparseRatings, factors: LatentFactors, samples) -> tuple[float, float]:
+    """(MAE, RMSE) of clamped Alg. 4 predictions (RMSE: BASELINE metric)."""
+    s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Tt.device)
+    return _errors(A, factors, s)
+
+
+class ValidationMae:
+    """Termination criterion tracking held-out MAE (cf.py:193-240).
+
+    After each block the factors are scored on the validation samples;
+    ``patience`` consecutive blocks improving the best MAE by less than
+    ``min_improvement`` stop the scan.  The best block's factors and the
+    (k, MAE, seconds) trace stay on the instance.  The Gram B B.T is grown
+    incrementally when successive states extend one another.
+    """
+
+    def __init__(self, train: SparseRatings, validation, patience: int = 2, min_improvement: float = 1e-4) -> None:
+        if patience < 1:
+            raise ValueError("patience must be at least 1")
+        if min_improvement < 0.0:
+            raise ValueError("min_improvement must be nonnegative")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        s = validation if isinstance(validation, _Samples) else _Samples(validation, dev)
+        if s.n == 0:
+            raise ValueError("validation set is empty")
+        s.check_bounds(train)
+        d = train.device(dev)
+        cnt = int(K.count_overlap(s.users, s.items, d.A).item())
+        if cnt:
+            raise ValueError(f"{cnt} validation samples are present in the training matrix")
+        self.train = train
+        self.samples = s
+        self.patience = patience
+        self.min_improvement = min_improvement
+        self.trace: list[BlockEval] = []
+        self.best_mae = np.inf
+        self.best_factors: LatentFactors | None = None
+        self.best_rmse = np.inf
+        self._stale = 0
+        self._start = time.perf_counter()
+        self._G = None
+        self._Gsrc = None
+
+    @property
+    def validation(self):
+        s = self.samples
+        return list(zip(s.users_np.tolist(), s.items_np.tolist(), s.truth_np.tolist()))
+
+    def _gram(self, Bt: torch.Tensor) -> torch.Tensor:
+        k = Bt.shape[1]
+        G0, src = self._G, self._Gsrc
+        if G0 is not None and src is not None and src.data_ptr() == Bt.data_ptr() and src.shape[1] < k and \
+                src.stride() == Bt.stride():
+            k0 = G0.shape[0]
+            G = torch.empty(k, k, dtype=F64, device=Bt.device)
+            G[:k0, :k0] = G0
+            K.gemm_tn(Bt, Bt[:, k0:k], G[:, k0:k])  # new columns
+            G[k0:k, :k0] = G[:k0, k0:k].T
+        else:
+            G = K.gemm_tn(Bt, Bt)
+        self._G, self._Gsrc = G, Bt
+        return G
+
+    def __call__(self, state: QbState) -> bool:
+        if state.rank == 0:
+            raise ValueError("empty factorization has no latent factors")
+        factors = _latent_device(state.Bt_device, self._gram(state.Bt_device))
+        score, rmse = _errors(self.train, factors, self.samples)
+        self.trace.append(BlockEval(k=state.rank, mae=score, seconds=time.perf_counter() - self._start))
+        if score < self.best_mae - self.min_improvement:
+            self._stale = 0
+        else:
+            self._stale += 1
+        if score < self.best_mae:
+            self.best_mae = score
+            self.best_rmse = rmse
+            self.best_factors = factors
+        return self._stale >= self.patience
+
+
+def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, passes: int = 10, patience: int = 2,
+                        min_improvement: float = 1e-4, seed: int = 0,
+                        max_rank: int | None = None) -> tuple[LatentFactors, list[BlockEval]]:
+    """Alg. 5: grow item factors until validation MAE stops improving
+    (cf.py:257-294).  ``max_rank`` (not in the reference) ends the scan once
+    that many factors are held and keeps the best block so far."""
+    if passes <= 2:
+        raise ValueError("passes must exceed 2")
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    if 2 * block_size > min(A.shape):
+        raise ValueError(f"block_size {block_size} too large for min(m, n) = {min(A.shape)}")
+    criterion = ValidationMae(A, validation, patience=patience, min_improvement=min_improvement)
+    stream = GaussianStream(seed)
+    for state in qb_pass_blocks(A, block_size, passes, stream, max_rank=max_rank):
+        if criterion(state):
+            break
+        if max_rank is not None and state.rank >= max_rank:
+            break
+    if criterion.best_factors is None:
+        raise RankExhaustedError("rank cap reached before any block was scored")
+    return criterion.best_factors, criterion.trace
+
+
+__all__ = ["BlockEval", "LatentFactors", "Prediction", "ValidationMae", "auto_latent_factors", "evaluate_errors",
+           "evaluate_mae", "latent_from_qb", "mae", "predict_many", "predict_rating"]

@@ -1,0 +1,163 @@
+// Tall-skinny LU with partial pivoting -> P.L (lu_lower_basis).
+//
+// Replaces scipy.linalg.lu(M, permute_l=True) in lu_lower_basis (reference
+// pkg/src/svdrec/linalg.py:84-97), the cheap range finder of Alg. 3
+// (rsvd.py:180, 190).  Right-looking partial pivoting, exactly as LAPACK
+// dgetf2 picks pivots (largest |value| among not-yet-pivoted rows; ties ->
+// lowest row index), but rows are never swapped: the result is already in
+// the original row order that permute_l=True returns.  One cooperative
+// kernel: per column, each CTA reduces its rows' pivot candidate, one grid
+// barrier publishes all candidates, every CTA picks the same winner and
+// eliminates its own rows against the pivot row.  b grid barriers total.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace svdrec {
+namespace {
+
+constexpr int kLuThreads = 256;
+
+struct Cand {
+  double a;
+  long long row;
+};
+
+__device__ __forceinline__ bool better(double a, long long ra, double b, long long rb) {
+  return a > b || (a == b && ra < rb);
+}
+
+__global__ void __launch_bounds__(kLuThreads) k_lu(int64_t r, int b, double* __restrict__ A, int64_t lda,
+                                                   double* __restrict__ udiag, int32_t* __restrict__ pivstep,
+                                                   Cand* __restrict__ slots, uint32_t* d_status) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sa[kLuThreads / 32];
+  __shared__ long long sr[kLuThreads / 32];
+  __shared__ long long piv_row;
+  __shared__ double piv_val;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  const int nblk = gridDim.x;
+  for (int64_t i = gt; i < r; i += gs) pivstep[i] = -1;
+  for (int j = 0; j < b; ++j) {
+    // local candidate
+    double best = -1.0;
+    long long brow = -1;
+    for (int64_t i = gt; i < r; i += gs) {
+      if (pivstep[i] >= 0) continue;
+      const double v = fabs(A[i * lda + j]);
+      if (better(v, i, best, brow) || brow < 0) {
+        best = v;
+        brow = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const long long orow = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (orow >= 0 && (brow < 0 || better(ob, orow, best, brow))) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+      sa[warp] = best;
+      sr[warp] = brow;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bb = -1.0;
+      long long br = -1;
+      for (int w = 0; w < kLuThreads / 32; ++w)
+        if (sr[w] >= 0 && (br < 0 || better(sa[w], sr[w], bb, br))) {
+          bb = sa[w];
+          br = sr[w];
+        }
+      slots[(size_t)(j & 1) * nblk + blockIdx.x] = Cand{bb, br};
+    }
+    grid.sync();
+    if (threadIdx.x == 0) {
+      double bb = -1.0;
+      long long br = -1;
+      const Cand* sl = slots + (size_t)(j & 1) * nblk;
+      for (int k = 0; k < nblk; ++k) {
+        const Cand cc = sl[k];
+        if (cc.row >= 0 && (br < 0 || better(cc.a, cc.row, bb, br))) {
+          bb = cc.a;
+          br = cc.row;
+        }
+      }
+      piv_row = br;
+      piv_val = br >= 0 ? A[br * lda + j] : 0.0;
+    }
+    __syncthreads();
+    const long long p = piv_row;
+    const double pv = piv_val;
+    if (gt == 0) {
+      udiag[j] = pv;
+      if (pv == 0.0 && d_status) atomicOr(d_status, SVDREC_STATUS_ZERO_PIVOT);
+    }
+    for (int64_t i = gt; i < r; i += gs) {
+      if (i == p) {
+        pivstep[i] = j;
+        continue;
+      }
+      if (pivstep[i] >= 0 || pv == 0.0) continue;
+      double* row = A + i * lda;
+      const double l = row[j] / pv;
+      row[j] = l;
+      const double* prow = A + p * lda;
+      for (int c = j + 1; c < b; ++c) row[c] = fma(-l, prow[c], row[c]);
+    }
+    // make this step's row updates (and the pivot row) visible before the
+    // next step's candidate scan reads them from other CTAs' rows
+    __threadfence();
+  }
+  grid.sync();
+  for (int64_t i = gt; i < r; i += gs) {
+    const int s = pivstep[i];
+    if (s < 0) continue;
+    double* row = A + i * lda;
+    row[s] = 1.0;
+    for (int c = s + 1; c < b; ++c) row[c] = 0.0;
+  }
+}
+
+}  // namespace
+}  // namespace svdrec
+
+using namespace svdrec;
+
+extern "C" size_t svdrec_lu_workspace_bytes(int64_t r, int32_t b) {
+  (void)b;
+  return align_up((size_t)r * 4) + align_up(2 * sizeof(Cand) * (size_t)sm_count() * 8) + 256;
+}
+
+extern "C" int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag, void* d_work,
+                               size_t work_bytes, uint32_t* d_status, void* stream) {
+  SVDREC_ARG(b >= 1 && r >= b && lda >= b, "lu_lower: needs rows >= cols >= 1");
+  if (work_bytes < svdrec_lu_workspace_bytes(r, b)) {
+    set_error("lu_lower: workspace too small");
+    return SVDREC_E_WORKSPACE;
+  }
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0;
+    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, 0));
+    max_blocks = per_sm * sm_count();
+    if (max_blocks > sm_count() * 8) max_blocks = sm_count() * 8;
+    if (max_blocks < 1) max_blocks = 1;
+  }
+  int64_t want = (r + kLuThreads - 1) / kLuThreads;
+  int nblk = (int)(want < max_blocks ? want : max_blocks);
+  if (nblk < 1) nblk = 1;
+  char* w = static_cast<char*>(d_work);
+  int32_t* pivstep = reinterpret_cast<int32_t*>(w);
+  Cand* slots = reinterpret_cast<Cand*>(w + align_up((size_t)r * 4));
+  int32_t bb = b;
+  void* args[] = {&r, &bb, &d_A, &lda, &d_udiag, &pivstep, &slots, &d_status};
+  SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_lu, dim3(nblk), dim3(kLuThreads), args, 0, as_stream(stream)));
+  return 0;
+}

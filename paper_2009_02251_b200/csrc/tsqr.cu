@@ -1,0 +1,256 @@
+// Tall-skinny Householder QR (TSQR) -> explicit orthonormal Q.
+//
+// Replaces orthonormal_basis (reference pkg/src/svdrec/linalg.py:54-81,
+// scipy.linalg.qr economic = LAPACK dgeqrf + dorgqr), called 2-4 times per
+// block by the QB engines (rsvd.py:136-142, 186-193).  A flat Householder
+// QR is b sequential column steps over all m rows; here the rows are cut
+// into chunks that fit one CTA's shared memory, each CTA factors its chunk
+// with Householder reflections entirely on-chip, the b x b R factors are
+// stacked and factored again (a reduction tree, 2-4 levels for m <= 10^7),
+// and the explicit Q is rebuilt top-down by applying each chunk's
+// reflectors to its b x b block of the coarser Q.  Every matrix element is
+// read once and written once per direction, there are no grid-wide
+// barriers, and the result is orthonormal to working precision even for
+// rank-deficient input (the reference's check_rank=False contract).
+// Q is unique up to column signs; all consumers downstream are sign
+// invariant (B = Q.T A rows flip, B.T B, Q B and row energies do not).
+#include <vector>
+
+#include "common.cuh"
+
+namespace svdrec {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr size_t kChunkBytes = 96 * 1024;  // one chunk's panel in smem
+
+inline int rc_max_for(int b) { return (int)(kChunkBytes / (8 * (size_t)b)); }
+
+struct Level {
+  int64_t rows, nc;
+  size_t off_v, off_tau, off_next, off_q;
+};
+
+struct Plan {
+  int b;
+  int rcmax;
+  std::vector<Level> lv;
+  size_t total;
+};
+
+Plan make_plan(int64_t r, int b) {
+  Plan p;
+  p.b = b;
+  p.rcmax = rc_max_for(b);
+  size_t o = 0;
+  int64_t rows = r;
+  while (true) {
+    Level L{};
+    L.rows = rows;
+    L.nc = (rows + p.rcmax - 1) / p.rcmax;
+    L.off_v = o;
+    o = align_up(o + (size_t)rows * b * 8);
+    L.off_tau = o;
+    o = align_up(o + (size_t)L.nc * b * 8);
+    L.off_next = o;
+    o = align_up(o + (size_t)L.nc * b * b * 8);
+    L.off_q = o;
+    o = align_up(o + (p.lv.empty() ? 0 : (size_t)rows * b * 8));
+    p.lv.push_back(L);
+    if (L.nc == 1) break;
+    rows = L.nc * b;
+  }
+  p.total = o;
+  return p;
+}
+
+__device__ __forceinline__ void chunk_range(int64_t rows, int64_t nc, int64_t c, int64_t& a, int64_t& e) {
+  a = (c * rows) / nc;
+  e = ((c + 1) * rows) / nc;
+}
+
+// Householder QR of one chunk.  M is column-major in smem: M[col*ldm + row].
+__global__ void __launch_bounds__(kThreads) k_factor(int64_t rows, int64_t nc, int b, const double* __restrict__ in,
+                                                     int64_t ldin, double* __restrict__ vout,
+                                                     double* __restrict__ tau, double* __restrict__ rout) {
+  extern __shared__ double sm[];
+  __shared__ double dots[128];
+  __shared__ double wv[128];
+  __shared__ double coef[3];  // tau, beta, scale
+  const int64_t c = blockIdx.x;
+  int64_t a, e;
+  chunk_range(rows, nc, c, a, e);
+  const int rc = (int)(e - a);
+  const int ldm = rc | 1;
+  double* M = sm;
+  for (int t = threadIdx.x; t < rc * b; t += kThreads) {
+    const int i = t / b, col = t - i * b;
+    M[col * ldm + i] = in[(a + i) * ldin + col];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jmax = min(b, rc);
+  for (int j = 0; j < jmax; ++j) {
+    const double* xj = M + j * ldm;
+    for (int col = j + warp; col < b; col += kThreads / 32) {
+      const double* mc = M + col * ldm;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < rc; i += 32) s = fma(xj[i], mc[i], s);
+      s = warp_sum(s);
+      if (lane == 0) dots[col] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double alpha = xj[j], sigma = dots[j];
+      double t = 0.0, beta = alpha, scale = 0.0;
+      if (sigma != 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, sigma));
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        t = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      coef[0] = t;
+      coef[1] = beta;
+      coef[2] = scale;
+    }
+    __syncthreads();
+    const double t = coef[0], scale = coef[2];
+    for (int col = j + 1 + threadIdx.x; col < b; col += kThreads) wv[col] = t * fma(scale, dots[col], M[col * ldm + j]);
+    // v into column j (v_j = 1 implicit)
+    for (int i = j + 1 + threadIdx.x; i < rc; i += kThreads) M[j * ldm + i] *= scale;
+    __syncthreads();
+    const int ncol = b - j - 1, nrow = rc - j;
+    for (int q = threadIdx.x; q < ncol * nrow; q += kThreads) {
+      const int cc = j + 1 + q / nrow, i = j + q % nrow;
+      const double vi = (i == j) ? 1.0 : M[j * ldm + i];
+      M[cc * ldm + i] -= wv[cc] * vi;
+    }
+    if (threadIdx.x == 0) {
+      tau[c * b + j] = t;
+      M[j * ldm + j] = coef[1];  // R_jj
+    }
+    __syncthreads();
+  }
+  for (int j = jmax; j < b; ++j)
+    if (threadIdx.x == 0) tau[c * b + j] = 0.0;
+  // R (b x b row-major, upper) -> rout rows c*b .. c*b+b-1
+  for (int t = threadIdx.x; t < b * b; t += kThreads) {
+    const int i = t / b, col = t - i * b;
+    rout[(c * b + i) * (int64_t)b + col] = (col >= i && i < rc) ? M[col * ldm + i] : 0.0;
+  }
+  // reflectors (strict lower part) -> vout rows a..e-1 (row-major, ld b)
+  for (int t = threadIdx.x; t < rc * b; t += kThreads) {
+    const int i = t / b, col = t - i * b;
+    vout[(a + i) * (int64_t)b + col] = i > col ? M[col * ldm + i] : 0.0;
+  }
+}
+
+// Apply one chunk's reflectors to E = [Qc ; 0] (Qc = rows c*b.. of the
+// coarser explicit Q, or the identity at the top) and store the chunk's
+// rows of this level's explicit Q.
+__global__ void __launch_bounds__(kThreads) k_buildq(int64_t rows, int64_t nc, int b, const double* __restrict__ vin,
+                                                     const double* __restrict__ tau,
+                                                     const double* __restrict__ qcoarse, double* __restrict__ qout,
+                                                     int64_t ldq) {
+  extern __shared__ double sm[];
+  __shared__ double wv[128];
+  const int64_t c = blockIdx.x;
+  int64_t a, e;
+  chunk_range(rows, nc, c, a, e);
+  const int rc = (int)(e - a);
+  const int ldm = rc | 1;
+  double* V = sm;
+  double* E = sm + (size_t)b * ldm;
+  for (int t = threadIdx.x; t < rc * b; t += kThreads) {
+    const int i = t / b, col = t - i * b;
+    V[col * ldm + i] = vin[(a + i) * (int64_t)b + col];
+    double ev = 0.0;
+    if (i < b) ev = qcoarse ? qcoarse[(c * b + i) * (int64_t)b + col] : (i == col ? 1.0 : 0.0);
+    E[col * ldm + i] = ev;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jmax = min(b, rc);
+  for (int j = jmax - 1; j >= 0; --j) {
+    const double t = tau[c * b + j];
+    if (t == 0.0) continue;  // uniform across the block
+    const double* v = V + j * ldm;
+    for (int col = warp; col < b; col += kThreads / 32) {
+      const double* ec = E + col * ldm;
+      double s = lane == 0 ? ec[j] : 0.0;
+      for (int i = j + 1 + lane; i < rc; i += 32) s = fma(v[i], ec[i], s);
+      s = warp_sum(s);
+      if (lane == 0) wv[col] = t * s;
+    }
+    __syncthreads();
+    const int nrow = rc - j;
+    for (int q = threadIdx.x; q < b * nrow; q += kThreads) {
+      const int col = q / nrow, i = j + q % nrow;
+      const double vi = (i == j) ? 1.0 : v[i];
+      E[col * ldm + i] -= wv[col] * vi;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < rc * b; t += kThreads) {
+    const int i = t / b, col = t - i * b;
+    qout[(a + i) * ldq + col] = E[col * ldm + i];
+  }
+}
+
+}  // namespace
+}  // namespace svdrec
+
+using namespace svdrec;
+
+extern "C" size_t svdrec_tsqr_workspace_bytes(int64_t r, int32_t b) {
+  if (b < 1 || b > 80 || r < b) return 256;
+  return make_plan(r, b).total + 256;
+}
+
+extern "C" int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
+                           double* d_R, void* d_work, size_t work_bytes, void* stream) {
+  SVDREC_ARG(b >= 1 && b <= 80, "tsqr: block width %d outside [1, 80]", b);
+  SVDREC_ARG(r >= b, "tsqr: needs rows >= cols (%lld < %d)", (long long)r, b);
+  SVDREC_ARG(lda >= b && ldq >= b, "tsqr: bad leading dimension");
+  const Plan p = make_plan(r, b);
+  if (work_bytes < p.total) {
+    set_error("tsqr: workspace %zu < %zu", work_bytes, p.total);
+    return SVDREC_E_WORKSPACE;
+  }
+  static bool attr_set = false;
+  const size_t smem_f = (size_t)b * ((p.rcmax + 1) | 1) * 8;
+  const size_t smem_q = 2 * smem_f;
+  if (!attr_set) {
+    SVDREC_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
+    SVDREC_CUDA(cudaFuncSetAttribute(k_buildq, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
+    attr_set = true;
+  }
+  cudaStream_t s = as_stream(stream);
+  char* w = static_cast<char*>(d_work);
+  const int nl = (int)p.lv.size();
+  const double* in = d_A;
+  int64_t ldin = lda;
+  for (int l = 0; l < nl; ++l) {
+    const Level& L = p.lv[l];
+    double* rout = (l == nl - 1) ? d_R : reinterpret_cast<double*>(w + L.off_next);
+    k_factor<<<(unsigned)L.nc, kThreads, smem_f, s>>>(L.rows, L.nc, b, in, ldin,
+                                                      reinterpret_cast<double*>(w + L.off_v),
+                                                      reinterpret_cast<double*>(w + L.off_tau), rout);
+    int rc = check_launch("tsqr_factor");
+    if (rc) return rc;
+    in = rout;
+    ldin = b;
+  }
+  const double* coarse = nullptr;
+  for (int l = nl - 1; l >= 0; --l) {
+    const Level& L = p.lv[l];
+    double* qo = l == 0 ? d_Q : reinterpret_cast<double*>(w + L.off_q);
+    const int64_t ldo = l == 0 ? ldq : b;
+    k_buildq<<<(unsigned)L.nc, kThreads, smem_q, s>>>(L.rows, L.nc, b, reinterpret_cast<double*>(w + L.off_v),
+                                                      reinterpret_cast<double*>(w + L.off_tau), coarse, qo, ldo);
+    int rc = check_launch("tsqr_buildq");
+    if (rc) return rc;
+    coarse = qo;
+  }
+  return 0;
+}

@@ -1,0 +1,206 @@
+"""Typed wrappers: torch CUDA tensors in, C-ABI calls, torch tensors out.
+
+Every function here is one (or two) calls into libsvdrec_b200.so on the
+current CUDA stream.  Dense operands are 2-d float64 tensors whose rows are
+contiguous (``stride(1) == 1``); their ``stride(0)`` is the leading
+dimension, so column blocks such as ``Q[:, k0:k1]`` are passed without
+copies.  Nothing here synchronises the device.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import call, ptr, query, scratch, stream_handle
+
+F64 = torch.float64
+
+
+def _mat(t: torch.Tensor, name: str) -> int:
+    if t.dim() != 2 or t.dtype != F64 or not t.is_cuda:
+        raise ValueError(f"{name}: expected a 2-d float64 CUDA tensor, got {tuple(t.shape)} {t.dtype} {t.device}")
+    if t.stride(1) != 1 and t.shape[1] > 1:
+        raise ValueError(f"{name}: rows must be contiguous (stride {t.stride()})")
+    return max(t.stride(0), t.shape[1], 1)
+
+
+def new_status(device) -> torch.Tensor:
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def normal_fill(key: tuple[int, int], pos: torch.Tensor, rows: int, cols: int, out: torch.Tensor,
+                status: torch.Tensor, row_perm: torch.Tensor | None = None) -> torch.Tensor:
+    ld = _mat(out, "normal.out")
+    count = rows * cols
+    ws, nb = scratch(out.device).get(query("svdrec_normal_workspace_bytes", count))
+    call("svdrec_normal_fill", key[0], key[1], ptr(pos), count, cols, ptr(row_perm), ptr(out), ld, ws, nb,
+         ptr(status), stream_handle())
+    return out
+
+
+def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
+    """Y = A @ X for the CSR described by ``plan`` (a sparse.DeviceCSR)."""
+    ldx, ldy = _mat(X, "spmm.X"), _mat(Y, "spmm.Y")
+    b = X.shape[1]
+    if Y.shape[1] != b or X.shape[0] != plan.n or Y.shape[0] != plan.m:
+        raise ValueError(f"spmm: shape mismatch A{(plan.m, plan.n)} X{tuple(X.shape)} Y{tuple(Y.shape)}")
+    part = plan.partial(b)
+    call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
+         ptr(plan.indices), ptr(plan.values), ptr(X), ldx, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
+         ptr(plan.long_s0), ptr(plan.long_s1), ptr(part), stream_handle())
+    return Y
+
+
+def gemm_tn(X: torch.Tensor, Y: torch.Tensor, C: torch.Tensor | None = None, alpha: float = 1.0,
+            beta: float = 0.0) -> torch.Tensor:
+    """C = alpha X.T @ Y + beta C (reduction over the tall dimension)."""
+    ldx, ldy = _mat(X, "gemm_tn.X"), _mat(Y, "gemm_tn.Y")
+    r, p = X.shape
+    q = Y.shape[1]
+    if Y.shape[0] != r:
+        raise ValueError("gemm_tn: row mismatch")
+    if C is None:
+        C = torch.empty(p, q, dtype=F64, device=X.device)
+    ldc = _mat(C, "gemm_tn.C")
+    ws, nb = scratch(X.device).get(query("svdrec_gemm_tn_workspace_bytes", r, p, q))
+    call("svdrec_gemm_tn", r, p, q, float(alpha), ptr(X), ldx, ptr(Y), ldy, float(beta), ptr(C), ldc, ws, nb,
+         stream_handle())
+    return C
+
+
+def gemm_nn(X: torch.Tensor, Cm: torch.Tensor, Y: torch.Tensor | None = None, alpha: float = 1.0,
+            beta: float = 0.0) -> torch.Tensor:
+    """Y = alpha X @ Cm + beta Y."""
+    ldx, ldc = _mat(X, "gemm_nn.X"), _mat(Cm, "gemm_nn.C")
+    r, p = X.shape
+    q = Cm.shape[1]
+    if Cm.shape[0] != p:
+        raise ValueError("gemm_nn: inner mismatch")
+    if Y is None:
+        Y = torch.empty(r, q, dtype=F64, device=X.device)
+    ldy = _mat(Y, "gemm_nn.Y")
+    call("svdrec_gemm_nn", r, p, q, float(alpha), ptr(X), ldx, ptr(Cm), ldc, float(beta), ptr(Y), ldy,
+         stream_handle())
+    return Y
+
+
+def sumsq(X: torch.Tensor, colsq: torch.Tensor | None = None, total: torch.Tensor | None = None):
+    ldx = _mat(X, "sumsq.X")
+    r, q = X.shape
+    ws, nb = scratch(X.device).get(query("svdrec_sumsq_workspace_bytes", r, q))
+    call("svdrec_sumsq", r, q, ptr(X), ldx, ptr(colsq), ptr(total), ws, nb, stream_handle())
+    return colsq, total
+
+
+def vec_sum(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(1, dtype=F64, device=x.device)
+    ws, nb = scratch(x.device).get(query("svdrec_vec_sum_workspace_bytes", x.numel()))
+    call("svdrec_vec_sum", x.numel(), ptr(x), ptr(out), ws, nb, stream_handle())
+    return out
+
+
+def tsqr(A: torch.Tensor, Q: torch.Tensor | None = None, R: torch.Tensor | None = None):
+    """Householder TSQR; Q may alias A."""
+    lda = _mat(A, "tsqr.A")
+    r, b = A.shape
+    if Q is None:
+        Q = torch.empty(r, b, dtype=F64, device=A.device)
+    if R is None:
+        R = torch.empty(b, b, dtype=F64, device=A.device)
+    ldq = _mat(Q, "tsqr.Q")
+    ws, nb = scratch(A.device).get(query("svdrec_tsqr_workspace_bytes", r, b))
+    call("svdrec_tsqr", r, b, ptr(A), lda, ptr(Q), ldq, ptr(R), ws, nb, stream_handle())
+    return Q, R
+
+
+def lu_lower(A: torch.Tensor, status: torch.Tensor, udiag: torch.Tensor | None = None) -> torch.Tensor:
+    """In-place P.L of partial-pivoting LU; returns U's diagonal (device)."""
+    lda = _mat(A, "lu.A")
+    r, b = A.shape
+    if udiag is None:
+        udiag = torch.empty(b, dtype=F64, device=A.device)
+    ws, nb = scratch(A.device).get(query("svdrec_lu_workspace_bytes", r, b))
+    call("svdrec_lu_lower", r, b, ptr(A), lda, ptr(udiag), ws, nb, ptr(status), stream_handle())
+    return udiag
+
+
+def syev(G: torch.Tensor, status: torch.Tensor):
+    """Eigen-decomposition of a symmetric PSD k x k: (w ascending, V columns)."""
+    ldg = _mat(G, "syev.G")
+    k = G.shape[0]
+    w = torch.empty(k, dtype=F64, device=G.device)
+    V = torch.empty(k, k, dtype=F64, device=G.device)
+    ws, nb = scratch(G.device).get(query("svdrec_syev_workspace_bytes", k))
+    call("svdrec_syev", k, ptr(G), ldg, ptr(w), ptr(V), k, ws, nb, ptr(status), stream_handle())
+    return w, V
+
+
+def gesvj(A: torch.Tensor, status: torch.Tensor):
+    """One-sided Jacobi SVD of a tall block: (s descending, U, V)."""
+    lda = _mat(A, "gesvj.A")
+    rows, k = A.shape
+    s = torch.empty(k, dtype=F64, device=A.device)
+    U = torch.empty(rows, k, dtype=F64, device=A.device)
+    V = torch.empty(k, k, dtype=F64, device=A.device)
+    ws, nb = scratch(A.device).get(query("svdrec_gesvj_workspace_bytes", rows, k))
+    call("svdrec_gesvj", rows, k, ptr(A), lda, ptr(s), ptr(U), k, ptr(V), k, ws, nb, ptr(status), stream_handle())
+    return s, U, V
+
+
+def cf_normalize(Tt: torch.Tensor):
+    ldt = _mat(Tt, "cf.Tt")
+    n, k = Tt.shape
+    Tn = torch.empty(n, k, dtype=F64, device=Tt.device)
+    norm = torch.empty(n, dtype=F64, device=Tt.device)
+    call("svdrec_cf_normalize", n, k, ptr(Tt), ldt, ptr(Tn), k, ptr(norm), stream_handle())
+    return Tn, norm
+
+
+def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Tn: torch.Tensor,
+               norm: torch.Tensor, gmean: float, lo: float, hi: float):
+    ldn = _mat(Tn, "cf.Tn")
+    ns = users.shape[0]
+    val = torch.empty(ns, dtype=F64, device=Tn.device)
+    raw = torch.empty(ns, dtype=F64, device=Tn.device)
+    fb = torch.empty(ns, dtype=torch.uint8, device=Tn.device)
+    call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
+         ptr(csr.indices), ptr(csr.values), Tn.shape[1], ptr(Tn), ldn, ptr(norm), float(gmean), float(lo),
+         float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
+    return val, raw, fb
+
+
+def err_sum(pred: torch.Tensor, truth: torch.Tensor) -> torch.Tensor:
+    """Device (sum |p - t|, sum (p - t)^2)."""
+    out = torch.empty(2, dtype=F64, device=pred.device)
+    n = pred.shape[0]
+    ws, nb = scratch(pred.device).get(query("svdrec_err_sum_workspace_bytes", n))
+    call("svdrec_err_sum", n, ptr(pred), ptr(truth), ptr(out), ws, nb, stream_handle())
+    return out
+
+
+def count_overlap(users: torch.Tensor, items: torch.Tensor, csr) -> torch.Tensor:
+    cnt = torch.empty(1, dtype=torch.int32, device=users.device)
+    call("svdrec_count_overlap", users.shape[0], ptr(users), ptr(items), ptr(csr.indptr), ptr(csr.indices),
+         ptr(cnt), stream_handle())
+    return cnt
+
+
+def lowrank_predict(users: torch.Tensor, items: torch.Tensor, U: torch.Tensor, s: torch.Tensor, V: torch.Tensor,
+                    mu: float) -> torch.Tensor:
+    ldu, ldv = _mat(U, "lowrank.U"), _mat(V, "lowrank.V")
+    pred = torch.empty(users.shape[0], dtype=F64, device=U.device)
+    call("svdrec_lowrank_predict", users.shape[0], ptr(users), ptr(items), U.shape[1], ptr(U), ldu, ptr(s),
+         ptr(V), ldv, float(mu), ptr(pred), stream_handle())
+    return pred
+
+
+def check_status(status: torch.Tensor) -> int:
+    """Synchronising read of a status word (then cleared)."""
+    v = int(status.item())
+    if v:
+        status.zero_()
+    return v
+
+
+__all__ = [n for n in dir() if not n.startswith("_")] + ["_lib"]

@@ -1,0 +1,394 @@
+"""Randomized QB factorizations on the B200: Algs. 1-3 of the paper.
+
+Mirrors ``svdrec.rsvd`` (reference pkg/src/svdrec/rsvd.py): basic_rsvd,
+fixed_precision_qb (randQB_EI, Alg. 2), adaptive_pca (Alg. 3) and the two
+block generators, with the same signatures, stop rules, rank caps and
+exceptions.
+
+Device layout (all float64, HBM-resident for the whole factorization):
+  Q  : m x cap row-major; block l occupies columns [l*b, (l+1)*b)
+  Bt : n x cap row-major = B.T, so appending B's block is writing columns
+  work buffers: two m x b, one n x b
+Per block the host reads back exactly one small vector (||B_l||_F^2 and the
+b row energies) to evaluate the termination criterion; everything else --
+sketch generation, SpMM, deflation, LU, TSQR -- is queued on one stream.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Iterator
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from ._lib import STATUS_NEAR_SINGULAR, STATUS_STREAM_SHORT, STATUS_ZERO_PIVOT
+from .linalg import (EIG_FLOOR, GaussianStream, NearSingularError, RankDeficientError, SvdTriplet, _check_rank,
+                     sparse_dense_mul)
+from .sparse import SparseRatings
+
+F64 = torch.float64
+
+
+class QbState:
+    """Snapshot of a growing QB factorization after a completed block.
+
+    Same fields as the reference's QbState (rsvd.py:40-59).  ``Q`` and
+    ``B`` are numpy arrays materialised lazily from the device views
+    ``Q_device`` (m x k) and ``Bt_device`` (n x k, = B.T).
+    """
+
+    def __init__(self, Q_device, Bt_device, err, blocks, block_size, frob_sq, row_energy=None):
+        self.Q_device = Q_device
+        self.Bt_device = Bt_device
+        self.err = float(err)
+        self.blocks = int(blocks)
+        self.block_size = int(block_size)
+        self.frob_sq = float(frob_sq)
+        self.row_energy = row_energy
+        self._Q = None
+        self._B = None
+
+    @property
+    def rank(self) -> int:
+        return int(self.Q_device.shape[1])
+
+    @property
+    def Q(self) -> np.ndarray:
+        if self._Q is None:
+            self._Q = self.Q_device.cpu().numpy()
+        return self._Q
+
+    @property
+    def B(self) -> np.ndarray:
+        if self._B is None:
+            self._B = np.ascontiguousarray(self.Bt_device.cpu().numpy().T)
+        return self._B
+
+
+class RankExhaustedError(RuntimeError):
+    """The factorization hit its rank cap before the stop condition held."""
+
+    def __init__(self, message: str, state: QbState | None = None) -> None:
+        super().__init__(message)
+        self.state = state
+
+
+@dataclass(frozen=True)
+class FixedRank:
+    """Stop once the factorization holds at least ``k`` columns."""
+
+    k: int
+
+    def __post_init__(self) -> None:
+        if self.k < 1:
+            raise ValueError("k must be positive")
+
+    def __call__(self, state: QbState) -> bool:
+        return state.rank >= self.k
+
+
+@dataclass(frozen=True)
+class FrobTolerance:
+    """Stop once ``||A - QB||_F <= eps * ||A||_F`` by the running estimate."""
+
+    eps: float
+
+    def __post_init__(self) -> None:
+        if not 0.0 < self.eps < 1.0:
+            raise ValueError("eps must lie in (0, 1)")
+
+    def __call__(self, state: QbState) -> bool:
+        return state.err < self.eps * self.eps * state.frob_sq
+
+
+TerminationCriterion = Callable[[QbState], bool]
+
+
+class _QbEngine:
+    """Device state of one growing QB factorization."""
+
+    def __init__(self, A: SparseRatings, b: int, stream: GaussianStream, cap: int):
+        self.A = A
+        self.dev = stream.device
+        self.d = A.device(self.dev)
+        self.m, self.n = A.shape
+        self.b = b
+        self.stream = stream
+        cap = max(b, min(cap, min(self.m, self.n)))
+        self.cap = cap
+        self.Q = torch.empty(self.m, self._alloc_cols(0), dtype=F64, device=self.dev)
+        self.Bt = torch.empty(self.n, self._alloc_cols(0), dtype=F64, device=self.dev)
+        self.K = 0
+        self.ym = torch.empty(self.m, b, dtype=F64, device=self.dev)
+        self.ym2 = torch.empty(self.m, b, dtype=F64, device=self.dev)
+        self.yn = torch.empty(self.n, b, dtype=F64, device=self.dev)
+        self.stat = torch.empty(b + 1, dtype=F64, device=self.dev)
+        self.status = K.new_status(self.dev)
+        self.frob = self.d.frob_sq if A.nnz else 0.0
+        self.err = self.frob
+        self.blocks = 0
+        self.row_energy: list[float] = []
+
+    def _alloc_cols(self, need: int) -> int:
+        c = max(need, 4 * self.b, 64)
+        c = 1 << (c - 1).bit_length() if c < self.cap else self.cap
+        return min(max(c, need), max(self.cap, need))
+
+    def _ensure(self, need: int) -> None:
+        if need <= self.Q.shape[1]:
+            return
+        c = self._alloc_cols(max(need, 2 * self.Q.shape[1]))
+        Q = torch.empty(self.m, c, dtype=F64, device=self.dev)
+        Bt = torch.empty(self.n, c, dtype=F64, device=self.dev)
+        if self.K:
+            Q[:, : self.K].copy_(self.Q[:, : self.K])
+            Bt[:, : self.K].copy_(self.Bt[:, : self.K])
+        self.Q, self.Bt = Q, Bt
+
+    # -- products through the (monkeypatchable) sparse_dense_mul -----------
+    def A_mul(self, X, out):
+        return sparse_dense_mul(self.A, X, False, out=out)
+
+    def AT_mul(self, X, out):
+        return sparse_dense_mul(self.A, X, True, out=out)
+
+    # -- deflations ----------------------------------------------------------
+    def minus_QBX(self, Y, X):
+        """Y -= Q @ (B @ X)   (rsvd.py:135, 140, 179, 187)."""
+        if self.K:
+            C = K.gemm_tn(self.Bt[:, : self.K], X)
+            K.gemm_nn(self.Q[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
+
+    def minus_BtQtX(self, Y, X):
+        """Y -= B.T @ (Q.T @ X)   (rsvd.py:138)."""
+        if self.K:
+            C = K.gemm_tn(self.Q[:, : self.K], X)
+            K.gemm_nn(self.Bt[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
+
+    def minus_QQtX(self, Y):
+        """Y -= Q @ (Q.T @ Y)   (rsvd.py:142, 193)."""
+        if self.K:
+            C = K.gemm_tn(self.Q[:, : self.K], Y)
+            K.gemm_nn(self.Q[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
+
+    def lu(self, Y):
+        K.lu_lower(Y, self.status)
+
+    def orth_into(self, Y, dst):
+        K.tsqr(Y, dst)
+
+    def append(self, src):
+        """Re-orthogonalise ``src`` against Q, append it and B_l = q.T A."""
+        b, k0 = self.b, self.K
+        self._ensure(k0 + b)
+        self.minus_QQtX(src)
+        qdst = self.Q[:, k0 : k0 + b]
+        self.orth_into(src, qdst)
+        bdst = self.Bt[:, k0 : k0 + b]
+        self.AT_mul(qdst, bdst)
+        K.sumsq(bdst, self.stat[:b], self.stat[b : b + 1])
+        st = self.stat.cpu().numpy()  # the one host sync per block
+        flags = K.check_status(self.status) | K.check_status(self.stream.status)
+        if flags & STATUS_STREAM_SHORT:
+            raise RuntimeError("Gaussian stream window exhausted (internal sizing error)")
+        if flags & STATUS_ZERO_PIVOT:
+            raise RankDeficientError("exactly singular pivot in LU factorization")
+        self.K = k0 + b
+        self.blocks += 1
+        self.err = max(self.err - float(st[b]), 0.0)
+        self.row_energy.extend(float(x) for x in st[:b])
+
+    def state(self) -> QbState:
+        return QbState(self.Q[:, : self.K], self.Bt[:, : self.K], self.err, self.blocks, self.b, self.frob,
+                       np.asarray(self.row_energy))
+
+
+def qb_power_blocks(A: SparseRatings, block_size: int, power: int, stream: GaussianStream,
+                    max_rank: int | None = None) -> Iterator[QbState]:
+    """Alg. 2 block generator with power iteration (rsvd.py:112-148)."""
+    m, n = A.shape
+    b = block_size
+    cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
+    E = _QbEngine(A, b, stream, cap)
+    while (E.blocks + 1) * b <= min(m, n):
+        om = stream.normal_device(n, b, out=E.yn)
+        y = E.A_mul(om, E.ym)
+        E.minus_QBX(y, om)
+        E.orth_into(y, y)
+        for _ in range(power):
+            g = E.AT_mul(y, E.yn)
+            E.minus_BtQtX(g, y)
+            E.orth_into(g, g)
+            y = E.A_mul(g, E.ym)
+            E.minus_QBX(y, g)
+            E.orth_into(y, y)
+        E.append(y)
+        yield E.state()
+
+
+def qb_pass_blocks(A: SparseRatings, block_size: int, passes: int, stream: GaussianStream,
+                   max_rank: int | None = None) -> Iterator[QbState]:
+    """Alg. 3 pass-capped block generator (rsvd.py:151-199)."""
+    m, n = A.shape
+    b = block_size
+    if passes < 2:
+        raise ValueError("passes must be at least 2")
+    cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
+    E = _QbEngine(A, b, stream, cap)
+    nsteps = (passes - 1) // 2
+    while (E.blocks + 1) * b <= min(m, n) - b:
+        if passes % 2 == 0:
+            om = stream.normal_device(n, b, out=E.yn)
+            ql = E.A_mul(om, E.ym)
+            E.minus_QBX(ql, om)
+            E.lu(ql)
+        else:
+            ql = stream.normal_device(m, b, out=E.ym)
+        for t in range(1, nsteps + 1):
+            r = E.AT_mul(ql, E.yn)
+            y = E.A_mul(r, E.ym2 if ql is E.ym else E.ym)
+            if t == nsteps:
+                E.minus_QBX(y, r)
+                E.orth_into(y, y)
+            else:
+                E.lu(y)
+            ql = y
+        E.append(ql)
+        yield E.state()
+
+
+def _refined_rank(row_energy: np.ndarray, frob_sq: float, eps: float) -> tuple[int, float]:
+    """Smallest prefix of B's rows meeting eps (rsvd.py:202-214)."""
+    cum = np.cumsum(row_energy)
+    hits = np.nonzero(frob_sq - cum < eps * eps * frob_sq)[0]
+    k = int(hits[0]) + 1 if hits.size else row_energy.size
+    return k, max(float(frob_sq - cum[k - 1]), 0.0)
+
+
+def basic_rsvd(A: SparseRatings, k: int, power: int = 0, oversample: int = 0, seed: int = 0) -> SvdTriplet:
+    """Alg. 1: rank-k randomized SVD with a single sketch (rsvd.py:217-264)."""
+    m, n = A.shape
+    if k < 1:
+        raise ValueError("k must be positive")
+    if power < 0 or oversample < 0:
+        raise ValueError("power and oversample must be nonnegative")
+    ell = k + oversample
+    if ell > min(m, n):
+        raise ValueError(f"k + oversample = {ell} exceeds min(m, n) = {min(m, n)}")
+    stream = GaussianStream(seed)
+    dev = stream.device
+    om = stream.normal_device(n, ell)
+    y = sparse_dense_mul(A, om)
+    q, R = K.tsqr(y)
+    _check_rank(y, R)
+    for _ in range(power):
+        g = sparse_dense_mul(A, q, True)
+        gq, R = K.tsqr(g)
+        _check_rank(g, R)
+        y = sparse_dense_mul(A, gq)
+        q, R = K.tsqr(y)
+        _check_rank(y, R)
+    bt = sparse_dense_mul(A, q, True)  # b.T (n x ell)
+    st = K.new_status(dev)
+    s, Ub, Vb = K.gesvj(bt, st)  # b.T = Ub diag(s) Vb.T  ->  b = Vb diag(s) Ub.T
+    u = K.gemm_nn(q, Vb[:, :k].contiguous())
+    return SvdTriplet(u.cpu().numpy(), s[:k].cpu().numpy(), Ub[:, :k].cpu().numpy(), k)
+
+
+def fixed_precision_qb(A: SparseRatings, tol: float, block_size: int = 20, power: int = 0, seed: int = 0,
+                       max_rank: int | None = None) -> QbState:
+    """Alg. 2 (randQB_EI): grow QB until ||A - QB||_F <= tol ||A||_F, then
+    trim the last block to the smallest sufficient rank (rsvd.py:267-319).
+
+    ``max_rank`` (not in the reference) caps the scan; hitting it raises
+    RankExhaustedError with the state, like the reference's own cap.
+    """
+    if not 0.0 < tol < 1.0:
+        raise ValueError("tol must lie in (0, 1)")
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    if power < 0:
+        raise ValueError("power must be nonnegative")
+    if block_size > min(A.shape):
+        raise ValueError(f"block_size {block_size} exceeds min(m, n) = {min(A.shape)}")
+    if A.nnz == 0 or A.device().frob_sq == 0.0:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        return QbState(torch.empty(A.m, 0, dtype=F64, device=dev), torch.empty(A.n, 0, dtype=F64, device=dev),
+                       0.0, 0, block_size, 0.0, np.empty(0))
+    stream = GaussianStream(seed)
+    last = None
+    for state in qb_power_blocks(A, block_size, power, stream, max_rank=max_rank):
+        last = state
+        if state.err < tol * tol * state.frob_sq:
+            k, err = _refined_rank(state.row_energy, state.frob_sq, tol)
+            return QbState(state.Q_device[:, :k], state.Bt_device[:, :k], err, state.blocks, block_size,
+                           state.frob_sq, state.row_energy[:k])
+        if max_rank is not None and state.rank >= max_rank:
+            break
+    raise RankExhaustedError(f"residual target {tol:.3e} unmet at rank cap", state=last)
+
+
+def _svd_from_qb(Qm: torch.Tensor, Btm: torch.Tensor, k: int):
+    """Top-k singular triplets of Q B through eig_svd(B.T) (rsvd.py:384-389)."""
+    st = K.new_status(Qm.device)
+    G = K.gemm_tn(Btm, Btm)  # B B.T
+    w, V = K.syev(G, st)
+    if K.check_status(st) & STATUS_NEAR_SINGULAR:
+        raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
+                                f"{EIG_FLOOR * float(torch.trace(G)):.3e}")
+    r = G.shape[0]
+    idx = torch.arange(r - 1, r - 1 - k, -1, device=Qm.device)
+    Vk = V[:, idx].contiguous()
+    s = torch.sqrt(torch.clamp(w[idx], min=0.0))
+    u = K.gemm_nn(Qm, Vk)  # Q @ dec.v[:, idx]
+    v = K.gemm_nn(Btm, Vk)  # dec.u[:, idx] = (B.T @ V) / s
+    v.div_(s)
+    return u, s, v
+
+
+def adaptive_pca(A: SparseRatings, criterion: TerminationCriterion, block_size: int = 20, passes: int = 10,
+                 seed: int = 0, max_rank: int | None = None, device_output: bool = False) -> SvdTriplet:
+    """Alg. 3: blocked randomized SVD, fixed pass budget, pluggable stop
+    (rsvd.py:322-392).  ``device_output`` keeps u, s, v as CUDA tensors."""
+    if passes <= 2:
+        raise ValueError("passes must exceed 2")
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    m, n = A.shape
+    work = A.transposed() if m > n else A
+    b = block_size
+    if isinstance(criterion, FixedRank):
+        b = min(b, criterion.k)
+    if 2 * b > min(m, n):
+        raise ValueError(f"block_size {b} too large for min(m, n) = {min(m, n)}")
+    stream = GaussianStream(seed)
+    met = last = None
+    for state in qb_pass_blocks(work, b, passes, stream, max_rank=max_rank):
+        last = state
+        if criterion(state):
+            met = state
+            break
+        if max_rank is not None and state.rank >= max_rank:
+            break
+    if met is None:
+        raise RankExhaustedError("termination criterion never met", state=last)
+    if isinstance(criterion, FixedRank):
+        k = criterion.k
+        Qm, Btm = met.Q_device, met.Bt_device
+    elif isinstance(criterion, FrobTolerance):
+        k, _ = _refined_rank(met.row_energy, met.frob_sq, criterion.eps)
+        Qm, Btm = met.Q_device[:, :k], met.Bt_device[:, :k]
+    else:
+        k = met.rank
+        Qm, Btm = met.Q_device, met.Bt_device
+    u, s, v = _svd_from_qb(Qm, Btm, k)
+    if m > n:
+        u, v = v, u
+    if device_output:
+        return SvdTriplet(u, s, v, int(k))
+    return SvdTriplet(u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy(), int(k))
+
+
+__all__ = ["FixedRank", "FrobTolerance", "QbState", "RankExhaustedError", "TerminationCriterion", "adaptive_pca",
+           "basic_rsvd", "fixed_precision_qb", "qb_pass_blocks", "qb_power_blocks"]
