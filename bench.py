@@ -1,0 +1,292 @@
+#!/usr/bin/env python3
+"""Headline benchmark: time-to-converged-k of the adaptive-PCA CF pipeline.
+
+Workload (BASELINE.json configs[3]): a 138,493 x 26,744 synthetic rating
+matrix with 20,000,263 ratings (half stars, rank-40 model, Zipf(1.2) items,
+log-normal(4, 1.2) user degrees, >= 20 ratings/user), split 90/5/5 with
+seed 0.  One step = the reference's Alg. 5 pipeline
+``auto_latent_factors(train, validation, block_size=20, passes=4 (p=1),
+patience=2, min_improvement=1e-4, seed=0)`` capped at k = 400, followed by
+test-set scoring (MAE and RMSE of the Alg. 4 predictions).  The value is the
+device-timed seconds of one step (lower is better).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the CPU oracle (a numpy restatement of the
+reference, oracle/svdrec_oracle.py) on a bounded sample of the same
+workload and extrapolates to the full step (the reference's per-sample
+Python scoring loop makes a full run take hours).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG = "c3_20m"
+BLOCK, PASSES, PATIENCE, MIN_IMPROVEMENT, SEED, K_CAP = 20, 4, 2, 1e-4, 0, 400
+SPLIT = (0.9, 0.05, 0.05)
+METRIC = "time-to-converged-k (s), adaptive-PCA CF pipeline, 138k x 27k / 20M nnz"
+# blocks the pipeline runs on this workload (deterministic; measured by the
+# b200 arm, used by the reference arm's extrapolation)
+REF_BLOCKS = None
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _workload():
+    from paper_2009_02251_b200 import synth
+    cfg = synth.CONFIGS[CONFIG]
+    t = time.perf_counter()
+    M = synth.generate(cfg)
+    tr, va, te = synth.split_holdout(M, SPLIT, seed=0)
+    gen_s = time.perf_counter() - t
+    return cfg, M, tr, va, te, gen_s
+
+
+def _config_dict(cfg, tr):
+    return {
+        "workload": f"{CONFIG}: ML-20M-shaped synthetic {cfg.users}x{cfg.items}, {cfg.nnz} ratings "
+                    f"(train {tr.nnz}), rank {cfg.rank}, Zipf({cfg.zipf}) items, half stars",
+        "pipeline": "auto_latent_factors (Alg. 5, ValidationMae stop) + test MAE/RMSE",
+        "block_size": BLOCK, "passes": PASSES, "power": (PASSES - 2) // 2, "patience": PATIENCE,
+        "k_cap": K_CAP, "split": "0.9/0.05/0.05 seed 0", "dtype": "float64",
+        "l2": "inputs exceed L2 (CSR of A and A.T, 2 x 216 MB > 126 MB); no explicit flush",
+    }
+
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-i", str(index), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
+        sm = [float(r[0]) for r in rows if len(r) >= 6 and r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 6 and r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 6 for i in range(4) if "Active" == r[2 + i].strip()})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_estimate(tr, va, te, nblocks: int, n_samples: int = 600):
+    """Time the oracle on a bounded sample and extrapolate to the full step.
+
+    Measured: the oracle's first two QB blocks (K = 20, 40) on the full
+    train matrix, latent_T at K = 20 / 40, and Alg. 4 scoring of
+    ``n_samples`` validation samples at K = 20 / 40.  Each cost is
+    extrapolated linearly in K to the nblocks of the real run; scoring cost
+    is scaled to the full validation (per block) and test (once) sets.
+    """
+    from oracle import svdrec_oracle as O
+    import threadpoolctl
+
+    t_qb, t_lat, t_ps = [], [], []
+    gen = O.pass_blocks(tr, BLOCK, PASSES, O.Stream(SEED))
+    sub = (va[0][:n_samples], va[1][:n_samples])
+    t_all = time.perf_counter()
+    for _ in range(2):
+        t = time.perf_counter()
+        s = next(gen)
+        t_qb.append(time.perf_counter() - t)
+        t = time.perf_counter()
+        T = O.latent_T(s.B)
+        t_lat.append(time.perf_counter() - t)
+        t = time.perf_counter()
+        O.predict_many(tr, T, 0.5, 5.0, *sub)
+        t_ps.append((time.perf_counter() - t) / n_samples)
+    measured = time.perf_counter() - t_all
+
+    def at(vals, k):  # linear in K through the two measured points (K = 20, 40)
+        return max(vals[0] + (vals[1] - vals[0]) * (k - BLOCK) / BLOCK, vals[0])
+
+    nv, nt = len(va[0]), len(te[0])
+    total = 0.0
+    for l in range(1, nblocks + 1):
+        k = l * BLOCK
+        total += at(t_qb, k) + at(t_lat, k) + nv * at(t_ps, k)
+    total += nt * at(t_ps, nblocks * BLOCK)
+    info = threadpoolctl.threadpool_info()
+    cores = max([i.get("num_threads", 1) for i in info] + [1])
+    sample = (f"oracle: 2 QB blocks on the full train matrix + latent_T + Alg. 4 scoring of {n_samples} "
+              f"validation samples at K=20,40 ({measured:.1f} s measured); extrapolated linearly in K to "
+              f"{nblocks} blocks x {nv} validation + {nt} test samples")
+    return total, cores, sample, measured
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    cfg, M, tr, va, te, _ = _workload()
+    nblocks = args.blocks or REF_BLOCKS or 6
+    vals = []
+    for i in range(args.warmup + args.steps):
+        total, cores, sample, _ = cpu_estimate(tr, va, te, nblocks, n_samples=300 if i < args.warmup else 600)
+        if i >= args.warmup:
+            vals.append(total)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config_dict(cfg, tr),
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2009_02251_b200 as P
+    from paper_2009_02251_b200 import _lib, kernels as K
+    from paper_2009_02251_b200.cf import _Samples
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    cfg, M, tr, va, te, gen_s = _workload()
+    lo, hi = cfg.bounds
+    A = P.SparseRatings(tr, lo, hi)
+    d = A.device(dev)
+    vs, ts = _Samples(va, dev), _Samples(te, dev)
+    torch.cuda.synchronize()
+
+    def step():
+        f, trace = P.auto_latent_factors(A, vs, block_size=BLOCK, passes=PASSES, patience=PATIENCE,
+                                         min_improvement=MIN_IMPROVEMENT, seed=SEED, max_rank=K_CAP)
+        mae, rmse = P.evaluate_errors(A, f, ts)
+        return f, trace, mae, rmse
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    K.PROFILE = []
+    launches0 = lib.svdrec_launch_count()
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        f, trace, mae, rmse = step()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    launches = (lib.svdrec_launch_count() - launches0) // args.steps
+    prof = K.profile_summary(K.PROFILE)
+    K.PROFILE = None
+    ck = clocks.stop()
+    t_step = max(times)
+    if ws > 1:
+        tt = torch.tensor([t_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        t_step = float(tt.item())
+
+    # e2e: the public API from host buffers, upload + results read inside
+    e2e_times, h2d = [], 0
+    for _ in range(max(1, min(args.steps, 2))):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        A2 = P.SparseRatings(tr, lo, hi)
+        f2, tr2 = P.auto_latent_factors(A2, va, block_size=BLOCK, passes=PASSES, patience=PATIENCE,
+                                        min_improvement=MIN_IMPROVEMENT, seed=SEED, max_rank=K_CAP)
+        mae2, rmse2 = P.evaluate_errors(A2, f2, te)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1) / 1e3)
+        d2 = A2.device(dev)
+        h2d = d2.h2d_bytes + 2 * (len(va[0]) * 16) + len(te[0]) * 16
+    nb = len(trace)
+    d2h = nb * ((BLOCK + 1) * 8 + 4 * 3 + 16) + 16
+
+    sp = prof.get("spmm", (0, 0.0, 0))
+    achieved = (sp[2] / (sp[1] / 1e3)) / 1e9 if sp[1] > 0 else None
+    peaks_p = ROOT / "MEASURED_PEAKS.json"
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if peaks_p.is_file():
+        peak, peak_src = float(json.loads(peaks_p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    breakdown = {k: {"calls": v[0] // args.steps, "ms": round(v[1] / args.steps, 3),
+                     "share": round(v[1] / (sum(x[1] for x in prof.values()) or 1), 4)} for k, v in prof.items()}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(t_step, 6), "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": False,
+        "scaling": "strong" if ws == 1 else "replicas", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(cfg, tr),
+        "k": int(f.k), "blocks": nb, "test_mae": mae, "test_rmse": rmse, "val_mae": min(e.mae for e in trace),
+        "roofline": {"kernel": "svdrec_spmm (k_spmm<2>)", "bound": "hbm",
+                     "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                     "peak_source": peak_src, "calls_per_step": sp[0] // args.steps,
+                     "algorithmic_bytes_per_call": int(sp[2] / max(sp[0], 1))},
+        "kernel_breakdown": breakdown,
+        "e2e": {"value": round(max(e2e_times), 6), "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "clocks": ck,
+        "setup": {"generate_split_s": round(gen_s, 2)},
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        total, cores, sample, _ = cpu_estimate(tr, va, te, nb)
+        line["cpu_baseline"] = {"value": round(total, 3), "unit": "s", "cores": cores, "kind": "port",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--blocks", type=int, default=None, help="reference arm: block count to extrapolate to")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

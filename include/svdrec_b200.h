@@ -46,6 +46,8 @@ extern "C" {
 int svdrec_abi_version(void);
 const char* svdrec_last_error(void);
 int svdrec_device_sm_count(void);
+/* Number of kernels this library has launched in the process so far. */
+long long svdrec_launch_count(void);
 
 /* ---------------------------------------------------------------------
  * Gaussian stream.  Replaces GaussianStream.normal / gaussian_matrix

@@ -10,8 +10,12 @@
 namespace svdrec {
 
 void set_error(const char* fmt, ...);
+void note_launches(int n);
 
-inline int check_launch(const char* what) {
+// Check the last launch(es) and count ``n`` kernel launches issued by this
+// library (svdrec_launch_count).
+inline int check_launch(const char* what, int n = 1) {
+  note_launches(n);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));

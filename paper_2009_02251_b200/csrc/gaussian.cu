@@ -333,5 +333,5 @@ extern "C" int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_p
   k_chain<<<1, 1, 0, s>>>(agg, p.nblocks, count, ccfg, coff, d_status);
   k_emit_from<<<grid, tb, 0, s>>>(key_lo, key_hi, d_pos, pos0, p.nchunks, incl, ccfg, coff, count, cols,
                                    d_row_perm, d_out, ld);
-  return check_launch("normal_fill");
+  return check_launch("normal_fill", 5);
 }

@@ -1,5 +1,6 @@
 // Library plumbing: error reporting, device attributes, ABI version.
 #include <cstdarg>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -14,6 +15,10 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+
+static std::atomic<long long> g_launches{0};
+
+void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int sm_count() {
   static int n = 0;
@@ -31,3 +36,4 @@ int sm_count() {
 extern "C" int svdrec_abi_version(void) { return 1; }
 extern "C" const char* svdrec_last_error(void) { return svdrec::g_err; }
 extern "C" int svdrec_device_sm_count(void) { return svdrec::sm_count(); }
+extern "C" long long svdrec_launch_count(void) { return svdrec::g_launches.load(); }

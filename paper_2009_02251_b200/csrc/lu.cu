@@ -159,5 +159,6 @@ extern "C" int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, d
   int32_t bb = b;
   void* args[] = {&r, &bb, &d_A, &lda, &d_udiag, &pivstep, &slots, &d_status};
   SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_lu, dim3(nblk), dim3(kLuThreads), args, 0, as_stream(stream)));
+  note_launches(1);
   return 0;
 }

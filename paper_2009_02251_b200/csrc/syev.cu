@@ -176,6 +176,7 @@ int run_jacobi(int64_t rows, int k, const double* A, int64_t lda, double* W, dou
     void* args[] = {&rr, &kk32, &W, &V, &flags, &tol, &d_status};
     SVDREC_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), s));
     SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, dim3(nblk), dim3(kJThreads), args, 0, s));
+    note_launches(1);
   }
   k_norms<<<k, 128, 0, s>>>(rows, W, lam);
   return check_launch("jacobi_norms");

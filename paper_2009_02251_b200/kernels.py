@@ -15,6 +15,40 @@ from ._lib import call, ptr, query, scratch, stream_handle
 
 F64 = torch.float64
 
+# Optional live instrumentation: when ``PROFILE`` is a list, every wrapper
+# below appends (name, start_event, end_event, algorithmic_bytes) recorded
+# on the launching stream.  bench.py uses it for the roofline numbers.
+PROFILE: list | None = None
+
+
+class _span:
+    __slots__ = ("name", "nbytes", "e0")
+
+    def __init__(self, name: str, nbytes: int = 0):
+        self.name, self.nbytes, self.e0 = name, nbytes, None
+
+    def __enter__(self):
+        if PROFILE is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        if self.e0 is not None and exc[0] is None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            PROFILE.append((self.name, self.e0, e1, self.nbytes))
+        return False
+
+
+def profile_summary(records) -> dict:
+    """{name: (calls, total_ms, total_algorithmic_bytes)} after a sync."""
+    out: dict = {}
+    for name, e0, e1, nb in records:
+        c, t, b = out.get(name, (0, 0.0, 0))
+        out[name] = (c + 1, t + e0.elapsed_time(e1), b + nb)
+    return out
+
 
 def _mat(t: torch.Tensor, name: str) -> int:
     if t.dim() != 2 or t.dtype != F64 or not t.is_cuda:
@@ -33,8 +67,9 @@ def normal_fill(key: tuple[int, int], pos: torch.Tensor, rows: int, cols: int, o
     ld = _mat(out, "normal.out")
     count = rows * cols
     ws, nb = scratch(out.device).get(query("svdrec_normal_workspace_bytes", count))
-    call("svdrec_normal_fill", key[0], key[1], ptr(pos), count, cols, ptr(row_perm), ptr(out), ld, ws, nb,
-         ptr(status), stream_handle())
+    with _span("normal", count * 8):
+        call("svdrec_normal_fill", key[0], key[1], ptr(pos), count, cols, ptr(row_perm), ptr(out), ld, ws, nb,
+             ptr(status), stream_handle())
     return out
 
 
@@ -45,9 +80,11 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
     if Y.shape[1] != b or X.shape[0] != plan.n or Y.shape[0] != plan.m:
         raise ValueError(f"spmm: shape mismatch A{(plan.m, plan.n)} X{tuple(X.shape)} Y{tuple(Y.shape)}")
     part = plan.partial(b)
-    call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
-         ptr(plan.indices), ptr(plan.values), ptr(X), ldx, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
-         ptr(plan.long_s0), ptr(plan.long_s1), ptr(part), stream_handle())
+    nbytes = plan.nnz * 12 + (plan.m + 1) * 8 + (plan.n + plan.m) * b * 8
+    with _span("spmm", nbytes):
+        call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
+             ptr(plan.indices), ptr(plan.values), ptr(X), ldx, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
+             ptr(plan.long_s0), ptr(plan.long_s1), ptr(part), stream_handle())
     return Y
 
 
@@ -63,8 +100,9 @@ def gemm_tn(X: torch.Tensor, Y: torch.Tensor, C: torch.Tensor | None = None, alp
         C = torch.empty(p, q, dtype=F64, device=X.device)
     ldc = _mat(C, "gemm_tn.C")
     ws, nb = scratch(X.device).get(query("svdrec_gemm_tn_workspace_bytes", r, p, q))
-    call("svdrec_gemm_tn", r, p, q, float(alpha), ptr(X), ldx, ptr(Y), ldy, float(beta), ptr(C), ldc, ws, nb,
-         stream_handle())
+    with _span("gemm_tn", (r * (p + q) + p * q) * 8):
+        call("svdrec_gemm_tn", r, p, q, float(alpha), ptr(X), ldx, ptr(Y), ldy, float(beta), ptr(C), ldc, ws, nb,
+             stream_handle())
     return C
 
 
@@ -79,8 +117,9 @@ def gemm_nn(X: torch.Tensor, Cm: torch.Tensor, Y: torch.Tensor | None = None, al
     if Y is None:
         Y = torch.empty(r, q, dtype=F64, device=X.device)
     ldy = _mat(Y, "gemm_nn.Y")
-    call("svdrec_gemm_nn", r, p, q, float(alpha), ptr(X), ldx, ptr(Cm), ldc, float(beta), ptr(Y), ldy,
-         stream_handle())
+    with _span("gemm_nn", (r * (p + 2 * q) + p * q) * 8):
+        call("svdrec_gemm_nn", r, p, q, float(alpha), ptr(X), ldx, ptr(Cm), ldc, float(beta), ptr(Y), ldy,
+             stream_handle())
     return Y
 
 
@@ -88,7 +127,8 @@ def sumsq(X: torch.Tensor, colsq: torch.Tensor | None = None, total: torch.Tenso
     ldx = _mat(X, "sumsq.X")
     r, q = X.shape
     ws, nb = scratch(X.device).get(query("svdrec_sumsq_workspace_bytes", r, q))
-    call("svdrec_sumsq", r, q, ptr(X), ldx, ptr(colsq), ptr(total), ws, nb, stream_handle())
+    with _span("sumsq", r * q * 8):
+        call("svdrec_sumsq", r, q, ptr(X), ldx, ptr(colsq), ptr(total), ws, nb, stream_handle())
     return colsq, total
 
 
@@ -110,7 +150,8 @@ def tsqr(A: torch.Tensor, Q: torch.Tensor | None = None, R: torch.Tensor | None 
         R = torch.empty(b, b, dtype=F64, device=A.device)
     ldq = _mat(Q, "tsqr.Q")
     ws, nb = scratch(A.device).get(query("svdrec_tsqr_workspace_bytes", r, b))
-    call("svdrec_tsqr", r, b, ptr(A), lda, ptr(Q), ldq, ptr(R), ws, nb, stream_handle())
+    with _span("tsqr", 2 * r * b * 8):
+        call("svdrec_tsqr", r, b, ptr(A), lda, ptr(Q), ldq, ptr(R), ws, nb, stream_handle())
     return Q, R
 
 
@@ -121,7 +162,8 @@ def lu_lower(A: torch.Tensor, status: torch.Tensor, udiag: torch.Tensor | None =
     if udiag is None:
         udiag = torch.empty(b, dtype=F64, device=A.device)
     ws, nb = scratch(A.device).get(query("svdrec_lu_workspace_bytes", r, b))
-    call("svdrec_lu_lower", r, b, ptr(A), lda, ptr(udiag), ws, nb, ptr(status), stream_handle())
+    with _span("lu", 2 * r * b * 8):
+        call("svdrec_lu_lower", r, b, ptr(A), lda, ptr(udiag), ws, nb, ptr(status), stream_handle())
     return udiag
 
 
@@ -132,7 +174,8 @@ def syev(G: torch.Tensor, status: torch.Tensor):
     w = torch.empty(k, dtype=F64, device=G.device)
     V = torch.empty(k, k, dtype=F64, device=G.device)
     ws, nb = scratch(G.device).get(query("svdrec_syev_workspace_bytes", k))
-    call("svdrec_syev", k, ptr(G), ldg, ptr(w), ptr(V), k, ws, nb, ptr(status), stream_handle())
+    with _span("syev", 2 * k * k * 8):
+        call("svdrec_syev", k, ptr(G), ldg, ptr(w), ptr(V), k, ws, nb, ptr(status), stream_handle())
     return w, V
 
 
@@ -153,7 +196,8 @@ def cf_normalize(Tt: torch.Tensor):
     n, k = Tt.shape
     Tn = torch.empty(n, k, dtype=F64, device=Tt.device)
     norm = torch.empty(n, dtype=F64, device=Tt.device)
-    call("svdrec_cf_normalize", n, k, ptr(Tt), ldt, ptr(Tn), k, ptr(norm), stream_handle())
+    with _span("cf_normalize", 2 * n * k * 8):
+        call("svdrec_cf_normalize", n, k, ptr(Tt), ldt, ptr(Tn), k, ptr(norm), stream_handle())
     return Tn, norm
 
 
@@ -164,9 +208,10 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     val = torch.empty(ns, dtype=F64, device=Tn.device)
     raw = torch.empty(ns, dtype=F64, device=Tn.device)
     fb = torch.empty(ns, dtype=torch.uint8, device=Tn.device)
-    call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
-         ptr(csr.indices), ptr(csr.values), Tn.shape[1], ptr(Tn), ldn, ptr(norm), float(gmean), float(lo),
-         float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
+    with _span("cf_predict", 0):
+        call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
+             ptr(csr.indices), ptr(csr.values), Tn.shape[1], ptr(Tn), ldn, ptr(norm), float(gmean), float(lo),
+             float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
     return val, raw, fb
 
 

@@ -157,6 +157,7 @@ class DeviceCSR:
         self.long_s1 = t(s1, np.int32)
         self.nslots = nslots
         self._partial = {}
+        self.h2d_bytes = (self.m + 1) * 8 + self.nnz * 12 + self.nseg * 24 + self.nlong * 12
 
     def partial(self, b: int) -> torch.Tensor | None:
         if self.nslots == 0:
@@ -181,6 +182,7 @@ class DeviceRatings:
         self.rating_min, self.rating_max = ratings.rating_min, ratings.rating_max
         self.A = DeviceCSR(ratings.matrix, device)
         self.AT = DeviceCSR(ratings.matrix.T.tocsr(), device)
+        self.h2d_bytes = self.A.h2d_bytes + self.AT.h2d_bytes
         # ||A||_F^2 and the global mean (fro_norm_sq, linalg.py:161-168;
         # _global_mean, cf.py:102-105) reduced on the device, read once.
         from . import kernels as K
