@@ -90,13 +90,17 @@ class LatentFactors:
         return cls(Tt)
 
 
-def _latent_device(Bt: torch.Tensor, G: torch.Tensor | None = None) -> LatentFactors:
-    """T.T = B.T V diag(s^-1/2) with eig(B B.T) descending (cf.py:77-92)."""
-    st = K.new_status(Bt.device)
+def _latent_device(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor | None = None
+                   ) -> LatentFactors:
+    """T.T = B.T V diag(s^-1/2) with eig(B B.T) descending (cf.py:77-92).
+
+    With ``status`` given, the near-singular flag is left in it for the
+    caller's next batched read instead of being checked here."""
+    st = K.new_status(Bt.device) if status is None else status
     if G is None:
         G = K.gemm_tn(Bt, Bt)
     w, V = K.syev(G, st)
-    if K.check_status(st) & STATUS_NEAR_SINGULAR:
+    if status is None and K.check_status(st) & STATUS_NEAR_SINGULAR:
         raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
                                 f"{EIG_FLOOR * float(torch.trace(G)):.3e}")
     Wm = V.flip(1) * torch.rsqrt(torch.sqrt(torch.clamp(w.flip(0), min=0.0)))
@@ -253,6 +257,10 @@ class ValidationMae:
         self._start = time.perf_counter()
         self._G = None
         self._Gsrc = None
+        self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1))
+        if train.nnz == 0:
+            raise ValueError("cannot take the mean of a matrix with no ratings")
+        self._gmean = d.global_mean
 
     @property
     def validation(self):
@@ -277,8 +285,15 @@ class ValidationMae:
     def __call__(self, state: QbState) -> bool:
         if state.rank == 0:
             raise ValueError("empty factorization has no latent factors")
-        factors = _latent_device(state.Bt_device, self._gram(state.Bt_device))
-        score, rmse = _errors(self.train, factors, self.samples)
+        mb = self._mb
+        factors = _latent_device(state.Bt_device, self._gram(state.Bt_device), status=mb["status"])
+        s = self.samples
+        val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+        K.err_sum(val, s.truth, out=mb["sums"])
+        got = mb.read()  # one host read per block: error sums + eig status
+        if int(got["status"][0]) & STATUS_NEAR_SINGULAR:
+            raise NearSingularError("Gram eigenvalue below floor in latent_from_qb")
+        score, rmse = float(got["sums"][0] / s.n), float(np.sqrt(got["sums"][1] / s.n))
         self.trace.append(BlockEval(k=state.rank, mae=score, seconds=time.perf_counter() - self._start))
         if score < self.best_mae - self.min_improvement:
             self._stale = 0

@@ -10,9 +10,11 @@
 // transducer with three states -- S (start of a sample), T+ / T- (inside the
 // exponential-tail loop, carrying the sample's sign) -- whose moves consume
 // one or two raw words.  The parse is parallelised exactly:
-//   A. each thread owns a chunk of 64 raw positions and tabulates, for each
+//   A. each thread owns a chunk of 32 raw positions and tabulates, for each
 //      of the 6 possible entry configurations (entry offset 0/1 x state),
-//      the exit configuration and the number of samples emitted;
+//      the exit configuration and the number of samples emitted (the five
+//      secondary entries stop as soon as they meet the primary walk's
+//      trajectory, usually within one or two moves);
 //   B. each CTA composes its 1024 chunk tables with an inclusive
 //      Hillis-Steele scan (composition of finite maps is associative);
 //   C. one thread threads the true entry configuration through the CTA
@@ -25,7 +27,7 @@
 namespace svdrec {
 namespace {
 
-constexpr int kChunk = 64;
+constexpr int kChunk = 32;
 constexpr int kScan = 1024;
 constexpr int kCfg = 6;
 constexpr uint64_t kM0 = 0xD2E7470EE14C6C93ULL, kM1 = 0xCA5A826395121157ULL;
@@ -160,19 +162,48 @@ __global__ void k_tables(uint64_t k0, uint64_t k1, const int64_t* __restrict__ d
   const uint64_t base = (uint64_t)*d_pos + (uint64_t)c * kChunk, end = base + kChunk;
   Raw raw;
   raw.init(k0, k1);
-  for (int cfg = 0; cfg < kCfg; ++cfg) {
-    uint64_t p = base + (cfg / 3);
-    int st = cfg % 3;
-    uint32_t cnt = 0;
-    while (p < end) {
+  // primary walk from (offset 0, S); remember which (position, state) it
+  // visits and how many samples it had emitted before each.
+  uint8_t vis[kChunk + 1];
+  uint8_t cum[kChunk + 1];
+#pragma unroll
+  for (int i = 0; i <= kChunk; ++i) vis[i] = 0xff;
+  uint64_t p = base;
+  int st = 0;
+  uint32_t cnt = 0;
+  while (p < end) {
+    vis[p - base] = (uint8_t)st;
+    cum[p - base] = (uint8_t)cnt;
+    int nst;
+    bool emit;
+    double v;
+    p += move(st, p, raw, nst, emit, v);
+    st = nst;
+    cnt += emit;
+  }
+  const uint32_t p_exit = (uint32_t)((p - end) * 3 + st), p_cnt = cnt;
+  tab[c * kCfg] = (p_cnt << 3) | p_exit;
+  // the other five entries follow the primary as soon as they meet it
+  for (int cfg = 1; cfg < kCfg; ++cfg) {
+    uint64_t q = base + (cfg / 3);
+    int s2 = cfg % 3;
+    uint32_t c2 = 0;
+    bool merged = false;
+    while (q < end) {
+      const uint32_t off = (uint32_t)(q - base);
+      if (vis[off] == (uint8_t)s2) {
+        c2 += p_cnt - cum[off];
+        merged = true;
+        break;
+      }
       int nst;
       bool emit;
       double v;
-      p += move(st, p, raw, nst, emit, v);
-      st = nst;
-      cnt += emit;
+      q += move(s2, q, raw, nst, emit, v);
+      s2 = nst;
+      c2 += emit;
     }
-    tab[c * kCfg + cfg] = (cnt << 3) | (uint32_t)((p - end) * 3 + st);
+    tab[c * kCfg + cfg] = merged ? ((c2 << 3) | p_exit) : ((c2 << 3) | (uint32_t)((q - end) * 3 + s2));
   }
 }
 

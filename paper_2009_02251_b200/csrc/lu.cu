@@ -78,19 +78,42 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(int64_t r, int b, double* __r
       slots[(size_t)(j & 1) * nblk + blockIdx.x] = Cand{bb, br};
     }
     grid.sync();
-    if (threadIdx.x == 0) {
+    {
+      // every block reduces all candidates in parallel (same fixed result)
       double bb = -1.0;
       long long br = -1;
       const Cand* sl = slots + (size_t)(j & 1) * nblk;
-      for (int k = 0; k < nblk; ++k) {
+      for (int k = threadIdx.x; k < nblk; k += blockDim.x) {
         const Cand cc = sl[k];
         if (cc.row >= 0 && (br < 0 || better(cc.a, cc.row, bb, br))) {
           bb = cc.a;
           br = cc.row;
         }
       }
-      piv_row = br;
-      piv_val = br >= 0 ? A[br * lda + j] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, bb, o);
+        const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+        if (orow >= 0 && (br < 0 || better(ob, orow, bb, br))) {
+          bb = ob;
+          br = orow;
+        }
+      }
+      if (lane == 0) {
+        sa[warp] = bb;
+        sr[warp] = br;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double b2 = -1.0;
+        long long r2 = -1;
+        for (int w = 0; w < kLuThreads / 32; ++w)
+          if (sr[w] >= 0 && (r2 < 0 || better(sa[w], sr[w], b2, r2))) {
+            b2 = sa[w];
+            r2 = sr[w];
+          }
+        piv_row = r2;
+        piv_val = r2 >= 0 ? A[r2 * lda + j] : 0.0;
+      }
     }
     __syncthreads();
     const long long p = piv_row;
@@ -147,7 +170,8 @@ extern "C" int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, d
     int per_sm = 0;
     SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, 0));
     max_blocks = per_sm * sm_count();
-    if (max_blocks > sm_count() * 8) max_blocks = sm_count() * 8;
+    // grid barrier cost grows with the block count: 2 CTAs per SM is plenty
+    if (max_blocks > sm_count() * 2) max_blocks = sm_count() * 2;
     if (max_blocks < 1) max_blocks = 1;
   }
   int64_t want = (r + kLuThreads - 1) / kLuThreads;

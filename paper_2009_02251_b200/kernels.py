@@ -8,6 +8,7 @@ copies.  Nothing here synchronises the device.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -60,6 +61,42 @@ def _mat(t: torch.Tensor, name: str) -> int:
 
 def new_status(device) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+class Mailbox:
+    """Small device buffer holding several result fields (float64 vectors
+    and uint32 status words) that the host reads back with ONE copy."""
+
+    def __init__(self, device, **fields):
+        self.off = {}
+        o = 0
+        for name, spec in fields.items():
+            kind, n = spec
+            size = 8 * n if kind == "f8" else 4 * n
+            o = (o + 7) // 8 * 8
+            self.off[name] = (kind, o, n)
+            o += size
+        self.buf = torch.zeros((o + 7) // 8 * 8, dtype=torch.uint8, device=device)
+
+    def __getitem__(self, name) -> torch.Tensor:
+        kind, o, n = self.off[name]
+        view = self.buf[o: o + (8 if kind == "f8" else 4) * n]
+        return view.view(F64) if kind == "f8" else view.view(torch.int32)
+
+    def read(self) -> dict:
+        host = self.buf.cpu().numpy()
+        out = {}
+        dirty = False
+        for name, (kind, o, n) in self.off.items():
+            a = host[o: o + (8 if kind == "f8" else 4) * n].view(np.float64 if kind == "f8" else np.uint32)
+            out[name] = a.copy()
+            if kind == "u4" and a.any():
+                dirty = True
+        if dirty:
+            for name, (kind, o, n) in self.off.items():
+                if kind == "u4":
+                    self[name].zero_()
+        return out
 
 
 def normal_fill(key: tuple[int, int], pos: torch.Tensor, rows: int, cols: int, out: torch.Tensor,
@@ -215,9 +252,10 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     return val, raw, fb
 
 
-def err_sum(pred: torch.Tensor, truth: torch.Tensor) -> torch.Tensor:
+def err_sum(pred: torch.Tensor, truth: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """Device (sum |p - t|, sum (p - t)^2)."""
-    out = torch.empty(2, dtype=F64, device=pred.device)
+    if out is None:
+        out = torch.empty(2, dtype=F64, device=pred.device)
     n = pred.shape[0]
     ws, nb = scratch(pred.device).get(query("svdrec_err_sum_workspace_bytes", n))
     call("svdrec_err_sum", n, ptr(pred), ptr(truth), ptr(out), ws, nb, stream_handle())

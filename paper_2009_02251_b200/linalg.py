@@ -74,10 +74,12 @@ class GaussianStream:
         self.status = K.new_status(self.device)
 
     def normal_device(self, rows: int, cols: int, out: torch.Tensor | None = None,
-                      row_perm: torch.Tensor | None = None) -> torch.Tensor:
+                      row_perm: torch.Tensor | None = None, status: torch.Tensor | None = None) -> torch.Tensor:
+        """Draw on the device; ``status`` (a uint32 word) overrides the
+        stream's own status word so callers can batch their status reads."""
         if out is None:
             out = torch.empty(rows, cols, dtype=torch.float64, device=self.device)
-        K.normal_fill(self.key, self.pos, rows, cols, out, self.status, row_perm)
+        K.normal_fill(self.key, self.pos, rows, cols, out, self.status if status is None else status, row_perm)
         return out
 
     def check(self) -> None:

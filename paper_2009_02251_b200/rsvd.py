@@ -123,8 +123,9 @@ class _QbEngine:
         self.ym = torch.empty(self.m, b, dtype=F64, device=self.dev)
         self.ym2 = torch.empty(self.m, b, dtype=F64, device=self.dev)
         self.yn = torch.empty(self.n, b, dtype=F64, device=self.dev)
-        self.stat = torch.empty(b + 1, dtype=F64, device=self.dev)
-        self.status = K.new_status(self.dev)
+        # one host read per block: ||B_l||_F^2, row energies, status flags
+        self.mb = K.Mailbox(self.dev, colsq=("f8", b), total=("f8", 1), status=("u4", 1))
+        self.status = self.mb["status"]
         self.frob = self.d.frob_sq if A.nnz else 0.0
         self.err = self.frob
         self.blocks = 0
@@ -187,17 +188,20 @@ class _QbEngine:
         self.orth_into(src, qdst)
         bdst = self.Bt[:, k0 : k0 + b]
         self.AT_mul(qdst, bdst)
-        K.sumsq(bdst, self.stat[:b], self.stat[b : b + 1])
-        st = self.stat.cpu().numpy()  # the one host sync per block
-        flags = K.check_status(self.status) | K.check_status(self.stream.status)
+        K.sumsq(bdst, self.mb["colsq"], self.mb["total"])
+        got = self.mb.read()  # the one host sync per block
+        flags = int(got["status"][0])
         if flags & STATUS_STREAM_SHORT:
             raise RuntimeError("Gaussian stream window exhausted (internal sizing error)")
         if flags & STATUS_ZERO_PIVOT:
             raise RankDeficientError("exactly singular pivot in LU factorization")
         self.K = k0 + b
         self.blocks += 1
-        self.err = max(self.err - float(st[b]), 0.0)
-        self.row_energy.extend(float(x) for x in st[:b])
+        self.err = max(self.err - float(got["total"][0]), 0.0)
+        self.row_energy.extend(float(x) for x in got["colsq"])
+
+    def normal(self, rows: int, cols: int, out):
+        return self.stream.normal_device(rows, cols, out=out, status=self.status)
 
     def state(self) -> QbState:
         return QbState(self.Q[:, : self.K], self.Bt[:, : self.K], self.err, self.blocks, self.b, self.frob,
@@ -212,7 +216,7 @@ def qb_power_blocks(A: SparseRatings, block_size: int, power: int, stream: Gauss
     cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
     E = _QbEngine(A, b, stream, cap)
     while (E.blocks + 1) * b <= min(m, n):
-        om = stream.normal_device(n, b, out=E.yn)
+        om = E.normal(n, b, E.yn)
         y = E.A_mul(om, E.ym)
         E.minus_QBX(y, om)
         E.orth_into(y, y)
@@ -239,12 +243,12 @@ def qb_pass_blocks(A: SparseRatings, block_size: int, passes: int, stream: Gauss
     nsteps = (passes - 1) // 2
     while (E.blocks + 1) * b <= min(m, n) - b:
         if passes % 2 == 0:
-            om = stream.normal_device(n, b, out=E.yn)
+            om = E.normal(n, b, E.yn)
             ql = E.A_mul(om, E.ym)
             E.minus_QBX(ql, om)
             E.lu(ql)
         else:
-            ql = stream.normal_device(m, b, out=E.ym)
+            ql = E.normal(m, b, E.ym)
         for t in range(1, nsteps + 1):
             r = E.AT_mul(ql, E.yn)
             y = E.A_mul(r, E.ym2 if ql is E.ym else E.ym)
