@@ -144,14 +144,16 @@ int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_ud
 /* ---------------------------------------------------------------------
  * Symmetric eigendecomposition for eig_svd (linalg.py:108-138): the
  * k x k Gram G (row-major, symmetric PSD) -> eigenvalues ascending in
- * d_w and eigenvectors as columns of d_V (k x k row-major).  Parallel
- * one-sided Jacobi in one cooperative kernel.  Flags
+ * d_w and eigenvectors as columns of d_V (k x k row-major).  Blocked
+ * one-sided Jacobi in one cooperative kernel (k <= 760; scalar rounds
+ * beyond).  d_V0 (nullable, k x k row-major orthonormal) warm-starts the
+ * sweeps, e.g. with the previous block's eigenvectors padded by I.  Flags
  * SVDREC_STATUS_NEAR_SINGULAR when w[0] <= 0 or w[0] < 1e-14 trace(G).
  * ------------------------------------------------------------------- */
 size_t svdrec_syev_workspace_bytes(int32_t k);
-int svdrec_syev(int32_t k, const double* d_G, int64_t ldg, double* d_w, double* d_V,
-                int64_t ldv, void* d_work, size_t work_bytes, uint32_t* d_status,
-                void* stream);
+int svdrec_syev(int32_t k, const double* d_G, int64_t ldg, const double* d_V0, int64_t ldv0,
+                double* d_w, double* d_V, int64_t ldv, void* d_work, size_t work_bytes,
+                uint32_t* d_status, void* stream);
 
 /* One-sided Jacobi SVD of a tall rows x k block (rows >= k): singular
  * values descending in d_s, left vectors d_U (rows x k), right vectors as

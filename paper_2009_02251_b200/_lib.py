@@ -44,7 +44,7 @@ SIGNATURES = {
     "svdrec_lu_workspace_bytes": (_sz, [_i64, _i32]),
     "svdrec_lu_lower": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _sz, _p, _p]),
     "svdrec_syev_workspace_bytes": (_sz, [_i32]),
-    "svdrec_syev": (C.c_int, [_i32, _p, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
+    "svdrec_syev": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_gesvj_workspace_bytes": (_sz, [_i64, _i32]),
     "svdrec_gesvj": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _i64, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_cf_normalize": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p]),

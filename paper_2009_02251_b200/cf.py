@@ -90,16 +90,19 @@ class LatentFactors:
         return cls(Tt)
 
 
-def _latent_device(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor | None = None
-                   ) -> LatentFactors:
+def _latent_device(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor | None = None,
+                   V0: torch.Tensor | None = None, keep: list | None = None) -> LatentFactors:
     """T.T = B.T V diag(s^-1/2) with eig(B B.T) descending (cf.py:77-92).
 
     With ``status`` given, the near-singular flag is left in it for the
-    caller's next batched read instead of being checked here."""
+    caller's next batched read instead of being checked here.  ``V0``
+    warm-starts the eigensolver; ``keep`` receives the eigenvectors."""
     st = K.new_status(Bt.device) if status is None else status
     if G is None:
         G = K.gemm_tn(Bt, Bt)
-    w, V = K.syev(G, st)
+    w, V = K.syev(G, st, V0)
+    if keep is not None:
+        keep.append(V)
     if status is None and K.check_status(st) & STATUS_NEAR_SINGULAR:
         raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
                                 f"{EIG_FLOOR * float(torch.trace(G)):.3e}")
@@ -257,6 +260,8 @@ class ValidationMae:
         self._start = time.perf_counter()
         self._G = None
         self._Gsrc = None
+        self._Gsrc_prev_ok = False
+        self._V = None
         self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1))
         if train.nnz == 0:
             raise ValueError("cannot take the mean of a matrix with no ratings")
@@ -268,8 +273,11 @@ class ValidationMae:
         return list(zip(s.users_np.tolist(), s.items_np.tolist(), s.truth_np.tolist()))
 
     def _gram(self, Bt: torch.Tensor) -> torch.Tensor:
+        """B B.T, grown by the new block's rows when ``Bt`` extends the
+        previous state's columns (same buffer); else recomputed."""
         k = Bt.shape[1]
         G0, src = self._G, self._Gsrc
+        self._Gsrc_prev_ok = False
         if G0 is not None and src is not None and src.data_ptr() == Bt.data_ptr() and src.shape[1] < k and \
                 src.stride() == Bt.stride():
             k0 = G0.shape[0]
@@ -277,6 +285,7 @@ class ValidationMae:
             G[:k0, :k0] = G0
             K.gemm_tn(Bt, Bt[:, k0:k], G[:, k0:k])  # new columns
             G[k0:k, :k0] = G[:k0, k0:k].T
+            self._Gsrc_prev_ok = True
         else:
             G = K.gemm_tn(Bt, Bt)
         self._G, self._Gsrc = G, Bt
@@ -286,7 +295,15 @@ class ValidationMae:
         if state.rank == 0:
             raise ValueError("empty factorization has no latent factors")
         mb = self._mb
-        factors = _latent_device(state.Bt_device, self._gram(state.Bt_device), status=mb["status"])
+        G = self._gram(state.Bt_device)
+        V0 = None
+        if self._V is not None and self._V.shape[0] < G.shape[0] and self._Gsrc_prev_ok:
+            k0 = self._V.shape[0]
+            V0 = torch.eye(G.shape[0], dtype=F64, device=G.device)
+            V0[:k0, :k0] = self._V
+        keep: list = []
+        factors = _latent_device(state.Bt_device, G, status=mb["status"], V0=V0, keep=keep)
+        self._V = keep[0]
         s = self.samples
         val, _, _ = _predict_device(self.train, factors, s, self._gmean)
         K.err_sum(val, s.truth, out=mb["sums"])

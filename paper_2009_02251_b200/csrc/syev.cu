@@ -34,8 +34,8 @@ __device__ __forceinline__ void pair_of(int n, int round, int p, int& i, int& j)
 
 // W column-major rows x k (column c at W + c*rows), V column-major k x k.
 __global__ void __launch_bounds__(kJThreads) k_jacobi(int64_t rows, int k, double* __restrict__ W,
-                                                      double* __restrict__ V, int* __restrict__ flags, double tol,
-                                                      uint32_t* d_status) {
+                                                      double* __restrict__ V, int* __restrict__ flags, double tol, const double* __restrict__ gnorm_p, uint32_t* d_status) {
+  const double gabs = gnorm_p ? 8.0 * 2.220446049250313e-16 * (*gnorm_p) : 0.0;
   cg::grid_group grid = cg::this_grid();
   const int n = (k + 1) & ~1;
   const int npairs = n / 2;
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kJThreads) k_jacobi(int64_t rows, int k, doubl
         a = warp_sum(a);
         bq = warp_sum(bq);
         g = warp_sum(g);
-        if (fabs(g) <= tol * sqrt(a * bq) || g == 0.0) continue;
+        if (g == 0.0 || fabs(g) <= tol * sqrt(a * bq) || fabs(g) <= gabs * (sqrt(a) + sqrt(bq))) continue;
         const double zeta = (bq - a) / (2.0 * g);
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double c = 1.0 / sqrt(fma(t, t, 1.0));
@@ -149,14 +149,198 @@ __global__ void k_init(int64_t rows, int k, const double* __restrict__ A, int64_
   if (t < (int64_t)k * k) V[t] = (t / k == t % k) ? 1.0 : 0.0;
 }
 
+// Warm start: V <- V0 (row-major k x k, columns = start basis),
+// W <- G V0 (column-major).  The previous block's eigenvectors padded with
+// the identity make the new Gram nearly diagonal, so few sweeps remain.
+__global__ void k_init_warm(int k, const double* __restrict__ G, int64_t ldg, const double* __restrict__ V0,
+                            int64_t ldv0, double* __restrict__ W, double* __restrict__ V) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)k * k) return;
+  const int c = (int)(t / k), e = (int)(t % k);
+  double acc = 0.0;
+  for (int q = 0; q < k; ++q) acc = fma(G[(int64_t)e * ldg + q], V0[(int64_t)q * ldv0 + c], acc);
+  W[t] = acc;
+  V[t] = V0[(int64_t)e * ldv0 + c];
+}
+
+// ---- blocked one-sided Jacobi --------------------------------------------
+// Columns are grouped in blocks of kBW; each outer round pairs blocks
+// (circle method over the blocks), one CTA per block pair loads the pair's
+// 2*kBW columns of W into shared memory, runs one full inner one-sided
+// sweep over those columns (kBW warps, one column pair each per inner
+// round, __syncthreads between inner rounds), writes them back and applies
+// the accumulated 2kBW x 2kBW rotation to the same columns of V.  One grid
+// barrier per outer round: (nblocks - 1) per sweep instead of (k - 1).
+constexpr int kBW = 16;
+constexpr int kBT = kBW * 32;  // threads per CTA: one warp per inner pair
+
+__device__ __forceinline__ void circle(int n, int round, int p, int& i, int& j) {
+  if (p == 0) {
+    i = n - 1;
+    j = round;
+  } else {
+    i = (round + p) % (n - 1);
+    j = (round - p + (n - 1)) % (n - 1);
+  }
+}
+
+__global__ void __launch_bounds__(kBT) k_bjacobi(int rows, int k, double* __restrict__ W, double* __restrict__ V,
+                                                 int* __restrict__ flags, double tol, const double* __restrict__ gnorm_p,
+                                                 uint32_t* d_status) {
+  cg::grid_group grid = cg::this_grid();
+  const double gabs = gnorm_p ? 8.0 * 2.220446049250313e-16 * (*gnorm_p) : 0.0;
+  extern __shared__ double sw[];                 // [2*kBW][ldw]
+  __shared__ double Jm[2 * kBW][2 * kBW + 1];    // accumulated rotation (column-major: Jm[col][row])
+  __shared__ int cols[2 * kBW];
+  const int ldw = rows | 1;
+  const int nb = (k + kBW - 1) / kBW;
+  const int nbp = (nb + 1) & ~1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) flags[(sweep + 1) % 3] = 0;
+    for (int round = 0; round < (nbp > 1 ? nbp - 1 : 1); ++round) {
+      for (int g = blockIdx.x; g < (nbp > 1 ? nbp / 2 : 1); g += gridDim.x) {
+        int bi, bj;
+        if (nbp > 1) {
+          circle(nbp, round, g, bi, bj);
+        } else {
+          bi = 0;
+          bj = 1;  // single block: the second half is empty
+        }
+        if (threadIdx.x < 2 * kBW) {
+          const int l = threadIdx.x;
+          const int c = (l < kBW) ? bi * kBW + l : bj * kBW + (l - kBW);
+          cols[l] = (c < k && (l < kBW ? bi : bj) < nb) ? c : -1;
+        }
+        for (int t = threadIdx.x; t < 2 * kBW * 2 * kBW; t += kBT) Jm[t / (2 * kBW)][t % (2 * kBW)] = 0.0;
+        __syncthreads();
+        if (threadIdx.x < 2 * kBW) Jm[threadIdx.x][threadIdx.x] = 1.0;
+        for (int t = threadIdx.x; t < 2 * kBW * rows; t += kBT) {
+          const int l = t / rows, e = t - l * rows;
+          sw[l * ldw + e] = cols[l] >= 0 ? W[(int64_t)cols[l] * rows + e] : 0.0;
+        }
+        __syncthreads();
+        bool rotated = false;
+        for (int ir = 0; ir < 2 * kBW - 1; ++ir) {
+          int a, b;
+          circle(2 * kBW, ir, warp, a, b);
+          if (cols[a] >= 0 && cols[b] >= 0) {
+            double* wa = sw + a * ldw;
+            double* wb = sw + b * ldw;
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int e = lane; e < rows; e += 32) {
+              const double x = wa[e], y = wb[e];
+              al = fma(x, x, al);
+              be = fma(y, y, be);
+              ga = fma(x, y, ga);
+            }
+            al = warp_sum(al);
+            be = warp_sum(be);
+            ga = warp_sum(ga);
+            if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be) && fabs(ga) > gabs * (sqrt(al) + sqrt(be))) {
+              const double zeta = (be - al) / (2.0 * ga);
+              const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              const double c = 1.0 / sqrt(fma(t, t, 1.0));
+              const double s = c * t;
+              for (int e = lane; e < rows; e += 32) {
+                const double x = wa[e], y = wb[e];
+                wa[e] = c * x - s * y;
+                wb[e] = s * x + c * y;
+              }
+              const double x = Jm[a][lane], y = Jm[b][lane];
+              Jm[a][lane] = c * x - s * y;
+              Jm[b][lane] = s * x + c * y;
+              rotated = true;
+            }
+          }
+          __syncthreads();
+        }
+        if (rotated && lane == 0) flags[sweep % 3] = 1;
+        for (int t = threadIdx.x; t < 2 * kBW * rows; t += kBT) {
+          const int l = t / rows, e = t - l * rows;
+          if (cols[l] >= 0) W[(int64_t)cols[l] * rows + e] = sw[l * ldw + e];
+        }
+        __syncthreads();
+        // V[:, cols] <- V[:, cols] @ Jm, rows of V in chunks staged in sw
+        for (int e0 = 0; e0 < k; e0 += (rows > 64 ? 64 : rows)) {
+          const int ch = min(rows > 64 ? 64 : rows, k - e0);
+          for (int t = threadIdx.x; t < 2 * kBW * ch; t += kBT) {
+            const int l = t / ch, e = t - l * ch;
+            sw[l * ldw + e] = cols[l] >= 0 ? V[(int64_t)cols[l] * k + e0 + e] : 0.0;
+          }
+          __syncthreads();
+          for (int t = threadIdx.x; t < 2 * kBW * ch; t += kBT) {
+            const int l = t / ch, e = t - l * ch;
+            if (cols[l] < 0) continue;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int q = 0; q < 2 * kBW; ++q) acc = fma(sw[q * ldw + e], Jm[l][q], acc);
+            V[(int64_t)cols[l] * k + e0 + e] = acc;
+          }
+          __syncthreads();
+        }
+      }
+      grid.sync();
+    }
+    if (*(volatile int*)&flags[sweep % 3] == 0) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) flags[3] = sweep;  // diagnostics: sweeps used
+  if (sweep == 60 && blockIdx.x == 0 && threadIdx.x == 0 && d_status) atomicOr(d_status, SVDREC_STATUS_NO_CONVERGE);
+}
+
+constexpr int kBRowsMax = 760;  // 2*kBW*ldw*8 <= 200 KB
+
+// Frobenius norm of n contiguous doubles; applied to W right after the
+// (warm) init, where ||G V0||_F = ||G||_F.
+__global__ void k_fro(int64_t n, const double* __restrict__ G, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(G[i], G[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = sqrt(s);
+}
+
 // shared driver: one-sided Jacobi on the rows x k block A
 int run_jacobi(int64_t rows, int k, const double* A, int64_t lda, double* W, double* V, double* lam, int* flags,
-               uint32_t* d_status, cudaStream_t s) {
+               uint32_t* d_status, cudaStream_t s, const double* V0 = nullptr, int64_t ldv0 = 0, bool absolute = false) {
   const int64_t tot = rows * k > (int64_t)k * k ? rows * k : (int64_t)k * k;
-  k_init<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(rows, k, A, lda, W, V);
+  if (V0 && rows == k)
+    k_init_warm<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(k, A, lda, V0, ldv0, W, V);
+  else
+    k_init<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(rows, k, A, lda, W, V);
   int rc = check_launch("jacobi_init");
   if (rc) return rc;
-  if (k > 1) {
+  // symmetric input: stop rotating once |w_i.w_j| is at the eps*||G|| level of
+  // the columns themselves (their absolute error), as LAPACK eigh guarantees
+  const double* gnp = nullptr;
+  if (absolute) {
+    k_fro<<<1, 256, 0, s>>>(rows * k, W, lam);
+    rc = check_launch("jacobi_fro");
+    if (rc) return rc;
+    gnp = lam;
+  }
+  const double tol_b = fmin(1e-10, 2.220446049250313e-16 * (double)(rows > 4 ? rows : 4));
+  if (k > 1 && rows <= kBRowsMax) {
+    static int max_blocks_b = 0;
+    const size_t smem = (size_t)2 * kBW * (kBRowsMax | 1) * 8;
+    if (!max_blocks_b) {
+      SVDREC_CUDA(cudaFuncSetAttribute(k_bjacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, kBT, smem));
+      max_blocks_b = per_sm * sm_count();
+      if (max_blocks_b < 1) max_blocks_b = 1;
+    }
+    const int nb = (k + kBW - 1) / kBW;
+    const int npairs = nb > 1 ? ((nb + 1) & ~1) / 2 : 1;
+    int nblk = npairs < max_blocks_b ? npairs : max_blocks_b;
+    int r32 = (int)rows, kk32 = k;
+    double tol = tol_b;
+    void* args[] = {&r32, &kk32, &W, &V, &flags, &tol, &gnp, &d_status};
+    SVDREC_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), s));
+    SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_bjacobi, dim3(nblk), dim3(kBT), args, smem, s));
+    note_launches(1);
+  } else if (k > 1) {
     static int max_blocks = 0;
     if (!max_blocks) {
       int per_sm = 0;
@@ -173,7 +357,7 @@ int run_jacobi(int64_t rows, int k, const double* A, int64_t lda, double* W, dou
     if (tol > 1e-10) tol = 1e-10;
     int64_t rr = rows;
     int kk32 = k;
-    void* args[] = {&rr, &kk32, &W, &V, &flags, &tol, &d_status};
+    void* args[] = {&rr, &kk32, &W, &V, &flags, &tol, &gnp, &d_status};
     SVDREC_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), s));
     SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, dim3(nblk), dim3(kJThreads), args, 0, s));
     note_launches(1);
@@ -191,8 +375,9 @@ extern "C" size_t svdrec_syev_workspace_bytes(int32_t k) {
   return 2 * align_up((size_t)k * k * 8) + align_up((size_t)k * 8) + 256;
 }
 
-extern "C" int svdrec_syev(int32_t k, const double* d_G, int64_t ldg, double* d_w, double* d_V, int64_t ldv,
-                           void* d_work, size_t work_bytes, uint32_t* d_status, void* stream) {
+extern "C" int svdrec_syev(int32_t k, const double* d_G, int64_t ldg, const double* d_V0, int64_t ldv0, double* d_w,
+                           double* d_V, int64_t ldv, void* d_work, size_t work_bytes, uint32_t* d_status,
+                           void* stream) {
   SVDREC_ARG(k >= 1 && ldg >= k && ldv >= k, "syev: bad arguments");
   if (work_bytes < svdrec_syev_workspace_bytes(k)) {
     set_error("syev: workspace too small");
@@ -204,7 +389,8 @@ extern "C" int svdrec_syev(int32_t k, const double* d_G, int64_t ldg, double* d_
   double* V = reinterpret_cast<double*>(w + align_up((size_t)k * k * 8));
   double* lam = reinterpret_cast<double*>(w + 2 * align_up((size_t)k * k * 8));
   int* flags = reinterpret_cast<int*>(w + 2 * align_up((size_t)k * k * 8) + align_up((size_t)k * 8));
-  int rc = run_jacobi(k, k, d_G, ldg, W, V, lam, flags, d_status, s);
+  SVDREC_ARG(!d_V0 || ldv0 >= k, "syev: bad ldv0");
+  int rc = run_jacobi(k, k, d_G, ldg, W, V, lam, flags, d_status, s, d_V0, ldv0, true);
   if (rc) return rc;
   k_sort_out<<<k, 128, 0, s>>>(k, lam, V, d_w, d_V, ldv, d_G, ldg, d_status, 0, 0, nullptr, nullptr, 0);
   return check_launch("syev_sort");

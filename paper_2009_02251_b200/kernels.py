@@ -204,15 +204,19 @@ def lu_lower(A: torch.Tensor, status: torch.Tensor, udiag: torch.Tensor | None =
     return udiag
 
 
-def syev(G: torch.Tensor, status: torch.Tensor):
-    """Eigen-decomposition of a symmetric PSD k x k: (w ascending, V columns)."""
+def syev(G: torch.Tensor, status: torch.Tensor, V0: torch.Tensor | None = None):
+    """Eigen-decomposition of a symmetric PSD k x k: (w ascending, V columns).
+
+    ``V0`` (k x k orthonormal columns) warm-starts the Jacobi sweeps."""
     ldg = _mat(G, "syev.G")
+    ldv0 = _mat(V0, "syev.V0") if V0 is not None else 0
     k = G.shape[0]
     w = torch.empty(k, dtype=F64, device=G.device)
     V = torch.empty(k, k, dtype=F64, device=G.device)
     ws, nb = scratch(G.device).get(query("svdrec_syev_workspace_bytes", k))
     with _span("syev", 2 * k * k * 8):
-        call("svdrec_syev", k, ptr(G), ldg, ptr(w), ptr(V), k, ws, nb, ptr(status), stream_handle())
+        call("svdrec_syev", k, ptr(G), ldg, ptr(V0), ldv0, ptr(w), ptr(V), k, ws, nb, ptr(status),
+             stream_handle())
     return w, V
 
 
