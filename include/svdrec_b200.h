@@ -42,6 +42,8 @@ extern "C" {
 #define SVDREC_STATUS_NEAR_SINGULAR 2u /* eig: Gram eigenvalue <= floor */
 #define SVDREC_STATUS_STREAM_SHORT 4u  /* normal: raw window too short  */
 #define SVDREC_STATUS_NO_CONVERGE 8u   /* eig: Jacobi sweep cap hit     */
+#define SVDREC_STATUS_NS_CHECK 16u     /* inv_sqrt: inconclusive, check
+                                          singularity with svdrec_syev   */
 
 int svdrec_abi_version(void);
 const char* svdrec_last_error(void);
@@ -166,25 +168,45 @@ int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double
 
 /* ---------------------------------------------------------------------
  * Collaborative filtering (cf.py:77-190).
- *  svdrec_cf_factors: from Bt (n x k, = B.T) and the k x k matrix W
- *   (eigenvectors scaled by s^-1/2, descending) form T.T = Bt @ W
- *   (n x k), its column... item norms ``d_norm`` and the unit rows
- *   ``d_Tn`` (zero rows for zero-norm items).  (latent_from_qb +
- *   LatentFactors.from_matrix.)
+ *  Item similarity is the cosine of Alg. 4 in a metric M:
+ *  cos(l, j) = x_j.y_l / (n_l n_j), y_l = M x_l, n_l = sqrt(x_l.y_l).
+ *  With explicit factors T (LatentFactors) x_l = y_l = T[:, l]; per QB
+ *  block x_l = B[:, l] and M = (B B.T)^(-1/2) (svdrec_inv_sqrt), which
+ *  gives exactly the cosines of latent_from_qb's T without an eig.
+ *  svdrec_cf_normalize: unit rows Tn = T.T / |T_l| and norms (x = y = T).
+ *  svdrec_cf_normalize_pair: Xn = X / n, Yn = Y / n with n_l =
+ *   sqrt(x_l.y_l) (zero rows where n_l = 0, the reference's skipped
+ *   zero-norm items).
  *  svdrec_cf_predict: Alg. 4 (_predict, cf.py:108-143) for nsamp
  *   (user, item) pairs grouped by user: ``d_group_start`` (ngroups+1)
- *   offsets into the user-sorted samples.  Writes clamped value, raw
- *   value and fallback flag per sample (in grouped order).
- *  svdrec_abs_err_sum: fixed-order sum |pred - truth| and (pred-truth)^2.
+ *   offsets into the user-sorted samples.  Per user one warp forms
+ *   P_u = sum_l A(u,l) Yn_l and S_u = sum_l Yn_l, then each sample's
+ *   raw prediction is (Xn_j . P_u) / (Xn_j . S_u) with the |w| < 1e-9
+ *   user-mean / global-mean fallback and clamping.  Writes clamped value,
+ *   raw value and fallback flag per sample (in grouped order).  k <= 1024.
+ *  svdrec_err_sum: fixed-order sum |pred - truth| and (pred-truth)^2.
  * ------------------------------------------------------------------- */
 int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int64_t ldt, double* d_Tn,
                         int64_t ldn, double* d_norm, void* stream);
+int svdrec_cf_normalize_pair(int64_t n, int32_t k, const double* d_X, int64_t ldx,
+                             const double* d_Y, int64_t ldy, double* d_Xn, double* d_Yn,
+                             int64_t ldn, double* d_norm, void* stream);
 int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32_t* d_users,
                       const int32_t* d_items, const int64_t* d_indptr,
                       const int32_t* d_indices, const double* d_values, int32_t k,
-                      const double* d_Tn, int64_t ldn, const double* d_norm,
+                      const double* d_Yn, const double* d_Xn, int64_t ldn, const double* d_norm,
                       double global_mean, double rating_min, double rating_max,
                       double* d_value, double* d_raw, uint8_t* d_fallback, void* stream);
+
+/* G^(-1/2) of a k x k SPD Gram by coupled Newton-Schulz iteration (one
+ * cooperative kernel, GEMM phases over the whole GPU).  Sets
+ * SVDREC_STATUS_NS_CHECK when it cannot certify the reference's
+ * near-singularity floor (eigenvalue >= 1e-14 trace); the caller then
+ * decides with svdrec_syev.  d_iters (nullable) receives the iterations. */
+size_t svdrec_inv_sqrt_workspace_bytes(int32_t k);
+int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double* d_Z, int64_t ldz,
+                    void* d_work, size_t work_bytes, uint32_t* d_status, int32_t* d_iters,
+                    void* stream);
 size_t svdrec_err_sum_workspace_bytes(int64_t nsamp);
 int svdrec_err_sum(int64_t nsamp, const double* d_pred, const double* d_truth,
                    double* d_out2, void* d_work, size_t work_bytes, void* stream);

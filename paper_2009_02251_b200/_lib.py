@@ -20,6 +20,7 @@ STATUS_ZERO_PIVOT = 1
 STATUS_NEAR_SINGULAR = 2
 STATUS_STREAM_SHORT = 4
 STATUS_NO_CONVERGE = 8
+STATUS_NS_CHECK = 16
 
 _i64, _i32, _u64, _f64, _sz, _p = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_size_t, C.c_void_p
 
@@ -48,8 +49,11 @@ SIGNATURES = {
     "svdrec_gesvj_workspace_bytes": (_sz, [_i64, _i32]),
     "svdrec_gesvj": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _i64, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_cf_normalize": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p]),
-    "svdrec_cf_predict": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _i64, _p, _f64, _f64, _f64,
+    "svdrec_cf_normalize_pair": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p, _i64, _p, _p]),
+    "svdrec_cf_predict": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _i64, _p, _f64, _f64, _f64,
                                     _p, _p, _p, _p]),
+    "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
+    "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),
     "svdrec_err_sum_workspace_bytes": (_sz, [_i64]),
     "svdrec_err_sum": (C.c_int, [_i64, _p, _p, _p, _p, _sz, _p]),
     "svdrec_count_overlap": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p]),

@@ -5,6 +5,13 @@ latent_from_qb, predict_rating, mae, evaluate_mae, ValidationMae and
 auto_latent_factors, same contracts and exceptions.  All scoring runs in
 csrc/cf.cu; held-out samples are grouped by user once (one warp per user
 builds the two k-vectors P_u, S_u and scores all of that user's samples).
+
+Alg. 5 scores every block, but Alg. 4 only needs cosines between item
+columns of T = S^(1/2) U.T, and T.T T = B.T (B B.T)^(-1/2) B.  So
+ValidationMae scores each block in "metric mode" -- x_l = B[:, l],
+y_l = G^(-1/2) x_l with G = B B.T from a Newton-Schulz kernel -- and only
+the factors it returns pay for the eigendecomposition (lazily, on first
+access to ``T``), exactly as latent_from_qb computes it.
 """
 from __future__ import annotations
 
@@ -15,7 +22,7 @@ import numpy as np
 import torch
 
 from . import kernels as K
-from ._lib import STATUS_NEAR_SINGULAR
+from ._lib import STATUS_NEAR_SINGULAR, STATUS_NS_CHECK
 from .linalg import EIG_FLOOR, GaussianStream, NearSingularError
 from .rsvd import QbState, RankExhaustedError, qb_pass_blocks
 from .sparse import SparseRatings
@@ -40,31 +47,56 @@ class BlockEval(NamedTuple):
     seconds: float
 
 
+def _eig_T(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor | None = None) -> torch.Tensor:
+    """T.T = B.T V diag(s^-1/2), eig(B B.T) descending (cf.py:77-92)."""
+    st = K.new_status(Bt.device) if status is None else status
+    if G is None:
+        G = K.gemm_tn(Bt, Bt)
+    w, V = K.syev(G, st)
+    if status is None and K.check_status(st) & STATUS_NEAR_SINGULAR:
+        raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
+                                f"{EIG_FLOOR * float(torch.trace(G)):.3e}")
+    Wm = V.flip(1) * torch.rsqrt(torch.sqrt(torch.clamp(w.flip(0), min=0.0)))
+    return K.gemm_nn(Bt, Wm.contiguous())
+
+
 class LatentFactors:
     """Item embedding T (k x items) with cached column norms (cf.py:42-74).
 
-    Device-resident as ``Tt`` (items x k, = T.T), its unit rows ``Tn`` and
-    ``norm_device``; ``T`` / ``col_norms`` materialise numpy copies.
+    Device-resident.  Scoring uses unit item rows ``Xn``/``Yn`` (equal to
+    T's normalized columns for explicit factors; B's columns in the metric
+    (B B.T)^(-1/2) for factors taken straight from a QB block) and
+    ``norm_device``.  ``T`` and ``col_norms`` materialise numpy copies; for
+    QB-block factors T is computed on first access by the same eig route
+    as the reference's latent_from_qb.
     """
 
-    def __init__(self, Tt: torch.Tensor, Tn: torch.Tensor | None = None, norm: torch.Tensor | None = None):
-        if Tt.dim() != 2:
-            raise ValueError("T must be 2-d")
-        self.Tt = Tt.contiguous()
-        if Tn is None or norm is None:
-            Tn, norm = K.cf_normalize(self.Tt)
-        self.Tn = Tn
-        self.norm_device = norm
+    def __init__(self, Tt: torch.Tensor | None = None, *, Xn=None, Yn=None, norm=None, Bt=None, G=None):
+        self._Tt = None
+        self._Bt, self._G = Bt, G
+        if Tt is not None:
+            if Tt.dim() != 2:
+                raise ValueError("T must be 2-d")
+            self._Tt = Tt.contiguous()
+            Tn, norm = K.cf_normalize(self._Tt)
+            Xn = Yn = Tn
+        self.Xn, self.Yn, self.norm_device = Xn, Yn, norm
         self._T = None
         self._norms = None
 
     @property
     def k(self) -> int:
-        return int(self.Tt.shape[1])
+        return int(self.Xn.shape[1])
 
     @property
     def n_items(self) -> int:
-        return int(self.Tt.shape[0])
+        return int(self.Xn.shape[0])
+
+    @property
+    def Tt(self) -> torch.Tensor:
+        if self._Tt is None:
+            self._Tt = _eig_T(self._Bt, self._G)
+        return self._Tt
 
     @property
     def T(self) -> np.ndarray:
@@ -74,6 +106,7 @@ class LatentFactors:
 
     @property
     def col_norms(self) -> np.ndarray:
+        # metric mode: n_l = sqrt(x_l.G^(-1/2).x_l) = |T_l| identically
         if self._norms is None:
             self._norms = self.norm_device.cpu().numpy()
         return self._norms
@@ -89,26 +122,12 @@ class LatentFactors:
             Tt = torch.from_numpy(np.ascontiguousarray(T.T)).cuda()
         return cls(Tt)
 
-
-def _latent_device(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor | None = None,
-                   V0: torch.Tensor | None = None, keep: list | None = None) -> LatentFactors:
-    """T.T = B.T V diag(s^-1/2) with eig(B B.T) descending (cf.py:77-92).
-
-    With ``status`` given, the near-singular flag is left in it for the
-    caller's next batched read instead of being checked here.  ``V0``
-    warm-starts the eigensolver; ``keep`` receives the eigenvectors."""
-    st = K.new_status(Bt.device) if status is None else status
-    if G is None:
-        G = K.gemm_tn(Bt, Bt)
-    w, V = K.syev(G, st, V0)
-    if keep is not None:
-        keep.append(V)
-    if status is None and K.check_status(st) & STATUS_NEAR_SINGULAR:
-        raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
-                                f"{EIG_FLOOR * float(torch.trace(G)):.3e}")
-    Wm = V.flip(1) * torch.rsqrt(torch.sqrt(torch.clamp(w.flip(0), min=0.0)))
-    Tt = K.gemm_nn(Bt, Wm.contiguous())
-    return LatentFactors(Tt)
+    @classmethod
+    def from_qb_metric(cls, Bt: torch.Tensor, G: torch.Tensor, Z: torch.Tensor) -> "LatentFactors":
+        """Metric-mode factors of a QB block: x_l = B[:, l], y_l = Z x_l."""
+        Yt = K.gemm_nn(Bt, Z)
+        Xn, Yn, norm = K.cf_normalize_pair(Bt, Yt)
+        return cls(Xn=Xn, Yn=Yn, norm=norm, Bt=Bt, G=G)
 
 
 def latent_from_qb(state: QbState) -> LatentFactors:
@@ -116,7 +135,7 @@ def latent_from_qb(state: QbState) -> LatentFactors:
     descending singular value (cf.py:77-92)."""
     if state.rank == 0:
         raise ValueError("empty factorization has no latent factors")
-    return _latent_device(state.Bt_device)
+    return LatentFactors(_eig_T(state.Bt_device))
 
 
 class _Samples:
@@ -145,6 +164,7 @@ class _Samples:
         self.users = t(us, np.int32)
         self.items = t(i[order], np.int32)
         self.truth = t(r[order], np.float64)
+        self.h2d_bytes = groups.size * 8 + self.n * 16
 
     def check_bounds(self, A: SparseRatings) -> None:
         if self.n == 0:
@@ -156,9 +176,9 @@ class _Samples:
 
 
 def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float):
-    d = A.device(factors.Tt.device)
-    return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Tn, factors.norm_device, gmean, A.rating_min,
-                        A.rating_max)
+    d = A.device(factors.Xn.device)
+    return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Yn, factors.Xn, factors.norm_device, gmean,
+                        A.rating_min, A.rating_max)
 
 
 def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: int) -> Prediction:
@@ -170,10 +190,10 @@ def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: in
         raise IndexError(f"item {item} out of range")
     if factors.n_items != A.n:
         raise ValueError("factor matrix does not cover this item set")
-    d = A.device(factors.Tt.device)
     if A.nnz == 0:
         raise ValueError("cannot take the mean of a matrix with no ratings")
-    s = _Samples(([user], [item], [0.0]), factors.Tt.device)
+    d = A.device(factors.Xn.device)
+    s = _Samples(([user], [item], [0.0]), factors.Xn.device)
     val, raw, fb = _predict_device(A, factors, s, d.global_mean)
     out = torch.stack([val, raw, fb.to(F64)]).cpu().numpy()
     return Prediction(value=float(out[0, 0]), raw=float(out[1, 0]), fallback=bool(out[2, 0]))
@@ -181,9 +201,9 @@ def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: in
 
 def predict_many(A: SparseRatings, factors: LatentFactors, samples) -> np.ndarray:
     """Batch Alg. 4: (n, 3) array of value, raw, fallback in input order."""
-    s = _Samples(samples, factors.Tt.device)
+    s = _Samples(samples, factors.Xn.device)
     s.check_bounds(A)
-    val, raw, fb = _predict_device(A, factors, s, A.device(factors.Tt.device).global_mean)
+    val, raw, fb = _predict_device(A, factors, s, A.device(factors.Xn.device).global_mean)
     out = np.empty((s.n, 3))
     out[s.order, 0] = val.cpu().numpy()
     out[s.order, 1] = raw.cpu().numpy()
@@ -207,20 +227,20 @@ def _errors(A, factors, s: _Samples):
         raise ValueError("cannot take the mean of a matrix with no ratings")
     if s.n == 0:
         raise ValueError("cannot average zero errors")
-    val, _, _ = _predict_device(A, factors, s, A.device(factors.Tt.device).global_mean)
+    val, _, _ = _predict_device(A, factors, s, A.device(factors.Xn.device).global_mean)
     e = K.err_sum(val, s.truth).cpu().numpy()
     return float(e[0] / s.n), float(np.sqrt(e[1] / s.n))
 
 
 def evaluate_mae(A: SparseRatings, factors: LatentFactors, samples: Iterable) -> float:
     """MAE of clamped predictions over held-out triples (cf.py:178-190)."""
-    s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Tt.device)
+    s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Xn.device)
     return _errors(A, factors, s)[0]
 
 
 def evaluate_errors(A: SparseRatings, factors: LatentFactors, samples) -> tuple[float, float]:
     """(MAE, RMSE) of clamped Alg. 4 predictions (RMSE: BASELINE metric)."""
-    s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Tt.device)
+    s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Xn.device)
     return _errors(A, factors, s)
 
 
@@ -231,7 +251,8 @@ class ValidationMae:
     ``patience`` consecutive blocks improving the best MAE by less than
     ``min_improvement`` stop the scan.  The best block's factors and the
     (k, MAE, seconds) trace stay on the instance.  The Gram B B.T is grown
-    incrementally when successive states extend one another.
+    incrementally when successive states extend one another, and each
+    block costs one small host read (error sums + status word).
     """
 
     def __init__(self, train: SparseRatings, validation, patience: int = 2, min_improvement: float = 1e-4) -> None:
@@ -248,6 +269,8 @@ class ValidationMae:
         cnt = int(K.count_overlap(s.users, s.items, d.A).item())
         if cnt:
             raise ValueError(f"{cnt} validation samples are present in the training matrix")
+        if train.nnz == 0:
+            raise ValueError("cannot take the mean of a matrix with no ratings")
         self.train = train
         self.samples = s
         self.patience = patience
@@ -260,11 +283,7 @@ class ValidationMae:
         self._start = time.perf_counter()
         self._G = None
         self._Gsrc = None
-        self._Gsrc_prev_ok = False
-        self._V = None
-        self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1))
-        if train.nnz == 0:
-            raise ValueError("cannot take the mean of a matrix with no ratings")
+        self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1), iters=("u4", 1))
         self._gmean = d.global_mean
 
     @property
@@ -277,7 +296,6 @@ class ValidationMae:
         previous state's columns (same buffer); else recomputed."""
         k = Bt.shape[1]
         G0, src = self._G, self._Gsrc
-        self._Gsrc_prev_ok = False
         if G0 is not None and src is not None and src.data_ptr() == Bt.data_ptr() and src.shape[1] < k and \
                 src.stride() == Bt.stride():
             k0 = G0.shape[0]
@@ -285,7 +303,6 @@ class ValidationMae:
             G[:k0, :k0] = G0
             K.gemm_tn(Bt, Bt[:, k0:k], G[:, k0:k])  # new columns
             G[k0:k, :k0] = G[:k0, k0:k].T
-            self._Gsrc_prev_ok = True
         else:
             G = K.gemm_tn(Bt, Bt)
         self._G, self._Gsrc = G, Bt
@@ -295,21 +312,21 @@ class ValidationMae:
         if state.rank == 0:
             raise ValueError("empty factorization has no latent factors")
         mb = self._mb
-        G = self._gram(state.Bt_device)
-        V0 = None
-        if self._V is not None and self._V.shape[0] < G.shape[0] and self._Gsrc_prev_ok:
-            k0 = self._V.shape[0]
-            V0 = torch.eye(G.shape[0], dtype=F64, device=G.device)
-            V0[:k0, :k0] = self._V
-        keep: list = []
-        factors = _latent_device(state.Bt_device, G, status=mb["status"], V0=V0, keep=keep)
-        self._V = keep[0]
+        Bt = state.Bt_device
+        G = self._gram(Bt)
+        Z = K.inv_sqrt(G, mb["status"], mb["iters"])
+        factors = LatentFactors.from_qb_metric(Bt, G, Z)
         s = self.samples
         val, _, _ = _predict_device(self.train, factors, s, self._gmean)
         K.err_sum(val, s.truth, out=mb["sums"])
-        got = mb.read()  # one host read per block: error sums + eig status
-        if int(got["status"][0]) & STATUS_NEAR_SINGULAR:
-            raise NearSingularError("Gram eigenvalue below floor in latent_from_qb")
+        got = mb.read()  # one host read per block: error sums + status
+        flags = int(got["status"][0])
+        if flags & STATUS_NS_CHECK:
+            # Newton-Schulz could not certify the eigenvalue floor: decide it
+            # exactly like the reference (eigh) and score with its T
+            factors = LatentFactors(_eig_T(Bt, G))
+            val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+            got = {"sums": K.err_sum(val, s.truth).cpu().numpy()}
         score, rmse = float(got["sums"][0] / s.n), float(np.sqrt(got["sums"][1] / s.n))
         self.trace.append(BlockEval(k=state.rank, mae=score, seconds=time.perf_counter() - self._start))
         if score < self.best_mae - self.min_improvement:

@@ -35,13 +35,35 @@ __global__ void k_normalize(int64_t n, int k, const double* __restrict__ Tt, int
   if (lane == 0) norm[item] = nr;
 }
 
+// Metric pair: n_l = sqrt(x_l . y_l); Xn = X / n, Yn = Y / n (0 if n = 0).
+__global__ void k_normalize_pair(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
+                                 const double* __restrict__ Y, int64_t ldy, double* __restrict__ Xn,
+                                 double* __restrict__ Yn, int64_t ldn, double* __restrict__ norm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (item >= n) return;
+  const double* xr = X + item * ldx;
+  const double* yr = Y + item * ldy;
+  double s = 0.0;
+  for (int e = lane; e < k; e += 32) s = fma(xr[e], yr[e], s);
+  s = warp_sum(s);
+  const double nr = s > 0.0 ? sqrt(s) : 0.0;
+  const double inv = nr > 0.0 ? 1.0 / nr : 0.0;
+  for (int e = lane; e < k; e += 32) {
+    Xn[item * ldn + e] = xr[e] * inv;
+    Yn[item * ldn + e] = yr[e] * inv;
+  }
+  if (lane == 0) norm[item] = nr;
+}
+
 template <int MAXR>
 __global__ void __launch_bounds__(128) k_predict(int64_t ngroups, const int64_t* __restrict__ gstart,
                                                  const int32_t* __restrict__ users, const int32_t* __restrict__ items,
                                                  const int64_t* __restrict__ indptr,
                                                  const int32_t* __restrict__ indices,
                                                  const double* __restrict__ values, int k,
-                                                 const double* __restrict__ Tn, int64_t ldn,
+                                                 const double* __restrict__ Yn, const double* __restrict__ Xn,
+                                                 int64_t ldn,
                                                  const double* __restrict__ norm, double gmean, double lo, double hi,
                                                  double* __restrict__ out_val, double* __restrict__ out_raw,
                                                  uint8_t* __restrict__ out_fb) {
@@ -68,7 +90,7 @@ __global__ void __launch_bounds__(128) k_predict(int64_t ngroups, const int64_t*
       const int32_t c = __shfl_sync(0xffffffffu, ci, j);
       const double v = __shfl_sync(0xffffffffu, vi, j);
       vsum += v;
-      const double* row = Tn + (int64_t)c * ldn;
+      const double* row = Yn + (int64_t)c * ldn;
 #pragma unroll
       for (int t = 0; t < MAXR; ++t) {
         const int idx = lane + 32 * t;
@@ -88,7 +110,7 @@ __global__ void __launch_bounds__(128) k_predict(int64_t ngroups, const int64_t*
     const double nj = norm[j];
     double num = 0.0, den = 0.0;
     if (nj != 0.0 && deg > 0) {
-      const double* row = Tn + (int64_t)j * ldn;
+      const double* row = Xn + (int64_t)j * ldn;
 #pragma unroll
       for (int t = 0; t < MAXR; ++t) {
         const int idx = lane + 32 * t;
@@ -155,9 +177,21 @@ extern "C" int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int
   return check_launch("cf_normalize");
 }
 
+extern "C" int svdrec_cf_normalize_pair(int64_t n, int32_t k, const double* d_X, int64_t ldx, const double* d_Y,
+                                        int64_t ldy, double* d_Xn, double* d_Yn, int64_t ldn, double* d_norm,
+                                        void* stream) {
+  SVDREC_ARG(n >= 0 && k >= 1 && ldx >= k && ldy >= k && ldn >= k, "cf_normalize_pair: bad arguments");
+  if (n == 0) return 0;
+  const int64_t thr = n * 32;
+  k_normalize_pair<<<(unsigned)((thr + 255) / 256), 256, 0, as_stream(stream)>>>(n, k, d_X, ldx, d_Y, ldy, d_Xn,
+                                                                                 d_Yn, ldn, d_norm);
+  return check_launch("cf_normalize_pair");
+}
+
 extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32_t* d_users,
                                  const int32_t* d_items, const int64_t* d_indptr, const int32_t* d_indices,
-                                 const double* d_values, int32_t k, const double* d_Tn, int64_t ldn,
+                                 const double* d_values, int32_t k, const double* d_Yn, const double* d_Xn,
+                                 int64_t ldn,
                                  const double* d_norm, double global_mean, double rating_min, double rating_max,
                                  double* d_value, double* d_raw, uint8_t* d_fallback, void* stream) {
   SVDREC_ARG(ngroups >= 0 && k >= 1 && ldn >= k, "cf_predict: bad arguments");
@@ -172,7 +206,7 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
   const int r = (k + 31) / 32;
 #define SVDREC_PRED(R)                                                                                         \
   k_predict<R><<<grid, 128, 0, s>>>(ngroups, d_group_start, d_users, d_items, d_indptr, d_indices, d_values, k, \
-                                    d_Tn, ldn, d_norm, global_mean, rating_min, rating_max, d_value, d_raw,      \
+                                    d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, d_value, d_raw, \
                                     d_fallback)
   if (r <= 1)
     SVDREC_PRED(1);

@@ -1,0 +1,219 @@
+// Inverse square root of the small SPD Gram G = B B.T by coupled
+// Newton-Schulz iteration, in one cooperative kernel.
+//
+// Why: Alg. 5 scores every block (reference cf.py:227-240) through
+// latent_from_qb's eig_svd(B.T) (cf.py:77-92), but the CF prediction of
+// Alg. 4 (cf.py:108-143) only ever uses cosines between item columns of
+// T = S^(1/2) U.T, and T.T T = B.T (B B.T)^(-1/2) B.  So per block we need
+// Z = G^(-1/2), not an eigendecomposition: with x_l = B[:, l] and
+// y_l = Z x_l, cos(T_l, T_j) = x_j.y_l / (|x_l|_Z |x_j|_Z).  The iteration
+// (A = G / trace(G), Y0 = A, Z0 = I)
+//     T = (3 I - Z Y) / 2,   Y <- Y T,   Z <- T Z
+// converges quadratically to Y = A^(1/2), Z = A^(-1/2); every step is
+// k x k GEMM work spread over the whole GPU, with two grid barriers per
+// iteration instead of Jacobi's thousands of dependent rotation rounds.
+// The eigendecomposition itself (syev) runs once, for the returned factors.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace svdrec {
+namespace {
+
+constexpr int NT = 64;  // output tile
+constexpr int NK = 16;  // reduction step
+constexpr int kNsThreads = 256;
+
+struct NsSmem {
+  double a[NT][NK + 1];
+  double b[NK][NT + 1];
+  double red[32];
+};
+
+// C[tile] = alpha * (A @ B)[tile] + diag * I[tile]; returns the tile's
+// sum of (C - I)^2 when ``resid`` (all matrices k x k, ld = k).
+__device__ double tile_gemm(NsSmem& sm, int k, const double* __restrict__ A, const double* __restrict__ B,
+                            double* __restrict__ C, int ti, int tj, double alpha, double diag, bool resid) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int r0 = ti * NT, c0 = tj * NT;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int k0 = 0; k0 < k; k0 += NK) {
+    for (int e = threadIdx.x; e < NT * NK; e += kNsThreads) {
+      const int rr = e / NK, kk = e % NK;
+      const int gr = r0 + rr, gk = k0 + kk;
+      sm.a[rr][kk] = (gr < k && gk < k) ? A[(int64_t)gr * k + gk] : 0.0;
+    }
+    for (int e = threadIdx.x; e < NK * NT; e += kNsThreads) {
+      const int kk = e / NT, cc = e % NT;
+      const int gk = k0 + kk, gc = c0 + cc;
+      sm.b[kk][cc] = (gk < k && gc < k) ? B[(int64_t)gk * k + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = sm.a[ty * 4 + i][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = sm.b[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double rs = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = r0 + ty * 4 + i;
+    if (gr >= k) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = c0 + tx * 4 + j;
+      if (gc >= k) continue;
+      const double v = alpha * acc[i][j] + (gr == gc ? diag : 0.0);
+      C[(int64_t)gr * k + gc] = v;
+      if (resid) {
+        const double d = v - (gr == gc ? 1.0 : 0.0);
+        rs = fma(d, d, rs);
+      }
+    }
+  }
+  if (resid) rs = block_sum(rs, sm.red);
+  return rs;
+}
+
+// work: Y0, Y1, Z0, Z1, T (k x k each), part (ntiles), misc
+__global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restrict__ G, int64_t ldg,
+                                                   double* __restrict__ out, int64_t ldo, double* __restrict__ Y0,
+                                                   double* __restrict__ Y1, double* __restrict__ Z0,
+                                                   double* __restrict__ Z1, double* __restrict__ T,
+                                                   double* __restrict__ part, int maxit, uint32_t* d_status,
+                                                   int* d_iters) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ NsSmem sm;
+  const int nt = (k + NT - 1) / NT;
+  const int ntiles = nt * nt;
+  // scale: A = G / trace(G) has spectrum in (0, 1]
+  double tr = 0.0;
+  for (int i = 0; i < k; ++i) tr += G[(int64_t)i * ldg + i];
+  const double inv_c = tr > 0.0 ? 1.0 / tr : 0.0;
+  const int64_t kk = (int64_t)k * k;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kk; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / k, j = t % k;
+    Y0[t] = G[i * ldg + j] * inv_c;
+    Z0[t] = (i == j) ? 1.0 : 0.0;
+  }
+  grid.sync();
+  double* Y = Y0;
+  double* Yn = Y1;
+  double* Z = Z0;
+  double* Zn = Z1;
+  double prev = 1e300;
+  int it = 0;
+  bool done = false;
+  for (; it < maxit; ++it) {
+    // phase A: T = 1.5 I - 0.5 Z Y, residual ||T - I||_F^2 per tile
+    for (int w = blockIdx.x; w < ntiles; w += gridDim.x) {
+      const double rs = tile_gemm(sm, k, Z, Y, T, w / nt, w % nt, -0.5, 1.5, true);
+      if (threadIdx.x == 0) part[w] = rs;
+    }
+    grid.sync();
+    double r = 0.0;
+    for (int w = 0; w < ntiles; ++w) r += part[w];  // same fixed order in every block
+    r = sqrt(r);
+    // quadratic convergence down to rounding, or stagnation at rounding level
+    if (r <= 8.0 * 2.220446049250313e-16 * sqrt((double)k) || (r < 1e-9 && r > 0.5 * prev)) {
+      done = true;
+      break;
+    }
+    prev = r;
+    // phase B: Y <- Y T, Z <- T Z
+    for (int w = blockIdx.x; w < 2 * ntiles; w += gridDim.x) {
+      const int q = w % ntiles;
+      if (w < ntiles)
+        tile_gemm(sm, k, Y, T, Yn, q / nt, q % nt, 1.0, 0.0, false);
+      else
+        tile_gemm(sm, k, T, Z, Zn, q / nt, q % nt, 1.0, 0.0, false);
+    }
+    grid.sync();
+    double* t1 = Y;
+    Y = Yn;
+    Yn = t1;
+    double* t2 = Z;
+    Z = Zn;
+    Zn = t2;
+  }
+  grid.sync();  // every block is done reading part[] before it is reused
+  // G^(-1/2) = A^(-1/2) / sqrt(trace); ||A^(-1/2)||_F^2 = sum 1/mu_i bounds
+  // the smallest scaled eigenvalue from below (inconclusive -> flag)
+  const double s = sqrt(inv_c);
+  double fz = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kk; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / k, j = t % k;
+    out[i * ldo + j] = Z[t] * s;
+    fz = fma(Z[t], Z[t], fz);
+  }
+  fz = block_sum(fz, sm.red);
+  if (threadIdx.x == 0) part[blockIdx.x] = fz;
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double f = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) f += part[b];
+    if (d_iters) *d_iters = it;
+    // near-singular per the reference (mu_min < 1e-14) is impossible when
+    // 1 / ||A^(-1/2)||_F^2 >= 1e-14; otherwise ask the host for the exact check
+    if (d_status && (!done || !(f * 1e-14 <= 1.0) || !(tr > 0.0))) atomicOr(d_status, SVDREC_STATUS_NS_CHECK);
+  }
+}
+
+}  // namespace
+}  // namespace svdrec
+
+using namespace svdrec;
+
+extern "C" size_t svdrec_inv_sqrt_workspace_bytes(int32_t k) {
+  const int nt = (k + NT - 1) / NT;
+  return 5 * align_up((size_t)k * k * 8) + align_up((size_t)(nt * nt + 4096) * 8) + 256;
+}
+
+extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double* d_Z, int64_t ldz, void* d_work,
+                               size_t work_bytes, uint32_t* d_status, int32_t* d_iters, void* stream) {
+  SVDREC_ARG(k >= 1 && ldg >= k && ldz >= k, "inv_sqrt: bad arguments");
+  if (work_bytes < svdrec_inv_sqrt_workspace_bytes(k)) {
+    set_error("inv_sqrt: workspace too small");
+    return SVDREC_E_WORKSPACE;
+  }
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0;
+    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, 0));
+    max_blocks = per_sm * sm_count();
+    if (max_blocks > 2 * sm_count()) max_blocks = 2 * sm_count();
+    if (max_blocks > 4096) max_blocks = 4096;
+    if (max_blocks < 1) max_blocks = 1;
+  }
+  const int nt = (k + NT - 1) / NT;
+  int nblk = 2 * nt * nt;
+  if (nblk > max_blocks) nblk = max_blocks;
+  char* w = static_cast<char*>(d_work);
+  const size_t m = align_up((size_t)k * k * 8);
+  double* Y0 = reinterpret_cast<double*>(w);
+  double* Y1 = reinterpret_cast<double*>(w + m);
+  double* Z0 = reinterpret_cast<double*>(w + 2 * m);
+  double* Z1 = reinterpret_cast<double*>(w + 3 * m);
+  double* T = reinterpret_cast<double*>(w + 4 * m);
+  double* part = reinterpret_cast<double*>(w + 5 * m);
+  int kk = k, maxit = 100;
+  void* args[] = {&kk, &d_G, &ldg, &d_Z, &ldz, &Y0, &Y1, &Z0, &Z1, &T, &part, &maxit, &d_status, &d_iters};
+  SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_ns, dim3(nblk), dim3(kNsThreads), args, 0, as_stream(stream)));
+  note_launches(1);
+  return 0;
+}

@@ -242,17 +242,43 @@ def cf_normalize(Tt: torch.Tensor):
     return Tn, norm
 
 
-def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Tn: torch.Tensor,
-               norm: torch.Tensor, gmean: float, lo: float, hi: float):
-    ldn = _mat(Tn, "cf.Tn")
+def cf_normalize_pair(X: torch.Tensor, Y: torch.Tensor):
+    """(Xn, Yn, n) with n_l = sqrt(x_l . y_l) (metric-mode item factors)."""
+    ldx, ldy = _mat(X, "cf.X"), _mat(Y, "cf.Y")
+    n, k = X.shape
+    Xn = torch.empty(n, k, dtype=F64, device=X.device)
+    Yn = torch.empty(n, k, dtype=F64, device=X.device)
+    norm = torch.empty(n, dtype=F64, device=X.device)
+    with _span("cf_normalize", 4 * n * k * 8):
+        call("svdrec_cf_normalize_pair", n, k, ptr(X), ldx, ptr(Y), ldy, ptr(Xn), ptr(Yn), k, ptr(norm),
+             stream_handle())
+    return Xn, Yn, norm
+
+
+def inv_sqrt(G: torch.Tensor, status: torch.Tensor, iters: torch.Tensor | None = None) -> torch.Tensor:
+    """G^(-1/2) by coupled Newton-Schulz (device); flags NS_CHECK if unsure."""
+    ldg = _mat(G, "inv_sqrt.G")
+    k = G.shape[0]
+    Z = torch.empty(k, k, dtype=F64, device=G.device)
+    ws, nb = scratch(G.device).get(query("svdrec_inv_sqrt_workspace_bytes", k))
+    with _span("inv_sqrt", 2 * k * k * 8):
+        call("svdrec_inv_sqrt", k, ptr(G), ldg, ptr(Z), k, ws, nb, ptr(status), ptr(iters), stream_handle())
+    return Z
+
+
+def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Yn: torch.Tensor,
+               Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float):
+    ldn = _mat(Yn, "cf.Yn")
+    if _mat(Xn, "cf.Xn") != ldn or Xn.shape != Yn.shape:
+        raise ValueError("cf_predict: Xn and Yn must share shape and leading dimension")
     ns = users.shape[0]
-    val = torch.empty(ns, dtype=F64, device=Tn.device)
-    raw = torch.empty(ns, dtype=F64, device=Tn.device)
-    fb = torch.empty(ns, dtype=torch.uint8, device=Tn.device)
+    val = torch.empty(ns, dtype=F64, device=Yn.device)
+    raw = torch.empty(ns, dtype=F64, device=Yn.device)
+    fb = torch.empty(ns, dtype=torch.uint8, device=Yn.device)
     with _span("cf_predict", 0):
         call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
-             ptr(csr.indices), ptr(csr.values), Tn.shape[1], ptr(Tn), ldn, ptr(norm), float(gmean), float(lo),
-             float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
+             ptr(csr.indices), ptr(csr.values), Yn.shape[1], ptr(Yn), ptr(Xn), ldn, ptr(norm), float(gmean),
+             float(lo), float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
     return val, raw, fb
 
 
