@@ -184,6 +184,12 @@ int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double
  *   raw prediction is (Xn_j . P_u) / (Xn_j . S_u) with the |w| < 1e-9
  *   user-mean / global-mean fallback and clamping.  Writes clamped value,
  *   raw value and fallback flag per sample (in grouped order).  k <= 1024.
+ *   d_hot_items (nullable) lists items by descending training degree and
+ *   d_item_rank is its inverse; the first items whose Yn rows fit in
+ *   ~200 KB of shared memory are staged on-chip in every CTA.  Warps fetch
+ *   groups dynamically through d_counter (one device int32, reset here) in
+ *   the order d_group_order (nullable; heaviest users first balances the
+ *   persistent grid).
  *  svdrec_err_sum: fixed-order sum |pred - truth| and (pred-truth)^2.
  * ------------------------------------------------------------------- */
 int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int64_t ldt, double* d_Tn,
@@ -196,6 +202,8 @@ int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32
                       const int32_t* d_indices, const double* d_values, int32_t k,
                       const double* d_Yn, const double* d_Xn, int64_t ldn, const double* d_norm,
                       double global_mean, double rating_min, double rating_max,
+                      const int32_t* d_item_rank, const int32_t* d_hot_items, int32_t nhot_avail,
+                      const int32_t* d_group_order, int32_t* d_counter,
                       double* d_value, double* d_raw, uint8_t* d_fallback, void* stream);
 
 /* G^(-1/2) of a k x k SPD Gram by coupled Newton-Schulz iteration (one

@@ -165,6 +165,21 @@ class _Samples:
         self.items = t(i[order], np.int32)
         self.truth = t(r[order], np.float64)
         self.h2d_bytes = groups.size * 8 + self.n * 16
+        self.group_users = us[groups[:-1]] if us.size else np.empty(0, np.int64)
+        self.device = device
+        self.counter = torch.zeros(1, dtype=torch.int32, device=device)
+        self._order = {}
+
+    def order_for(self, A: SparseRatings) -> torch.Tensor | None:
+        """Group order, heaviest training rows first (cached per matrix)."""
+        o = self._order.get(id(A))
+        if o is None:
+            if self.group_users.size == 0:
+                return None
+            deg = np.diff(A.matrix.indptr)[self.group_users]
+            perm = np.argsort(-deg, kind="stable").astype(np.int32)
+            o = self._order[id(A)] = torch.from_numpy(perm).to(self.device)
+        return o
 
     def check_bounds(self, A: SparseRatings) -> None:
         if self.n == 0:
@@ -178,7 +193,7 @@ class _Samples:
 def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float):
     d = A.device(factors.Xn.device)
     return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Yn, factors.Xn, factors.norm_device, gmean,
-                        A.rating_min, A.rating_max)
+                        A.rating_min, A.rating_max, s.order_for(A), s.counter)
 
 
 def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: int) -> Prediction:

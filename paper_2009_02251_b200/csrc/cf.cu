@@ -57,19 +57,37 @@ __global__ void k_normalize_pair(int64_t n, int k, const double* __restrict__ X,
 }
 
 template <int MAXR>
-__global__ void __launch_bounds__(128) k_predict(int64_t ngroups, const int64_t* __restrict__ gstart,
-                                                 const int32_t* __restrict__ users, const int32_t* __restrict__ items,
-                                                 const int64_t* __restrict__ indptr,
-                                                 const int32_t* __restrict__ indices,
-                                                 const double* __restrict__ values, int k,
-                                                 const double* __restrict__ Yn, const double* __restrict__ Xn,
-                                                 int64_t ldn,
-                                                 const double* __restrict__ norm, double gmean, double lo, double hi,
-                                                 double* __restrict__ out_val, double* __restrict__ out_raw,
-                                                 uint8_t* __restrict__ out_fb) {
+__global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ngroups,
+                                                                      const int64_t* __restrict__ gstart,
+                                                    const int32_t* __restrict__ users,
+                                                    const int32_t* __restrict__ items,
+                                                    const int64_t* __restrict__ indptr,
+                                                    const int32_t* __restrict__ indices,
+                                                    const double* __restrict__ values, int k,
+                                                    const double* __restrict__ Yn, const double* __restrict__ Xn,
+                                                    int64_t ldn, const double* __restrict__ norm, double gmean,
+                                                    double lo, double hi, const int32_t* __restrict__ rank,
+                                                    const int32_t* __restrict__ hot, int nhot,
+                                                    const int32_t* __restrict__ order, int* __restrict__ counter,
+                                                    double* __restrict__ out_val, double* __restrict__ out_raw,
+                                                    uint8_t* __restrict__ out_fb) {
+  // hot items (highest training degree) keep their unit rows in shared
+  // memory: under Zipf popularity they carry most of the gathers
+  extern __shared__ double hs[];
+  for (int64_t t = threadIdx.x; t < (int64_t)nhot * k; t += blockDim.x) {
+    const int64_t h = t / k, e = t - h * k;
+    hs[t] = Yn[(int64_t)hot[h] * ldn + e];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (g >= ngroups) return;
+  // dynamic work fetch over user groups, heaviest users first (``order``):
+  // a static split leaves SMs idle behind the few 10^4-rating users
+  while (true) {
+  int gi = 0;
+  if (lane == 0) gi = atomicAdd(counter, 1);
+  gi = __shfl_sync(0xffffffffu, gi, 0);
+  if (gi >= ngroups) break;
+  const int64_t g = order ? (int64_t)order[gi] : (int64_t)gi;
   const int64_t s0 = gstart[g], s1 = gstart[g + 1];
   const int32_t u = users[s0];
   const int64_t a = indptr[u], e = indptr[u + 1];
@@ -79,25 +97,48 @@ __global__ void __launch_bounds__(128) k_predict(int64_t ngroups, const int64_t*
   double vsum = 0.0;
   for (int64_t base = a; base < e; base += 32) {
     const int64_t my = base + lane;
-    int32_t ci = 0;
+    int32_t ci = 0, rk = 0x7fffffff;
     double vi = 0.0;
     if (my < e) {
       ci = __ldg(indices + my);
       vi = __ldg(values + my);
+      rk = rank ? __ldg(rank + ci) : 0x7fffffff;
     }
     const int nv = (int)min64(32, e - base);
-    for (int j = 0; j < nv; ++j) {
-      const int32_t c = __shfl_sync(0xffffffffu, ci, j);
-      const double v = __shfl_sync(0xffffffffu, vi, j);
-      vsum += v;
-      const double* row = Yn + (int64_t)c * ldn;
+    // four nonzeros per step, branch-free (generic pointers into shared or
+    // global memory), so each lane keeps 4 * MAXR independent loads in
+    // flight; the accumulation order is still nonzero by nonzero
+    for (int j = 0; j < nv; j += 4) {
+      const double* rows[4];
+      double vv[4], mk[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int jj = (j + q) & 31;
+        const int32_t c = __shfl_sync(0xffffffffu, ci, jj);
+        const int32_t r = __shfl_sync(0xffffffffu, rk, jj);
+        const double v = __shfl_sync(0xffffffffu, vi, jj);
+        const bool ok = j + q < nv;
+        rows[q] = (r < nhot) ? hs + (int64_t)r * k : Yn + (int64_t)c * ldn;
+        vv[q] = ok ? v : 0.0;
+        mk[q] = ok ? 1.0 : 0.0;
+      }
+      vsum += vv[0];
+      vsum += vv[1];
+      vsum += vv[2];
+      vsum += vv[3];
 #pragma unroll
       for (int t = 0; t < MAXR; ++t) {
         const int idx = lane + 32 * t;
         if (idx < k) {
-          const double x = __ldg(row + idx);
-          P[t] = fma(v, x, P[t]);
-          S[t] += x;
+          const double x0 = rows[0][idx], x1 = rows[1][idx], x2 = rows[2][idx], x3 = rows[3][idx];
+          P[t] = fma(vv[0], x0, P[t]);
+          P[t] = fma(vv[1], x1, P[t]);
+          P[t] = fma(vv[2], x2, P[t]);
+          P[t] = fma(vv[3], x3, P[t]);
+          S[t] = fma(mk[0], x0, S[t]);
+          S[t] = fma(mk[1], x1, S[t]);
+          S[t] = fma(mk[2], x2, S[t]);
+          S[t] = fma(mk[3], x3, S[t]);
         }
       }
     }
@@ -131,6 +172,7 @@ __global__ void __launch_bounds__(128) k_predict(int64_t ngroups, const int64_t*
       out_fb[sidx] = fb ? 1 : 0;
     }
   }
+  }  // dynamic loop over user groups
 }
 
 __global__ void k_overlap(int64_t ns, const int32_t* __restrict__ users, const int32_t* __restrict__ items,
@@ -193,6 +235,8 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
                                  const double* d_values, int32_t k, const double* d_Yn, const double* d_Xn,
                                  int64_t ldn,
                                  const double* d_norm, double global_mean, double rating_min, double rating_max,
+                                 const int32_t* d_item_rank, const int32_t* d_hot_items, int32_t nhot_avail,
+                                 const int32_t* d_group_order, int32_t* d_counter,
                                  double* d_value, double* d_raw, uint8_t* d_fallback, void* stream) {
   SVDREC_ARG(ngroups >= 0 && k >= 1 && ldn >= k, "cf_predict: bad arguments");
   if (k > 1024) {
@@ -200,14 +244,35 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
     return SVDREC_E_UNSUPPORTED;
   }
   if (ngroups == 0) return 0;
-  const int64_t thr = ngroups * 32;
-  const unsigned grid = (unsigned)((thr + 127) / 128);
+  SVDREC_ARG(d_counter != nullptr, "cf_predict: d_counter (one device int) is required");
+  SVDREC_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), as_stream(stream)));
   cudaStream_t s = as_stream(stream);
   const int r = (k + 31) / 32;
-#define SVDREC_PRED(R)                                                                                         \
-  k_predict<R><<<grid, 128, 0, s>>>(ngroups, d_group_start, d_users, d_items, d_indptr, d_indices, d_values, k, \
-                                    d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, d_value, d_raw, \
-                                    d_fallback)
+  // two 16-warp CTAs per SM (k <= 256) keep enough gathers in flight; each
+  // stages ~100 KB of the hottest item rows
+  const int per_sm = r <= 4 ? 2 : 1;
+  const size_t kHotBytes = per_sm == 2 ? 100 * 1024 : 200 * 1024;
+  int nhot = d_item_rank && d_hot_items ? (int)(kHotBytes / ((size_t)k * 8)) : 0;
+  if (nhot > nhot_avail) nhot = nhot_avail;
+  if (nhot < 0) nhot = 0;
+  const size_t smem = (size_t)nhot * k * 8;
+  // persistent: one 16-warp CTA per SM, warps stride over user groups
+  const int64_t want = (ngroups + 15) / 16;
+  const int64_t slots = (int64_t)per_sm * sm_count();
+  const unsigned grid = (unsigned)(want < slots ? (want > 0 ? want : 1) : slots);
+#define SVDREC_PRED(R)                                                                                           \
+  do {                                                                                                           \
+    static bool attr = false;                                                                                    \
+    if (!attr) {                                                                                                 \
+      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                       210 * 1024));                                                  \
+      attr = true;                                                                                               \
+    }                                                                                                            \
+    k_predict<R><<<grid, 512, smem, s>>>(ngroups, d_group_start, d_users, d_items, d_indptr, d_indices,         \
+                                         d_values, k, d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min,         \
+                                         rating_max, d_item_rank, d_hot_items, nhot, d_group_order, d_counter,    \
+                                         d_value, d_raw, d_fallback);                                             \
+  } while (0)
   if (r <= 1)
     SVDREC_PRED(1);
   else if (r <= 2)

@@ -181,8 +181,16 @@ class DeviceRatings:
         self.nnz = ratings.nnz
         self.rating_min, self.rating_max = ratings.rating_min, ratings.rating_max
         self.A = DeviceCSR(ratings.matrix, device)
-        self.AT = DeviceCSR(ratings.matrix.T.tocsr(), device)
-        self.h2d_bytes = self.A.h2d_bytes + self.AT.h2d_bytes
+        at = ratings.matrix.T.tocsr()
+        self.AT = DeviceCSR(at, device)
+        # item popularity order (column degree, descending) for on-chip
+        # staging of the hottest items' rows in the CF scoring kernel
+        order = np.argsort(-np.diff(at.indptr), kind="stable").astype(np.int32)
+        rank = np.empty(self.n, dtype=np.int32)
+        rank[order] = np.arange(self.n, dtype=np.int32)
+        self.A.hot_items = torch.from_numpy(order).to(device)
+        self.A.item_rank = torch.from_numpy(rank).to(device)
+        self.h2d_bytes = self.A.h2d_bytes + self.AT.h2d_bytes + 8 * self.n
         # ||A||_F^2 and the global mean (fro_norm_sq, linalg.py:161-168;
         # _global_mean, cf.py:102-105) reduced on the device, read once.
         from . import kernels as K
