@@ -83,14 +83,24 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t nseg, const int32_t* __res
           vi = __ldg(values + my);
         }
         const int nvalid = (int)min64(32, end - base);
-        for (int j = 0; j < nvalid; j += npw) {
-          const int src = j + slot;
-          const int32_t c = __shfl_sync(0xffffffffu, ci, src & 31);
-          const double v = __shfl_sync(0xffffffffu, vi, src & 31);
-          if (colok && src < nvalid) {
-            const V x = *reinterpret_cast<const V*>(X + (int64_t)c * ldx + col);
-            fma_v(acc, v, x);
+        // four gathers in flight per lane, then the FMAs in nonzero order
+        for (int j = 0; j < nvalid; j += 4 * npw) {
+          V xs[4];
+          double vs[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int src = j + q * npw + slot;
+            const int32_t c = __shfl_sync(0xffffffffu, ci, src & 31);
+            const double v = __shfl_sync(0xffffffffu, vi, src & 31);
+            const bool ok = colok && src < nvalid;
+            vs[q] = ok ? v : 0.0;
+            if (ok)
+              xs[q] = *reinterpret_cast<const V*>(X + (int64_t)c * ldx + col);
+            else
+              zero_v(xs[q]);
           }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) fma_v(acc, vs[q], xs[q]);
         }
       }
       // fold the npw slot groups onto slot 0 (fixed order)

@@ -24,7 +24,15 @@ namespace {
 constexpr int kThreads = 256;
 constexpr size_t kChunkBytes = 96 * 1024;  // one chunk's panel in smem
 
-inline int rc_max_for(int b) { return (int)(kChunkBytes / (8 * (size_t)b)); }
+// Rows per chunk: small panels (~32 KB) so several CTAs share an SM and hide
+// each other's barrier latency, but >= 2b so every tree level halves the
+// rows, and <= the 2-matrix shared-memory budget of the Q builder.
+inline int rc_max_for(int b) {
+  int rc = (int)(32768 / (8 * (size_t)b));
+  if (rc < 2 * b) rc = 2 * b;
+  const int cap = (int)(kChunkBytes / (8 * (size_t)b));
+  return rc < cap ? rc : cap;
+}
 
 struct Level {
   int64_t rows, nc;
