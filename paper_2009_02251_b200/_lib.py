@@ -143,9 +143,12 @@ _SCRATCH: dict = {}
 
 
 def scratch(device=None) -> Scratch:
+    """Scratch for (device, current stream): calls on one stream are ordered,
+    so they can share it; concurrent streams each get their own."""
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    key = (dev.index if dev.index is not None else torch.cuda.current_device())
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    key = (idx, torch.cuda.current_stream(idx).cuda_stream)
     s = _SCRATCH.get(key)
     if s is None:
-        s = _SCRATCH[key] = Scratch(torch.device("cuda", key))
+        s = _SCRATCH[key] = Scratch(torch.device("cuda", idx))
     return s

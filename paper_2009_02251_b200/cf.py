@@ -300,6 +300,7 @@ class ValidationMae:
         self._Gsrc = None
         self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1), iters=("u4", 1))
         self._gmean = d.global_mean
+        self._stream = torch.cuda.Stream(device=dev)
 
     @property
     def validation(self):
@@ -323,25 +324,47 @@ class ValidationMae:
         self._G, self._Gsrc = G, Bt
         return G
 
-    def __call__(self, state: QbState) -> bool:
+    def submit(self, state: QbState):
+        """Queue the scoring of ``state`` on the criterion's own stream and
+        return a handle; nothing waits.  The QB engine can meanwhile queue
+        its next block on the current stream (see auto_latent_factors)."""
         if state.rank == 0:
             raise ValueError("empty factorization has no latent factors")
-        mb = self._mb
+        cur = torch.cuda.current_stream()
+        s2 = self._stream
+        s2.wait_stream(cur)  # block l's columns of B are complete
         Bt = state.Bt_device
-        G = self._gram(Bt)
-        Z = K.inv_sqrt(G, mb["status"], mb["iters"])
-        factors = LatentFactors.from_qb_metric(Bt, G, Z)
-        s = self.samples
-        val, _, _ = _predict_device(self.train, factors, s, self._gmean)
-        K.err_sum(val, s.truth, out=mb["sums"])
-        got = mb.read()  # one host read per block: error sums + status
+        Bt.record_stream(s2)
+        mb = self._mb
+        with torch.cuda.stream(s2):
+            G = self._gram(Bt)
+            Z = K.inv_sqrt(G, mb["status"], mb["iters"])
+            factors = LatentFactors.from_qb_metric(Bt, G, Z)
+            s = self.samples
+            val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+            K.err_sum(val, s.truth, out=mb["sums"])
+            mb.read_async()
+        return state, factors
+
+    def collect(self, pending) -> bool:
+        """Wait for a submitted block's score, update the trace, and return
+        the stop decision (cf.py:227-240)."""
+        state, factors = pending
+        state.check()  # the engine's deferred per-block errors, if any
+        mb = self._mb
+        got = mb.get()  # one host read per block: error sums + status
         flags = int(got["status"][0])
+        s = self.samples
+        if flags:
+            with torch.cuda.stream(self._stream):
+                mb["status"].zero_()
         if flags & STATUS_NS_CHECK:
             # Newton-Schulz could not certify the eigenvalue floor: decide it
             # exactly like the reference (eigh) and score with its T
-            factors = LatentFactors(_eig_T(Bt, G))
-            val, _, _ = _predict_device(self.train, factors, s, self._gmean)
-            got = {"sums": K.err_sum(val, s.truth).cpu().numpy()}
+            with torch.cuda.stream(self._stream):
+                factors = LatentFactors(_eig_T(state.Bt_device, factors._G))
+                val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+                got = {"sums": K.err_sum(val, s.truth).cpu().numpy()}
         score, rmse = float(got["sums"][0] / s.n), float(np.sqrt(got["sums"][1] / s.n))
         self.trace.append(BlockEval(k=state.rank, mae=score, seconds=time.perf_counter() - self._start))
         if score < self.best_mae - self.min_improvement:
@@ -353,6 +376,20 @@ class ValidationMae:
             self.best_rmse = rmse
             self.best_factors = factors
         return self._stale >= self.patience
+
+    def __call__(self, state: QbState) -> bool:
+        return self.collect(self.submit(state))
+
+    def join(self) -> None:
+        """Make the current stream wait for everything scored so far and
+        keep the best factors alive across streams."""
+        cur = torch.cuda.current_stream()
+        cur.wait_stream(self._stream)
+        f = self.best_factors
+        if f is not None:
+            for t in (f.Xn, f.Yn, f.norm_device, f._G):
+                if t is not None:
+                    t.record_stream(cur)
 
 
 def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, passes: int = 10, patience: int = 2,
@@ -369,11 +406,20 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
         raise ValueError(f"block_size {block_size} too large for min(m, n) = {min(A.shape)}")
     criterion = ValidationMae(A, validation, patience=patience, min_improvement=min_improvement)
     stream = GaussianStream(seed)
-    for state in qb_pass_blocks(A, block_size, passes, stream, max_rank=max_rank):
-        if criterion(state):
+    gen = qb_pass_blocks(A, block_size, passes, stream, max_rank=max_rank)
+    # Same criterion sequence as the reference's ``for state in ...: if
+    # criterion(state): break``, pipelined: block l is scored on the
+    # criterion's stream while block l+1 is factored on this one (a block
+    # computed past the stop is simply discarded).
+    state = next(gen, None)
+    while state is not None:
+        pending = criterion.submit(state)
+        capped = max_rank is not None and state.rank >= max_rank
+        nxt = None if capped else next(gen, None)
+        if criterion.collect(pending) or capped:
             break
-        if max_rank is not None and state.rank >= max_rank:
-            break
+        state = nxt
+    criterion.join()
     if criterion.best_factors is None:
         raise RankExhaustedError("rank cap reached before any block was scored")
     return criterion.best_factors, criterion.trace

@@ -83,8 +83,23 @@ class Mailbox:
         view = self.buf[o: o + (8 if kind == "f8" else 4) * n]
         return view.view(F64) if kind == "f8" else view.view(torch.int32)
 
+    def read_async(self) -> "Mailbox":
+        """Queue the device->host copy (pinned) on the current stream; get()
+        then waits for just that copy, not for later work on the stream."""
+        self._host = torch.empty(self.buf.numel(), dtype=torch.uint8, pin_memory=True)
+        self._host.copy_(self.buf, non_blocking=True)
+        self._ev = torch.cuda.Event()
+        self._ev.record()
+        return self
+
+    def get(self) -> dict:
+        self._ev.synchronize()
+        return self._parse(self._host.numpy(), reset=False)
+
     def read(self) -> dict:
-        host = self.buf.cpu().numpy()
+        return self._parse(self.buf.cpu().numpy(), reset=True)
+
+    def _parse(self, host, reset: bool) -> dict:
         out = {}
         dirty = False
         for name, (kind, o, n) in self.off.items():
@@ -92,7 +107,7 @@ class Mailbox:
             out[name] = a.copy()
             if kind == "u4" and a.any():
                 dirty = True
-        if dirty:
+        if dirty and reset:
             for name, (kind, o, n) in self.off.items():
                 if kind == "u4":
                     self[name].zero_()

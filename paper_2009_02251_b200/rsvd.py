@@ -35,19 +35,44 @@ class QbState:
 
     Same fields as the reference's QbState (rsvd.py:40-59).  ``Q`` and
     ``B`` are numpy arrays materialised lazily from the device views
-    ``Q_device`` (m x k) and ``Bt_device`` (n x k, = B.T).
+    ``Q_device`` (m x k) and ``Bt_device`` (n x k, = B.T).  ``err`` and
+    ``row_energy`` of an engine snapshot are read back from the device only
+    when first used, so a criterion that ignores them (ValidationMae) costs
+    no host round trip per block.
     """
 
-    def __init__(self, Q_device, Bt_device, err, blocks, block_size, frob_sq, row_energy=None):
+    def __init__(self, Q_device, Bt_device, err, blocks, block_size, frob_sq, row_energy=None, engine=None):
         self.Q_device = Q_device
         self.Bt_device = Bt_device
-        self.err = float(err)
+        self._err = None if err is None else float(err)
         self.blocks = int(blocks)
         self.block_size = int(block_size)
         self.frob_sq = float(frob_sq)
-        self.row_energy = row_energy
+        self._row_energy = row_energy
+        self._engine = engine
         self._Q = None
         self._B = None
+
+    def _materialise(self) -> None:
+        if self._err is None:
+            self._engine.flush(self.blocks)
+            self._err = self._engine.errs[self.blocks - 1]
+            self._row_energy = np.asarray(self._engine.row_energy[: self.rank])
+
+    @property
+    def err(self) -> float:
+        self._materialise()
+        return self._err
+
+    @property
+    def row_energy(self) -> np.ndarray:
+        self._materialise()
+        return self._row_energy
+
+    def check(self) -> None:
+        """Raise the deferred device-side errors of this block (if any)."""
+        if self._engine is not None:
+            self._engine.flush(self.blocks)
 
     @property
     def rank(self) -> int:
@@ -123,13 +148,35 @@ class _QbEngine:
         self.ym = torch.empty(self.m, b, dtype=F64, device=self.dev)
         self.ym2 = torch.empty(self.m, b, dtype=F64, device=self.dev)
         self.yn = torch.empty(self.n, b, dtype=F64, device=self.dev)
-        # one host read per block: ||B_l||_F^2, row energies, status flags
-        self.mb = K.Mailbox(self.dev, colsq=("f8", b), total=("f8", 1), status=("u4", 1))
-        self.status = self.mb["status"]
+        # per block: a small mailbox (||B_l||_F^2, row energies, status
+        # flags of the block's LU / sketch draws), copied back asynchronously
+        # and parsed only when someone needs err / row energies / errors
+        self._new_mailbox()
         self.frob = self.d.frob_sq if A.nnz else 0.0
         self.err = self.frob
+        self.errs: list[float] = []
         self.blocks = 0
         self.row_energy: list[float] = []
+        self._pending: list = []
+
+    def _new_mailbox(self) -> None:
+        self.mb = K.Mailbox(self.dev, colsq=("f8", self.b), total=("f8", 1), status=("u4", 1))
+        self.status = self.mb["status"]
+
+    def flush(self, upto: int | None = None) -> None:
+        """Parse the read-backs of blocks 1..upto (default: all), in order;
+        waits only for those blocks, not for work queued after them."""
+        upto = self.blocks if upto is None else upto
+        while self._pending and len(self.errs) < upto:
+            got = self._pending.pop(0).get()
+            flags = int(got["status"][0])
+            if flags & STATUS_STREAM_SHORT:
+                raise RuntimeError("Gaussian stream window exhausted (internal sizing error)")
+            if flags & STATUS_ZERO_PIVOT:
+                raise RankDeficientError("exactly singular pivot in LU factorization")
+            self.err = max(self.err - float(got["total"][0]), 0.0)
+            self.errs.append(self.err)
+            self.row_energy.extend(float(x) for x in got["colsq"])
 
     def _alloc_cols(self, need: int) -> int:
         c = max(need, 4 * self.b, 64)
@@ -189,23 +236,17 @@ class _QbEngine:
         bdst = self.Bt[:, k0 : k0 + b]
         self.AT_mul(qdst, bdst)
         K.sumsq(bdst, self.mb["colsq"], self.mb["total"])
-        got = self.mb.read()  # the one host sync per block
-        flags = int(got["status"][0])
-        if flags & STATUS_STREAM_SHORT:
-            raise RuntimeError("Gaussian stream window exhausted (internal sizing error)")
-        if flags & STATUS_ZERO_PIVOT:
-            raise RankDeficientError("exactly singular pivot in LU factorization")
+        self._pending.append(self.mb.read_async())  # parsed lazily by flush()
+        self._new_mailbox()
         self.K = k0 + b
         self.blocks += 1
-        self.err = max(self.err - float(got["total"][0]), 0.0)
-        self.row_energy.extend(float(x) for x in got["colsq"])
 
     def normal(self, rows: int, cols: int, out):
         return self.stream.normal_device(rows, cols, out=out, status=self.status)
 
     def state(self) -> QbState:
-        return QbState(self.Q[:, : self.K], self.Bt[:, : self.K], self.err, self.blocks, self.b, self.frob,
-                       np.asarray(self.row_energy))
+        return QbState(self.Q[:, : self.K], self.Bt[:, : self.K], None, self.blocks, self.b, self.frob,
+                       None, engine=self)
 
 
 def qb_power_blocks(A: SparseRatings, block_size: int, power: int, stream: GaussianStream,
@@ -375,6 +416,8 @@ def adaptive_pca(A: SparseRatings, criterion: TerminationCriterion, block_size: 
             break
         if max_rank is not None and state.rank >= max_rank:
             break
+    if last is not None:
+        last.check()  # deferred LU / stream errors surface like the reference's
     if met is None:
         raise RankExhaustedError("termination criterion never met", state=last)
     if isinstance(criterion, FixedRank):
