@@ -187,9 +187,13 @@ int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double
  *   d_hot_items (nullable) lists items by descending training degree and
  *   d_item_rank is its inverse; the first items whose Yn rows fit in
  *   ~200 KB of shared memory are staged on-chip in every CTA.  Warps fetch
- *   groups dynamically through d_counter (one device int32, reset here) in
- *   the order d_group_order (nullable; heaviest users first balances the
- *   persistent grid).
+ *   work items dynamically through d_counter (one device int32, reset
+ *   here): d_work holds nwork (group, chunk) pairs, heaviest users first;
+ *   d_ginfo holds per group (nchunks, first partial slot, done index).
+ *   Users with more than ``chunk`` ratings are split across warps; each
+ *   chunk stores (P, S, sum v) in d_partial ((2k+1) doubles per slot) and
+ *   the warp completing the group (d_done counters, ndone of them, reset
+ *   here) adds the slots in order and scores the group's samples.
  *  svdrec_err_sum: fixed-order sum |pred - truth| and (pred-truth)^2.
  * ------------------------------------------------------------------- */
 int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int64_t ldt, double* d_Tn,
@@ -203,7 +207,8 @@ int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32
                       const double* d_Yn, const double* d_Xn, int64_t ldn, const double* d_norm,
                       double global_mean, double rating_min, double rating_max,
                       const int32_t* d_item_rank, const int32_t* d_hot_items, int32_t nhot_avail,
-                      const int32_t* d_group_order, int32_t* d_counter,
+                      int64_t nwork, const int32_t* d_work, const int32_t* d_ginfo, int32_t chunk,
+                      int32_t* d_done, int64_t ndone, double* d_partial, int32_t* d_counter,
                       double* d_value, double* d_raw, uint8_t* d_fallback, void* stream);
 
 /* G^(-1/2) of a k x k SPD Gram by coupled Newton-Schulz iteration (one

@@ -15,6 +15,7 @@ access to ``T``), exactly as latent_from_qb computes it.
 """
 from __future__ import annotations
 
+import os
 import time
 from typing import Iterable, NamedTuple, Sequence
 
@@ -29,6 +30,9 @@ from .sparse import SparseRatings
 
 WEIGHT_FLOOR = 1e-9  # cf.py:23
 F64 = torch.float64
+# Score block l on a side stream while block l+1 is factored (SVDREC_PIPELINE=1).
+# Off by default: measured slower on B200 (the two streams thrash L2).
+PIPELINE = os.environ.get("SVDREC_PIPELINE", "0") == "1"
 
 
 class Prediction(NamedTuple):
@@ -138,6 +142,49 @@ def latent_from_qb(state: QbState) -> LatentFactors:
     return LatentFactors(_eig_T(state.Bt_device))
 
 
+class WorkPlan:
+    """Work items of the CF scoring kernel for one (samples, matrix) pair.
+
+    Groups (one per user with samples) are cut into chunks of at most
+    ``CHUNK`` training ratings; items are ordered heaviest user first so the
+    dynamic scheduler never ends behind a long row.
+    """
+
+    CHUNK = 512
+
+    def __init__(self, group_deg: np.ndarray, device):
+        ng = group_deg.size
+        nch = np.maximum(1, -(-group_deg // self.CHUNK)).astype(np.int64)
+        split = nch > 1
+        slot0 = np.full(ng, -1, dtype=np.int64)
+        slot0[split] = np.cumsum(nch[split]) - nch[split]
+        done = np.full(ng, -1, dtype=np.int64)
+        done[split] = np.arange(int(split.sum()))
+        order = np.argsort(-group_deg, kind="stable")
+        wg = np.repeat(order, nch[order])
+        first = np.repeat(np.cumsum(nch[order]) - nch[order], nch[order])
+        wc = np.arange(wg.size) - first
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)  # noqa: E731
+        self.nwork = int(wg.size)
+        self.work = t(np.stack([wg, wc], axis=1).ravel()) if wg.size else torch.zeros(2, dtype=torch.int32,
+                                                                                        device=device)
+        self.ginfo = t(np.stack([nch, slot0, done], axis=1).ravel()) if ng else torch.zeros(3, dtype=torch.int32,
+                                                                                             device=device)
+        self.ndone = int(split.sum())
+        self.nslots = int(nch[split].sum())
+        self.done = torch.zeros(max(self.ndone, 1), dtype=torch.int32, device=device)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=device)
+        self.chunk = self.CHUNK
+        self.device = device
+        self._part = None
+
+    def partial(self, k: int) -> torch.Tensor:
+        need = max(self.nslots * (2 * k + 1), 1)
+        if self._part is None or self._part.numel() < need:
+            self._part = torch.empty(need, dtype=torch.float64, device=self.device)
+        return self._part
+
+
 class _Samples:
     """Held-out (user, item, rating) triples, user-grouped, on the device."""
 
@@ -167,19 +214,14 @@ class _Samples:
         self.h2d_bytes = groups.size * 8 + self.n * 16
         self.group_users = us[groups[:-1]] if us.size else np.empty(0, np.int64)
         self.device = device
-        self.counter = torch.zeros(1, dtype=torch.int32, device=device)
-        self._order = {}
+        self._plans = {}
 
-    def order_for(self, A: SparseRatings) -> torch.Tensor | None:
-        """Group order, heaviest training rows first (cached per matrix)."""
-        o = self._order.get(id(A))
-        if o is None:
-            if self.group_users.size == 0:
-                return None
-            deg = np.diff(A.matrix.indptr)[self.group_users]
-            perm = np.argsort(-deg, kind="stable").astype(np.int32)
-            o = self._order[id(A)] = torch.from_numpy(perm).to(self.device)
-        return o
+    def plan_for(self, A: SparseRatings) -> "WorkPlan":
+        """Scoring work plan against training matrix ``A`` (cached)."""
+        p = self._plans.get(id(A))
+        if p is None:
+            p = self._plans[id(A)] = WorkPlan(np.diff(A.matrix.indptr)[self.group_users], self.device)
+        return p
 
     def check_bounds(self, A: SparseRatings) -> None:
         if self.n == 0:
@@ -193,7 +235,7 @@ class _Samples:
 def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float):
     d = A.device(factors.Xn.device)
     return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Yn, factors.Xn, factors.norm_device, gmean,
-                        A.rating_min, A.rating_max, s.order_for(A), s.counter)
+                        A.rating_min, A.rating_max, s.plan_for(A))
 
 
 def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: int) -> Prediction:
@@ -411,13 +453,19 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
     # criterion(state): break``, pipelined: block l is scored on the
     # criterion's stream while block l+1 is factored on this one (a block
     # computed past the stop is simply discarded).
+    pipeline = PIPELINE
     state = next(gen, None)
     while state is not None:
         pending = criterion.submit(state)
         capped = max_rank is not None and state.rank >= max_rank
-        nxt = None if capped else next(gen, None)
-        if criterion.collect(pending) or capped:
-            break
+        if pipeline:
+            nxt = None if capped else next(gen, None)
+            if criterion.collect(pending) or capped:
+                break
+        else:
+            if criterion.collect(pending) or capped:
+                break
+            nxt = next(gen, None)
         state = nxt
     criterion.join()
     if criterion.best_factors is None:

@@ -68,7 +68,10 @@ __global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ng
                                                     int64_t ldn, const double* __restrict__ norm, double gmean,
                                                     double lo, double hi, const int32_t* __restrict__ rank,
                                                     const int32_t* __restrict__ hot, int nhot,
-                                                    const int32_t* __restrict__ order, int* __restrict__ counter,
+                                                    int64_t nwork, const int32_t* __restrict__ work,
+                                                    const int32_t* __restrict__ ginfo, int chunk,
+                                                    int* __restrict__ done, double* __restrict__ part,
+                                                    int* __restrict__ counter,
                                                     double* __restrict__ out_val, double* __restrict__ out_raw,
                                                     uint8_t* __restrict__ out_fb) {
   // hot items (highest training degree) keep their unit rows in shared
@@ -80,17 +83,23 @@ __global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ng
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  // dynamic work fetch over user groups, heaviest users first (``order``):
-  // a static split leaves SMs idle behind the few 10^4-rating users
+  // Work items are (group, chunk) pairs, heaviest users first.  Users with
+  // more than ``chunk`` ratings are split across warps: each chunk leaves
+  // (P, S, sum v) in its partial slot and the warp that completes the group
+  // last adds the slots in order (deterministic) and scores the samples.
   while (true) {
-  int gi = 0;
-  if (lane == 0) gi = atomicAdd(counter, 1);
-  gi = __shfl_sync(0xffffffffu, gi, 0);
-  if (gi >= ngroups) break;
-  const int64_t g = order ? (int64_t)order[gi] : (int64_t)gi;
+  int wi = 0;
+  if (lane == 0) wi = atomicAdd(counter, 1);
+  wi = __shfl_sync(0xffffffffu, wi, 0);
+  if (wi >= nwork) break;
+  const int64_t g = work[2 * (int64_t)wi];
+  const int c = work[2 * (int64_t)wi + 1];
+  const int nch = ginfo[3 * g];
   const int64_t s0 = gstart[g], s1 = gstart[g + 1];
   const int32_t u = users[s0];
-  const int64_t a = indptr[u], e = indptr[u + 1];
+  const int64_t ra = indptr[u], re = indptr[u + 1];
+  const int64_t a = nch > 1 ? ra + (int64_t)c * chunk : ra;
+  const int64_t e = nch > 1 ? min64(re, a + chunk) : re;
   double P[MAXR], S[MAXR];
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
@@ -143,7 +152,42 @@ __global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ng
       }
     }
   }
-  const int64_t deg = e - a;
+  if (nch > 1) {
+    const int64_t slot0 = ginfo[3 * g + 1];
+    const int64_t pw = 2 * (int64_t)k + 1;
+    double* mine = part + (slot0 + c) * pw;
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int idx = lane + 32 * t;
+      if (idx < k) {
+        mine[idx] = P[t];
+        mine[k + idx] = S[t];
+      }
+    }
+    if (lane == 0) mine[2 * k] = vsum;
+    __threadfence();
+    int prev = 0;
+    if (lane == 0) prev = atomicAdd(done + ginfo[3 * g + 2], 1);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != nch - 1) continue;  // not the last chunk of this user
+    __threadfence();
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
+    vsum = 0.0;
+    for (int q = 0; q < nch; ++q) {
+      const double* ps = part + (slot0 + q) * pw;
+#pragma unroll
+      for (int t = 0; t < MAXR; ++t) {
+        const int idx = lane + 32 * t;
+        if (idx < k) {
+          P[t] += __ldcg(ps + idx);
+          S[t] += __ldcg(ps + k + idx);
+        }
+      }
+      vsum += __ldcg(ps + 2 * k);
+    }
+  }
+  const int64_t deg = re - ra;
   const double mean = deg > 0 ? vsum / (double)deg : gmean;
   const double fb_val = fmin(fmax(mean, lo), hi);
   for (int64_t sidx = s0; sidx < s1; ++sidx) {
@@ -236,7 +280,8 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
                                  int64_t ldn,
                                  const double* d_norm, double global_mean, double rating_min, double rating_max,
                                  const int32_t* d_item_rank, const int32_t* d_hot_items, int32_t nhot_avail,
-                                 const int32_t* d_group_order, int32_t* d_counter,
+                                 int64_t nwork, const int32_t* d_work, const int32_t* d_ginfo, int32_t chunk,
+                                 int32_t* d_done, int64_t ndone, double* d_partial, int32_t* d_counter,
                                  double* d_value, double* d_raw, uint8_t* d_fallback, void* stream) {
   SVDREC_ARG(ngroups >= 0 && k >= 1 && ldn >= k, "cf_predict: bad arguments");
   if (k > 1024) {
@@ -244,8 +289,9 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
     return SVDREC_E_UNSUPPORTED;
   }
   if (ngroups == 0) return 0;
-  SVDREC_ARG(d_counter != nullptr, "cf_predict: d_counter (one device int) is required");
+  SVDREC_ARG(d_counter && d_work && d_ginfo && nwork >= ngroups, "cf_predict: work plan required");
   SVDREC_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), as_stream(stream)));
+  if (ndone > 0) SVDREC_CUDA(cudaMemsetAsync(d_done, 0, (size_t)ndone * sizeof(int32_t), as_stream(stream)));
   cudaStream_t s = as_stream(stream);
   const int r = (k + 31) / 32;
   // two 16-warp CTAs per SM (k <= 256) keep enough gathers in flight; each
@@ -270,7 +316,8 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
     }                                                                                                            \
     k_predict<R><<<grid, 512, smem, s>>>(ngroups, d_group_start, d_users, d_items, d_indptr, d_indices,         \
                                          d_values, k, d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min,         \
-                                         rating_max, d_item_rank, d_hot_items, nhot, d_group_order, d_counter,    \
+                                         rating_max, d_item_rank, d_hot_items, nhot, nwork, d_work, d_ginfo, chunk, \
+                                         d_done, d_partial, d_counter,                                            \
                                          d_value, d_raw, d_fallback);                                             \
   } while (0)
   if (r <= 1)

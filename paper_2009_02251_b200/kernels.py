@@ -282,8 +282,9 @@ def inv_sqrt(G: torch.Tensor, status: torch.Tensor, iters: torch.Tensor | None =
 
 
 def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Yn: torch.Tensor,
-               Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float,
-               order: torch.Tensor | None = None, counter: torch.Tensor | None = None):
+               Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float, plan):
+    """Alg. 4 over user-grouped samples.  ``plan`` is a cf.WorkPlan (work
+    items, per-group chunk info, completion counters, counter)."""
     ldn = _mat(Yn, "cf.Yn")
     if _mat(Xn, "cf.Xn") != ldn or Xn.shape != Yn.shape:
         raise ValueError("cf_predict: Xn and Yn must share shape and leading dimension")
@@ -296,9 +297,9 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
         rank = getattr(csr, "item_rank", None)
         call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
              ptr(csr.indices), ptr(csr.values), Yn.shape[1], ptr(Yn), ptr(Xn), ldn, ptr(norm), float(gmean),
-             float(lo), float(hi), ptr(rank), ptr(hot), 0 if hot is None else hot.numel(), ptr(order),
-             ptr(counter if counter is not None else torch.empty(1, dtype=torch.int32, device=Yn.device)),
-             ptr(val), ptr(raw), ptr(fb), stream_handle())
+             float(lo), float(hi), ptr(rank), ptr(hot), 0 if hot is None else hot.numel(), plan.nwork,
+             ptr(plan.work), ptr(plan.ginfo), plan.chunk, ptr(plan.done), plan.ndone,
+             ptr(plan.partial(Yn.shape[1])), ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
     return val, raw, fb
 
 
