@@ -252,6 +252,7 @@ def run_b200(args):
         "scaling": "strong" if ws == 1 else "replicas", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(cfg, tr),
         "k": int(f.k), "blocks": nb, "test_mae": mae, "test_rmse": rmse, "val_mae": min(e.mae for e in trace),
+        "step_times_s": [round(t, 6) for t in times],
         "roofline": {"kernel": "svdrec_spmm (k_spmm<2>)", "bound": "hbm",
                      "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,

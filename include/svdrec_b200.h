@@ -132,6 +132,16 @@ size_t svdrec_tsqr_workspace_bytes(int64_t r, int32_t b);
 int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q,
                 int64_t ldq, double* d_R, void* d_work, size_t work_bytes, void* stream);
 
+/* Orthonormal basis without R, as the QB engines use it (rsvd.py:136-142,
+ * 186-193): CholeskyQR2 (two passes of Gram + Cholesky + triangular apply,
+ * same Q up to column signs as Householder) with a device-side check --
+ * non-positive pivot or kappa > 1e6 -- that gates a Householder TSQR of the
+ * untouched input launched behind it.  No host round trip; Q may alias A.
+ * b <= 64 takes the fast path, 64 < b <= 80 goes to TSQR directly. */
+size_t svdrec_orth_workspace_bytes(int64_t r, int32_t b);
+int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
+                void* d_work, size_t work_bytes, void* stream);
+
 /* ---------------------------------------------------------------------
  * lu_lower_basis (linalg.py:84-97): partial-pivoting LU of the tall
  * r x b block, in place, returning P.L (original row order, unit

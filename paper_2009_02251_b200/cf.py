@@ -33,6 +33,14 @@ F64 = torch.float64
 # Score block l on a side stream while block l+1 is factored (SVDREC_PIPELINE=1).
 # Off by default: measured slower on B200 (the two streams thrash L2).
 PIPELINE = os.environ.get("SVDREC_PIPELINE", "0") == "1"
+_SIDE: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    s = _SIDE.get(dev.index)
+    if s is None:
+        s = _SIDE[dev.index] = torch.cuda.Stream(device=dev)
+    return s
 
 
 class Prediction(NamedTuple):
@@ -342,7 +350,10 @@ class ValidationMae:
         self._Gsrc = None
         self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1), iters=("u4", 1))
         self._gmean = d.global_mean
-        self._stream = torch.cuda.Stream(device=dev)
+        # scoring stream: the caller's unless pipelining; one cached side
+        # stream per device (a fresh stream per call would defeat the caching
+        # allocator, whose free blocks are tied to the stream they served)
+        self._stream = _side_stream(dev) if PIPELINE else torch.cuda.current_stream(dev)
 
     @property
     def validation(self):

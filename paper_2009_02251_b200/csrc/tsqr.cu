@@ -80,7 +80,9 @@ __device__ __forceinline__ void chunk_range(int64_t rows, int64_t nc, int64_t c,
 // Householder QR of one chunk.  M is column-major in smem: M[col*ldm + row].
 __global__ void __launch_bounds__(kThreads) k_factor(int64_t rows, int64_t nc, int b, const double* __restrict__ in,
                                                      int64_t ldin, double* __restrict__ vout,
-                                                     double* __restrict__ tau, double* __restrict__ rout) {
+                                                     double* __restrict__ tau, double* __restrict__ rout,
+                                                     const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;  // CholeskyQR2 succeeded: fallback not needed
   extern __shared__ double sm[];
   __shared__ double dots[128];
   __shared__ double wv[128];
@@ -159,7 +161,8 @@ __global__ void __launch_bounds__(kThreads) k_factor(int64_t rows, int64_t nc, i
 __global__ void __launch_bounds__(kThreads) k_buildq(int64_t rows, int64_t nc, int b, const double* __restrict__ vin,
                                                      const double* __restrict__ tau,
                                                      const double* __restrict__ qcoarse, double* __restrict__ qout,
-                                                     int64_t ldq) {
+                                                     int64_t ldq, const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ double sm[];
   __shared__ double wv[128];
   const int64_t c = blockIdx.x;
@@ -215,16 +218,13 @@ extern "C" size_t svdrec_tsqr_workspace_bytes(int64_t r, int32_t b) {
   return make_plan(r, b).total + 256;
 }
 
-extern "C" int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
-                           double* d_R, void* d_work, size_t work_bytes, void* stream) {
-  SVDREC_ARG(b >= 1 && b <= 80, "tsqr: block width %d outside [1, 80]", b);
-  SVDREC_ARG(r >= b, "tsqr: needs rows >= cols (%lld < %d)", (long long)r, b);
-  SVDREC_ARG(lda >= b && ldq >= b, "tsqr: bad leading dimension");
-  const Plan p = make_plan(r, b);
-  if (work_bytes < p.total) {
-    set_error("tsqr: workspace %zu < %zu", work_bytes, p.total);
-    return SVDREC_E_WORKSPACE;
-  }
+namespace svdrec {
+namespace {
+
+// TSQR launch sequence; with ``gate`` non-null every kernel returns at once
+// unless *gate != 0 (the CholeskyQR2 fast path flagged itself unreliable).
+int run_tsqr(const Plan& p, int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
+             double* d_R, char* w, const uint32_t* gate, cudaStream_t s) {
   static bool attr_set = false;
   const size_t smem_f = (size_t)b * ((p.rcmax + 1) | 1) * 8;
   const size_t smem_q = 2 * smem_f;
@@ -233,8 +233,6 @@ extern "C" int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda,
     SVDREC_CUDA(cudaFuncSetAttribute(k_buildq, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
     attr_set = true;
   }
-  cudaStream_t s = as_stream(stream);
-  char* w = static_cast<char*>(d_work);
   const int nl = (int)p.lv.size();
   const double* in = d_A;
   int64_t ldin = lda;
@@ -243,7 +241,7 @@ extern "C" int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda,
     double* rout = (l == nl - 1) ? d_R : reinterpret_cast<double*>(w + L.off_next);
     k_factor<<<(unsigned)L.nc, kThreads, smem_f, s>>>(L.rows, L.nc, b, in, ldin,
                                                       reinterpret_cast<double*>(w + L.off_v),
-                                                      reinterpret_cast<double*>(w + L.off_tau), rout);
+                                                      reinterpret_cast<double*>(w + L.off_tau), rout, gate);
     int rc = check_launch("tsqr_factor");
     if (rc) return rc;
     in = rout;
@@ -255,10 +253,219 @@ extern "C" int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda,
     double* qo = l == 0 ? d_Q : reinterpret_cast<double*>(w + L.off_q);
     const int64_t ldo = l == 0 ? ldq : b;
     k_buildq<<<(unsigned)L.nc, kThreads, smem_q, s>>>(L.rows, L.nc, b, reinterpret_cast<double*>(w + L.off_v),
-                                                      reinterpret_cast<double*>(w + L.off_tau), coarse, qo, ldo);
+                                                      reinterpret_cast<double*>(w + L.off_tau), coarse, qo, ldo,
+                                                      gate);
     int rc = check_launch("tsqr_buildq");
     if (rc) return rc;
     coarse = qo;
   }
   return 0;
+}
+
+// ---- CholeskyQR2 fast path -------------------------------------------------
+// G = Y.T Y over a row range per CTA (upper triangle pairs), fixed-order sum.
+constexpr int kGramRows = 32;
+
+__global__ void __launch_bounds__(256) k_gram_part(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
+                                                   int64_t rows_per, double* __restrict__ part) {
+  __shared__ double ys[kGramRows][65];
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min64(r, r0 + rows_per);
+  const int npairs = b * (b + 1) / 2;
+  double acc[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+  for (int64_t base = r0; base < r1; base += kGramRows) {
+    for (int t = threadIdx.x; t < kGramRows * b; t += blockDim.x) {
+      const int rr = t / b, c = t - rr * b;
+      const int64_t gr = base + rr;
+      ys[rr][c] = gr < r1 ? Y[gr * ldy + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+      const int pidx = threadIdx.x + q * 256;
+      if (pidx < npairs) {
+        // pair index -> (i, j), i <= j, row-major upper triangle
+        int i = (int)((2 * b + 1 - sqrt((double)(2 * b + 1) * (2 * b + 1) - 8.0 * pidx)) / 2);
+        while (i > 0 && i * b - i * (i - 1) / 2 > pidx) --i;
+        while ((i + 1) * b - (i + 1) * i / 2 <= pidx) ++i;
+        const int j = i + (pidx - (i * b - i * (i - 1) / 2));
+        double a = acc[q];
+        for (int rr = 0; rr < kGramRows; ++rr) a = fma(ys[rr][i], ys[rr][j], a);
+        acc[q] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+    const int pidx = threadIdx.x + q * 256;
+    if (pidx < npairs) part[(int64_t)blockIdx.x * npairs + pidx] = acc[q];
+  }
+}
+
+// Sum the partial Grams in order, Cholesky G = R.T R (upper R), invert R.
+// flag |= 1 when a pivot is non-positive or (min R_jj / max R_jj)^2 < 1e-12
+// (kappa(Y) > 1e6: CholeskyQR2 would not reach working-precision
+// orthogonality), in which case the TSQR fallback runs.
+__global__ void __launch_bounds__(256) k_chol_inv(int b, int nparts, const double* __restrict__ part,
+                                                  double* __restrict__ Rinv, uint32_t* __restrict__ flag) {
+  __shared__ double G[64][65];
+
+  __shared__ int bad;
+  const int npairs = b * (b + 1) / 2;
+  if (threadIdx.x == 0) bad = 0;
+  for (int pidx = threadIdx.x; pidx < npairs; pidx += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nparts; ++k) s += part[(int64_t)k * npairs + pidx];
+    int i = 0, off = 0;
+    while (off + (b - i) <= pidx) {
+      off += b - i;
+      ++i;
+    }
+    const int j = i + (pidx - off);
+    G[i][j] = s;
+    G[j][i] = s;
+  }
+  __syncthreads();
+  double dmax = 0.0, dmin = 1e300;
+  for (int j = 0; j < b; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = G[j][j];
+      if (!(d > 0.0)) bad = 1;
+      G[j][j] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    const double rjj = G[j][j];
+    for (int c = j + 1 + threadIdx.x; c < b; c += blockDim.x) G[j][c] /= rjj;
+    __syncthreads();
+    const int nt = b - j - 1;
+    for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+      const int c1 = j + 1 + t / nt, c2 = j + 1 + t % nt;
+      if (c2 >= c1) G[c1][c2] -= G[j][c1] * G[j][c2];
+    }
+    __syncthreads();
+    dmax = fmax(dmax, rjj);
+    dmin = fmin(dmin, rjj);
+  }
+  if (threadIdx.x == 0 && (bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
+  // Rinv: column c solves R x = e_c (back substitution), one thread per column
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    for (int i = b - 1; i >= 0; --i) {
+      double x = (i == c) ? 1.0 : 0.0;
+      for (int t = i + 1; t <= c; ++t) x -= G[i][t] * Rinv[t * b + c];
+      Rinv[i * b + c] = (i <= c) ? x / G[i][i] : 0.0;
+    }
+  }
+  __syncthreads();
+
+}
+
+// out = Y @ Rinv (upper triangular); with ``only_if_clear`` the store is
+// skipped when the flag is set (the TSQR fallback owns the output then).
+__global__ void __launch_bounds__(256) k_trapply(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
+                                                 const double* __restrict__ Rinv, double* __restrict__ out,
+                                                 int64_t ldo, const uint32_t* __restrict__ flag, int only_if_clear) {
+  __shared__ double Rs[64 * 64];
+  if (only_if_clear && *flag) return;
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) Rs[t] = Rinv[t];
+  __syncthreads();
+  const int64_t total = r * b;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / b;
+    const int j = (int)(t - i * b);
+    const double* yr = Y + i * ldy;
+    double a = 0.0;
+    for (int q = 0; q <= j; ++q) a = fma(yr[q], Rs[q * b + j], a);
+    out[i * ldo + j] = a;
+  }
+}
+
+struct OrthLayout {
+  size_t off_flag, off_rinv, off_part, off_tmp, off_tsqr, total;
+  int nparts;
+  int64_t rows_per;
+};
+
+OrthLayout orth_layout(int64_t r, int b) {
+  OrthLayout L{};
+  L.nparts = 2 * sm_count();
+  L.rows_per = (r + L.nparts - 1) / L.nparts;
+  if (L.rows_per < kGramRows) {
+    L.rows_per = kGramRows;
+    L.nparts = (int)((r + kGramRows - 1) / kGramRows);
+  }
+  size_t o = 0;
+  L.off_flag = o;
+  o = align_up(o + 16);
+  L.off_rinv = o;
+  o = align_up(o + (size_t)b * b * 8);
+  L.off_part = o;
+  o = align_up(o + (size_t)L.nparts * (b * (b + 1) / 2) * 8);
+  L.off_tmp = o;
+  o = align_up(o + (size_t)r * b * 8);
+  L.off_tsqr = o;
+  o = align_up(o + make_plan(r, b).total);
+  L.total = o;
+  return L;
+}
+
+int cholqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_t ldo, const OrthLayout& L,
+                char* w, int only_if_clear, cudaStream_t s) {
+  double* part = reinterpret_cast<double*>(w + L.off_part);
+  double* rinv = reinterpret_cast<double*>(w + L.off_rinv);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(w + L.off_flag);
+  k_gram_part<<<(unsigned)L.nparts, 256, 0, s>>>(r, b, Y, ldy, L.rows_per, part);
+  k_chol_inv<<<1, 256, 0, s>>>(b, L.nparts, part, rinv, flag);
+  const int64_t grid = min64((r * b + 255) / 256, (int64_t)sm_count() * 8);
+  k_trapply<<<(unsigned)grid, 256, 0, s>>>(r, b, Y, ldy, rinv, out, ldo, flag, only_if_clear);
+  return check_launch("cholqr_pass", 3);
+}
+
+}  // namespace
+}  // namespace svdrec
+
+extern "C" int svdrec_tsqr(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
+                           double* d_R, void* d_work, size_t work_bytes, void* stream) {
+  SVDREC_ARG(b >= 1 && b <= 80, "tsqr: block width %d outside [1, 80]", b);
+  SVDREC_ARG(r >= b, "tsqr: needs rows >= cols (%lld < %d)", (long long)r, b);
+  SVDREC_ARG(lda >= b && ldq >= b, "tsqr: bad leading dimension");
+  const Plan p = make_plan(r, b);
+  if (work_bytes < p.total) {
+    set_error("tsqr: workspace %zu < %zu", work_bytes, p.total);
+    return SVDREC_E_WORKSPACE;
+  }
+  return run_tsqr(p, r, b, d_A, lda, d_Q, ldq, d_R, static_cast<char*>(d_work), nullptr, as_stream(stream));
+}
+
+extern "C" size_t svdrec_orth_workspace_bytes(int64_t r, int32_t b) {
+  if (b < 1 || b > 80 || r < b) return 256;
+  return orth_layout(r, b).total + 256;
+}
+
+extern "C" int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
+                           void* d_work, size_t work_bytes, void* stream) {
+  SVDREC_ARG(b >= 1 && b <= 80, "orth: block width %d outside [1, 80]", b);
+  SVDREC_ARG(r >= b, "orth: needs rows >= cols (%lld < %d)", (long long)r, b);
+  SVDREC_ARG(lda >= b && ldq >= b, "orth: bad leading dimension");
+  const OrthLayout L = orth_layout(r, b);
+  if (work_bytes < L.total) {
+    set_error("orth: workspace %zu < %zu", work_bytes, L.total);
+    return SVDREC_E_WORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  char* w = static_cast<char*>(d_work);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(w + L.off_flag);
+  double* tmp = reinterpret_cast<double*>(w + L.off_tmp);
+  if (b > 64)  // CholeskyQR2 tiles hold b <= 64: Householder directly
+    return run_tsqr(make_plan(r, b), r, b, d_A, lda, d_Q, ldq, reinterpret_cast<double*>(w + L.off_rinv),
+                    w + L.off_tsqr, nullptr, s);
+  SVDREC_CUDA(cudaMemsetAsync(flag, 0, 16, s));
+  int rc = cholqr_pass(r, b, d_A, lda, tmp, b, L, w, 0, s);  // Q1 = A R1^-1
+  if (rc) return rc;
+  rc = cholqr_pass(r, b, tmp, b, d_Q, ldq, L, w, 1, s);  // Q = Q1 R2^-1 (if both passes are sound)
+  if (rc) return rc;
+  // fallback: Householder TSQR from the untouched input, only if flagged
+  double* dummy_r = reinterpret_cast<double*>(w + L.off_rinv);
+  return run_tsqr(make_plan(r, b), r, b, d_A, lda, d_Q, ldq, dummy_r, w + L.off_tsqr, flag, s);
 }

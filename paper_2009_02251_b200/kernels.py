@@ -207,6 +207,19 @@ def tsqr(A: torch.Tensor, Q: torch.Tensor | None = None, R: torch.Tensor | None 
     return Q, R
 
 
+def orth(A: torch.Tensor, Q: torch.Tensor | None = None) -> torch.Tensor:
+    """Orthonormal basis (CholeskyQR2 with in-device TSQR fallback); Q may alias A."""
+    lda = _mat(A, "orth.A")
+    r, b = A.shape
+    if Q is None:
+        Q = torch.empty(r, b, dtype=F64, device=A.device)
+    ldq = _mat(Q, "orth.Q")
+    ws, nb = scratch(A.device).get(query("svdrec_orth_workspace_bytes", r, b))
+    with _span("orth", 2 * r * b * 8):
+        call("svdrec_orth", r, b, ptr(A), lda, ptr(Q), ldq, ws, nb, stream_handle())
+    return Q
+
+
 def lu_lower(A: torch.Tensor, status: torch.Tensor, udiag: torch.Tensor | None = None) -> torch.Tensor:
     """In-place P.L of partial-pivoting LU; returns U's diagonal (device)."""
     lda = _mat(A, "lu.A")

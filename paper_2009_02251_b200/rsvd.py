@@ -224,7 +224,7 @@ class _QbEngine:
         K.lu_lower(Y, self.status)
 
     def orth_into(self, Y, dst):
-        K.tsqr(Y, dst)
+        K.orth(Y, dst)
 
     def append(self, src):
         """Re-orthogonalise ``src`` against Q, append it and B_l = q.T A."""

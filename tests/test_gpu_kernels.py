@@ -144,3 +144,31 @@ def test_fro_norm_exact_on_grid(gpu):
     dense, M = inputs.rand_sparse(30, 50, 0.15, seed=13)
     assert P.fro_norm_sq(P.SparseRatings(M, 0.5, 5.0)) == float(np.sum(dense * dense))
     assert P.fro_norm_sq(dense) == float(np.sum(dense * dense))
+
+
+def test_orth_cholqr2_and_fallback(gpu):
+    """svdrec_orth: CholeskyQR2 on well-conditioned input, TSQR fallback on
+    ill-conditioned / rank-deficient input -- orthonormal either way, and the
+    same columns (up to sign) as Householder QR."""
+    import torch
+    from paper_2009_02251_b200 import kernels as K
+    rng = np.random.default_rng(11)
+    cases = []
+    M = rng.standard_normal((138493, 20))
+    cases.append(M)
+    U = np.linalg.qr(rng.standard_normal((5000, 16)))[0]
+    cases.append(U * np.geomspace(1, 1e-9, 16))  # kappa 1e9 -> fallback
+    base = rng.standard_normal((3000, 4))
+    cases.append(np.hstack([base, base[:, :2], np.zeros((3000, 2))]))  # rank deficient -> fallback
+    cases.append(rng.standard_normal((70, 64)))
+    for M in cases:
+        Md = torch.from_numpy(M).cuda()
+        Q = K.orth(Md.clone()).cpu().numpy()
+        b = M.shape[1]
+        assert np.linalg.norm(Q.T @ Q - np.eye(b)) <= 1e-12 * np.sqrt(b)
+        if np.linalg.matrix_rank(M) == b:
+            ref = scipy.linalg.qr(M, mode="economic")[0]
+            np.testing.assert_allclose(np.abs(np.sum(Q * ref, axis=0)), np.ones(b), atol=1e-7)
+        # in place
+        Q2 = K.orth(Md, Md).cpu().numpy()
+        assert np.array_equal(Q2, Q)
