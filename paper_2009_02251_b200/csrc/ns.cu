@@ -7,7 +7,7 @@
 // T = S^(1/2) U.T, and T.T T = B.T (B B.T)^(-1/2) B.  So per block we need
 // Z = G^(-1/2), not an eigendecomposition: with x_l = B[:, l] and
 // y_l = Z x_l, cos(T_l, T_j) = x_j.y_l / (|x_l|_Z |x_j|_Z).  The iteration
-// (A = G / trace(G), Y0 = A, Z0 = I)
+// (A = G / ||G||_F, Y0 = A, Z0 = I)
 //     T = (3 I - Z Y) / 2,   Y <- Y T,   Z <- T Z
 // converges quadratically to Y = A^(1/2), Z = A^(-1/2); every step is
 // k x k GEMM work spread over the whole GPU, with two grid barriers per
@@ -22,7 +22,8 @@ namespace cg = cooperative_groups;
 namespace svdrec {
 namespace {
 
-constexpr int NT = 64;  // output tile
+constexpr int NT = 32;  // output tile (k=240 -> 64 tiles per GEMM phase)
+constexpr int NR = NT / 16;  // outputs per thread per dimension
 constexpr int NK = 16;  // reduction step
 constexpr int kNsThreads = 256;
 
@@ -38,11 +39,11 @@ __device__ double tile_gemm(NsSmem& sm, int k, const double* __restrict__ A, con
                             double* __restrict__ C, int ti, int tj, double alpha, double diag, bool resid) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int r0 = ti * NT, c0 = tj * NT;
-  double acc[4][4];
+  double acc[NR][NR];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < NR; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < NR; ++j) acc[i][j] = 0.0;
   for (int k0 = 0; k0 < k; k0 += NK) {
     for (int e = threadIdx.x; e < NT * NK; e += kNsThreads) {
       const int rr = e / NK, kk = e % NK;
@@ -57,26 +58,26 @@ __device__ double tile_gemm(NsSmem& sm, int k, const double* __restrict__ A, con
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
-      double av[4], bv[4];
+      double av[NR], bv[NR];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = sm.a[ty * 4 + i][kk];
+      for (int i = 0; i < NR; ++i) av[i] = sm.a[ty * NR + i][kk];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = sm.b[kk][tx * 4 + j];
+      for (int j = 0; j < NR; ++j) bv[j] = sm.b[kk][tx * NR + j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < NR; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < NR; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
     __syncthreads();
   }
   double rs = 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gr = r0 + ty * 4 + i;
+  for (int i = 0; i < NR; ++i) {
+    const int gr = r0 + ty * NR + i;
     if (gr >= k) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gc = c0 + tx * 4 + j;
+    for (int j = 0; j < NR; ++j) {
+      const int gc = c0 + tx * NR + j;
       if (gc >= k) continue;
       const double v = alpha * acc[i][j] + (gr == gc ? diag : 0.0);
       C[(int64_t)gr * k + gc] = v;
@@ -101,11 +102,27 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
   __shared__ NsSmem sm;
   const int nt = (k + NT - 1) / NT;
   const int ntiles = nt * nt;
-  // scale: A = G / trace(G) has spectrum in (0, 1]
+  // scale: A = G / ||G||_F has spectrum in (0, 1] and a larger smallest
+  // eigenvalue than G / trace(G) (fewer iterations); trace kept for the
+  // reference's singularity floor
+  const int64_t kk = (int64_t)k * k;
+  {
+    double fs = 0.0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kk; t += (int64_t)gridDim.x * blockDim.x) {
+      const double g = G[(t / k) * ldg + t % k];
+      fs = fma(g, g, fs);
+    }
+    fs = block_sum(fs, sm.red);
+    if (threadIdx.x == 0) part[blockIdx.x] = fs;
+  }
+  grid.sync();
+  double fro2 = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) fro2 += part[b];
   double tr = 0.0;
   for (int i = 0; i < k; ++i) tr += G[(int64_t)i * ldg + i];
-  const double inv_c = tr > 0.0 ? 1.0 / tr : 0.0;
-  const int64_t kk = (int64_t)k * k;
+  const double c_scale = sqrt(fro2);
+  const double inv_c = c_scale > 0.0 ? 1.0 / c_scale : 0.0;
+  grid.sync();  // part[] is reused below
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kk; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / k, j = t % k;
     Y0[t] = G[i * ldg + j] * inv_c;
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     Zn = t2;
   }
   grid.sync();  // every block is done reading part[] before it is reused
-  // G^(-1/2) = A^(-1/2) / sqrt(trace); ||A^(-1/2)||_F^2 = sum 1/mu_i bounds
+  // G^(-1/2) = A^(-1/2) / sqrt(||G||_F); ||A^(-1/2)||_F^2 = sum 1/mu_i bounds
   // the smallest scaled eigenvalue from below (inconclusive -> flag)
   const double s = sqrt(inv_c);
   double fz = 0.0;
@@ -168,9 +185,12 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     double f = 0.0;
     for (int b = 0; b < (int)gridDim.x; ++b) f += part[b];
     if (d_iters) *d_iters = it;
-    // near-singular per the reference (mu_min < 1e-14) is impossible when
-    // 1 / ||A^(-1/2)||_F^2 >= 1e-14; otherwise ask the host for the exact check
-    if (d_status && (!done || !(f * 1e-14 <= 1.0) || !(tr > 0.0))) atomicOr(d_status, SVDREC_STATUS_NS_CHECK);
+    // the reference raises when lambda_min < 1e-14 trace(G); with
+    // mu = lambda / ||G||_F and mu_min >= 1 / ||A^(-1/2)||_F^2 = 1 / f that is
+    // impossible when f * 1e-14 * trace / ||G||_F <= 1; otherwise ask the
+    // host for the exact check
+    if (d_status && (!done || !(f * 1e-14 * tr * inv_c <= 1.0) || !(tr > 0.0)))
+      atomicOr(d_status, SVDREC_STATUS_NS_CHECK);
   }
 }
 
@@ -196,7 +216,7 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
     int per_sm = 0;
     SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, 0));
     max_blocks = per_sm * sm_count();
-    if (max_blocks > 2 * sm_count()) max_blocks = 2 * sm_count();
+    if (max_blocks > 4 * sm_count()) max_blocks = 4 * sm_count();
     if (max_blocks > 4096) max_blocks = 4096;
     if (max_blocks < 1) max_blocks = 1;
   }
