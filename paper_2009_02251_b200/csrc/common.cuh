@@ -49,6 +49,13 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 int sm_count();
 
+// skinny.cu: tall-skinny GEMMs for q <= 32 (see the file header)
+int64_t tn_skinny_slabs(int64_t r, int64_t p);
+int launch_nn_skinny(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C,
+                     int64_t ldc, double beta, double* Y, int64_t ldy, cudaStream_t s);
+int launch_tn_skinny(int64_t r, int64_t p, int q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                     double* part, int64_t nslab, cudaStream_t s);
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

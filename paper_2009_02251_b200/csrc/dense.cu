@@ -241,7 +241,12 @@ using namespace svdrec;
 extern "C" size_t svdrec_gemm_tn_workspace_bytes(int64_t r, int64_t p, int64_t q) {
   // fewest possible tiles -> most splits: an upper bound for any call
   const int64_t tiles = ((p + TP - 1) / TP) * ((q + 63) / 64);
-  return align_up((size_t)tn_splits(r, tiles) * (size_t)p * (size_t)q * 8 + 256) + 4096;
+  size_t b = (size_t)tn_splits(r, tiles) * (size_t)p * (size_t)q * 8;
+  if (q <= 32) {
+    const size_t bs = (size_t)tn_skinny_slabs(r, p) * (size_t)p * (size_t)q * 8;
+    if (bs > b) b = bs;
+  }
+  return align_up(b + 256) + 4096;
 }
 
 extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, const double* d_X, int64_t ldx,
@@ -250,6 +255,20 @@ extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, con
   SVDREC_ARG(r >= 0 && p >= 0 && q >= 0 && ldx >= p && ldy >= q && ldc >= q, "gemm_tn: bad arguments");
   if (p == 0 || q == 0) return 0;
   cudaStream_t s = as_stream(stream);
+  if (q <= 32 && r > 0) {  // tall-skinny path: stream X once, slab partials
+    const int64_t ns = tn_skinny_slabs(r, p);
+    const size_t need = (size_t)ns * (size_t)p * (size_t)q * 8;
+    if (need > work_bytes) {
+      set_error("gemm_tn: workspace %zu < %zu", work_bytes, need);
+      return SVDREC_E_WORKSPACE;
+    }
+    double* part = static_cast<double*>(d_work);
+    int rc = launch_tn_skinny(r, p, (int)q, d_X, ldx, d_Y, ldy, part, ns, s);
+    if (rc) return rc;
+    const int64_t tot = p * q;
+    k_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(p, q, ns, part, alpha, beta, d_C, ldc);
+    return check_launch("gemm_tn_reduce");
+  }
   const bool narrow = q <= 32;
   const int64_t TQ = narrow ? 32 : 64;
   const int64_t gp = (p + TP - 1) / TP, gq = (q + TQ - 1) / TQ;
@@ -279,6 +298,7 @@ extern "C" int svdrec_gemm_nn(int64_t r, int64_t p, int64_t q, double alpha, con
   SVDREC_ARG(r >= 0 && p >= 0 && q >= 0 && ldx >= p && ldc >= q && ldy >= q, "gemm_nn: bad arguments");
   if (r == 0 || q == 0) return 0;
   cudaStream_t s = as_stream(stream);
+  if (q <= 32 && p > 0) return launch_nn_skinny(r, p, (int)q, alpha, d_X, ldx, d_C, ldc, beta, d_Y, ldy, s);
   const bool narrow = q <= 32;
   const int64_t TQ = narrow ? 32 : 64;
   dim3 grid((unsigned)((r + TP - 1) / TP), (unsigned)((q + TQ - 1) / TQ));
