@@ -12,7 +12,13 @@
 // item rows) plus one k-dot pair per held-out sample, instead of
 // deg(u) * k per sample.  One warp owns one user's group of samples and
 // keeps P_u, S_u in registers (k <= 1024).
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace svdrec {
 namespace {
@@ -76,12 +82,23 @@ __global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ng
                                                     uint8_t* __restrict__ out_fb) {
   // hot items (highest training degree) keep their unit rows in shared
   // memory: under Zipf popularity they carry most of the gathers
+  // With a thread-block cluster the hot set is spread over the cluster's
+  // distributed shared memory: hot item h lives in CTA h % csize at slot
+  // h / csize, so a cluster of 8 stages 8x the rows one SM could hold, and
+  // remote rows are read over DSMEM (bandwidth additive to L2's).  ``nhot``
+  // is the cluster-wide count.
   extern __shared__ double hs[];
-  for (int64_t t = threadIdx.x; t < (int64_t)nhot * k; t += blockDim.x) {
-    const int64_t h = t / k, e = t - h * k;
-    hs[t] = Yn[(int64_t)hot[h] * ldn + e];
+  __shared__ const double* peer[16];
+  cg::cluster_group cl = cg::this_cluster();
+  const int csize = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int nloc = (nhot - crank + csize - 1) / csize;  // slots this CTA holds
+  for (int64_t t = threadIdx.x; t < (int64_t)nloc * k; t += blockDim.x) {
+    const int64_t sl = t / k, e = t - sl * k;
+    hs[t] = Yn[(int64_t)hot[sl * csize + crank] * ldn + e];
   }
-  __syncthreads();
+  if (threadIdx.x < csize) peer[threadIdx.x] = cl.map_shared_rank(hs, threadIdx.x);
+  cl.sync();  // every CTA's slice is staged before anyone reads it
   const int lane = threadIdx.x & 31;
   // Work items are (group, chunk) pairs, heaviest users first.  Users with
   // more than ``chunk`` ratings are split across warps: each chunk leaves
@@ -127,7 +144,8 @@ __global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ng
         const int32_t r = __shfl_sync(0xffffffffu, rk, jj);
         const double v = __shfl_sync(0xffffffffu, vi, jj);
         const bool ok = j + q < nv;
-        rows[q] = (r < nhot) ? hs + (int64_t)r * k : Yn + (int64_t)c * ldn;
+        rows[q] = r >= nhot ? Yn + (int64_t)c * ldn
+                            : (csize == 1 ? hs + (int64_t)r * k : peer[r % csize] + (int64_t)(r / csize) * k);
         vv[q] = ok ? v : 0.0;
         mk[q] = ok ? 1.0 : 0.0;
       }
@@ -217,6 +235,7 @@ __global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ng
     }
   }
   }  // dynamic loop over user groups
+  cl.sync();  // peers may still be reading this CTA's slice
 }
 
 __global__ void k_overlap(int64_t ns, const int32_t* __restrict__ users, const int32_t* __restrict__ items,
@@ -294,31 +313,47 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
   if (ndone > 0) SVDREC_CUDA(cudaMemsetAsync(d_done, 0, (size_t)ndone * sizeof(int32_t), as_stream(stream)));
   cudaStream_t s = as_stream(stream);
   const int r = (k + 31) / 32;
-  // two 16-warp CTAs per SM (k <= 256) keep enough gathers in flight; each
-  // stages ~100 KB of the hottest item rows
-  const int per_sm = r <= 4 ? 2 : 1;
+  // 16-warp CTAs, persistent: two per SM for k <= 128 (more gathers in
+  // flight), else one; each stages the hottest item rows in its shared
+  // memory.  SVDREC_CF_CLUSTER=c (2..8) spreads the hot set over a c-CTA
+  // cluster's distributed shared memory instead -- measured slower on B200
+  // (remote 8-byte reads cost more than the L2 hits they replace: cluster 1 /
+  // 2 / 4 / 8 -> 33.7 / 35.1 / 42.7 / 52.7 ms per bench step), so off.
+  static const int csize_env = getenv("SVDREC_CF_CLUSTER") ? atoi(getenv("SVDREC_CF_CLUSTER")) : 1;
+  int csize = csize_env >= 1 && csize_env <= 8 ? csize_env : 1;
+  const int per_sm = (csize == 1 && r <= 4) ? 2 : 1;
   const size_t kHotBytes = per_sm == 2 ? 100 * 1024 : 200 * 1024;
-  int nhot = d_item_rank && d_hot_items ? (int)(kHotBytes / ((size_t)k * 8)) : 0;
+  int nhot = d_item_rank && d_hot_items ? (int)(kHotBytes / ((size_t)k * 8)) * csize : 0;
   if (nhot > nhot_avail) nhot = nhot_avail;
   if (nhot < 0) nhot = 0;
-  const size_t smem = (size_t)nhot * k * 8;
-  // persistent: one 16-warp CTA per SM, warps stride over user groups
+  const size_t smem = (size_t)((nhot + csize - 1) / csize) * k * 8;
   const int64_t want = (ngroups + 15) / 16;
-  const int64_t slots = (int64_t)per_sm * sm_count();
-  const unsigned grid = (unsigned)(want < slots ? (want > 0 ? want : 1) : slots);
-#define SVDREC_PRED(R)                                                                                           \
-  do {                                                                                                           \
-    static bool attr = false;                                                                                    \
-    if (!attr) {                                                                                                 \
-      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
-                                       210 * 1024));                                                  \
-      attr = true;                                                                                               \
-    }                                                                                                            \
-    k_predict<R><<<grid, 512, smem, s>>>(ngroups, d_group_start, d_users, d_items, d_indptr, d_indices,         \
-                                         d_values, k, d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min,         \
-                                         rating_max, d_item_rank, d_hot_items, nhot, nwork, d_work, d_ginfo, chunk, \
-                                         d_done, d_partial, d_counter,                                            \
-                                         d_value, d_raw, d_fallback);                                             \
+  int64_t grid = (int64_t)(per_sm * sm_count() / csize) * csize;
+  if (want < grid) grid = ((want + csize - 1) / csize) * csize;
+  if (grid < csize) grid = csize;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define SVDREC_PRED(R)                                                                                       \
+  do {                                                                                                       \
+    static bool attr_set = false;                                                                            \
+    if (!attr_set) {                                                                                         \
+      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024)); \
+      attr_set = true;                                                                                       \
+    }                                                                                                        \
+    SVDREC_CUDA(cudaLaunchKernelEx(&cfg, k_predict<R>, ngroups, d_group_start, d_users, d_items, d_indptr,   \
+                                   d_indices, d_values, k, d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min, \
+                                   rating_max, d_item_rank, d_hot_items, nhot, nwork, d_work, d_ginfo, chunk, \
+                                   d_done, d_partial, d_counter, d_value, d_raw, d_fallback));                \
   } while (0)
   if (r <= 1)
     SVDREC_PRED(1);
