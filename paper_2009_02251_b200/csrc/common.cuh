@@ -62,6 +62,17 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Deterministic sum of p[k * stride] for k < n by one warp: lane l takes
+// k = l, l+32, ... in order, then a fixed butterfly (valid in every lane).
+// Replaces one-thread loops over split partials, which serialise n L2 round
+// trips per output.
+__device__ __forceinline__ double warp_strided_sum(const double* __restrict__ p, int64_t n, int64_t stride) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int64_t k = lane; k < n; k += 32) s += p[k * stride];
+  return warp_sum(s);
+}
+
 // Fixed-order block sum (result valid in every thread). ``scratch`` holds
 // blockDim.x/32 doubles.
 __device__ __forceinline__ double block_sum(double v, double* scratch) {

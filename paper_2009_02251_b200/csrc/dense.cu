@@ -79,15 +79,18 @@ __global__ void __launch_bounds__(256) k_gemm_tn(int64_t r, int64_t p, int64_t q
   }
 }
 
+// one warp per output element: the split partials are summed by the lanes
+// (fixed strided subsets + butterfly), not serially by one thread
 __global__ void k_tn_reduce(int64_t p, int64_t q, int64_t nsplit, const double* __restrict__ part, double alpha,
                             double beta, double* __restrict__ C, int64_t ldc) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= p * q) return;
-  double s = 0.0;
-  for (int64_t k = 0; k < nsplit; ++k) s += part[k * p * q + t];
-  const int64_t i = t / q, j = t - i * q;
-  double* c = C + i * ldc + j;
-  *c = beta == 0.0 ? alpha * s : fma(alpha, s, beta * *c);
+  const double s = warp_strided_sum(part + t, nsplit, p * q);
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t i = t / q, j = t - i * q;
+    double* c = C + i * ldc + j;
+    *c = beta == 0.0 ? alpha * s : fma(alpha, s, beta * *c);
+  }
 }
 
 // ---- gemm_nn: Y = alpha X @ C + beta Y -------------------------------------
@@ -177,11 +180,13 @@ __global__ void k_sumsq_final(int64_t q, int64_t nblk, const double* __restrict_
                               double* total) {
   __shared__ double red[256];
   double mine = 0.0;
-  for (int64_t c = threadIdx.x; c < q; c += blockDim.x) {
-    double s = 0.0;
-    for (int64_t k = 0; k < nblk; ++k) s += part[k * q + c];
-    if (colsq) colsq[c] = s;
-    mine += s;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c = warp; c < q; c += nw) {
+    const double s = warp_strided_sum(part + c, nblk, q);
+    if ((threadIdx.x & 31) == 0) {
+      if (colsq) colsq[c] = s;
+      mine += s;
+    }
   }
   const double t = block_sum(mine, red);
   if (threadIdx.x == 0 && total) *total = t;
@@ -208,12 +213,9 @@ __global__ void __launch_bounds__(256) k_err_part(int64_t n, const double* __res
 }
 
 __global__ void k_err_final(int64_t nblk, const double* __restrict__ part, double* out2) {
+  const double a = warp_strided_sum(part, nblk, 2);
+  const double q = warp_strided_sum(part + 1, nblk, 2);
   if (threadIdx.x == 0) {
-    double a = 0.0, q = 0.0;
-    for (int64_t k = 0; k < nblk; ++k) {
-      a += part[2 * k];
-      q += part[2 * k + 1];
-    }
     out2[0] = a;
     out2[1] = q;
   }
@@ -266,7 +268,7 @@ extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, con
     int rc = launch_tn_skinny(r, p, (int)q, d_X, ldx, d_Y, ldy, part, ns, s);
     if (rc) return rc;
     const int64_t tot = p * q;
-    k_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(p, q, ns, part, alpha, beta, d_C, ldc);
+    k_tn_reduce<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, s>>>(p, q, ns, part, alpha, beta, d_C, ldc);
     return check_launch("gemm_tn_reduce");
   }
   const bool narrow = q <= 32;
@@ -288,7 +290,7 @@ extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, con
   int rc = check_launch("gemm_tn");
   if (rc) return rc;
   const int64_t tot = p * q;
-  k_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(p, q, ns, part, alpha, beta, d_C, ldc);
+  k_tn_reduce<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, s>>>(p, q, ns, part, alpha, beta, d_C, ldc);
   return check_launch("gemm_tn_reduce");
 }
 
@@ -365,11 +367,8 @@ __global__ void __launch_bounds__(256) k_vsum_part(int64_t n, const double* __re
   if (threadIdx.x == 0) part[blockIdx.x] = a;
 }
 __global__ void k_vsum_final(int64_t nblk, const double* __restrict__ part, double* out) {
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int64_t k = 0; k < nblk; ++k) a += part[k];
-    *out = a;
-  }
+  const double a = warp_strided_sum(part, nblk, 1);
+  if (threadIdx.x == 0) *out = a;
 }
 }  // namespace
 }  // namespace svdrec

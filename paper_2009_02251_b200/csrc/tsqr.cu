@@ -264,16 +264,35 @@ int run_tsqr(const Plan& p, int64_t r, int32_t b, const double* d_A, int64_t lda
 
 // ---- CholeskyQR2 fast path -------------------------------------------------
 // G = Y.T Y over a row range per CTA (upper triangle pairs), fixed-order sum.
-constexpr int kGramRows = 32;
+constexpr int kGramRows = 64;
+constexpr int kApplyRows = 128;
 
+// G = Y.T Y partial per CTA row slab.  Rows are staged 64 at a time in
+// shared memory; each thread owns up to 12 (i <= j) pairs whose indices are
+// computed once, then accumulates over the slab.
 __global__ void __launch_bounds__(256) k_gram_part(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
                                                    int64_t rows_per, double* __restrict__ part) {
   __shared__ double ys[kGramRows][65];
   const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min64(r, r0 + rows_per);
   const int npairs = b * (b + 1) / 2;
+  int pi[12], pj[12];
   double acc[12];
 #pragma unroll
-  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+  for (int q = 0; q < 12; ++q) {
+    const int pidx = threadIdx.x + q * 256;
+    acc[q] = 0.0;
+    pi[q] = -1;
+    pj[q] = 0;
+    if (pidx < npairs) {
+      int i = 0, off = 0;
+      while (off + (b - i) <= pidx) {
+        off += b - i;
+        ++i;
+      }
+      pi[q] = i;
+      pj[q] = i + (pidx - off);
+    }
+  }
   for (int64_t base = r0; base < r1; base += kGramRows) {
     for (int t = threadIdx.x; t < kGramRows * b; t += blockDim.x) {
       const int rr = t / b, c = t - rr * b;
@@ -283,14 +302,10 @@ __global__ void __launch_bounds__(256) k_gram_part(int64_t r, int b, const doubl
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 12; ++q) {
-      const int pidx = threadIdx.x + q * 256;
-      if (pidx < npairs) {
-        // pair index -> (i, j), i <= j, row-major upper triangle
-        int i = (int)((2 * b + 1 - sqrt((double)(2 * b + 1) * (2 * b + 1) - 8.0 * pidx)) / 2);
-        while (i > 0 && i * b - i * (i - 1) / 2 > pidx) --i;
-        while ((i + 1) * b - (i + 1) * i / 2 <= pidx) ++i;
-        const int j = i + (pidx - (i * b - i * (i - 1) / 2));
+      if (pi[q] >= 0) {
+        const int i = pi[q], j = pj[q];
         double a = acc[q];
+#pragma unroll 8
         for (int rr = 0; rr < kGramRows; ++rr) a = fma(ys[rr][i], ys[rr][j], a);
         acc[q] = a;
       }
@@ -304,28 +319,34 @@ __global__ void __launch_bounds__(256) k_gram_part(int64_t r, int b, const doubl
   }
 }
 
-// Sum the partial Grams in order, Cholesky G = R.T R (upper R), invert R.
+// Fixed-order sum of the per-CTA Gram partials, one warp per pair.
+__global__ void k_pairs_reduce(int npairs, int nparts, const double* __restrict__ part, double* __restrict__ out) {
+  const int t = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (t >= npairs) return;
+  const double s = warp_strided_sum(part + t, nparts, npairs);
+  if ((threadIdx.x & 31) == 0) out[t] = s;
+}
+
+// Cholesky G = R.T R (upper R) of the reduced Gram pairs, then R^-1.
 // flag |= 1 when a pivot is non-positive or (min R_jj / max R_jj)^2 < 1e-12
 // (kappa(Y) > 1e6: CholeskyQR2 would not reach working-precision
-// orthogonality), in which case the TSQR fallback runs.
-__global__ void __launch_bounds__(256) k_chol_inv(int b, int nparts, const double* __restrict__ part,
-                                                  double* __restrict__ Rinv, uint32_t* __restrict__ flag) {
+// orthogonality), in which case the TSQR fallback runs.  R^-1 is built in
+// the lower triangle of the same shared array (column c by thread c).
+__global__ void __launch_bounds__(256) k_chol_inv(int b, const double* __restrict__ pairs, double* __restrict__ Rinv,
+                                                  uint32_t* __restrict__ flag) {
   __shared__ double G[64][65];
-
+  __shared__ double dinv[64];
   __shared__ int bad;
   const int npairs = b * (b + 1) / 2;
   if (threadIdx.x == 0) bad = 0;
   for (int pidx = threadIdx.x; pidx < npairs; pidx += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < nparts; ++k) s += part[(int64_t)k * npairs + pidx];
     int i = 0, off = 0;
     while (off + (b - i) <= pidx) {
       off += b - i;
       ++i;
     }
     const int j = i + (pidx - off);
-    G[i][j] = s;
-    G[j][i] = s;
+    G[i][j] = pairs[pidx];
   }
   __syncthreads();
   double dmax = 0.0, dmin = 1e300;
@@ -334,6 +355,7 @@ __global__ void __launch_bounds__(256) k_chol_inv(int b, int nparts, const doubl
       const double d = G[j][j];
       if (!(d > 0.0)) bad = 1;
       G[j][j] = d > 0.0 ? sqrt(d) : 1.0;
+      dinv[j] = 1.0 / G[j][j];
     }
     __syncthreads();
     const double rjj = G[j][j];
@@ -349,40 +371,61 @@ __global__ void __launch_bounds__(256) k_chol_inv(int b, int nparts, const doubl
     dmin = fmin(dmin, rjj);
   }
   if (threadIdx.x == 0 && (bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
-  // Rinv: column c solves R x = e_c (back substitution), one thread per column
-  for (int c = threadIdx.x; c < b; c += blockDim.x) {
-    for (int i = b - 1; i >= 0; --i) {
-      double x = (i == c) ? 1.0 : 0.0;
-      for (int t = i + 1; t <= c; ++t) x -= G[i][t] * Rinv[t * b + c];
-      Rinv[i * b + c] = (i <= c) ? x / G[i][i] : 0.0;
+  // column c of R^-1: x_c = 1/R_cc, x_i = -(sum_{t=i+1..c} R_it x_t) / R_ii,
+  // stored at G[c][i] (strict lower triangle, row owned by thread c)
+  const int c = threadIdx.x;
+  if (c < b) {
+    for (int i = c - 1; i >= 0; --i) {
+      double x = G[i][c] * dinv[c];
+      for (int t = i + 1; t < c; ++t) x = fma(G[i][t], G[c][t], x);
+      G[c][i] = -x * dinv[i];
     }
   }
   __syncthreads();
-
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+    const int i = t / b, cc = t - i * b;
+    Rinv[t] = i == cc ? dinv[cc] : (i < cc ? G[cc][i] : 0.0);
+  }
 }
 
-// out = Y @ Rinv (upper triangular); with ``only_if_clear`` the store is
-// skipped when the flag is set (the TSQR fallback owns the output then).
-__global__ void __launch_bounds__(256) k_trapply(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
-                                                 const double* __restrict__ Rinv, double* __restrict__ out,
-                                                 int64_t ldo, const uint32_t* __restrict__ flag, int only_if_clear) {
-  __shared__ double Rs[64 * 64];
+// out = Y @ Rinv (upper triangular), one thread per row over a 128-row
+// tile staged (and written back) through shared memory for coalescing;
+// with ``only_if_clear`` nothing is stored when the flag is set (the TSQR
+// fallback owns the output then).
+__global__ void __launch_bounds__(kApplyRows) k_trapply(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
+                                                        const double* __restrict__ Rinv, double* __restrict__ out,
+                                                        int64_t ldo, const uint32_t* __restrict__ flag,
+                                                        int only_if_clear) {
+  extern __shared__ double sm[];
   if (only_if_clear && *flag) return;
+  const int ldp = b | 1;
+  double* Ys = sm;
+  double* Rs = sm + kApplyRows * ldp;
   for (int t = threadIdx.x; t < b * b; t += blockDim.x) Rs[t] = Rinv[t];
+  const int64_t r0 = (int64_t)blockIdx.x * kApplyRows;
+  const int nr = (int)min64(kApplyRows, r - r0);
+  for (int t = threadIdx.x; t < nr * b; t += blockDim.x) {
+    const int rr = t / b, c = t - rr * b;
+    Ys[rr * ldp + c] = Y[(r0 + rr) * ldy + c];
+  }
   __syncthreads();
-  const int64_t total = r * b;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / b;
-    const int j = (int)(t - i * b);
-    const double* yr = Y + i * ldy;
-    double a = 0.0;
-    for (int q = 0; q <= j; ++q) a = fma(yr[q], Rs[q * b + j], a);
-    out[i * ldo + j] = a;
+  if (threadIdx.x < nr) {
+    double* yr = Ys + threadIdx.x * ldp;
+    for (int j = b - 1; j >= 0; --j) {  // descending: in-place overwrite is safe
+      double a = 0.0;
+      for (int q = 0; q <= j; ++q) a = fma(yr[q], Rs[q * b + j], a);
+      yr[j] = a;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nr * b; t += blockDim.x) {
+    const int rr = t / b, c = t - rr * b;
+    out[(r0 + rr) * ldo + c] = Ys[rr * ldp + c];
   }
 }
 
 struct OrthLayout {
-  size_t off_flag, off_rinv, off_part, off_tmp, off_tsqr, total;
+  size_t off_flag, off_rinv, off_red, off_part, off_tmp, off_tsqr, total;
   int nparts;
   int64_t rows_per;
 };
@@ -398,6 +441,8 @@ OrthLayout orth_layout(int64_t r, int b) {
   size_t o = 0;
   L.off_flag = o;
   o = align_up(o + 16);
+  L.off_red = o;
+  o = align_up(o + (size_t)b * (b + 1) / 2 * 8);
   L.off_rinv = o;
   o = align_up(o + (size_t)b * b * 8);
   L.off_part = o;
@@ -416,10 +461,19 @@ int cholqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int
   double* rinv = reinterpret_cast<double*>(w + L.off_rinv);
   uint32_t* flag = reinterpret_cast<uint32_t*>(w + L.off_flag);
   k_gram_part<<<(unsigned)L.nparts, 256, 0, s>>>(r, b, Y, ldy, L.rows_per, part);
-  k_chol_inv<<<1, 256, 0, s>>>(b, L.nparts, part, rinv, flag);
-  const int64_t grid = min64((r * b + 255) / 256, (int64_t)sm_count() * 8);
-  k_trapply<<<(unsigned)grid, 256, 0, s>>>(r, b, Y, ldy, rinv, out, ldo, flag, only_if_clear);
-  return check_launch("cholqr_pass", 3);
+  double* red = reinterpret_cast<double*>(w + L.off_red);
+  const int npairs = b * (b + 1) / 2;
+  k_pairs_reduce<<<(unsigned)((npairs * 32 + 255) / 256), 256, 0, s>>>(npairs, L.nparts, part, red);
+  k_chol_inv<<<1, 256, 0, s>>>(b, red, rinv, flag);
+  const size_t smem = ((size_t)kApplyRows * (b | 1) + (size_t)b * b) * 8;
+  static bool attr = false;
+  if (!attr) {
+    SVDREC_CUDA(cudaFuncSetAttribute(k_trapply, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    attr = true;
+  }
+  k_trapply<<<(unsigned)((r + kApplyRows - 1) / kApplyRows), kApplyRows, smem, s>>>(r, b, Y, ldy, rinv, out, ldo,
+                                                                                     flag, only_if_clear);
+  return check_launch("cholqr_pass", 4);
 }
 
 }  // namespace
