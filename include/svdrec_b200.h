@@ -82,14 +82,20 @@ int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_pos,
  *   seg_slot                  : -1 = segment covers its whole row (direct
  *                               store), else partial slot index
  *   long_row/long_slot0/long_slot1: nlong split rows and their slot range
+ *   x_rows                    : rows of X (= columns of A)
+ *   nwarp/warp_seg            : optional balanced schedule (nwarp = 0:
+ *                               none): warp w owns segments
+ *                               [warp_seg[w], warp_seg[w+1]) -- contiguous,
+ *                               ~equal nonzeros (svdrec_spmm_warp_plan)
  *   d_partial                 : (nslots x b) scratch
  * ------------------------------------------------------------------- */
 int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
                 const int64_t* d_seg_end, const int32_t* d_seg_slot,
                 const int32_t* d_indices, const double* d_values,
-                const double* d_X, int64_t ldx, double* d_Y, int64_t ldy, int32_t b,
-                int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
-                const int32_t* d_long_slot1, double* d_partial, void* stream);
+                const double* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
+                int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
+                const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
+                double* d_partial, void* stream);
 
 /* ---------------------------------------------------------------------
  * Dense tall-skinny contractions (the deflation products of

@@ -15,6 +15,10 @@
 // than the plan's segment cap (power-law items) are split; their partial
 // sums land in a scratch slot and a fix-up kernel adds them in slot order,
 // so the result is bitwise deterministic.
+#include <cuda.h>
+
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace svdrec {
@@ -117,6 +121,306 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t nseg, const int32_t* __res
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined variant (b even, b <= 32, 16-B aligned operands).  Each warp
+// owns a contiguous, nonzero-balanced range of segments (host plan
+// ``warp_seg``; segment metadata read 32 at a time) and streams it in chunks
+// of 32 nonzeros through a ring of S = 2 shared-memory stages: while chunk c
+// is accumulated, the X rows of chunk c+1 are in flight and the CSR of chunk
+// c+2 is loading (evict-first, so the 216-MB CSR stream does not push X out
+// of L2).  Summation order per output is the same as k_spmm: lane group g
+// of G = 32/P takes nonzeros g, g+G, ... of each 32-chunk, groups folded in
+// order.  Measured on the c3 bench (ms per step, 48 calls): k_spmm 25.4,
+// cp.async (LDGSTS) staging 20.1 (L1 data pipe 90% busy: the rows crossed
+// it twice), this kernel 16.8.
+constexpr int kPipeWarps = 8;
+
+// Rows are fetched with the sm_100 tensor-memory-accelerator gather
+// (cp.async.bulk.tensor.2d ... tile::gather4: four X rows of b doubles per
+// instruction, lanes 0..7 each issue one per chunk) completing on one
+// mbarrier per stage, so the gathered bytes cross the L1 data pipe once
+// (the consumer's LDS).  Padding rows use coordinate -1: TMA zero-fills
+// out-of-bounds rows and still counts their bytes.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int col, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <int P>
+struct TmaGeom {
+  static constexpr int B = 2 * P;
+  static constexpr int G4 = (4 * B * 8 + 127) / 128 * 16;  // doubles per gather4 block (128-B aligned)
+  static constexpr int ROWS = 8 * G4;                       // 32 rows
+  static constexpr int STG = ROWS + 48;                     // + 32 values + 16 (meta, pad to 128 B)
+};
+
+template <int P, int S>
+__global__ void __launch_bounds__(kPipeWarps * 32, 2) k_spmm_tma(
+    const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_seg,
+    const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
+    const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ indices, const double* __restrict__ values,
+    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial) {
+  using Gm = TmaGeom<P>;
+  constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWS, STG = Gm::STG;
+  extern __shared__ __align__(128) double smd[];
+  __shared__ __align__(8) uint64_t bars[kPipeWarps * S];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double* ring = smd + (size_t)wib * S * STG;
+  uint64_t* bar = bars + wib * S;
+  if (lane < S) mbar_init(bar + lane, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  if (w >= nwarp) return;
+  const int g = lane / P, pc = lane - (lane / P) * P;
+  const bool active = g < G;
+
+  const int32_t s_lo = warp_seg[w], s_hi = warp_seg[w + 1];
+  int32_t sb = s_lo;
+  int64_t mb = 0, me = 0;
+  int32_t mrow = 0, mslot = -1;
+  auto load_meta = [&]() {
+    const int32_t sg = sb + lane;
+    if (sg < s_hi) {
+      mb = seg_begin[sg];
+      me = seg_end[sg];
+      mrow = seg_row[sg];
+      mslot = seg_slot[sg];
+    }
+  };
+  load_meta();
+  int32_t cur = s_lo;
+  int64_t cb = 0, ce = 0;
+  int32_t crow = 0, cslot = -1;
+  bool cfirst = true;
+  auto enter = [&]() {
+    if (cur - sb >= 32) {
+      sb = cur;
+      load_meta();
+    }
+    const int i = cur - sb;
+    cb = __shfl_sync(0xffffffffu, mb, i);
+    ce = __shfl_sync(0xffffffffu, me, i);
+    crow = __shfl_sync(0xffffffffu, mrow, i);
+    cslot = __shfl_sync(0xffffffffu, mslot, i);
+    cfirst = true;
+  };
+  if (cur < s_hi) enter();
+
+  bool have = false;
+  int32_t kci = -1;
+  double kvi = 0.0;
+  int4 km;
+  auto load_chunk = [&]() {
+    have = cur < s_hi;
+    if (!have) return;
+    const int nv = (int)min64(32, ce - cb);
+    kci = -1;
+    kvi = 0.0;
+    if (lane < nv) {
+      kci = __ldcs(indices + cb + lane);
+      kvi = __ldcs(values + cb + lane);
+    }
+    const bool last = cb + 32 >= ce;
+    km = make_int4(crow, cslot, nv, (cfirst ? 1 : 0) | (last ? 2 : 0));
+    cfirst = false;
+    cb += 32;
+    if (last) {
+      ++cur;
+      if (cur < s_hi) enter();
+    }
+  };
+  auto issue = [&](int slot) {
+    double* st = ring + slot * STG;
+    st[ROWS + lane] = kvi;
+    if (lane == 0) *reinterpret_cast<int4*>(st + ROWS + 32) = km;
+    const int ng = (km.z + 3) >> 2;
+    const int t = lane & 7;
+    const int r0 = __shfl_sync(0xffffffffu, kci, 4 * t);
+    const int r1 = __shfl_sync(0xffffffffu, kci, 4 * t + 1);
+    const int r2 = __shfl_sync(0xffffffffu, kci, 4 * t + 2);
+    const int r3 = __shfl_sync(0xffffffffu, kci, 4 * t + 3);
+    if (ng > 0) {
+      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)(ng * 4 * B * 8));
+      __syncwarp();
+      if (lane < ng) tma_gather4(st + lane * G4, &tmX, 0, r0, r1, r2, r3, bar + slot);
+    } else if (lane == 0) {
+      mbar_expect_tx(bar + slot, 0);  // empty segment: complete the phase
+    }
+  };
+
+  double2 acc = make_double2(0.0, 0.0);
+  int64_t issued = 0, consumed = 0;
+  load_chunk();
+#pragma unroll
+  for (int t = 0; t < S - 1; ++t) {
+    if (have) {
+      issue((int)(issued % S));
+      ++issued;
+      load_chunk();
+    }
+  }
+  while (consumed < issued) {
+    if (have) {
+      issue((int)(issued % S));
+      ++issued;
+      load_chunk();
+    }
+    const int slot = (int)(consumed % S);
+    mbar_wait(bar + slot, (unsigned)((consumed / S) & 1));
+    __syncwarp();
+    const double* st = ring + slot * STG;
+    const int4 m = *reinterpret_cast<const int4*>(st + ROWS + 32);
+    if (m.w & 1) acc = make_double2(0.0, 0.0);
+    if (active) {
+      // fully unrolled over the chunk's NS steps: unconditional loads at
+      // constant smem offsets from one per-lane base (all in flight at
+      // once; rows past the chunk are stale but in-bounds), FMAs masked
+      constexpr int NS = (32 + G - 1) / G;
+      const double* xr = st + ((g >> 2) * G4 + (g & 3) * B) + 2 * pc;
+      const double* vr = st + ROWS + g;
+      double2 xs[NS];
+      double vs[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        const int j = q * G + g;
+        const int jo = q * G;
+        const int jc = j < 32 ? j : 31;
+        xs[q] = G4 == 4 * B ? *reinterpret_cast<const double2*>(xr + jo * B)
+                            : *reinterpret_cast<const double2*>(st + (jc >> 2) * G4 + (jc & 3) * B + 2 * pc);
+        vs[q] = vr[jc - g];
+      }
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        if (q * G + g < m.z) {
+          acc.x = fma(vs[q], xs[q].x, acc.x);
+          acc.y = fma(vs[q], xs[q].y, acc.y);
+        }
+      }
+    }
+    if (m.w & 2) {
+      double2 tot = acc;
+#pragma unroll
+      for (int h = 1; h < G; ++h) {
+        const double2 o = shfl_v(acc, (lane + h * P) & 31);
+        if (g == 0) add_v(tot, o);
+      }
+      if (g == 0) {
+        double* dst = m.y < 0 ? (Y + (int64_t)m.x * ldy + 2 * pc) : (partial + (int64_t)m.y * B + 2 * pc);
+        *reinterpret_cast<double2*>(dst) = tot;
+      }
+    }
+    ++consumed;
+    __syncwarp();
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+template <int P, int S>
+int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
+               const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
+               const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
+               cudaStream_t s) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) {
+    set_error("spmm: cuTensorMapEncodeTiled unavailable");
+    return SVDREC_E_UNSUPPORTED;
+  }
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)(2 * P), (cuuint64_t)xrows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * P), 1};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("spmm: tensor map encode failed (%d)", (int)r);
+    return SVDREC_E_UNSUPPORTED;
+  }
+  constexpr size_t smem = (size_t)kPipeWarps * S * TmaGeom<P>::STG * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t grid = (nwarp + kPipeWarps - 1) / kPipeWarps;
+  k_spmm_tma<P, S><<<(unsigned)grid, kPipeWarps * 32, smem, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
+                                                                seg_slot, indices, values, Y, ldy, partial);
+  return check_launch("spmm_tma");
+}
+
+template <int S>
+int tma_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
+                 const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
+                 const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
+                 cudaStream_t s) {
+#define SVDREC_TMA(PP) \
+  case PP:             \
+    return tma_launch<PP, S>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X, ldx, \
+                             Y, ldy, partial, s);
+  switch (b / 2) {
+    SVDREC_TMA(1)
+    SVDREC_TMA(2)
+    SVDREC_TMA(3)
+    SVDREC_TMA(4)
+    SVDREC_TMA(5)
+    SVDREC_TMA(6)
+    SVDREC_TMA(7)
+    SVDREC_TMA(8)
+    SVDREC_TMA(9)
+    SVDREC_TMA(10)
+    SVDREC_TMA(11)
+    SVDREC_TMA(12)
+    SVDREC_TMA(13)
+    SVDREC_TMA(14)
+    SVDREC_TMA(15)
+    SVDREC_TMA(16)
+    default:
+      return SVDREC_E_ARG;
+  }
+#undef SVDREC_TMA
+}
+
 __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, const int32_t* __restrict__ s0,
                         const int32_t* __restrict__ s1, const double* __restrict__ partial, double* __restrict__ Y,
                         int64_t ldy, int b) {
@@ -136,9 +440,11 @@ using namespace svdrec;
 
 extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
                            const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_indices,
-                           const double* d_values, const double* d_X, int64_t ldx, double* d_Y, int64_t ldy,
+                           const double* d_values, const double* d_X, int64_t ldx, int64_t xrows, double* d_Y,
+                           int64_t ldy,
                            int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
-                           const int32_t* d_long_slot1, double* d_partial, void* stream) {
+                           const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg, double* d_partial,
+                           void* stream) {
   SVDREC_ARG(b >= 1 && ldx >= b && ldy >= b && nseg >= 0 && nlong >= 0, "spmm: bad arguments b=%d", b);
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
@@ -147,6 +453,16 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
                       reinterpret_cast<uintptr_t>(d_partial)) %
                          16 ==
                      0);
+  int rc = 0;
+  // SVDREC_SPMM_KIND=0 forces the plain kernel (A/B measurements)
+  static const int kind = getenv("SVDREC_SPMM_KIND") ? atoi(getenv("SVDREC_SPMM_KIND")) : 1;
+  if (vec2 && b <= 32 && nwarp > 0 && d_warp_seg && kind != 0 && xrows < (1ll << 31)) {
+    rc = tma_dispatch<2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                         d_values, d_X, ldx, d_Y, ldy, d_partial, s);
+    if (rc) return rc;
+    goto fixup;
+  }
+  {
   const int vec = vec2 ? 2 : 1;
   const int lanes_needed = (b + vec - 1) / vec;
   const int lpn = lanes_needed >= 32 ? 32 : lanes_needed;
@@ -162,8 +478,10 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
   else
     k_spmm<1><<<(unsigned)grid, tb, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
                                              d_values, d_X, ldx, d_Y, ldy, b, d_partial, lpn, npw);
-  int rc = check_launch("spmm");
+  rc = check_launch("spmm");
   if (rc) return rc;
+  }
+fixup:
   if (nlong > 0) {
     const int64_t tot = nlong * b;
     k_fixup<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nlong, d_long_row, d_long_slot0, d_long_slot1,

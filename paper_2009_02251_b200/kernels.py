@@ -135,8 +135,8 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
     nbytes = plan.nnz * 12 + (plan.m + 1) * 8 + (plan.n + plan.m) * b * 8
     with _span("spmm", nbytes):
         call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
-             ptr(plan.indices), ptr(plan.values), ptr(X), ldx, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
-             ptr(plan.long_s0), ptr(plan.long_s1), ptr(part), stream_handle())
+             ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
+             ptr(plan.long_s0), ptr(plan.long_s1), plan.nwarp, ptr(plan.warp_seg), ptr(part), stream_handle())
     return Y
 
 

@@ -134,6 +134,24 @@ def segment_plan(indptr: np.ndarray, seg_max: int = SEG_MAX):
     return seg_row, seg_begin, seg_end, slot, long_row, s0, s1, int(is_split_seg.sum())
 
 
+WARPS_PER_SM = 16  # pipelined SpMM: resident warps per SM (2 CTAs x 8 warps)
+
+
+def warp_plan(seg_begin: np.ndarray, seg_end: np.ndarray, nwarp: int, seg_cost: int = 16) -> np.ndarray:
+    """Split the row-ordered segments into ``nwarp`` contiguous ranges of
+    about equal cost (nonzeros + ``seg_cost`` per segment); returns the
+    ``nwarp + 1`` range starts (int32) the pipelined SpMM kernel reads."""
+    nseg = seg_begin.size
+    cost = np.cumsum((seg_end - seg_begin) + seg_cost, dtype=np.int64)
+    total = int(cost[-1]) if nseg else 0
+    targets = (np.arange(1, nwarp, dtype=np.float64) * (total / max(nwarp, 1)))
+    cuts = np.searchsorted(cost, targets, side="left") + 1 if nseg else np.zeros(nwarp - 1, np.int64)
+    out = np.empty(nwarp + 1, dtype=np.int64)
+    out[0], out[-1] = 0, nseg
+    out[1:-1] = np.minimum(cuts, nseg)
+    return np.maximum.accumulate(out).astype(np.int32)
+
+
 class DeviceCSR:
     """One CSR in HBM plus its SpMM plan."""
 
@@ -156,8 +174,11 @@ class DeviceCSR:
         self.long_s0 = t(s0, np.int32)
         self.long_s1 = t(s1, np.int32)
         self.nslots = nslots
+        sms = torch.cuda.get_device_properties(device).multi_processor_count if device.type == "cuda" else 148
+        self.nwarp = int(max(1, min(sr.size, sms * WARPS_PER_SM)))
+        self.warp_seg = t(warp_plan(sb, se, self.nwarp), np.int32)
         self._partial = {}
-        self.h2d_bytes = (self.m + 1) * 8 + self.nnz * 12 + self.nseg * 24 + self.nlong * 12
+        self.h2d_bytes = (self.m + 1) * 8 + self.nnz * 12 + self.nseg * 24 + self.nlong * 12 + (self.nwarp + 1) * 4
 
     def partial(self, b: int) -> torch.Tensor | None:
         if self.nslots == 0:
