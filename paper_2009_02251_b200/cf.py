@@ -72,6 +72,9 @@ def _eig_T(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor
     return K.gemm_nn(Bt, Wm.contiguous())
 
 
+_DEBUG_NS = bool(os.environ.get("SVDREC_DEBUG_NS"))
+
+
 class LatentFactors:
     """Item embedding T (k x items) with cached column norms (cf.py:42-74).
 
@@ -407,6 +410,8 @@ class ValidationMae:
         mb = self._mb
         got = mb.get()  # one host read per block: error sums + status
         flags = int(got["status"][0])
+        if _DEBUG_NS:
+            print(f"[svdrec] k={state.rank} NS iterations={int(got['iters'][0])} status={flags}", flush=True)
         s = self.samples
         if flags:
             with torch.cuda.stream(self._stream):

@@ -22,53 +22,55 @@ namespace cg = cooperative_groups;
 namespace svdrec {
 namespace {
 
-constexpr int NT = 32;  // output tile (k=240 -> 64 tiles per GEMM phase)
+constexpr int NT = 32;   // output tile (k=240 -> 64 tiles per GEMM phase)
 constexpr int NR = NT / 16;  // outputs per thread per dimension
-constexpr int NK = 16;  // reduction step
+constexpr int KC = 384;  // reduction columns staged per pass (one pass for k <= 384)
 constexpr int kNsThreads = 256;
-
-struct NsSmem {
-  double a[NT][NK + 1];
-  double b[NK][NT + 1];
-  double red[32];
-};
+constexpr size_t kNsSmem = 2 * (size_t)NT * KC * sizeof(double);
 
 // C[tile] = alpha * (A @ B)[tile] + diag * I[tile]; returns the tile's
-// sum of (C - I)^2 when ``resid`` (all matrices k x k, ld = k).
-__device__ double tile_gemm(NsSmem& sm, int k, const double* __restrict__ A, const double* __restrict__ B,
-                            double* __restrict__ C, int ti, int tj, double alpha, double diag, bool resid) {
+// sum of (C - I)^2 when ``resid`` (all matrices k x k, ld = k).  The whole
+// 32 x k row panel of A and k x 32 column panel of B are staged in shared
+// memory with one burst of loads (one memory latency per tile instead of
+// one per 16-deep step), then reduced from shared memory.
+__device__ double tile_gemm(double* sm, double* red, int k, const double* __restrict__ A,
+                            const double* __restrict__ B, double* __restrict__ C, int ti, int tj, double alpha,
+                            double diag, bool resid) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int r0 = ti * NT, c0 = tj * NT;
+  double* sa = sm;            // [NT][KC]
+  double* sb = sm + NT * KC;  // [KC][NT]
   double acc[NR][NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i)
 #pragma unroll
     for (int j = 0; j < NR; ++j) acc[i][j] = 0.0;
-  for (int k0 = 0; k0 < k; k0 += NK) {
-    for (int e = threadIdx.x; e < NT * NK; e += kNsThreads) {
-      const int rr = e / NK, kk = e % NK;
-      const int gr = r0 + rr, gk = k0 + kk;
-      sm.a[rr][kk] = (gr < k && gk < k) ? A[(int64_t)gr * k + gk] : 0.0;
+  for (int k0 = 0; k0 < k; k0 += KC) {
+    const int kc = min(KC, k - k0);
+    __syncthreads();  // previous pass / tile done with the panels
+    for (int e = threadIdx.x; e < NT * kc; e += kNsThreads) {
+      const int rr = e / kc, kk = e - (e / kc) * kc;
+      const int gr = r0 + rr;
+      sa[rr * KC + kk] = gr < k ? A[(int64_t)gr * k + k0 + kk] : 0.0;
     }
-    for (int e = threadIdx.x; e < NK * NT; e += kNsThreads) {
+    for (int e = threadIdx.x; e < kc * NT; e += kNsThreads) {
       const int kk = e / NT, cc = e % NT;
-      const int gk = k0 + kk, gc = c0 + cc;
-      sm.b[kk][cc] = (gk < k && gc < k) ? B[(int64_t)gk * k + gc] : 0.0;
+      const int gc = c0 + cc;
+      sb[kk * NT + cc] = gc < k ? B[(int64_t)(k0 + kk) * k + gc] : 0.0;
     }
     __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < kc; ++kk) {
+      double av[NR];
 #pragma unroll
-    for (int kk = 0; kk < NK; ++kk) {
-      double av[NR], bv[NR];
+      for (int i = 0; i < NR; ++i) av[i] = sa[(ty * NR + i) * KC + kk];
+      const double2 bv = *reinterpret_cast<const double2*>(sb + kk * NT + tx * NR);
 #pragma unroll
-      for (int i = 0; i < NR; ++i) av[i] = sm.a[ty * NR + i][kk];
-#pragma unroll
-      for (int j = 0; j < NR; ++j) bv[j] = sm.b[kk][tx * NR + j];
-#pragma unroll
-      for (int i = 0; i < NR; ++i)
-#pragma unroll
-        for (int j = 0; j < NR; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      for (int i = 0; i < NR; ++i) {
+        acc[i][0] = fma(av[i], bv.x, acc[i][0]);
+        acc[i][1] = fma(av[i], bv.y, acc[i][1]);
+      }
     }
-    __syncthreads();
   }
   double rs = 0.0;
 #pragma unroll
@@ -87,7 +89,7 @@ __device__ double tile_gemm(NsSmem& sm, int k, const double* __restrict__ A, con
       }
     }
   }
-  if (resid) rs = block_sum(rs, sm.red);
+  if (resid) rs = block_sum(rs, red);
   return rs;
 }
 
@@ -99,7 +101,8 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
                                                    double* __restrict__ part, int maxit, uint32_t* d_status,
                                                    int* d_iters) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ NsSmem sm;
+  extern __shared__ __align__(16) double ns_sm[];
+  __shared__ double red[32];
   const int nt = (k + NT - 1) / NT;
   const int ntiles = nt * nt;
   // scale: A = G / ||G||_F has spectrum in (0, 1] and a larger smallest
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
       const double g = G[(t / k) * ldg + t % k];
       fs = fma(g, g, fs);
     }
-    fs = block_sum(fs, sm.red);
+    fs = block_sum(fs, red);
     if (threadIdx.x == 0) part[blockIdx.x] = fs;
   }
   grid.sync();
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
   for (; it < maxit; ++it) {
     // phase A: T = 1.5 I - 0.5 Z Y, residual ||T - I||_F^2 per tile
     for (int w = blockIdx.x; w < ntiles; w += gridDim.x) {
-      const double rs = tile_gemm(sm, k, Z, Y, T, w / nt, w % nt, -0.5, 1.5, true);
+      const double rs = tile_gemm(ns_sm, red, k, Z, Y, T, w / nt, w % nt, -0.5, 1.5, true);
       if (threadIdx.x == 0) part[w] = rs;
     }
     grid.sync();
@@ -156,9 +159,9 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     for (int w = blockIdx.x; w < 2 * ntiles; w += gridDim.x) {
       const int q = w % ntiles;
       if (w < ntiles)
-        tile_gemm(sm, k, Y, T, Yn, q / nt, q % nt, 1.0, 0.0, false);
+        tile_gemm(ns_sm, red, k, Y, T, Yn, q / nt, q % nt, 1.0, 0.0, false);
       else
-        tile_gemm(sm, k, T, Z, Zn, q / nt, q % nt, 1.0, 0.0, false);
+        tile_gemm(ns_sm, red, k, T, Z, Zn, q / nt, q % nt, 1.0, 0.0, false);
     }
     grid.sync();
     double* t1 = Y;
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     out[i * ldo + j] = Z[t] * s;
     fz = fma(Z[t], Z[t], fz);
   }
-  fz = block_sum(fz, sm.red);
+  fz = block_sum(fz, red);
   if (threadIdx.x == 0) part[blockIdx.x] = fz;
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -214,7 +217,8 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
   static int max_blocks = 0;
   if (!max_blocks) {
     int per_sm = 0;
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, 0));
+    SVDREC_CUDA(cudaFuncSetAttribute(k_ns, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNsSmem));
+    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, kNsSmem));
     max_blocks = per_sm * sm_count();
     if (max_blocks > 4 * sm_count()) max_blocks = 4 * sm_count();
     if (max_blocks > 4096) max_blocks = 4096;
@@ -233,7 +237,8 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
   double* part = reinterpret_cast<double*>(w + 5 * m);
   int kk = k, maxit = 100;
   void* args[] = {&kk, &d_G, &ldg, &d_Z, &ldz, &Y0, &Y1, &Z0, &Z1, &T, &part, &maxit, &d_status, &d_iters};
-  SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_ns, dim3(nblk), dim3(kNsThreads), args, 0, as_stream(stream)));
+  SVDREC_CUDA(
+      cudaLaunchCooperativeKernel((void*)k_ns, dim3(nblk), dim3(kNsThreads), args, kNsSmem, as_stream(stream)));
   note_launches(1);
   return 0;
 }

@@ -55,5 +55,9 @@ for k in (40, 120, 240, 400):
     msw, (w2, V2) = timed(lambda: K.syev(G, st, V0))
     sw2 = flags_sweeps(k)
     err2 = np.max(np.abs(w2.cpu().numpy() - ref)) / ref[-1]
+    it = torch.zeros(1, dtype=torch.int32, device=G.device)
+    msn, Z = timed(lambda: K.inv_sqrt(G, st, it))
+    Zr = (V2 * w2.rsqrt()) @ V2.T
+    errn = float((Z - Zr).norm() / Zr.norm())
     print(f"k={k}: cold {ms:.3f} ms sweeps={sw} relerr={err:.1e} | warm {msw:.3f} ms sweeps={sw2} relerr={err2:.1e} "
-          f"status={int(st.item())}", flush=True)
+          f"| NS {msn:.3f} ms iters={int(it.item())} relerr={errn:.1e} status={int(st.item())}", flush=True)
