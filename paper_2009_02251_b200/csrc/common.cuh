@@ -53,7 +53,10 @@ int sm_count();
 int64_t tn_skinny_slabs(int64_t r, int64_t p);
 int launch_nn_skinny(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C,
                      int64_t ldc, double beta, double* Y, int64_t ldy, cudaStream_t s);
-int launch_tn_skinny(int64_t r, int64_t p, int q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+bool launch_nn_wide(int64_t r, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx, const double* C,
+                    int64_t ldc, double beta, double* Y, int64_t ldy, cudaStream_t s, int* rc);
+bool tn_tma_able(int64_t r, int64_t p, int64_t q, const double* X, int64_t ldx, const double* Y, int64_t ldy);
+int launch_tn_skinny(int64_t r, int64_t p, int64_t q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                      double* part, int64_t nslab, cudaStream_t s);
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -244,7 +244,7 @@ extern "C" size_t svdrec_gemm_tn_workspace_bytes(int64_t r, int64_t p, int64_t q
   // fewest possible tiles -> most splits: an upper bound for any call
   const int64_t tiles = ((p + TP - 1) / TP) * ((q + 63) / 64);
   size_t b = (size_t)tn_splits(r, tiles) * (size_t)p * (size_t)q * 8;
-  if (q <= 32) {
+  {
     const size_t bs = (size_t)tn_skinny_slabs(r, p) * (size_t)p * (size_t)q * 8;
     if (bs > b) b = bs;
   }
@@ -257,7 +257,7 @@ extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, con
   SVDREC_ARG(r >= 0 && p >= 0 && q >= 0 && ldx >= p && ldy >= q && ldc >= q, "gemm_tn: bad arguments");
   if (p == 0 || q == 0) return 0;
   cudaStream_t s = as_stream(stream);
-  if (q <= 32 && r > 0) {  // tall-skinny path: stream X once, slab partials
+  if (r > 0 && (q <= 32 || tn_tma_able(r, p, q, d_X, ldx, d_Y, ldy))) {  // DMMA path, slab partials
     const int64_t ns = tn_skinny_slabs(r, p);
     const size_t need = (size_t)ns * (size_t)p * (size_t)q * 8;
     if (need > work_bytes) {
@@ -265,7 +265,7 @@ extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, con
       return SVDREC_E_WORKSPACE;
     }
     double* part = static_cast<double*>(d_work);
-    int rc = launch_tn_skinny(r, p, (int)q, d_X, ldx, d_Y, ldy, part, ns, s);
+    int rc = launch_tn_skinny(r, p, q, d_X, ldx, d_Y, ldy, part, ns, s);
     if (rc) return rc;
     const int64_t tot = p * q;
     k_tn_reduce<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, s>>>(p, q, ns, part, alpha, beta, d_C, ldc);
@@ -300,6 +300,10 @@ extern "C" int svdrec_gemm_nn(int64_t r, int64_t p, int64_t q, double alpha, con
   SVDREC_ARG(r >= 0 && p >= 0 && q >= 0 && ldx >= p && ldc >= q && ldy >= q, "gemm_nn: bad arguments");
   if (r == 0 || q == 0) return 0;
   cudaStream_t s = as_stream(stream);
+  if (p > 0 && r > 0) {
+    int rc = 0;
+    if (launch_nn_wide(r, p, q, alpha, d_X, ldx, d_C, ldc, beta, d_Y, ldy, s, &rc)) return rc;
+  }
   if (q <= 32 && p > 0) return launch_nn_skinny(r, p, (int)q, alpha, d_X, ldx, d_C, ldc, beta, d_Y, ldy, s);
   const bool narrow = q <= 32;
   const int64_t TQ = narrow ? 32 : 64;

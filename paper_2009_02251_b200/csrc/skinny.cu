@@ -202,13 +202,14 @@ template <int NT>
 __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensorMap tmX,
                                                 const __grid_constant__ CUtensorMap tmC, int64_t r, int64_t p, int q,
                                                 double alpha, double beta, double* __restrict__ Y, int64_t ldy,
-                                                int64_t ntiles, int tpc) {
+                                                int64_t ntiles, int tpc, int qb) {
   constexpr int MT = 4;  // 32 rows per warp
+  const int col0 = 32 * blockIdx.y;  // column block (q > 32: several, C box qb = 32 wide)
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar[kNnS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  const int xstage = kNnRT * kNnKP, cstage = kNnKP * q;
+  const int xstage = kNnRT * kNnKP, cstage = kNnKP * qb;
   const int stage = xstage + ((cstage + 15) & ~15);  // keep every TMA destination 128-B aligned
   const int64_t t0 = (int64_t)blockIdx.x * tpc;
   const int nt = (int)min64(tpc, ntiles - t0);
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
     double* xs = sm + slot * stage;
     mbar_expect_tx(bar + slot, (unsigned)((xstage + cstage) * 8));
     tma_load_2d(xs, &tmX, ps * kNnKP, (int)((t0 + pt) * kNnRT), bar + slot);
-    tma_load_2d(xs + xstage, &tmC, 0, ps * kNnKP, bar + slot);
+    tma_load_2d(xs + xstage, &tmC, col0, ps * kNnKP, bar + slot);
     if (++ps == nks) {
       ps = 0;
       ++pt;
@@ -241,14 +242,14 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
     const int slot = (int)(n % kNnS);
     mbar_wait(bar + slot, (unsigned)((n / kNnS) & 1));
     const double* xs = sm + slot * stage + (32 * warp + g) * kNnKP + tq;
-    const double* cs_ = sm + slot * stage + xstage + tq * q + g;
+    const double* cs_ = sm + slot * stage + xstage + tq * qb + g;
 #pragma unroll
     for (int kk = 0; kk < kNnKP / 4; ++kk) {
       double a[MT], b[NT];
 #pragma unroll
       for (int i = 0; i < MT; ++i) a[i] = xs[8 * i * kNnKP + 4 * kk];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = (8 * j + g < q) ? cs_[4 * kk * q + 8 * j] : 0.0;
+      for (int j = 0; j < NT; ++j) b[j] = (8 * j + g < qb && col0 + 8 * j + g < q) ? cs_[4 * kk * qb + 8 * j] : 0.0;
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -265,8 +266,9 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
           for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int col = 8 * j + 2 * tq + e;
-              if (col < q) yr[col] = beta == 0.0 ? alpha * acc[i][j][e] : fma(alpha, acc[i][j][e], beta * yr[col]);
+              const int col = col0 + 8 * j + 2 * tq + e;
+              if (col < q && 8 * j + 2 * tq + e < qb)
+                yr[col] = beta == 0.0 ? alpha * acc[i][j][e] : fma(alpha, acc[i][j][e], beta * yr[col]);
             }
         }
 #pragma unroll
@@ -288,13 +290,14 @@ constexpr int kTnRB = 32, kTnS2 = 4;  // rows per stage, stages
 template <int MT, int NT>
 __global__ void __launch_bounds__(128) k_tn_tma(const __grid_constant__ CUtensorMap tmX,
                                                 const __grid_constant__ CUtensorMap tmY, int64_t r, int64_t p, int q,
-                                                double* __restrict__ part, int64_t rows_per) {
+                                                double* __restrict__ part, int64_t rows_per, int qb) {
   constexpr int PB = 8 * MT;
+  const int col0 = 32 * blockIdx.z;  // column block of Y (q > 32: box qb = 32 wide)
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar[kTnS2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  const int xstage = kTnRB * PB, ystage = kTnRB * q;
+  const int xstage = kTnRB * PB, ystage = kTnRB * qb;
   const int stage = ((xstage + 15) & ~15) + ((ystage + 15) & ~15);
   const int yoff = (xstage + 15) & ~15;
   const int64_t p0 = (int64_t)blockIdx.y * PB;
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(128) k_tn_tma(const __grid_constant__ CUtensor
     mbar_expect_tx(bar + slot, (unsigned)((xstage + ystage) * 8));
     const int row = (int)(rs + (int64_t)n * kTnRB);
     tma_load_2d(xs, &tmX, (int)p0, row, bar + slot);
-    tma_load_2d(xs + yoff, &tmY, 0, row, bar + slot);
+    tma_load_2d(xs + yoff, &tmY, col0, row, bar + slot);
   };
   if (threadIdx.x == 0)
     for (int n = 0; n < kTnS2 - 1 && n < nst; ++n) issue(n);
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(128) k_tn_tma(const __grid_constant__ CUtensor
 #pragma unroll
       for (int i = 0; i < MT; ++i) a[i] = rok ? xs[kr * PB + 8 * i + g] : 0.0;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = (rok && 8 * j + g < q) ? ys[kr * q + 8 * j + g] : 0.0;
+      for (int j = 0; j < NT; ++j) b[j] = (rok && 8 * j + g < qb) ? ys[kr * qb + 8 * j + g] : 0.0;
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -368,20 +371,21 @@ __global__ void __launch_bounds__(128) k_tn_tma(const __grid_constant__ CUtensor
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t pr = p0 + 8 * i + g;
-          const int col = 8 * j + 2 * tq + e;
-          if (pr < p && col < q) dst[pr * q + col] = red[((i * NT + j) * 2 + e) * 32 + lane];
+          const int col = col0 + 8 * j + 2 * tq + e;
+          if (pr < p && col < q && 8 * j + 2 * tq + e < qb) dst[pr * q + col] = red[((i * NT + j) * 2 + e) * 32 + lane];
         }
   }
 }
 
 template <int NT>
-int nn_tma_launch(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C,
+int nn_tma_launch(int64_t r, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx, const double* C,
                   int64_t ldc, double beta, double* Y, int64_t ldy, cudaStream_t s) {
+  const int qb = q > 32 ? 32 : (int)q;
   CUtensorMap tx, tc;
   int rc = make_map_2d(&tx, X, r, p, ldx, kNnKP, kNnRT);
-  if (!rc) rc = make_map_2d(&tc, C, p, q, ldc, q, kNnKP);
+  if (!rc) rc = make_map_2d(&tc, C, p, q, ldc, qb, kNnKP);
   if (rc) return rc;
-  const int stage = kNnRT * kNnKP + ((kNnKP * q + 15) & ~15);
+  const int stage = kNnRT * kNnKP + ((kNnKP * qb + 15) & ~15);
   const size_t smem = (size_t)kNnS * stage * 8;
   static bool attr = false;
   if (!attr) {
@@ -389,26 +393,30 @@ int nn_tma_launch(int64_t r, int64_t p, int q, double alpha, const double* X, in
     attr = true;
   }
   const int64_t ntiles = (r + kNnRT - 1) / kNnRT;
-  static int per_sm = 0, per_q = -1;  // smem depends on q: re-query when it changes
-  if (per_q != q) {
+  const int64_t gy = (q + 31) / 32;
+  static int per_sm = 0, per_qb = -1;  // smem depends on qb: re-query when it changes
+  if (per_qb != qb) {
     SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<NT>, 128, smem));
-    per_q = q;
+    per_qb = qb;
   }
   const int64_t slots = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
-  const int tpc = (int)((ntiles + slots - 1) / slots);
+  const int64_t per_col = (slots + gy - 1) / gy;  // CTAs per column block
+  const int tpc = (int)((ntiles + per_col - 1) / per_col);
   const int64_t grid = (ntiles + tpc - 1) / tpc;
-  k_nn_tma<NT><<<(unsigned)grid, 128, smem, s>>>(tx, tc, r, p, q, alpha, beta, Y, ldy, ntiles, tpc);
+  k_nn_tma<NT><<<dim3((unsigned)grid, (unsigned)gy), 128, smem, s>>>(tx, tc, r, p, (int)q, alpha, beta, Y, ldy,
+                                                                     ntiles, tpc, qb);
   return check_launch("gemm_nn_tma");
 }
 
 template <int MT, int NT>
-int tn_tma_launch(int64_t r, int64_t p, int q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+int tn_tma_launch(int64_t r, int64_t p, int64_t q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                   double* part, int64_t nslab, int64_t rows_per, cudaStream_t s) {
+  const int qb = q > 32 ? 32 : (int)q;
   CUtensorMap tx, ty;
   int rc = make_map_2d(&tx, X, r, p, ldx, 8 * MT, kTnRB);
-  if (!rc) rc = make_map_2d(&ty, Y, r, q, ldy, q, kTnRB);
+  if (!rc) rc = make_map_2d(&ty, Y, r, q, ldy, qb, kTnRB);
   if (rc) return rc;
-  const int stage = ((kTnRB * 8 * MT + 15) & ~15) + ((kTnRB * q + 15) & ~15);
+  const int stage = ((kTnRB * 8 * MT + 15) & ~15) + ((kTnRB * qb + 15) & ~15);
   size_t smem = (size_t)kTnS2 * stage * 8;
   const size_t red = (size_t)MT * NT * 2 * 32 * 8;
   if (smem < red) smem = red;
@@ -417,8 +425,8 @@ int tn_tma_launch(int64_t r, int64_t p, int q, const double* X, int64_t ldx, con
     SVDREC_CUDA(cudaFuncSetAttribute(k_tn_tma<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     attr = true;
   }
-  dim3 grid((unsigned)nslab, (unsigned)((p + 8 * MT - 1) / (8 * MT)));
-  k_tn_tma<MT, NT><<<grid, 128, smem, s>>>(tx, ty, r, p, q, part, rows_per);
+  dim3 grid((unsigned)nslab, (unsigned)((p + 8 * MT - 1) / (8 * MT)), (unsigned)((q + 31) / 32));
+  k_tn_tma<MT, NT><<<grid, 128, smem, s>>>(tx, ty, r, p, (int)q, part, rows_per, qb);
   return check_launch("gemm_tn_tma");
 }
 
@@ -467,7 +475,7 @@ int64_t tn_skinny_slabs(int64_t r, int64_t p) {
 int launch_nn_skinny(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C,
                      int64_t ldc, double beta, double* Y, int64_t ldy, cudaStream_t s) {
   if (q % 2 == 0 && tma_ok(X, ldx) && tma_ok(C, ldc) && r < (1ll << 31) && p < (1ll << 31)) {
-    switch ((q + 7) / 8) {
+    switch (q > 32 ? 4 : (q + 7) / 8) {
       case 1: return nn_tma_launch<1>(r, p, q, alpha, X, ldx, C, ldc, beta, Y, ldy, s);
       case 2: return nn_tma_launch<2>(r, p, q, alpha, X, ldx, C, ldc, beta, Y, ldy, s);
       case 3: return nn_tma_launch<3>(r, p, q, alpha, X, ldx, C, ldc, beta, Y, ldy, s);
@@ -482,10 +490,24 @@ int launch_nn_skinny(int64_t r, int64_t p, int q, double alpha, const double* X,
   }
 }
 
-int launch_tn_skinny(int64_t r, int64_t p, int q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+// any q: the DMMA/TMA kernel over 32-column blocks of C (false: operands
+// not TMA-able, caller falls back)
+bool launch_nn_wide(int64_t r, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx, const double* C,
+                    int64_t ldc, double beta, double* Y, int64_t ldy, cudaStream_t s, int* rc) {
+  if (!(q % 2 == 0 && tma_ok(X, ldx) && tma_ok(C, ldc) && r < (1ll << 31) && p < (1ll << 31))) return false;
+  *rc = q > 32 ? nn_tma_launch<4>(r, p, q, alpha, X, ldx, C, ldc, beta, Y, ldy, s)
+               : launch_nn_skinny(r, p, (int)q, alpha, X, ldx, C, ldc, beta, Y, ldy, s);
+  return true;
+}
+
+bool tn_tma_able(int64_t r, int64_t p, int64_t q, const double* X, int64_t ldx, const double* Y, int64_t ldy) {
+  return q % 2 == 0 && tma_ok(X, ldx) && tma_ok(Y, ldy) && r < (1ll << 31) && p < (1ll << 31);
+}
+
+int launch_tn_skinny(int64_t r, int64_t p, int64_t q, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                      double* part, int64_t nslab, cudaStream_t s) {
   const int64_t rows_per = (r + nslab - 1) / nslab;
-  const int nt = (q + 7) / 8;
+  const int nt = q > 32 ? 4 : (q + 7) / 8;
   if (q % 2 == 0 && tma_ok(X, ldx) && tma_ok(Y, ldy) && r < (1ll << 31) && p < (1ll << 31)) {
 #define SVDREC_TNT(M)                                                                        \
   switch (nt) {                                                                             \
