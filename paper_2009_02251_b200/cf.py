@@ -33,6 +33,7 @@ F64 = torch.float64
 # Score block l on a side stream while block l+1 is factored (SVDREC_PIPELINE=1).
 # Off by default: measured slower on B200 (the two streams thrash L2).
 PIPELINE = os.environ.get("SVDREC_PIPELINE", "0") == "1"
+SPECULATE = os.environ.get("SVDREC_SPECULATE", "0") == "1"  # measured: no gain
 _SIDE: dict = {}
 
 
@@ -226,21 +227,25 @@ class _Samples:
         self.group_users = us[groups[:-1]] if us.size else np.empty(0, np.int64)
         self.device = device
         self._plans = {}
+        self._checked: set = set()  # matrix shapes the samples were bounds-checked against
+        self._overlap: dict = {}    # id(matrix) -> (matrix, samples also stored in it); the
+        #                             reference keeps the id from being reused
 
     def plan_for(self, A: SparseRatings) -> "WorkPlan":
         """Scoring work plan against training matrix ``A`` (cached)."""
-        p = self._plans.get(id(A))
-        if p is None:
-            p = self._plans[id(A)] = WorkPlan(np.diff(A.matrix.indptr)[self.group_users], self.device)
-        return p
+        hit = self._plans.get(id(A))  # (matrix, plan): the reference pins the id
+        if hit is None:
+            hit = self._plans[id(A)] = (A, WorkPlan(np.diff(A.matrix.indptr)[self.group_users], self.device))
+        return hit[1]
 
     def check_bounds(self, A: SparseRatings) -> None:
-        if self.n == 0:
+        if self.n == 0 or A.shape in self._checked:
             return
         bad = (self.users_np < 0) | (self.users_np >= A.m) | (self.items_np < 0) | (self.items_np >= A.n)
         if bad.any():
             j = int(np.flatnonzero(bad)[0])
             raise ValueError(f"sample ({self.users_np[j]}, {self.items_np[j]}) outside matrix bounds")
+        self._checked.add(A.shape)
 
 
 def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float):
@@ -334,7 +339,10 @@ class ValidationMae:
             raise ValueError("validation set is empty")
         s.check_bounds(train)
         d = train.device(dev)
-        cnt = int(K.count_overlap(s.users, s.items, d.A).item())
+        hit = s._overlap.get(id(train))
+        if hit is None:
+            hit = s._overlap[id(train)] = (train, int(K.count_overlap(s.users, s.items, d.A).item()))
+        cnt = hit[1]
         if cnt:
             raise ValueError(f"{cnt} validation samples are present in the training matrix")
         if train.nnz == 0:
@@ -469,7 +477,10 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
     # criterion(state): break``, pipelined: block l is scored on the
     # criterion's stream while block l+1 is factored on this one (a block
     # computed past the stop is simply discarded).
-    pipeline = PIPELINE
+    # the next block is enqueued before the host waits for this block's
+    # score (same stream unless PIPELINE), so the GPU never idles on the
+    # stop decision; a block computed past the stop is discarded
+    pipeline = PIPELINE or SPECULATE
     state = next(gen, None)
     while state is not None:
         pending = criterion.submit(state)

@@ -1,4 +1,9 @@
-"""Host-side timing probe of the headline pipeline (GPU box)."""
+"""Host-side cost of one bench step: cProfile of the Python/ctypes layer.
+
+python tools/probe_host.py   (GPU box)
+"""
+import cProfile
+import pstats
 import sys
 import time
 from pathlib import Path
@@ -11,18 +16,30 @@ import paper_2009_02251_b200 as P  # noqa: E402
 from paper_2009_02251_b200.cf import _Samples  # noqa: E402
 
 cfg, M, tr, va, te, _ = bench._workload()
-A = P.SparseRatings(tr, *cfg.bounds)
-A.device()
-vs, ts = _Samples(va, torch.device("cuda")), _Samples(te, torch.device("cuda"))
+lo, hi = cfg.bounds
+A = P.SparseRatings(tr, lo, hi)
+dev = torch.device("cuda")
+A.device(dev)
+vs, ts = _Samples(va, dev), _Samples(te, dev)
+
+
+def step():
+    f, trace = P.auto_latent_factors(A, vs, block_size=bench.BLOCK, passes=bench.PASSES, patience=bench.PATIENCE,
+                                     min_improvement=bench.MIN_IMPROVEMENT, seed=bench.SEED, max_rank=bench.K_CAP)
+    return P.evaluate_errors(A, f, ts)
+
+
+for _ in range(3):
+    step()
 torch.cuda.synchronize()
-for i in range(6):
-    t0 = time.perf_counter()
-    f, trace = P.auto_latent_factors(A, vs, block_size=20, passes=4, seed=0, max_rank=400)
-    t1 = time.perf_counter()
-    m = P.evaluate_errors(A, f, ts)
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    st = torch.cuda.memory_stats()
-    print(f"run {i}: alf {1e3*(t1-t0):.1f} ms  eval {1e3*(t2-t1):.1f} ms  blocks {len(trace)}  "
-          f"cudaMalloc retries {st.get('num_alloc_retries')}  segments {st.get('segment.all.current')}  "
-          f"reserved {st.get('reserved_bytes.all.current')/1e9:.2f} GB", flush=True)
+t = time.perf_counter()
+step()
+torch.cuda.synchronize()
+print(f"wall {1e3 * (time.perf_counter() - t):.2f} ms")
+pr = cProfile.Profile()
+pr.enable()
+step()
+torch.cuda.synchronize()
+pr.disable()
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(25)
