@@ -79,17 +79,31 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                       "-i", str(index), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-i", str(index), "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
 
-    def stop(self) -> dict:
+    def _rows(self):
+        self.f.flush()
+        return [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
+
+    def wait_first(self, timeout: float = 5.0) -> None:
+        """nvidia-smi's start-up stalls the driver for a moment: let it
+        finish (first sample written) before anything is timed."""
+        t = time.perf_counter()
+        while self.p is not None and not self._rows() and time.perf_counter() - t < timeout:
+            time.sleep(0.05)
+
+    def mark(self) -> int:
+        return len(self._rows()) if self.p is not None else 0
+
+    def stop(self, start: int = 0) -> dict:
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        end = self.mark()
         self.p.terminate()
         self.p.wait()
-        self.f.flush()
-        rows = [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
+        rows = self._rows()[start:max(end, start + 1)]  # samples taken during the timed region
         sm = [float(r[0]) for r in rows if len(r) >= 6 and r[0].strip().replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if len(r) >= 6 and r[1].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -189,12 +203,14 @@ def run_b200(args):
         mae, rmse = P.evaluate_errors(A, f, ts)
         return f, trace, mae, rmse
 
+    clocks = Clocks(local)
+    clocks.wait_first()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    clocks = Clocks(local)
+    ck0 = clocks.mark()
     launches0 = lib.svdrec_launch_count()
     # the K steps are one timed region (total / K); per-step events inside
     # it are reported for spread only
@@ -207,7 +223,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     times = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(args.steps)]
     launches = (lib.svdrec_launch_count() - launches0) // args.steps
-    ck = clocks.stop()
+    ck = clocks.stop(ck0)
     t_step = ev[0].elapsed_time(ev[-1]) / 1e3 / args.steps
     # kernel breakdown from one extra, untimed step with per-call CUDA-event
     # spans (their host cost stays out of the timed region)
@@ -237,7 +253,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         e2e_times.append(e0.elapsed_time(e1) / 1e3)
         d2 = A2.device(dev)
-        h2d = d2.h2d_bytes + 2 * (len(va[0]) * 16) + len(te[0]) * 16
+        h2d = d2.h2d_bytes + 24 * (len(va[0]) + len(te[0]))  # CSR of A + (u, i, r) triples
     nb = len(trace)
     d2h = nb * ((BLOCK + 1) * 8 + 4 * 3 + 16) + 16
 
@@ -283,7 +299,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--blocks", type=int, default=None, help="reference arm: block count to extrapolate to")

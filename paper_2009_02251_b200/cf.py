@@ -164,26 +164,30 @@ class WorkPlan:
 
     CHUNK = 512
 
-    def __init__(self, group_deg: np.ndarray, device):
-        ng = group_deg.size
-        nch = np.maximum(1, -(-group_deg // self.CHUNK)).astype(np.int64)
+    def __init__(self, group_deg: torch.Tensor, device):
+        """``group_deg``: training degree of each group's user (int64 tensor,
+        built and kept on ``device``)."""
+        gd = torch.as_tensor(group_deg, device=device).to(torch.int64)
+        ng = gd.numel()
+        nch = torch.clamp((gd + self.CHUNK - 1) // self.CHUNK, min=1)
         split = nch > 1
-        slot0 = np.full(ng, -1, dtype=np.int64)
-        slot0[split] = np.cumsum(nch[split]) - nch[split]
-        done = np.full(ng, -1, dtype=np.int64)
-        done[split] = np.arange(int(split.sum()))
-        order = np.argsort(-group_deg, kind="stable")
-        wg = np.repeat(order, nch[order])
-        first = np.repeat(np.cumsum(nch[order]) - nch[order], nch[order])
-        wc = np.arange(wg.size) - first
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)  # noqa: E731
-        self.nwork = int(wg.size)
-        self.work = t(np.stack([wg, wc], axis=1).ravel()) if wg.size else torch.zeros(2, dtype=torch.int32,
-                                                                                        device=device)
-        self.ginfo = t(np.stack([nch, slot0, done], axis=1).ravel()) if ng else torch.zeros(3, dtype=torch.int32,
-                                                                                             device=device)
-        self.ndone = int(split.sum())
-        self.nslots = int(nch[split].sum())
+        cs = torch.cumsum(torch.where(split, nch, torch.zeros_like(nch)), 0)
+        slot0 = torch.where(split, cs - nch, torch.full_like(nch, -1))
+        done = torch.where(split, torch.cumsum(split.to(torch.int64), 0) - 1, torch.full_like(nch, -1))
+        order = torch.sort(-gd, stable=True).indices
+        no = nch[order]
+        wg = torch.repeat_interleave(order, no)
+        first = torch.repeat_interleave(torch.cumsum(no, 0) - no, no)
+        wc = torch.arange(wg.numel(), device=device) - first
+        self.nwork = int(wg.numel())
+        self.work = torch.stack([wg, wc], 1).flatten().to(torch.int32) if self.nwork else \
+            torch.zeros(2, dtype=torch.int32, device=device)
+        self.ginfo = torch.stack([nch, slot0, done], 1).flatten().to(torch.int32) if ng else \
+            torch.zeros(3, dtype=torch.int32, device=device)
+        stats = torch.stack([split.sum(), torch.where(split, nch, torch.zeros_like(nch)).sum()]).cpu() if ng else \
+            torch.zeros(2, dtype=torch.int64)
+        self.ndone = int(stats[0])
+        self.nslots = int(stats[1])
         self.done = torch.zeros(max(self.ndone, 1), dtype=torch.int32, device=device)
         self.counter = torch.zeros(1, dtype=torch.int32, device=device)
         self.chunk = self.CHUNK
@@ -212,36 +216,54 @@ class _Samples:
             i = np.array([int(s[1]) for s in arr], dtype=np.int64)
             r = np.array([float(s[2]) for s in arr], dtype=np.float64)
         self.n = int(u.size)
-        order = np.argsort(u, kind="stable")
-        self.order = order
-        us = u[order]
-        starts = np.flatnonzero(np.r_[True, us[1:] != us[:-1]]) if us.size else np.empty(0, np.int64)
-        groups = np.r_[starts, us.size].astype(np.int64)
         self.users_np, self.items_np, self.truth_np = u, i, r
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).astype(dt)).to(device)  # noqa: E731
-        self.groups = t(groups, np.int64)
-        self.users = t(us, np.int32)
-        self.items = t(i[order], np.int32)
-        self.truth = t(r[order], np.float64)
-        self.h2d_bytes = groups.size * 8 + self.n * 16
-        self.group_users = us[groups[:-1]] if us.size else np.empty(0, np.int64)
+        # grouped by user on the device: stable sort of the raw arrays
+        ud = torch.from_numpy(u).to(device)
+        idev = torch.from_numpy(i).to(device)
+        rd = torch.from_numpy(r).to(device)
+        self.h2d_bytes = self.n * 24
+        order = torch.sort(ud, stable=True).indices if self.n else torch.zeros(0, dtype=torch.int64, device=device)
+        us = ud[order]
+        starts = torch.nonzero(us[1:] != us[:-1]).flatten() + 1 if self.n > 1 else \
+            torch.zeros(0, dtype=torch.int64, device=device)
+        self.groups = torch.cat([torch.zeros(1 if self.n else 0, dtype=torch.int64, device=device), starts,
+                                 torch.full((1,), self.n, dtype=torch.int64, device=device)])
+        self.users = us.to(torch.int32)
+        self.items = idev[order].to(torch.int32)
+        self.truth = rd[order]
+        self._order_dev = order
+        self._order = None
+        self.group_users_dev = us[self.groups[:-1]] if self.n else torch.zeros(0, dtype=torch.int64, device=device)
         self.device = device
         self._plans = {}
         self._checked: set = set()  # matrix shapes the samples were bounds-checked against
         self._overlap: dict = {}    # id(matrix) -> (matrix, samples also stored in it); the
         #                             reference keeps the id from being reused
 
+    @property
+    def order(self) -> np.ndarray:
+        """Input position of each user-sorted sample (host copy, on demand)."""
+        if self._order is None:
+            self._order = self._order_dev.cpu().numpy()
+        return self._order
+
     def plan_for(self, A: SparseRatings) -> "WorkPlan":
         """Scoring work plan against training matrix ``A`` (cached)."""
         hit = self._plans.get(id(A))  # (matrix, plan): the reference pins the id
         if hit is None:
-            hit = self._plans[id(A)] = (A, WorkPlan(np.diff(A.matrix.indptr)[self.group_users], self.device))
+            d = A.device(self.device)
+            deg = d.A.indptr[1:] - d.A.indptr[:-1]
+            hit = self._plans[id(A)] = (A, WorkPlan(deg[self.group_users_dev], self.device))
         return hit[1]
 
     def check_bounds(self, A: SparseRatings) -> None:
         if self.n == 0 or A.shape in self._checked:
             return
-        bad = (self.users_np < 0) | (self.users_np >= A.m) | (self.items_np < 0) | (self.items_np >= A.n)
+        u, i = self.users_np, self.items_np
+        if u.min() >= 0 and u.max() < A.m and i.min() >= 0 and i.max() < A.n:
+            self._checked.add(A.shape)
+            return
+        bad = (u < 0) | (u >= A.m) | (i < 0) | (i >= A.n)
         if bad.any():
             j = int(np.flatnonzero(bad)[0])
             raise ValueError(f"sample ({self.users_np[j]}, {self.items_np[j]}) outside matrix bounds")

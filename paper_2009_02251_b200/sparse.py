@@ -33,13 +33,29 @@ class SparseRatings:
         if not sp.issparse(matrix) or matrix.format != "csr":
             raise TypeError("matrix must be a scipy CSR matrix")
         mat = matrix.astype(np.float64, copy=False)
-        mat.sort_indices()
         object.__setattr__(self, "matrix", mat)
         object.__setattr__(self, "rating_min", float(rating_min))
         object.__setattr__(self, "rating_max", float(rating_max))
         object.__setattr__(self, "_dev", {})
         if self.rating_min > self.rating_max:
             raise ValueError("rating_min exceeds rating_max")
+        if torch.cuda.is_available() and mat.nnz:
+            # O(nnz) checks where the matrix is going anyway: upload once,
+            # check on the device, keep the image (see DeviceRatings.check)
+            d = self.device()
+            unsorted, finite, lo, hi = d.check()
+            if unsorted:  # order the columns on the host, then re-check
+                self._dev.clear()
+                self._check_host()
+                self.device()
+                return
+            self._raise_values(finite, lo, hi)
+        else:
+            self._check_host()
+
+    def _check_host(self) -> None:
+        mat = self.matrix
+        mat.sort_indices()
         ind, ptr = mat.indices, mat.indptr
         if ind.size > 1:
             d = np.diff(ind)
@@ -50,11 +66,13 @@ class SparseRatings:
             if np.any(d[inner] <= 0):
                 raise ValueError("duplicate or unsorted column indices in a row")
         if mat.data.size:
-            if not np.all(np.isfinite(mat.data)):
-                raise ValueError("ratings must be finite")
-            lo, hi = mat.data.min(), mat.data.max()
-            if lo < self.rating_min or hi > self.rating_max:
-                raise ValueError(f"ratings outside [{self.rating_min}, {self.rating_max}]: observed [{lo}, {hi}]")
+            self._raise_values(bool(np.all(np.isfinite(mat.data))), mat.data.min(), mat.data.max())
+
+    def _raise_values(self, finite: bool, lo, hi) -> None:
+        if not finite:
+            raise ValueError("ratings must be finite")
+        if lo < self.rating_min or hi > self.rating_max:
+            raise ValueError(f"ratings outside [{self.rating_min}, {self.rating_max}]: observed [{lo}, {hi}]")
 
     def __setattr__(self, k, v):
         raise AttributeError("SparseRatings is immutable")
@@ -152,33 +170,89 @@ def warp_plan(seg_begin: np.ndarray, seg_end: np.ndarray, nwarp: int, seg_cost: 
     return np.maximum.accumulate(out).astype(np.int32)
 
 
-class DeviceCSR:
-    """One CSR in HBM plus its SpMM plan."""
+def segment_plan_t(indptr: torch.Tensor, seg_max: int = SEG_MAX):
+    """segment_plan on torch tensors (any device; same arrays as the numpy
+    version): built where the CSR lives, so the upload path never walks the
+    rows on the host."""
+    dev = indptr.device
+    m = indptr.numel() - 1
+    deg = indptr[1:] - indptr[:-1]
+    nps = torch.clamp((deg + seg_max - 1) // seg_max, min=1)
+    seg_row = torch.repeat_interleave(torch.arange(m, device=dev), nps)
+    cum = torch.cumsum(nps, 0)
+    first_of_row = cum - nps
+    within = torch.arange(seg_row.numel(), device=dev) - first_of_row[seg_row]
+    seg_begin = indptr[seg_row] + within * seg_max
+    seg_end = torch.minimum(seg_begin + seg_max, indptr[seg_row + 1])
+    split = nps > 1
+    is_split_seg = split[seg_row]
+    slot = torch.where(is_split_seg, torch.cumsum(is_split_seg.to(torch.int64), 0) - 1,
+                       torch.full_like(seg_row, -1))
+    long_row = torch.nonzero(split).flatten()
+    s0 = slot[first_of_row[long_row]]
+    s1 = s0 + nps[long_row]
+    nslots = int(is_split_seg.sum().item()) if seg_row.numel() else 0
+    return seg_row, seg_begin, seg_end, slot, long_row, s0, s1, nslots
 
-    def __init__(self, csr: sp.csr_matrix, device: torch.device):
-        self.m, self.n = csr.shape
-        self.nnz = csr.nnz
-        self.device = device
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).astype(dt, copy=False)).to(device, non_blocking=True)  # noqa: E731
-        self.indptr = t(csr.indptr, np.int64)
-        self.indices = t(csr.indices, np.int32)
-        self.values = t(csr.data, np.float64)
-        sr, sb, se, sl, lr, s0, s1, nslots = segment_plan(csr.indptr.astype(np.int64))
-        self.nseg = int(sr.size)
-        self.seg_row = t(sr, np.int32)
-        self.seg_begin = t(sb, np.int64)
-        self.seg_end = t(se, np.int64)
-        self.seg_slot = t(sl, np.int32)
-        self.nlong = int(lr.size)
-        self.long_row = t(lr, np.int32)
-        self.long_s0 = t(s0, np.int32)
-        self.long_s1 = t(s1, np.int32)
+
+def warp_plan_t(seg_begin: torch.Tensor, seg_end: torch.Tensor, nwarp: int, seg_cost: int = 16) -> torch.Tensor:
+    """warp_plan on torch tensors (same result as the numpy version)."""
+    dev = seg_begin.device
+    nseg = seg_begin.numel()
+    out = torch.zeros(nwarp + 1, dtype=torch.int64, device=dev)
+    out[-1] = nseg
+    if nseg and nwarp > 1:
+        cost = torch.cumsum((seg_end - seg_begin) + seg_cost, 0)
+        total = cost[-1].to(torch.float64)
+        targets = torch.arange(1, nwarp, dtype=torch.float64, device=dev) * (total / nwarp)
+        cuts = torch.searchsorted(cost.to(torch.float64), targets, side="left") + 1
+        out[1:-1] = torch.clamp(cuts, max=nseg)
+    return torch.cummax(out, 0).values.to(torch.int32)
+
+
+class DeviceCSR:
+    """One CSR in HBM plus its SpMM plan (built on the device)."""
+
+    def __init__(self, indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, shape, h2d_bytes: int = 0):
+        self.m, self.n = int(shape[0]), int(shape[1])
+        self.device = indptr.device
+        self.indptr = indptr.to(torch.int64)
+        self.indices = indices.to(torch.int32)
+        self.values = values.to(torch.float64)
+        self.nnz = int(self.indices.numel())
+        sr, sb, se, sl, lr, s0, s1, nslots = segment_plan_t(self.indptr)
+        self.nseg = int(sr.numel())
+        self.seg_row = sr.to(torch.int32)
+        self.seg_begin = sb
+        self.seg_end = se
+        self.seg_slot = sl.to(torch.int32)
+        self.nlong = int(lr.numel())
+        self.long_row = lr.to(torch.int32)
+        self.long_s0 = s0.to(torch.int32)
+        self.long_s1 = s1.to(torch.int32)
         self.nslots = nslots
-        sms = torch.cuda.get_device_properties(device).multi_processor_count if device.type == "cuda" else 148
-        self.nwarp = int(max(1, min(sr.size, sms * WARPS_PER_SM)))
-        self.warp_seg = t(warp_plan(sb, se, self.nwarp), np.int32)
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count if self.device.type == "cuda" else 148
+        self.nwarp = int(max(1, min(self.nseg, sms * WARPS_PER_SM)))
+        self.warp_seg = warp_plan_t(sb, se, self.nwarp)
         self._partial = {}
-        self.h2d_bytes = (self.m + 1) * 8 + self.nnz * 12 + self.nseg * 24 + self.nlong * 12 + (self.nwarp + 1) * 4
+        self.h2d_bytes = h2d_bytes
+
+    @classmethod
+    def upload(cls, csr: sp.csr_matrix, device: torch.device) -> "DeviceCSR":
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).astype(dt, copy=False)).to(device)  # noqa: E731
+        return cls(t(csr.indptr, np.int64), t(csr.indices, np.int32), t(csr.data, np.float64), csr.shape,
+                   h2d_bytes=(csr.shape[0] + 1) * 8 + csr.nnz * 12)
+
+    def transposed(self) -> "DeviceCSR":
+        """CSR of the transpose, built on the device: a stable sort of the
+        column indices (rows stay ascending within each column)."""
+        rows = torch.repeat_interleave(torch.arange(self.m, dtype=torch.int32, device=self.device),
+                                       self.indptr[1:] - self.indptr[:-1])
+        perm = torch.sort(self.indices, stable=True).indices
+        counts = torch.bincount(self.indices, minlength=self.n)
+        indptr = torch.zeros(self.n + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(counts, 0, out=indptr[1:])
+        return DeviceCSR(indptr, rows[perm], self.values[perm], (self.n, self.m))
 
     def partial(self, b: int) -> torch.Tensor | None:
         if self.nslots == 0:
@@ -201,17 +275,17 @@ class DeviceRatings:
         self.m, self.n = ratings.shape
         self.nnz = ratings.nnz
         self.rating_min, self.rating_max = ratings.rating_min, ratings.rating_max
-        self.A = DeviceCSR(ratings.matrix, device)
-        at = ratings.matrix.T.tocsr()
-        self.AT = DeviceCSR(at, device)
+        self.A = DeviceCSR.upload(ratings.matrix, device)
+        self.AT = self.A.transposed()
         # item popularity order (column degree, descending) for on-chip
         # staging of the hottest items' rows in the CF scoring kernel
-        order = np.argsort(-np.diff(at.indptr), kind="stable").astype(np.int32)
-        rank = np.empty(self.n, dtype=np.int32)
-        rank[order] = np.arange(self.n, dtype=np.int32)
-        self.A.hot_items = torch.from_numpy(order).to(device)
-        self.A.item_rank = torch.from_numpy(rank).to(device)
-        self.h2d_bytes = self.A.h2d_bytes + self.AT.h2d_bytes + 8 * self.n
+        col_deg = self.AT.indptr[1:] - self.AT.indptr[:-1]
+        order = torch.sort(-col_deg, stable=True).indices
+        rank = torch.empty(self.n, dtype=torch.int32, device=device)
+        rank[order] = torch.arange(self.n, dtype=torch.int32, device=device)
+        self.A.hot_items = order.to(torch.int32)
+        self.A.item_rank = rank
+        self.h2d_bytes = self.A.h2d_bytes
         # ||A||_F^2 and the global mean (fro_norm_sq, linalg.py:161-168;
         # _global_mean, cf.py:102-105) reduced on the device, read once.
         from . import kernels as K
@@ -223,6 +297,25 @@ class DeviceRatings:
         s = stats.cpu().numpy()
         self.frob_sq = float(s[0])
         self.global_mean = float(s[1] / self.nnz) if self.nnz else float("nan")
+
+    def check(self):
+        """(any row not strictly increasing, all values finite, min, max) of
+        the uploaded CSR -- the reference's constructor checks
+        (sparse.py:11-59), one device pass and one small read."""
+        A = self.A
+        dev = self.device
+        bad = torch.zeros((), dtype=torch.bool, device=dev)
+        if A.nnz > 1:
+            dif = A.indices[1:] - A.indices[:-1]
+            cross = torch.zeros(A.nnz - 1, dtype=torch.bool, device=dev)
+            st = A.indptr[1:-1]
+            st = st[(st > 0) & (st < A.nnz)]
+            cross[st - 1] = True
+            bad = ((dif <= 0) & ~cross).any()
+        v = A.values
+        out = torch.stack([bad.to(torch.float64), torch.isfinite(v).all().to(torch.float64),
+                           torch.nan_to_num(v, nan=0.0).min(), torch.nan_to_num(v, nan=0.0).max()]).cpu().numpy()
+        return bool(out[0]), bool(out[1]), float(out[2]), float(out[3])
 
     def swapped(self) -> "DeviceRatings":
         """View of A.T (rows <-> columns) sharing the same buffers."""
