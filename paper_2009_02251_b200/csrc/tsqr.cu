@@ -16,6 +16,8 @@
 // invariant (B = Q.T A rows flip, B.T B, Q B and row energies do not).
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace svdrec {
@@ -332,28 +334,21 @@ __global__ void k_pairs_reduce(int npairs, int nparts, const double* __restrict_
 // (kappa(Y) > 1e6: CholeskyQR2 would not reach working-precision
 // orthogonality), in which case the TSQR fallback runs.  R^-1 is built in
 // the lower triangle of the same shared array (column c by thread c).
-__global__ void __launch_bounds__(256) k_chol_inv(int b, const double* __restrict__ pairs, double* __restrict__ Rinv,
-                                                  uint32_t* __restrict__ flag) {
-  __shared__ double G[64][65];
-  __shared__ double dinv[64];
-  __shared__ int bad;
-  const int npairs = b * (b + 1) / 2;
-  if (threadIdx.x == 0) bad = 0;
-  for (int pidx = threadIdx.x; pidx < npairs; pidx += blockDim.x) {
-    int i = 0, off = 0;
-    while (off + (b - i) <= pidx) {
-      off += b - i;
-      ++i;
-    }
-    const int j = i + (pidx - off);
-    G[i][j] = pairs[pidx];
-  }
+// Cholesky of the Gram held in G's upper triangle (b <= 64), then R^-1 into
+// Rinv (b x b, row-major).  flag |= 1 when a pivot is non-positive or
+// (min R_jj / max R_jj)^2 < 1e-12 (kappa(Y) > 1e6: CholeskyQR2 would not
+// reach working-precision orthogonality), in which case the TSQR fallback
+// runs.  R^-1 is built in the strict lower triangle of G (column c by
+// thread c).  Whole CTA; G, dinv, bad in shared memory.
+__device__ void chol_inv_smem(int b, double (*G)[65], double* dinv, int* bad, double* __restrict__ Rinv,
+                              uint32_t* __restrict__ flag) {
+  if (threadIdx.x == 0) *bad = 0;
   __syncthreads();
   double dmax = 0.0, dmin = 1e300;
   for (int j = 0; j < b; ++j) {
     if (threadIdx.x == 0) {
       const double d = G[j][j];
-      if (!(d > 0.0)) bad = 1;
+      if (!(d > 0.0)) *bad = 1;
       G[j][j] = d > 0.0 ? sqrt(d) : 1.0;
       dinv[j] = 1.0 / G[j][j];
     }
@@ -370,9 +365,7 @@ __global__ void __launch_bounds__(256) k_chol_inv(int b, const double* __restric
     dmax = fmax(dmax, rjj);
     dmin = fmin(dmin, rjj);
   }
-  if (threadIdx.x == 0 && (bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
-  // column c of R^-1: x_c = 1/R_cc, x_i = -(sum_{t=i+1..c} R_it x_t) / R_ii,
-  // stored at G[c][i] (strict lower triangle, row owned by thread c)
+  if (threadIdx.x == 0 && (*bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
   const int c = threadIdx.x;
   if (c < b) {
     for (int i = c - 1; i >= 0; --i) {
@@ -385,6 +378,267 @@ __global__ void __launch_bounds__(256) k_chol_inv(int b, const double* __restric
   for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
     const int i = t / b, cc = t - i * b;
     Rinv[t] = i == cc ? dinv[cc] : (i < cc ? G[cc][i] : 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_chol_inv(int b, const double* __restrict__ pairs, double* __restrict__ Rinv,
+                                                  uint32_t* __restrict__ flag) {
+  __shared__ double G[64][65];
+  __shared__ double dinv[64];
+  __shared__ int bad;
+  const int npairs = b * (b + 1) / 2;
+  for (int pidx = threadIdx.x; pidx < npairs; pidx += blockDim.x) {
+    int i = 0, off = 0;
+    while (off + (b - i) <= pidx) {
+      off += b - i;
+      ++i;
+    }
+    const int j = i + (pidx - off);
+    G[i][j] = pairs[pidx];
+  }
+  chol_inv_smem(b, G, dinv, &bad, Rinv, flag);
+}
+
+// ---------------------------------------------------------------------------
+// DMMA CholeskyQR pass for b <= 32 (NT = ceil(b/8) fragment tiles).
+//
+// k_cqr_gram: G = Y.T Y on the FP64 tensor cores.  A k-step is 4 rows; the
+// A fragment of m-tile i (A[8i+g][t] = Y[row t][8i+g]) and the B fragment of
+// n-tile j (B[t][8j+g] = Y[row t][8j+g]) are the same loads, so one 8-B load
+// per tile per lane feeds the NT(NT+1)/2 upper tiles.  Warp partials are
+// added in warp order in shared memory, CTA partials go to ``part``; the
+// CTA that finishes last (atomic ticket) sums them in CTA order, factors G
+// and writes R^-1 -- one launch for Gram, reduction, Cholesky and inverse.
+constexpr int kCqrThreads = 512, kCqrWarps = kCqrThreads / 32, kCqrKs = 8, kCqrGroup = 16;
+
+__device__ __forceinline__ void dmma_cq(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Cholesky G = R.T R and R^-1 for b <= 32 by a whole CTA (>= 32 warps'
+// worth of work is not needed; what matters is the dependent chain):
+//  * factorisation: ONE barrier per column -- every thread reads the pivot
+//    and forms 1/R_jj itself, the trailing update uses the unscaled row j
+//    (G_c1c2 -= G_jc1 G_jc2 / G_jj) while row j is scaled in place;
+//  * inverse: columns of R^-1 are independent -- warp w solves column c = w
+//    (, w + nwarps) with lane t holding x_t and a warp sum per row: no
+//    barriers at all.
+// Same flag rule as chol_inv_smem.  G: upper triangle in, destroyed.
+__device__ void chol_inv_cta(int b, double (*G)[65], double* dinv, double* __restrict__ Rinv,
+                             uint32_t* __restrict__ flag) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+  bool bad = false;
+  double dmax = 0.0, dmin = 1e300;
+  for (int j = 0; j < b; ++j) {
+    const double d = G[j][j];
+    const double dd = d > 0.0 ? d : 1.0;
+    const double inv = rsqrt(dd), rjj = dd * inv, invd = inv * inv;  // one MUFU-seeded op on the chain
+    bad |= !(d > 0.0);
+    dmax = fmax(dmax, rjj);
+    dmin = fmin(dmin, rjj);
+    // trailing update from the unscaled row j: 2-D thread map (c2 = t % 32,
+    // c1 = t / 32 + 16 k), no divisions
+    for (int t = tid; t < 32 * 32; t += nth) {
+      const int c1 = t >> 5, c2 = t & 31;
+      if (c1 > j && c2 >= c1 && c2 < b) G[c1][c2] = fma(-G[j][c1] * invd, G[j][c2], G[c1][c2]);
+    }
+    __syncthreads();  // the update has read row j (unscaled)
+    if (tid < 32) {
+      const int c = tid;
+      if (c == j) {
+        G[j][j] = rjj;
+        dinv[j] = inv;
+      } else if (c > j && c < b) {
+        G[j][c] *= inv;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && (bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
+  // X = R^-1, column c: x_c = 1/R_cc, x_i = -(sum_{t=i+1..c} R_it x_t) / R_ii
+  for (int c = warp; c < b; c += nwarps) {
+    double xl = lane == c ? dinv[c] : 0.0;  // x_lane
+    for (int i = c - 1; i >= 0; --i) {
+      double p = (lane > i && lane <= c) ? G[i][lane] * xl : 0.0;
+      p = warp_sum(p);
+      if (lane == i) xl = -p * dinv[i];
+    }
+    if (lane <= c) Rinv[lane * b + c] = xl;
+    else if (lane < b) Rinv[lane * b + c] = 0.0;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kCqrThreads) k_cqr_gram(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
+                                                          double* __restrict__ part, double* __restrict__ gpart,
+                                                          unsigned* __restrict__ tickets, double* __restrict__ Rinv,
+                                                          uint32_t* __restrict__ flag) {
+  constexpr int BP = 8 * NT, E = BP * BP;  // padded width, entries per partial
+  __shared__ double red[NT * NT * 2 * 32];
+  __shared__ double G[64][65];
+  __shared__ double dinv[64];
+  __shared__ unsigned arrive;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  // 32 rows (8 k-steps of 4) per warp, all loaded at once: one DRAM round
+  const int64_t ws = ((int64_t)blockIdx.x * kCqrWarps + warp) * (4 * kCqrKs);
+  double y[kCqrKs][NT];
+#pragma unroll
+  for (int s = 0; s < kCqrKs; ++s) {
+    const int64_t row = ws + 4 * s + tq;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int col = 8 * t + g;
+      y[s][t] = (row < r && col < b) ? __ldcs(Y + row * ldy + col) : 0.0;
+    }
+  }
+  double acc[NT][NT][2];
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < kCqrKs; ++s)
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = i; j < NT; ++j) dmma_cq(acc[i][j], y[s][i], y[s][j]);
+  // warp-ordered CTA sum
+  for (int w = 0; w < kCqrWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = i; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double* c = red + ((i * NT + j) * 2 + e) * 32 + lane;
+            *c = (w == 0 ? 0.0 : *c) + acc[i][j][e];
+          }
+    }
+    __syncthreads();
+  }
+  // CTA partial (BP x BP, lower tiles zero)
+  double* mine = part + (int64_t)blockIdx.x * E;
+  for (int t = threadIdx.x; t < E; t += kCqrThreads) mine[t] = 0.0;
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = i; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) mine[(8 * i + g) * BP + 8 * j + 2 * tq + e] = red[((i * NT + j) * 2 + e) * 32 + lane];
+  }
+  // two-level fixed-order reduction: the last CTA of each group of
+  // kCqrGroup sums the group's partials, the last group finisher sums the
+  // group partials (tickets rest at 0 between calls)
+  const unsigned ngroups = (gridDim.x + kCqrGroup - 1) / kCqrGroup;
+  const unsigned grp = blockIdx.x / kCqrGroup;
+  const unsigned g0 = grp * kCqrGroup, gn = min(gridDim.x, g0 + kCqrGroup) - g0;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) arrive = atomicAdd(tickets + 1 + grp, 1u);
+  __syncthreads();
+  if (arrive != gn - 1) return;
+  __threadfence();
+  for (int t = threadIdx.x; t < E; t += kCqrThreads) {
+    double x[kCqrGroup];  // all loads in flight, then the fixed-order sum
+#pragma unroll
+    for (int c = 0; c < kCqrGroup; ++c) x[c] = c < (int)gn ? __ldcg(part + (int64_t)(g0 + c) * E + t) : 0.0;
+    double v = 0.0;
+#pragma unroll
+    for (int c = 0; c < kCqrGroup; ++c) v += x[c];
+    gpart[(int64_t)grp * E + t] = v;
+  }
+  if (threadIdx.x == 0) tickets[1 + grp] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) arrive = atomicAdd(tickets, 1u);
+  __syncthreads();
+  if (arrive != ngroups - 1) return;
+  __threadfence();
+  for (int t = threadIdx.x; t < E; t += kCqrThreads) {
+    const int m = t / BP, n = t - m * BP;
+    double v = 0.0;
+    for (unsigned c0 = 0; c0 < ngroups; c0 += kCqrGroup) {
+      double x[kCqrGroup];
+#pragma unroll
+      for (int c = 0; c < kCqrGroup; ++c) x[c] = c0 + c < ngroups ? __ldcg(gpart + (int64_t)(c0 + c) * E + t) : 0.0;
+#pragma unroll
+      for (int c = 0; c < kCqrGroup; ++c) v += x[c];
+    }
+    if (m < b && n < b) G[m][n] = v;
+  }
+  if (threadIdx.x == 0) tickets[0] = 0u;
+  __syncthreads();
+  chol_inv_cta(b, G, dinv, Rinv, flag);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) k_cqr_apply(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
+                                                   const double* __restrict__ Rinv, double* __restrict__ out,
+                                                   int64_t ldo, const uint32_t* __restrict__ flag, int only_if_clear) {
+  constexpr int BP = 8 * NT, NK = 2 * NT, MT = 2;  // k-steps of 4 over the padded width; 16-row tiles
+  __shared__ double Rs[BP][BP + 1];
+  if (only_if_clear && *flag) return;
+  for (int t = threadIdx.x; t < BP * BP; t += blockDim.x) {
+    const int i = t / BP, j = t % BP;
+    Rs[i][j] = (i < b && j < b) ? Rinv[i * b + j] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (r + 8 * MT - 1) / (8 * MT);
+  auto ld = [&](int64_t tile, double (&a)[NK][MT]) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int64_t row = tile * (8 * MT) + 8 * i + g;
+#pragma unroll
+      for (int s = 0; s < NK; ++s) {
+        const int col = 4 * s + tq;
+        a[s][i] = (tile < ntiles && row < r && col < b) ? __ldcs(Y + row * ldy + col) : 0.0;
+      }
+    }
+  };
+  int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double a[NK][MT];
+  ld(tile, a);
+  for (; tile < ntiles; tile += nw) {
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < NK; ++s) {
+      double bf[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = Rs[4 * s + tq][8 * j + g];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma_cq(acc[i][j], a[s][i], bf[j]);
+    }
+    ld(tile + nw, a);
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int64_t row = tile * (8 * MT) + 8 * i + g;
+      if (row < r) {
+        double* o = out + row * ldo;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * j + 2 * tq + e;
+            if (col < b) o[col] = acc[i][j][e];
+          }
+      }
+    }
   }
 }
 
@@ -425,10 +679,12 @@ __global__ void __launch_bounds__(kApplyRows) k_trapply(int64_t r, int b, const 
 }
 
 struct OrthLayout {
-  size_t off_flag, off_rinv, off_red, off_part, off_tmp, off_tsqr, total;
+  size_t off_flag, off_rinv, off_red, off_part, off_tmp, off_tsqr, off_cqr, off_tickets, total;
   int nparts;
   int64_t rows_per;
 };
+
+int64_t cqr_ctas(int64_t r) { return (r + kCqrWarps * 4 * kCqrKs - 1) / (kCqrWarps * 4 * kCqrKs); }
 
 OrthLayout orth_layout(int64_t r, int b) {
   OrthLayout L{};
@@ -439,8 +695,9 @@ OrthLayout orth_layout(int64_t r, int b) {
     L.nparts = (int)((r + kGramRows - 1) / kGramRows);
   }
   size_t o = 0;
-  L.off_flag = o;
-  o = align_up(o + 16);
+  L.off_flag = o;  // flag words (4), then the DMMA path's reduction tickets
+  L.off_tickets = o + 16;
+  o = align_up(o + 16 + (size_t)(2 + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 4);
   L.off_red = o;
   o = align_up(o + (size_t)b * (b + 1) / 2 * 8);
   L.off_rinv = o;
@@ -451,8 +708,38 @@ OrthLayout orth_layout(int64_t r, int b) {
   o = align_up(o + (size_t)r * b * 8);
   L.off_tsqr = o;
   o = align_up(o + make_plan(r, b).total);
+  L.off_cqr = o;  // DMMA path: CTA partials + group partials (BP x BP each, BP <= 32) + tickets
+  o = align_up(o + (size_t)(cqr_ctas(r) + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 32 * 32 * 8);
   L.total = o;
   return L;
+}
+
+template <int NT>
+int cqr_pass_nt(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_t ldo, const OrthLayout& L,
+                char* w, int only_if_clear, cudaStream_t s) {
+  double* rinv = reinterpret_cast<double*>(w + L.off_rinv);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(w + L.off_flag);
+  const int64_t nc = cqr_ctas(r);
+  double* part = reinterpret_cast<double*>(w + L.off_cqr);
+  double* gpart = part + nc * (8 * NT) * (8 * NT);
+  unsigned* tickets = reinterpret_cast<unsigned*>(w + L.off_tickets);
+  k_cqr_gram<NT><<<(unsigned)nc, kCqrThreads, 0, s>>>(r, b, Y, ldy, part, gpart, tickets, rinv, flag);
+  const int64_t tiles = (r + 15) / 16;
+  int64_t grid = (tiles + 7) / 8;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (grid > cap) grid = cap;
+  k_cqr_apply<NT><<<(unsigned)grid, 256, 0, s>>>(r, b, Y, ldy, rinv, out, ldo, flag, only_if_clear);
+  return check_launch("cqr_pass", 2);
+}
+
+int cqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_t ldo, const OrthLayout& L, char* w,
+             int only_if_clear, cudaStream_t s) {
+  switch ((b + 7) / 8) {
+    case 1: return cqr_pass_nt<1>(r, b, Y, ldy, out, ldo, L, w, only_if_clear, s);
+    case 2: return cqr_pass_nt<2>(r, b, Y, ldy, out, ldo, L, w, only_if_clear, s);
+    case 3: return cqr_pass_nt<3>(r, b, Y, ldy, out, ldo, L, w, only_if_clear, s);
+    default: return cqr_pass_nt<4>(r, b, Y, ldy, out, ldo, L, w, only_if_clear, s);
+  }
 }
 
 int cholqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_t ldo, const OrthLayout& L,
@@ -514,10 +801,19 @@ extern "C" int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda,
   if (b > 64)  // CholeskyQR2 tiles hold b <= 64: Householder directly
     return run_tsqr(make_plan(r, b), r, b, d_A, lda, d_Q, ldq, reinterpret_cast<double*>(w + L.off_rinv),
                     w + L.off_tsqr, nullptr, s);
-  SVDREC_CUDA(cudaMemsetAsync(flag, 0, 16, s));
-  int rc = cholqr_pass(r, b, d_A, lda, tmp, b, L, w, 0, s);  // Q1 = A R1^-1
-  if (rc) return rc;
-  rc = cholqr_pass(r, b, tmp, b, d_Q, ldq, L, w, 1, s);  // Q = Q1 R2^-1 (if both passes are sound)
+  // flag and tickets (the scratch workspace is shared with other calls)
+  SVDREC_CUDA(cudaMemsetAsync(flag, 0, L.off_tickets - L.off_flag + (2 + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 4,
+                              s));
+  int rc;
+  if (b <= 32) {  // DMMA passes
+    rc = cqr_pass(r, b, d_A, lda, tmp, b, L, w, 0, s);  // Q1 = A R1^-1
+    if (rc) return rc;
+    rc = cqr_pass(r, b, tmp, b, d_Q, ldq, L, w, 1, s);  // Q = Q1 R2^-1 (if both passes are sound)
+  } else {
+    rc = cholqr_pass(r, b, d_A, lda, tmp, b, L, w, 0, s);
+    if (rc) return rc;
+    rc = cholqr_pass(r, b, tmp, b, d_Q, ldq, L, w, 1, s);
+  }
   if (rc) return rc;
   // fallback: Householder TSQR from the untouched input, only if flagged
   double* dummy_r = reinterpret_cast<double*>(w + L.off_rinv);
