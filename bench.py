@@ -83,6 +83,12 @@ class Clocks:
         except OSError:
             self.p = None
 
+    @classmethod
+    def disabled(cls) -> "Clocks":
+        c = object.__new__(cls)
+        c.p = None
+        return c
+
     def _rows(self):
         self.f.flush()
         return [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
@@ -203,13 +209,19 @@ def run_b200(args):
         mae, rmse = P.evaluate_errors(A, f, ts)
         return f, trace, mae, rmse
 
-    clocks = Clocks(local)
+    clocks = Clocks(local) if not os.environ.get("BENCH_NO_CLOCKS") else Clocks.disabled()
     clocks.wait_first()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
+    # start the timed region from a clean heap: collect, then freeze the
+    # set-up objects (data generation leaves millions of them) so a cyclic
+    # collection inside the timed steps does not walk them
+    import gc
+    gc.collect()
+    gc.freeze()
     ck0 = clocks.mark()
     launches0 = lib.svdrec_launch_count()
     # the K steps are one timed region (total / K); per-step events inside

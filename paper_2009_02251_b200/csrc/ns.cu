@@ -22,72 +22,84 @@ namespace cg = cooperative_groups;
 namespace svdrec {
 namespace {
 
-constexpr int NT = 32;   // output tile (k=240 -> 64 tiles per GEMM phase)
-constexpr int NR = NT / 16;  // outputs per thread per dimension
-constexpr int KC = 384;  // reduction columns staged per pass (one pass for k <= 384)
-constexpr int kNsThreads = 256;
-constexpr size_t kNsSmem = 2 * (size_t)NT * KC * sizeof(double);
+constexpr int NT = 32;    // output tile (k=240 -> 64 tiles per GEMM phase)
+constexpr int KC = 192;   // reduction columns staged per pass
+constexpr int kNsThreads = 128;  // 4 warps: warp w owns tile rows 8w..8w+7, all 32 columns
+constexpr int kLdA = KC + 4;     // A panel pitch: 8 fragment rows land in distinct 32-B bank quarters
+constexpr int kLdB = NT + 8;     // B panel pitch (320 B): the 4 fragment rows in 2 bank halves
+constexpr size_t kNsSmem = ((size_t)NT * kLdA + (size_t)KC * kLdB) * sizeof(double);
 
-// C[tile] = alpha * (A @ B)[tile] + diag * I[tile]; returns the tile's
-// sum of (C - I)^2 when ``resid`` (all matrices k x k, ld = k).  The whole
-// 32 x k row panel of A and k x 32 column panel of B are staged in shared
-// memory with one burst of loads (one memory latency per tile instead of
-// one per 16-deep step), then reduced from shared memory.
+__device__ __forceinline__ void cp_async8_zf(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
+}
+
+__device__ __forceinline__ void dmma_ns(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// C[tile] = alpha * (A @ B)[tile] + diag * I[tile] on the FP64 tensor cores
+// (DMMA m8n8k4); returns the tile's sum of (C - I)^2 when ``resid`` (all
+// matrices k x k, ld = k).  The 32 x k row panel of A and k x 32 column
+// panel of B are staged in shared memory in KC-wide passes.
 __device__ double tile_gemm(double* sm, double* red, int k, const double* __restrict__ A,
                             const double* __restrict__ B, double* __restrict__ C, int ti, int tj, double alpha,
                             double diag, bool resid) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
   const int r0 = ti * NT, c0 = tj * NT;
-  double* sa = sm;            // [NT][KC]
-  double* sb = sm + NT * KC;  // [KC][NT]
-  double acc[NR][NR];
+  double* sa = sm;             // [NT][kLdA]
+  double* sb = sm + NT * kLdA; // [KC][kLdB]
+  double acc[4][2];
 #pragma unroll
-  for (int i = 0; i < NR; ++i)
-#pragma unroll
-    for (int j = 0; j < NR; ++j) acc[i][j] = 0.0;
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
   for (int k0 = 0; k0 < k; k0 += KC) {
     const int kc = min(KC, k - k0);
+    const int kc4 = (kc + 3) & ~3;
     __syncthreads();  // previous pass / tile done with the panels
-    for (int e = threadIdx.x; e < NT * kc; e += kNsThreads) {
-      const int rr = e / kc, kk = e - (e / kc) * kc;
+    // coalesced panel loads as cp.async (all in flight at once; a plain
+    // load -> st.shared loop serialises on each load's L2 latency), zero
+    // fill outside the matrix
+    for (int rr = warp; rr < NT; rr += kNsThreads / 32) {
       const int gr = r0 + rr;
-      sa[rr * KC + kk] = gr < k ? A[(int64_t)gr * k + k0 + kk] : 0.0;
+      const double* src = A + (int64_t)(gr < k ? gr : 0) * k + k0;
+      for (int kk = lane; kk < kc4; kk += 32) cp_async8_zf(sa + rr * kLdA + kk, src + (kk < kc ? kk : 0), gr < k && kk < kc);
     }
-    for (int e = threadIdx.x; e < kc * NT; e += kNsThreads) {
-      const int kk = e / NT, cc = e % NT;
-      const int gc = c0 + cc;
-      sb[kk * NT + cc] = gc < k ? B[(int64_t)(k0 + kk) * k + gc] : 0.0;
+    for (int kk = warp; kk < kc4; kk += kNsThreads / 32) {
+      const int gc = c0 + lane;
+      cp_async8_zf(sb + kk * kLdB + lane, B + (int64_t)(k0 + (kk < kc ? kk : 0)) * k + (gc < k ? gc : 0),
+                   gc < k && kk < kc);
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
+    const double* ap = sa + (8 * warp + g) * kLdA + tq;
+    const double* bp = sb + tq * kLdB + g;
 #pragma unroll 4
-    for (int kk = 0; kk < kc; ++kk) {
-      double av[NR];
+    for (int s = 0; s < kc4 / 4; ++s) {
+      const double a = ap[4 * s];
 #pragma unroll
-      for (int i = 0; i < NR; ++i) av[i] = sa[(ty * NR + i) * KC + kk];
-      const double2 bv = *reinterpret_cast<const double2*>(sb + kk * NT + tx * NR);
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        acc[i][0] = fma(av[i], bv.x, acc[i][0]);
-        acc[i][1] = fma(av[i], bv.y, acc[i][1]);
-      }
+      for (int j = 0; j < 4; ++j) dmma_ns(acc[j], a, bp[4 * s * kLdB + 8 * j]);
     }
   }
   double rs = 0.0;
+  const int gr = r0 + 8 * warp + g;
+  if (gr < k) {
 #pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const int gr = r0 + ty * NR + i;
-    if (gr >= k) continue;
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      const int gc = c0 + tx * NR + j;
-      if (gc >= k) continue;
-      const double v = alpha * acc[i][j] + (gr == gc ? diag : 0.0);
-      C[(int64_t)gr * k + gc] = v;
-      if (resid) {
-        const double d = v - (gr == gc ? 1.0 : 0.0);
-        rs = fma(d, d, rs);
+      for (int e = 0; e < 2; ++e) {
+        const int gc = c0 + 8 * j + 2 * tq + e;
+        if (gc < k) {
+          const double v = alpha * acc[j][e] + (gr == gc ? diag : 0.0);
+          C[(int64_t)gr * k + gc] = v;
+          if (resid) {
+            const double d = v - (gr == gc ? 1.0 : 0.0);
+            rs = fma(d, d, rs);
+          }
+        }
       }
-    }
   }
   if (resid) rs = block_sum(rs, red);
   return rs;
@@ -119,10 +131,14 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     if (threadIdx.x == 0) part[blockIdx.x] = fs;
   }
   grid.sync();
+  // block-parallel loads, fixed-order block sums: every block gets the
+  // same values (no serial chain of dependent L2 reads)
   double fro2 = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) fro2 += part[b];
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) fro2 += part[b];
+  fro2 = block_sum(fro2, red);
   double tr = 0.0;
-  for (int i = 0; i < k; ++i) tr += G[(int64_t)i * ldg + i];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) tr += G[(int64_t)i * ldg + i];
+  tr = block_sum(tr, red);
   const double c_scale = sqrt(fro2);
   const double inv_c = c_scale > 0.0 ? 1.0 / c_scale : 0.0;
   grid.sync();  // part[] is reused below
@@ -147,8 +163,8 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     }
     grid.sync();
     double r = 0.0;
-    for (int w = 0; w < ntiles; ++w) r += part[w];  // same fixed order in every block
-    r = sqrt(r);
+    for (int w = threadIdx.x; w < ntiles; w += blockDim.x) r += part[w];
+    r = sqrt(block_sum(r, red));  // same fixed order in every block
     // quadratic convergence down to rounding, or stagnation at rounding level
     if (r <= 8.0 * 2.220446049250313e-16 * sqrt((double)k) || (r < 1e-9 && r > 0.5 * prev)) {
       done = true;
@@ -184,9 +200,11 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
   fz = block_sum(fz, red);
   if (threadIdx.x == 0) part[blockIdx.x] = fz;
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double f = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) f += part[b];
+  if (blockIdx.x != 0) return;
+  double f = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) f += part[b];
+  f = block_sum(f, red);
+  if (threadIdx.x == 0) {
     if (d_iters) *d_iters = it;
     // the reference raises when lambda_min < 1e-14 trace(G); with
     // mu = lambda / ||G||_F and mu_min >= 1 / ||A^(-1/2)||_F^2 = 1 / f that is
