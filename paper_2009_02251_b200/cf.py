@@ -184,10 +184,11 @@ class WorkPlan:
             torch.zeros(2, dtype=torch.int32, device=device)
         self.ginfo = torch.stack([nch, slot0, done], 1).flatten().to(torch.int32) if ng else \
             torch.zeros(3, dtype=torch.int32, device=device)
-        stats = torch.stack([split.sum(), torch.where(split, nch, torch.zeros_like(nch)).sum()]).cpu() if ng else \
-            torch.zeros(2, dtype=torch.int64)
+        stats = torch.stack([split.sum(), torch.where(split, nch, torch.zeros_like(nch)).sum(), gd.sum()]).cpu() \
+            if ng else torch.zeros(3, dtype=torch.int64)
         self.ndone = int(stats[0])
         self.nslots = int(stats[1])
+        self.rated = int(stats[2])  # training ratings streamed per scoring pass
         self.done = torch.zeros(max(self.ndone, 1), dtype=torch.int32, device=device)
         self.counter = torch.zeros(1, dtype=torch.int32, device=device)
         self.chunk = self.CHUNK

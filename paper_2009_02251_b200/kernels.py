@@ -132,7 +132,9 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
     if Y.shape[1] != b or X.shape[0] != plan.n or Y.shape[0] != plan.m:
         raise ValueError(f"spmm: shape mismatch A{(plan.m, plan.n)} X{tuple(X.shape)} Y{tuple(Y.shape)}")
     part = plan.partial(b)
-    nbytes = plan.nnz * 12 + (plan.m + 1) * 8 + (plan.n + plan.m) * b * 8
+    # algorithmic bytes: per nonzero its CSR entry (12 B) and the gathered
+    # row of X (8b, L2 resident); per output row 8b written
+    nbytes = plan.nnz * (12 + 8 * b) + plan.m * b * 8
     with _span("spmm", nbytes):
         call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
              ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
@@ -305,7 +307,12 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     val = torch.empty(ns, dtype=F64, device=Yn.device)
     raw = torch.empty(ns, dtype=F64, device=Yn.device)
     fb = torch.empty(ns, dtype=torch.uint8, device=Yn.device)
-    with _span("cf_predict", 0):
+    k = Yn.shape[1]
+    # algorithmic bytes: per streamed rating its CSR entry (12 B) and the
+    # rated item's unit row (k doubles, L2/shared-memory resident); per
+    # sample its ids, norm, Xn row and the three outputs
+    nbytes = getattr(plan, "rated", 0) * (12 + 8 * k) + ns * (8 * k + 4 + 4 + 8 + 17)
+    with _span("cf_predict", nbytes):
         hot = getattr(csr, "hot_items", None)
         rank = getattr(csr, "item_rank", None)
         call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
