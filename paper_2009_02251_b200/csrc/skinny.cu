@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
                                                 int64_t ntiles, int tpc, int qb) {
   constexpr int MT = 4;  // 32 rows per warp
   const int col0 = 32 * blockIdx.y;  // column block (q > 32: several, C box qb = 32 wide)
+  const bool vec2 = (ldy % 2 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar[kNnS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -263,13 +264,24 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
         if (row < r) {
           double* yr = Y + row * ldy;
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
+          for (int j = 0; j < NT; ++j) {
+            const int lc = 8 * j + 2 * tq, col = col0 + lc;
+            if (vec2 && col + 1 < q && lc + 1 < qb) {  // whole-sector 16-B store
+              double2* p2 = reinterpret_cast<double2*>(yr + col);
+              double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+              if (beta != 0.0) {
+                const double2 o = *p2;
+                v = make_double2(fma(alpha, acc[i][j][0], beta * o.x), fma(alpha, acc[i][j][1], beta * o.y));
+              }
+              *p2 = v;
+              continue;
+            }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int col = col0 + 8 * j + 2 * tq + e;
-              if (col < q && 8 * j + 2 * tq + e < qb)
-                yr[col] = beta == 0.0 ? alpha * acc[i][j][e] : fma(alpha, acc[i][j][e], beta * yr[col]);
+              if (col + e < q && lc + e < qb)
+                yr[col + e] = beta == 0.0 ? alpha * acc[i][j][e] : fma(alpha, acc[i][j][e], beta * yr[col + e]);
             }
+          }
         }
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;

@@ -585,6 +585,7 @@ __global__ void __launch_bounds__(256) k_cqr_apply(int64_t r, int b, const doubl
   constexpr int BP = 8 * NT, NK = 2 * NT, MT = 2;  // k-steps of 4 over the padded width; 16-row tiles
   __shared__ double Rs[BP][BP + 1];
   if (only_if_clear && *flag) return;
+  const bool vec2 = (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
   for (int t = threadIdx.x; t < BP * BP; t += blockDim.x) {
     const int i = t / BP, j = t % BP;
     Rs[i][j] = (i < b && j < b) ? Rinv[i * b + j] : 0.0;
@@ -630,12 +631,19 @@ __global__ void __launch_bounds__(256) k_cqr_apply(int64_t r, int b, const doubl
       const int64_t row = tile * (8 * MT) + 8 * i + g;
       if (row < r) {
         double* o = out + row * ldo;
+        // a lane's two fragment columns are adjacent: one 16-B store
+        // (whole sectors; 8-B stores left half-written sectors that cost
+        // ~10x the output bytes in DRAM writes)
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
+        for (int j = 0; j < NT; ++j) {
+          const int col = 8 * j + 2 * tq;
+          if (vec2 && col + 1 < b) {
+            *reinterpret_cast<double2*>(o + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+            continue;
+          }
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 8 * j + 2 * tq + e;
-            if (col < b) o[col] = acc[i][j][e];
+          for (int e = 0; e < 2; ++e)
+            if (col + e < b) o[col + e] = acc[i][j][e];
           }
       }
     }
