@@ -27,7 +27,7 @@
 namespace svdrec {
 namespace {
 
-constexpr int kChunk = 32;
+constexpr int kChunk = 8;  // raw words per chunk (small: the walks read a precomputed raw buffer)
 constexpr int kScan = 1024;
 constexpr int kCfg = 6;
 constexpr uint64_t kM0 = 0xD2E7470EE14C6C93ULL, kM1 = 0xCA5A826395121157ULL;
@@ -101,6 +101,36 @@ struct Raw {
   }
 };
 
+// Raw words precomputed by k_raw into a buffer covering [pos0, pos0 + n).
+struct RawBuf {
+  const uint64_t* buf;
+  uint64_t pos0;
+  __device__ uint64_t at(uint64_t g) const { return __ldg(buf + (g - pos0)); }
+  __device__ uint64_t ahead(uint64_t g) const { return __ldg(buf + (g + 1 - pos0)); }
+};
+
+// A thread's kChunk + 2 raw words staged in shared memory, transposed
+// (word i of thread t at [i][t]: conflict-free; the natural [t][i] layout
+// put a warp's loads 16-way on the same bank).
+constexpr int kGauThreads = 128;
+constexpr int kStage = kChunk + 2;
+
+struct RawSmem {
+  const uint64_t* sw;  // &stage[0][threadIdx.x]
+  uint64_t base;       // this thread's chunk start
+  __device__ uint64_t at(uint64_t g) const { return sw[(g - base) * kGauThreads]; }
+  __device__ uint64_t ahead(uint64_t g) const { return sw[(g + 1 - base) * kGauThreads]; }
+};
+
+__device__ __forceinline__ void stage_raw(uint64_t* sw, const uint64_t* __restrict__ rawbuf, uint64_t cta_off,
+                                          int64_t nraw) {
+#pragma unroll
+  for (int i = 0; i < kStage; ++i) {
+    const uint64_t j = cta_off + (uint64_t)threadIdx.x * kChunk + i;
+    sw[i * kGauThreads + threadIdx.x] = j < (uint64_t)nraw ? __ldg(rawbuf + j) : 0ull;
+  }
+}
+
 __device__ __forceinline__ double u01(uint64_t w) {
   return __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
 }
@@ -109,15 +139,30 @@ __device__ __forceinline__ double dbits(uint64_t b) { return __longlong_as_doubl
 
 // One transducer move from state st at raw position p (word w0 = raw[p]).
 // Returns words consumed; sets next state, emit flag and value.
-__device__ __forceinline__ int move(int st, uint64_t p, Raw& raw, int& nst, bool& emit, double& val) {
+// Ziggurat tables in shared memory: the 256-entry lookups are indexed by
+// random bytes, which __constant__ memory serialises across a warp.
+struct ZigSmem {
+  uint64_t ki[256], wi[256], fi[256];
+  __device__ void load() {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      ki[i] = svdrec_zig::kKi[i];
+      wi[i] = svdrec_zig::kWiBits[i];
+      fi[i] = svdrec_zig::kFiBits[i];
+    }
+  }
+};
+
+template <class RawT>
+__device__ __forceinline__ int move(int st, uint64_t p, RawT& raw, const ZigSmem& zt, int& nst, bool& emit,
+                                    double& val) {
   const uint64_t w0 = raw.at(p);
   if (st == 0) {
     const uint32_t idx = (uint32_t)(w0 & 0xff);
     const uint64_t r = w0 >> 8;
     const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-    double x = __dmul_rn((double)rabs, dbits(svdrec_zig::kWiBits[idx]));
+    double x = __dmul_rn((double)rabs, dbits(zt.wi[idx]));
     if (r & 1) x = -x;
-    if (rabs < svdrec_zig::kKi[idx]) {
+    if (rabs < zt.ki[idx]) {
       nst = 0;
       emit = true;
       val = x;
@@ -128,7 +173,7 @@ __device__ __forceinline__ int move(int st, uint64_t p, Raw& raw, int& nst, bool
       emit = false;
       return 1;
     }
-    const double fa = dbits(svdrec_zig::kFiBits[idx - 1]), fb = dbits(svdrec_zig::kFiBits[idx]);
+    const double fa = dbits(zt.fi[idx - 1]), fb = dbits(zt.fi[idx]);
     const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(fa, fb), u01(raw.ahead(p))), fb);
     nst = 0;
     emit = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x));
@@ -155,13 +200,36 @@ __device__ __forceinline__ uint32_t compose(uint32_t a_e, const uint32_t* b) {
   return (((a_e >> 3) + (bb >> 3)) << 3) | (bb & 7);
 }
 
-__global__ void k_tables(uint64_t k0, uint64_t k1, const int64_t* __restrict__ d_pos, int64_t nchunks,
-                         uint32_t* __restrict__ tab) {
+// A0. the raw words of [pos0, pos0 + n): one thread per Philox block
+__global__ void k_raw(uint64_t k0, uint64_t k1, const uint64_t* __restrict__ pos0p, int64_t n,
+                      uint64_t* __restrict__ buf) {
+  const uint64_t pos0 = *pos0p;
+  const uint64_t b0 = pos0 >> 2;
+  const uint64_t bi = b0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * bi >= pos0 + (uint64_t)n) return;
+  uint64_t w[4];
+  philox4x64(bi + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint64_t g = 4 * bi + j;
+    if (g >= pos0 && g < pos0 + (uint64_t)n) buf[g - pos0] = w[j];
+  }
+}
+
+__global__ void __launch_bounds__(kGauThreads) k_tables(const uint64_t* __restrict__ rawbuf,
+                                                        const uint64_t* __restrict__ pos0p, int64_t nchunks,
+                                                        int64_t nraw, uint32_t* __restrict__ tab) {
+  __shared__ uint64_t sw[kStage * kGauThreads];
+  __shared__ ZigSmem zt;
+  const uint64_t cta_off = (uint64_t)blockIdx.x * kGauThreads * kChunk;
+  stage_raw(sw, rawbuf, cta_off, nraw);
+  zt.load();
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
-  const uint64_t base = (uint64_t)*d_pos + (uint64_t)c * kChunk, end = base + kChunk;
-  Raw raw;
-  raw.init(k0, k1);
+  const uint64_t pos0 = *pos0p;
+  const uint64_t base = pos0 + (uint64_t)c * kChunk, end = base + kChunk;
+  RawSmem raw{sw + threadIdx.x, base};
   // primary walk from (offset 0, S); remember which (position, state) it
   // visits and how many samples it had emitted before each.
   uint8_t vis[kChunk + 1];
@@ -177,7 +245,7 @@ __global__ void k_tables(uint64_t k0, uint64_t k1, const int64_t* __restrict__ d
     int nst;
     bool emit;
     double v;
-    p += move(st, p, raw, nst, emit, v);
+    p += move(st, p, raw, zt, nst, emit, v);
     st = nst;
     cnt += emit;
   }
@@ -199,7 +267,7 @@ __global__ void k_tables(uint64_t k0, uint64_t k1, const int64_t* __restrict__ d
       int nst;
       bool emit;
       double v;
-      q += move(s2, q, raw, nst, emit, v);
+      q += move(s2, q, raw, zt, nst, emit, v);
       s2 = nst;
       c2 += emit;
     }
@@ -244,16 +312,25 @@ __global__ void __launch_bounds__(kScan) k_scan(const uint32_t* __restrict__ tab
   }
 }
 
-__global__ void k_chain(const uint32_t* __restrict__ agg, int64_t nblocks, int64_t count,
-                        uint32_t* __restrict__ cta_cfg, int64_t* __restrict__ cta_off,
-                        uint32_t* d_status) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// C. thread the true entry configuration through the CTA aggregates: the
+// aggregate tables are staged in shared memory by the whole CTA first, so
+// the sequential walk is shared-memory latency, not L2 latency, per step.
+constexpr int kChainMax = 1536;  // CTA aggregates staged in 36 KB (more: read from global)
+
+__global__ void __launch_bounds__(1024) k_chain(const uint32_t* __restrict__ agg, int64_t nblocks, int64_t count,
+                                                uint32_t* __restrict__ cta_cfg, int64_t* __restrict__ cta_off,
+                                                uint32_t* d_status) {
+  __shared__ uint32_t sa[kChainMax * kCfg];
+  const int64_t ns = nblocks < kChainMax ? nblocks : kChainMax;
+  for (int64_t i = threadIdx.x; i < ns * kCfg; i += blockDim.x) sa[i] = agg[i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   uint32_t cfg = 0;
   int64_t off = 0;
   for (int64_t g = 0; g < nblocks; ++g) {
     cta_cfg[g] = cfg;
     cta_off[g] = off;
-    const uint32_t a = agg[g * kCfg + cfg];
+    const uint32_t a = g < ns ? sa[g * kCfg + cfg] : agg[g * kCfg + cfg];
     off += a >> 3;
     cfg = a & 7;
   }
@@ -264,7 +341,8 @@ __global__ void k_read_pos(const int64_t* d_pos, uint64_t* dst) { *dst = (uint64
 
 struct NormalPlan {
   int64_t nchunks, nblocks;
-  size_t off_tab, off_incl, off_agg, off_cfg, off_off, off_pos, total;
+  size_t off_tab, off_incl, off_agg, off_cfg, off_off, off_pos, off_raw, total;
+  int64_t nraw;
 };
 
 NormalPlan plan_for(int64_t count) {
@@ -285,21 +363,31 @@ NormalPlan plan_for(int64_t count) {
   o = align_up(o + (size_t)p.nblocks * 8);
   p.off_pos = o;
   o = align_up(o + 8);
+  p.nraw = p.nchunks * kChunk + 4;  // + the look-ahead word of a chunk's last move
+  p.off_raw = o;
+  o = align_up(o + (size_t)p.nraw * 8);
   p.total = o;
   return p;
 }
 
-__global__ void k_emit_from(uint64_t k0, uint64_t k1, int64_t* __restrict__ d_pos, const uint64_t* pos0p,
+__global__ void __launch_bounds__(kGauThreads) k_emit_from(const uint64_t* __restrict__ rawbuf, int64_t nraw,
+                                                           int64_t* __restrict__ d_pos, const uint64_t* pos0p,
                             int64_t nchunks, const uint32_t* __restrict__ incl,
-                            const uint32_t* __restrict__ cta_cfg, const int64_t* __restrict__ cta_off,
+                            const uint32_t* __restrict__ cta_cfg, const int64_t* __restrict__ cta_off_,
                             int64_t count, int64_t cols, const int32_t* __restrict__ perm,
                             double* __restrict__ out, int64_t ld) {
+  __shared__ uint64_t sw[kStage * kGauThreads];
+  __shared__ ZigSmem zt;
+  const uint64_t cta_off = (uint64_t)blockIdx.x * kGauThreads * kChunk;
+  stage_raw(sw, rawbuf, cta_off, nraw);
+  zt.load();
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   const uint64_t pos0 = *pos0p;
   const int64_t g = c / kScan;
   uint32_t cfg = cta_cfg[g];
-  int64_t off = cta_off[g];
+  int64_t off = cta_off_[g];
   if (c % kScan) {
     const uint32_t a = incl[(c - 1) * kCfg + cfg];
     off += a >> 3;
@@ -309,18 +397,21 @@ __global__ void k_emit_from(uint64_t k0, uint64_t k1, int64_t* __restrict__ d_po
   const uint64_t base = pos0 + (uint64_t)c * kChunk, end = base + kChunk;
   uint64_t p = base + cfg / 3;
   int st = cfg % 3;
-  Raw raw;
-  raw.init(k0, k1);
+  int64_t row = off / cols, col = off - row * cols;  // one division; then carried
+  RawSmem raw{sw + threadIdx.x, base};
   while (p < end && off < count) {
     int nst;
     bool emit;
     double v;
-    const int used = move(st, p, raw, nst, emit, v);
+    const int used = move(st, p, raw, zt, nst, emit, v);
     if (emit) {
-      const int64_t row = off / cols, col = off - row * cols;
       out[(perm ? (int64_t)perm[row] : row) * ld + col] = v;
       if (off == count - 1) *d_pos = (int64_t)(p + used);
       ++off;
+      if (++col == cols) {
+        col = 0;
+        ++row;
+      }
     }
     p += used;
     st = nst;
@@ -356,13 +447,16 @@ extern "C" int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_p
   auto* coff = reinterpret_cast<int64_t*>(w + p.off_off);
   auto* pos0 = reinterpret_cast<uint64_t*>(w + p.off_pos);
   cudaStream_t s = as_stream(stream);
-  const int tb = 128;
+  const int tb = kGauThreads;
   const unsigned grid = (unsigned)((p.nchunks + tb - 1) / tb);
+  auto* rawbuf = reinterpret_cast<uint64_t*>(w + p.off_raw);
   k_read_pos<<<1, 1, 0, s>>>(d_pos, pos0);
-  k_tables<<<grid, tb, 0, s>>>(key_lo, key_hi, d_pos, p.nchunks, tab);
+  const int64_t nblk4 = p.nraw / 4 + 2;
+  k_raw<<<(unsigned)((nblk4 + 255) / 256), 256, 0, s>>>(key_lo, key_hi, pos0, p.nraw, rawbuf);
+  k_tables<<<grid, tb, 0, s>>>(rawbuf, pos0, p.nchunks, p.nraw, tab);
   k_scan<<<(unsigned)p.nblocks, kScan, 0, s>>>(tab, p.nchunks, incl, agg);
-  k_chain<<<1, 1, 0, s>>>(agg, p.nblocks, count, ccfg, coff, d_status);
-  k_emit_from<<<grid, tb, 0, s>>>(key_lo, key_hi, d_pos, pos0, p.nchunks, incl, ccfg, coff, count, cols,
-                                   d_row_perm, d_out, ld);
-  return check_launch("normal_fill", 5);
+  k_chain<<<1, 1024, 0, s>>>(agg, p.nblocks, count, ccfg, coff, d_status);
+  k_emit_from<<<grid, tb, 0, s>>>(rawbuf, p.nraw, d_pos, pos0, p.nchunks, incl, ccfg, coff, count, cols, d_row_perm,
+                                   d_out, ld);
+  return check_launch("normal_fill", 6);
 }
