@@ -141,6 +141,10 @@ int main() {
   };
   run_gather(k_gather<20>, 20, 256, 4);
   run_gather(k_gather<20>, 20, 256, 8);
+  run_gather(k_gather<24>, 24, 256, 8);
+  run_gather(k_gather<32>, 32, 256, 8);
+  run_gather(k_gather<16>, 16, 256, 8);
+  run_gather(k_gather<64>, 64, 256, 8);
   run_gather(k_gather<240>, 240, 256, 2);
   run_gather(k_gather<240>, 240, 256, 4);
   // bulk copies
