@@ -299,7 +299,7 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": round(t_step, 6), "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": False,
-        "scaling": "strong" if ws == 1 else "replicas", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "parallelism": "replicas" if ws > 1 else "single", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(cfg, tr),
         "k": int(f.k), "blocks": nb, "test_mae": mae, "test_rmse": rmse, "val_mae": min(e.mae for e in trace),
         "step_times_s": [round(t, 6) for t in times],
