@@ -176,7 +176,7 @@ def run_reference(args):
             vals.append(total)
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config_dict(cfg, tr),
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -245,11 +245,9 @@ def run_b200(args):
     prof = K.profile_summary(K.PROFILE)
     K.PROFILE = None
     psteps = 1
-    if ws > 1:
-        tt = torch.tensor([t_step], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dist.barrier()
-        t_step = float(tt.item())
+    if ws > 1:  # replicas: the slowest rank's time per step
+        from paper_2009_02251_b200.parallel import max_over_ranks
+        t_step = max_over_ranks(t_step, dev)
 
     # e2e: the public API from host buffers, upload + results read inside
     e2e_times, h2d = [], 0
