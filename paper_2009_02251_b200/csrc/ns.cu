@@ -15,7 +15,7 @@
 // The eigendecomposition itself (syev) runs once, for the returned factors.
 #include <cooperative_groups.h>
 
-#include "common.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -105,16 +105,89 @@ __device__ double tile_gemm(double* sm, double* red, int k, const double* __rest
   return rs;
 }
 
+// TMA variant of tile_gemm (k even): each operand panel is ONE tensor-map
+// copy into shared memory (A: 32 rows x kKcT columns, pitch 244 doubles =
+// 1952 B = 32 mod 128, so the 8 rows of an A fragment fall in distinct
+// bank quarters; B: kKcT rows x 40 columns, pitch 320 B = 2 bank halves),
+// zero fill past k.  The per-element cp.async loop it replaces spent ~10 us
+// per tile issuing 15 k copies through 128 threads.
+constexpr int kKcT = 244, kBwT = 40;
+constexpr size_t kNsSmemT = ((size_t)NT * kKcT + (size_t)kKcT * kBwT) * sizeof(double);
+
+struct NsMaps {
+  CUtensorMap a[5];  // A-operand boxes {kKcT cols, 32 rows} of Y0, Y1, Z0, Z1, T
+  CUtensorMap b[5];  // B-operand boxes {40 cols, kKcT rows}
+};
+
+__device__ double tile_gemm_tma(double* sm, uint64_t* bar, unsigned& phase, double* red, int k, const NsMaps& maps,
+                                int ia, int ib, double* __restrict__ C, int ti, int tj, double alpha, double diag,
+                                bool resid) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int r0 = ti * NT, c0 = tj * NT;
+  double* sa = sm;                // [NT][kKcT]
+  double* sb = sm + NT * kKcT;    // [kKcT][kBwT]
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int k0 = 0; k0 < k; k0 += kKcT) {
+    __syncthreads();  // previous pass / tile done with the panels
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, (unsigned)((NT * kKcT + kKcT * kBwT) * 8));
+      tma_load_2d(sa, &maps.a[ia], k0, r0, bar);
+      tma_load_2d(sb, &maps.b[ib], c0, k0, bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const int ks = (min(kKcT, k - k0) + 3) >> 2;
+    const double* ap = sa + (8 * warp + g) * kKcT + tq;
+    const double* bp = sb + tq * kBwT + g;
+#pragma unroll 4
+    for (int s = 0; s < ks; ++s) {
+      const double a = ap[4 * s];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_ns(acc[j], a, bp[4 * s * kBwT + 8 * j]);
+    }
+  }
+  double rs = 0.0;
+  const int gr = r0 + 8 * warp + g;
+  if (gr < k) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gc = c0 + 8 * j + 2 * tq + e;
+        if (gc < k) {
+          const double v = alpha * acc[j][e] + (gr == gc ? diag : 0.0);
+          C[(int64_t)gr * k + gc] = v;
+          if (resid) {
+            const double d = v - (gr == gc ? 1.0 : 0.0);
+            rs = fma(d, d, rs);
+          }
+        }
+      }
+  }
+  if (resid) rs = block_sum(rs, red);
+  return rs;
+}
+
 // work: Y0, Y1, Z0, Z1, T (k x k each), part (ntiles), misc
 __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restrict__ G, int64_t ldg,
                                                    double* __restrict__ out, int64_t ldo, double* __restrict__ Y0,
                                                    double* __restrict__ Y1, double* __restrict__ Z0,
                                                    double* __restrict__ Z1, double* __restrict__ T,
                                                    double* __restrict__ part, int maxit, uint32_t* d_status,
-                                                   int* d_iters) {
+                                                   int* d_iters, const __grid_constant__ NsMaps maps, int use_tma) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double ns_sm[];
+  extern __shared__ __align__(128) double ns_sm[];
   __shared__ double red[32];
+  __shared__ __align__(8) uint64_t tbar;
+  unsigned tphase = 0;
+  if (threadIdx.x == 0) mbar_init(&tbar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  // buffer ids of Y, Yn, Z, Zn for the tensor maps (0 Y0, 1 Y1, 2 Z0, 3 Z1, 4 T)
+  int iy = 0, iyn = 1, iz = 2, izn = 3;
   const int nt = (k + NT - 1) / NT;
   const int ntiles = nt * nt;
   // scale: A = G / ||G||_F has spectrum in (0, 1] and a larger smallest
@@ -158,7 +231,9 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
   for (; it < maxit; ++it) {
     // phase A: T = 1.5 I - 0.5 Z Y, residual ||T - I||_F^2 per tile
     for (int w = blockIdx.x; w < ntiles; w += gridDim.x) {
-      const double rs = tile_gemm(ns_sm, red, k, Z, Y, T, w / nt, w % nt, -0.5, 1.5, true);
+      const double rs = use_tma ? tile_gemm_tma(ns_sm, &tbar, tphase, red, k, maps, iz, iy, T, w / nt, w % nt, -0.5,
+                                                1.5, true)
+                                : tile_gemm(ns_sm, red, k, Z, Y, T, w / nt, w % nt, -0.5, 1.5, true);
       if (threadIdx.x == 0) part[w] = rs;
     }
     grid.sync();
@@ -174,10 +249,16 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     // phase B: Y <- Y T, Z <- T Z
     for (int w = blockIdx.x; w < 2 * ntiles; w += gridDim.x) {
       const int q = w % ntiles;
-      if (w < ntiles)
+      if (use_tma) {
+        if (w < ntiles)
+          tile_gemm_tma(ns_sm, &tbar, tphase, red, k, maps, iy, 4, Yn, q / nt, q % nt, 1.0, 0.0, false);
+        else
+          tile_gemm_tma(ns_sm, &tbar, tphase, red, k, maps, 4, iz, Zn, q / nt, q % nt, 1.0, 0.0, false);
+      } else if (w < ntiles) {
         tile_gemm(ns_sm, red, k, Y, T, Yn, q / nt, q % nt, 1.0, 0.0, false);
-      else
+      } else {
         tile_gemm(ns_sm, red, k, T, Z, Zn, q / nt, q % nt, 1.0, 0.0, false);
+      }
     }
     grid.sync();
     double* t1 = Y;
@@ -186,6 +267,12 @@ __global__ void __launch_bounds__(kNsThreads) k_ns(int k, const double* __restri
     double* t2 = Z;
     Z = Zn;
     Zn = t2;
+    const int u1 = iy;
+    iy = iyn;
+    iyn = u1;
+    const int u2 = iz;
+    iz = izn;
+    izn = u2;
   }
   grid.sync();  // every block is done reading part[] before it is reused
   // G^(-1/2) = A^(-1/2) / sqrt(||G||_F); ||A^(-1/2)||_F^2 = sum 1/mu_i bounds
@@ -232,11 +319,14 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
     set_error("inv_sqrt: workspace too small");
     return SVDREC_E_WORKSPACE;
   }
-  static int max_blocks = 0;
+  const int use_tma = (k % 2 == 0) && k >= 2;
+  const size_t smem = use_tma ? kNsSmemT : kNsSmem;
+  static int max_blocks_t[2] = {0, 0};
+  int& max_blocks = max_blocks_t[use_tma];
   if (!max_blocks) {
     int per_sm = 0;
-    SVDREC_CUDA(cudaFuncSetAttribute(k_ns, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNsSmem));
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, kNsSmem));
+    SVDREC_CUDA(cudaFuncSetAttribute(k_ns, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNsSmemT));
+    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, smem));
     max_blocks = per_sm * sm_count();
     if (max_blocks > 4 * sm_count()) max_blocks = 4 * sm_count();
     if (max_blocks > 4096) max_blocks = 4096;
@@ -253,10 +343,20 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
   double* Z1 = reinterpret_cast<double*>(w + 3 * m);
   double* T = reinterpret_cast<double*>(w + 4 * m);
   double* part = reinterpret_cast<double*>(w + 5 * m);
-  int kk = k, maxit = 100;
-  void* args[] = {&kk, &d_G, &ldg, &d_Z, &ldz, &Y0, &Y1, &Z0, &Z1, &T, &part, &maxit, &d_status, &d_iters};
-  SVDREC_CUDA(
-      cudaLaunchCooperativeKernel((void*)k_ns, dim3(nblk), dim3(kNsThreads), args, kNsSmem, as_stream(stream)));
+  NsMaps maps;
+  if (use_tma) {
+    double* bufs[5] = {Y0, Y1, Z0, Z1, T};
+    for (int i = 0; i < 5; ++i) {
+      int rc = make_map_2d(&maps.a[i], bufs[i], k, k, k, kKcT, NT);
+      if (!rc) rc = make_map_2d(&maps.b[i], bufs[i], k, k, k, kBwT, kKcT);
+      if (rc) return rc;
+    }
+  } else {
+    memset(&maps, 0, sizeof(maps));
+  }
+  int kk = k, maxit = 100, ut = use_tma;
+  void* args[] = {&kk, &d_G, &ldg, &d_Z, &ldz, &Y0, &Y1, &Z0, &Z1, &T, &part, &maxit, &d_status, &d_iters, &maps, &ut};
+  SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_ns, dim3(nblk), dim3(kNsThreads), args, smem, as_stream(stream)));
   note_launches(1);
   return 0;
 }
