@@ -18,7 +18,11 @@
 
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace svdrec {
 namespace {
@@ -80,16 +84,13 @@ __device__ __forceinline__ void chunk_range(int64_t rows, int64_t nc, int64_t c,
 }
 
 // Householder QR of one chunk.  M is column-major in smem: M[col*ldm + row].
-__global__ void __launch_bounds__(kThreads) k_factor(int64_t rows, int64_t nc, int b, const double* __restrict__ in,
-                                                     int64_t ldin, double* __restrict__ vout,
-                                                     double* __restrict__ tau, double* __restrict__ rout,
-                                                     const uint32_t* __restrict__ gate) {
-  if (gate && *gate == 0) return;  // CholeskyQR2 succeeded: fallback not needed
+__device__ void factor_chunk(int64_t c, int64_t rows, int64_t nc, int b, const double* __restrict__ in,
+                             int64_t ldin, double* __restrict__ vout, double* __restrict__ tau,
+                             double* __restrict__ rout) {
   extern __shared__ double sm[];
   __shared__ double dots[128];
   __shared__ double wv[128];
   __shared__ double coef[3];  // tau, beta, scale
-  const int64_t c = blockIdx.x;
   int64_t a, e;
   chunk_range(rows, nc, c, a, e);
   const int rc = (int)(e - a);
@@ -160,14 +161,11 @@ __global__ void __launch_bounds__(kThreads) k_factor(int64_t rows, int64_t nc, i
 // Apply one chunk's reflectors to E = [Qc ; 0] (Qc = rows c*b.. of the
 // coarser explicit Q, or the identity at the top) and store the chunk's
 // rows of this level's explicit Q.
-__global__ void __launch_bounds__(kThreads) k_buildq(int64_t rows, int64_t nc, int b, const double* __restrict__ vin,
-                                                     const double* __restrict__ tau,
-                                                     const double* __restrict__ qcoarse, double* __restrict__ qout,
-                                                     int64_t ldq, const uint32_t* __restrict__ gate) {
-  if (gate && *gate == 0) return;
+__device__ void buildq_chunk(int64_t c, int64_t rows, int64_t nc, int b, const double* __restrict__ vin,
+                             const double* __restrict__ tau, const double* __restrict__ qcoarse,
+                             double* __restrict__ qout, int64_t ldq) {
   extern __shared__ double sm[];
   __shared__ double wv[128];
-  const int64_t c = blockIdx.x;
   int64_t a, e;
   chunk_range(rows, nc, c, a, e);
   const int rc = (int)(e - a);
@@ -210,6 +208,64 @@ __global__ void __launch_bounds__(kThreads) k_buildq(int64_t rows, int64_t nc, i
   }
 }
 
+__global__ void __launch_bounds__(kThreads) k_factor(int64_t rows, int64_t nc, int b, const double* __restrict__ in,
+                                                     int64_t ldin, double* __restrict__ vout,
+                                                     double* __restrict__ tau, double* __restrict__ rout) {
+  factor_chunk(blockIdx.x, rows, nc, b, in, ldin, vout, tau, rout);
+}
+
+__global__ void __launch_bounds__(kThreads) k_buildq(int64_t rows, int64_t nc, int b, const double* __restrict__ vin,
+                                                     const double* __restrict__ tau,
+                                                     const double* __restrict__ qcoarse, double* __restrict__ qout,
+                                                     int64_t ldq) {
+  buildq_chunk(blockIdx.x, rows, nc, b, vin, tau, qcoarse, qout, ldq);
+}
+
+// The whole TSQR (every factor level, then every Q level) as ONE cooperative
+// launch, gated on a device flag: the CholeskyQR2 fallback costs a single
+// launch that returns at once when the flag is clear (it was 2 x levels
+// launches, ~20 us per orth call).
+constexpr int kMaxLevels = 12;
+struct CoopLevels {
+  int nl;
+  int64_t rows[kMaxLevels], nc[kMaxLevels];
+  double* v[kMaxLevels];
+  double* tau[kMaxLevels];
+  double* next[kMaxLevels];
+  double* q[kMaxLevels];
+};
+
+__global__ void __launch_bounds__(kThreads) k_tsqr_coop(const __grid_constant__ CoopLevels L, int b,
+                                                        const double* __restrict__ A, int64_t lda,
+                                                        double* __restrict__ Q, int64_t ldq, double* __restrict__ R,
+                                                        const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;  // uniform: CholeskyQR2 succeeded
+  cg::grid_group grid = cg::this_grid();
+  const double* in = A;
+  int64_t ldin = lda;
+  for (int l = 0; l < L.nl; ++l) {
+    double* rout = (l == L.nl - 1) ? R : L.next[l];
+    for (int64_t c = blockIdx.x; c < L.nc[l]; c += gridDim.x) {
+      factor_chunk(c, L.rows[l], L.nc[l], b, in, ldin, L.v[l], L.tau[l], rout);
+      __syncthreads();
+    }
+    grid.sync();
+    in = rout;
+    ldin = b;
+  }
+  const double* coarse = nullptr;
+  for (int l = L.nl - 1; l >= 0; --l) {
+    double* qo = l == 0 ? Q : L.q[l];
+    const int64_t ldo = l == 0 ? ldq : b;
+    for (int64_t c = blockIdx.x; c < L.nc[l]; c += gridDim.x) {
+      buildq_chunk(c, L.rows[l], L.nc[l], b, L.v[l], L.tau[l], coarse, qo, ldo);
+      __syncthreads();
+    }
+    grid.sync();
+    coarse = qo;
+  }
+}
+
 }  // namespace
 }  // namespace svdrec
 
@@ -243,7 +299,7 @@ int run_tsqr(const Plan& p, int64_t r, int32_t b, const double* d_A, int64_t lda
     double* rout = (l == nl - 1) ? d_R : reinterpret_cast<double*>(w + L.off_next);
     k_factor<<<(unsigned)L.nc, kThreads, smem_f, s>>>(L.rows, L.nc, b, in, ldin,
                                                       reinterpret_cast<double*>(w + L.off_v),
-                                                      reinterpret_cast<double*>(w + L.off_tau), rout, gate);
+                                                      reinterpret_cast<double*>(w + L.off_tau), rout);
     int rc = check_launch("tsqr_factor");
     if (rc) return rc;
     in = rout;
@@ -255,12 +311,50 @@ int run_tsqr(const Plan& p, int64_t r, int32_t b, const double* d_A, int64_t lda
     double* qo = l == 0 ? d_Q : reinterpret_cast<double*>(w + L.off_q);
     const int64_t ldo = l == 0 ? ldq : b;
     k_buildq<<<(unsigned)L.nc, kThreads, smem_q, s>>>(L.rows, L.nc, b, reinterpret_cast<double*>(w + L.off_v),
-                                                      reinterpret_cast<double*>(w + L.off_tau), coarse, qo, ldo,
-                                                      gate);
+                                                      reinterpret_cast<double*>(w + L.off_tau), coarse, qo, ldo);
     int rc = check_launch("tsqr_buildq");
     if (rc) return rc;
     coarse = qo;
   }
+  return 0;
+}
+
+// Gated cooperative TSQR (see k_tsqr_coop).
+int run_tsqr_gated(const Plan& p, int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
+                   double* d_R, char* w, const uint32_t* gate, cudaStream_t s) {
+  const size_t smem_f = (size_t)b * ((p.rcmax + 1) | 1) * 8;
+  const size_t smem_q = 2 * smem_f;
+  const int nl = (int)p.lv.size();
+  if (nl > kMaxLevels) {
+    set_error("orth: TSQR tree deeper than %d levels", kMaxLevels);
+    return SVDREC_E_UNSUPPORTED;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    SVDREC_CUDA(cudaFuncSetAttribute(k_tsqr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
+    attr_set = true;
+  }
+  CoopLevels L{};
+  L.nl = nl;
+  int64_t maxnc = 1;
+  for (int l = 0; l < nl; ++l) {
+    const Level& v = p.lv[l];
+    L.rows[l] = v.rows;
+    L.nc[l] = v.nc;
+    L.v[l] = reinterpret_cast<double*>(w + v.off_v);
+    L.tau[l] = reinterpret_cast<double*>(w + v.off_tau);
+    L.next[l] = reinterpret_cast<double*>(w + v.off_next);
+    L.q[l] = reinterpret_cast<double*>(w + v.off_q);
+    if (v.nc > maxnc) maxnc = v.nc;
+  }
+  int per_sm = 0;
+  SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr_coop, kThreads, smem_q));
+  int64_t grid = (int64_t)(per_sm > 0 ? per_sm : 1) * sm_count();
+  if (grid > maxnc) grid = maxnc;
+  int32_t bb = b;
+  void* args[] = {&L, &bb, &d_A, &lda, &d_Q, &ldq, &d_R, &gate};
+  SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_tsqr_coop, dim3((unsigned)grid), dim3(kThreads), args, smem_q, s));
+  note_launches(1);
   return 0;
 }
 
@@ -825,5 +919,5 @@ extern "C" int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda,
   if (rc) return rc;
   // fallback: Householder TSQR from the untouched input, only if flagged
   double* dummy_r = reinterpret_cast<double*>(w + L.off_rinv);
-  return run_tsqr(make_plan(r, b), r, b, d_A, lda, d_Q, ldq, dummy_r, w + L.off_tsqr, flag, s);
+  return run_tsqr_gated(make_plan(r, b), r, b, d_A, lda, d_Q, ldq, dummy_r, w + L.off_tsqr, flag, s);
 }

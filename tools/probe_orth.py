@@ -1,3 +1,4 @@
+"""Launch-list probe: svdrec_orth (CholeskyQR2 + gated TSQR) on 138493 x 20."""
 import sys
 from pathlib import Path
 import torch
