@@ -400,3 +400,52 @@ def test_adaptive_pca_criteria_and_validation(P):
         P.FrobTolerance(1.5)
     with pytest.raises(P.RankExhaustedError):
         P.adaptive_pca(A, P.FixedRank(500), block_size=4, passes=6, seed=1)
+
+
+# ---------------------------------------------------------------------------
+# acceptance-style properties (the reference's criteria 3, 4 and 8, on
+# seeded synthetic matrices)
+
+def test_pass_engine_matches_power_engine_at_matched_budget(P):
+    import inputs
+    dense, M = inputs.rand_sparse(200, 300, 0.05, 33, grid=False)
+    A = P.SparseRatings(M, 0.5, 5.0)
+    norm = np.linalg.norm(dense)
+    for power in (0, 1, 2):
+        s1 = next(P.qb_power_blocks(A, 20, power, P.GaussianStream(7)))
+        s2 = next(P.qb_pass_blocks(A, 20, 2 * power + 2, P.GaussianStream(7)))
+        assert np.linalg.norm(s1.Q @ s1.B - s2.Q @ s2.B) / norm <= 1e-6
+        assert np.linalg.norm(s1.Q @ s1.Q.T - s2.Q @ s2.Q.T) <= 1e-6
+
+
+def test_error_indicator_equals_explicit_residual(P):
+    import inputs
+    rng = np.random.default_rng(99)
+    worst = 0.0
+    for trial in range(8):
+        m, n = int(rng.integers(60, 400)), int(rng.integers(60, 400))
+        dense, M = inputs.rand_sparse(m, n, float(rng.uniform(0.02, 0.2)), 1000 + trial)
+        A = P.SparseRatings(M, 0.5, 5.0)
+        frob = float(np.sum(dense * dense))
+        for st in P.qb_power_blocks(A, int(rng.integers(10, 31)), trial % 2, P.GaussianStream(trial)):
+            explicit = np.linalg.norm(dense - st.Q @ st.B) ** 2
+            worst = max(worst, abs(st.err - explicit) / frob)
+            if st.blocks >= 4:
+                break
+    assert worst <= 1e-8
+
+
+def test_exact_rank_matrices_reconstructed_by_all_drivers(P):
+    import inputs
+    worst = 0.0
+    for r in (3, 7, 10):
+        dense, M = inputs.exact_rank(100, 80, r, 200 + r)
+        A = P.SparseRatings(M, float(dense.min()), float(dense.max()))
+        norm = np.linalg.norm(dense)
+        t = P.basic_rsvd(A, k=r, power=1, seed=r)
+        worst = max(worst, np.linalg.norm(dense - t.reconstruct()) / norm)
+        st = P.fixed_precision_qb(A, tol=1e-6, block_size=20, power=0, seed=r)
+        worst = max(worst, np.linalg.norm(dense - st.Q @ st.B) / norm)
+        tri = P.adaptive_pca(A, P.FrobTolerance(1e-6), block_size=20, passes=10, seed=r)
+        worst = max(worst, np.linalg.norm(dense - tri.reconstruct()) / norm)
+    assert worst <= 1e-8
