@@ -206,6 +206,8 @@ class _Samples:
     """Held-out (user, item, rating) triples, user-grouped, on the device."""
 
     def __init__(self, samples, device):
+        if hasattr(samples, "arrays") and not callable(samples.arrays):  # data.SampleList
+            samples = samples.arrays
         if isinstance(samples, tuple) and len(samples) == 3 and hasattr(samples[0], "__len__") and \
                 not isinstance(samples[0], (int, np.integer)):
             u = np.asarray(samples[0], dtype=np.int64)

@@ -55,3 +55,32 @@ def group_model(m, n, r, density, seed, holdout=0.1):
         return oi[idx].astype(np.int64), oj[idx].astype(np.int64), full[oi[idx], oj[idx]].astype(np.float64)
 
     return train, part(va), part(te)
+
+
+def ratings_csv_text(seed, nrows, nusers=60, nitems=40, delimiter=",", header=True, dup_frac=0.1):
+    """A delimited ratings file as text: string identifiers with stray
+    whitespace, half-star ratings, repeated (user, item) pairs."""
+    rng = np.random.default_rng(seed)
+    u = rng.integers(0, nusers, nrows)
+    i = rng.integers(0, nitems, nrows)
+    dup = rng.random(nrows) < dup_frac
+    src = rng.integers(0, max(nrows, 1), nrows)
+    u = np.where(dup, u[src], u)
+    i = np.where(dup, i[src], i)
+    r = rng.integers(1, 11, nrows) * 0.5
+    lines = ["userId{0}movieId{0}rating{0}timestamp".format(delimiter)] if header else []
+    for a, b, c in zip(u, i, r):
+        pad = " " if (a + b) % 7 == 0 else ""
+        lines.append(f"{pad}u{a}{delimiter}m{b}{pad}{delimiter}{c}{delimiter}1700000000")
+        if (a * 31 + b) % 97 == 0:
+            lines.append("")  # blank lines are skipped
+    return "\n".join(lines) + "\n"
+
+
+def matrix_market_text(seed, m, n, nnz, field="real"):
+    rng = np.random.default_rng(seed)
+    cells = rng.choice(m * n, size=nnz, replace=False)
+    vals = rng.integers(1, 11, nnz) * (0.5 if field == "real" else 1)
+    body = [f"{c // n + 1} {c % n + 1} {v if field == 'real' else int(v)}" for c, v in zip(cells, vals)]
+    return "\n".join([f"%%MatrixMarket matrix coordinate {field} general", "% a comment", f"{m} {n} {nnz}"]
+                     + body) + "\n"
