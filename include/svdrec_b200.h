@@ -148,6 +148,23 @@ size_t svdrec_orth_workspace_bytes(int64_t r, int32_t b);
 int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
                 void* d_work, size_t work_bytes, void* stream);
 
+/* Row-sharded CholeskyQR building blocks (the multi-GPU engine's
+ * orthonormalisation; no single reference function -- together they replace
+ * orthonormal_basis, linalg.py:54-81, and lu_lower_basis, linalg.py:84-97,
+ * when the rows of the block are spread over ranks).  svdrec_gram writes
+ * the full symmetric b x b Gram Y.T Y of this rank's r rows (fixed-order
+ * sum; r may be 0); the caller all-reduces it over the ranks;
+ * svdrec_chol_apply factors R = chol(G + shift_rel * trace(G) * I) (upper)
+ * and writes Q = Y R^-1 for this rank's rows (Q may alias Y).  A
+ * non-positive pivot sets SVDREC_STATUS_ZERO_PIVOT in d_status.  b <= 64. */
+size_t svdrec_gram_workspace_bytes(int64_t r, int32_t b);
+int svdrec_gram(int64_t r, int32_t b, const double* d_Y, int64_t ldy, double* d_G, void* d_work,
+                size_t work_bytes, void* stream);
+size_t svdrec_chol_apply_workspace_bytes(int32_t b);
+int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_t ldg, double shift_rel,
+                      const double* d_Y, int64_t ldy, double* d_Q, int64_t ldq, uint32_t* d_status,
+                      void* d_work, size_t work_bytes, void* stream);
+
 /* ---------------------------------------------------------------------
  * lu_lower_basis (linalg.py:84-97): partial-pivoting LU of the tall
  * r x b block, in place, returning P.L (original row order, unit

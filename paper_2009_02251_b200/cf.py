@@ -25,6 +25,7 @@ import torch
 from . import kernels as K
 from ._lib import STATUS_NEAR_SINGULAR, STATUS_NS_CHECK
 from .linalg import EIG_FLOOR, GaussianStream, NearSingularError
+from .parallel import ShardedRatings, local_samples
 from .rsvd import QbState, RankExhaustedError, qb_pass_blocks
 from .sparse import SparseRatings
 
@@ -323,6 +324,8 @@ def mae(predictions: Sequence[float], truths: Sequence[float]) -> float:
 def _errors(A, factors, s: _Samples):
     if A.nnz == 0:
         raise ValueError("cannot take the mean of a matrix with no ratings")
+    if isinstance(A, ShardedRatings):
+        return _sharded_errors(A, factors, s)
     if s.n == 0:
         raise ValueError("cannot average zero errors")
     val, _, _ = _predict_device(A, factors, s, A.device(factors.Xn.device).global_mean)
@@ -330,14 +333,63 @@ def _errors(A, factors, s: _Samples):
     return float(e[0] / s.n), float(np.sqrt(e[1] / s.n))
 
 
+def _shard_samples(A: ShardedRatings, samples, device) -> _Samples:
+    """This rank's held-out triples (users re-based to the shard), after
+    the bounds check against the global shape; ``n_total`` counts all ranks."""
+    u, i, r = local_samples(samples, 0, A.m)  # all of them, as arrays
+    if u.size != _count(samples):
+        raise ValueError("sample outside matrix bounds")
+    bad = (i < 0) | (i >= A.n)
+    if bad.any():
+        j = int(np.flatnonzero(bad)[0])
+        raise ValueError(f"sample ({u[j]}, {i[j]}) outside matrix bounds")
+    keep = (u >= A.row0) & (u < A.row1)
+    s = _Samples((u[keep] - A.row0, i[keep], r[keep]), device)
+    s.n_total = int(u.size)
+    s._checked.add(A.local.shape)
+    return s
+
+
+def _count(samples) -> int:
+    if hasattr(samples, "arrays") and not callable(samples.arrays):
+        samples = samples.arrays
+    if isinstance(samples, tuple) and len(samples) == 3 and hasattr(samples[0], "__len__"):
+        return len(samples[0])
+    return len(list(samples))
+
+
+def _local_err_sums(A: ShardedRatings, factors, s: _Samples, out: torch.Tensor) -> torch.Tensor:
+    """(sum |e|, sum e^2) over this rank's samples, then all-reduced."""
+    if s.n:
+        val, _, _ = _predict_device(A.local, factors, s, A.global_mean)
+        K.err_sum(val, s.truth, out=out)
+    else:
+        out.zero_()
+    return A.comm.all_reduce_(out)
+
+
+def _sharded_errors(A: ShardedRatings, factors, s):
+    dev = factors.Xn.device
+    if not isinstance(s, _Samples) or not hasattr(s, "n_total"):
+        s = _shard_samples(A, s, dev)
+    if s.n_total == 0:
+        raise ValueError("cannot average zero errors")
+    e = _local_err_sums(A, factors, s, torch.zeros(2, dtype=F64, device=dev)).cpu().numpy()
+    return float(e[0] / s.n_total), float(np.sqrt(e[1] / s.n_total))
+
+
 def evaluate_mae(A: SparseRatings, factors: LatentFactors, samples: Iterable) -> float:
     """MAE of clamped predictions over held-out triples (cf.py:178-190)."""
+    if isinstance(A, ShardedRatings):
+        return _errors(A, factors, samples)[0]
     s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Xn.device)
     return _errors(A, factors, s)[0]
 
 
 def evaluate_errors(A: SparseRatings, factors: LatentFactors, samples) -> tuple[float, float]:
     """(MAE, RMSE) of clamped Alg. 4 predictions (RMSE: BASELINE metric)."""
+    if isinstance(A, ShardedRatings):
+        return _errors(A, factors, samples)
     s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Xn.device)
     return _errors(A, factors, s)
 
@@ -359,20 +411,32 @@ class ValidationMae:
         if min_improvement < 0.0:
             raise ValueError("min_improvement must be nonnegative")
         dev = torch.device("cuda", torch.cuda.current_device())
-        s = validation if isinstance(validation, _Samples) else _Samples(validation, dev)
-        if s.n == 0:
-            raise ValueError("validation set is empty")
-        s.check_bounds(train)
+        self.shard = train if isinstance(train, ShardedRatings) else None
+        if self.shard is not None:
+            s = validation if isinstance(validation, _Samples) and hasattr(validation, "n_total") else \
+                _shard_samples(train, validation, dev)
+            if s.n_total == 0:
+                raise ValueError("validation set is empty")
+            train = train.local
+        else:
+            s = validation if isinstance(validation, _Samples) else _Samples(validation, dev)
+            if s.n == 0:
+                raise ValueError("validation set is empty")
+            s.check_bounds(train)
         d = train.device(dev)
         hit = s._overlap.get(id(train))
         if hit is None:
-            hit = s._overlap[id(train)] = (train, int(K.count_overlap(s.users, s.items, d.A).item()))
+            c = K.count_overlap(s.users, s.items, d.A).to(F64) if s.n else torch.zeros(1, dtype=F64, device=dev)
+            if self.shard is not None:
+                c = self.shard.comm.all_reduce_(c.reshape(1).clone())
+            hit = s._overlap[id(train)] = (train, int(c.item()))
         cnt = hit[1]
         if cnt:
             raise ValueError(f"{cnt} validation samples are present in the training matrix")
-        if train.nnz == 0:
+        if (self.shard or train).nnz == 0:
             raise ValueError("cannot take the mean of a matrix with no ratings")
-        self.train = train
+        self.train = train  # this rank's rows when sharded
+        self.n_total = s.n_total if self.shard is not None else s.n
         self.samples = s
         self.patience = patience
         self.min_improvement = min_improvement
@@ -385,7 +449,7 @@ class ValidationMae:
         self._G = None
         self._Gsrc = None
         self._mb = K.Mailbox(dev, sums=("f8", 2), status=("u4", 1), iters=("u4", 1))
-        self._gmean = d.global_mean
+        self._gmean = self.shard.global_mean if self.shard is not None else d.global_mean
         # scoring stream: the caller's unless pipelining; one cached side
         # stream per device (a fresh stream per call would defeat the caching
         # allocator, whose free blocks are tied to the stream they served)
@@ -430,8 +494,11 @@ class ValidationMae:
             Z = K.inv_sqrt(G, mb["status"], mb["iters"])
             factors = LatentFactors.from_qb_metric(Bt, G, Z)
             s = self.samples
-            val, _, _ = _predict_device(self.train, factors, s, self._gmean)
-            K.err_sum(val, s.truth, out=mb["sums"])
+            if self.shard is not None:
+                _local_err_sums(self.shard, factors, s, mb["sums"])
+            else:
+                val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+                K.err_sum(val, s.truth, out=mb["sums"])
             mb.read_async()
         return state, factors
 
@@ -454,9 +521,14 @@ class ValidationMae:
             # exactly like the reference (eigh) and score with its T
             with torch.cuda.stream(self._stream):
                 factors = LatentFactors(_eig_T(state.Bt_device, factors._G))
-                val, _, _ = _predict_device(self.train, factors, s, self._gmean)
-                got = {"sums": K.err_sum(val, s.truth).cpu().numpy()}
-        score, rmse = float(got["sums"][0] / s.n), float(np.sqrt(got["sums"][1] / s.n))
+                if self.shard is not None:
+                    sums = _local_err_sums(self.shard, factors, s, torch.zeros(2, dtype=F64, device=s.device))
+                else:
+                    val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+                    sums = K.err_sum(val, s.truth)
+                got = {"sums": sums.cpu().numpy()}
+        n = self.n_total
+        score, rmse = float(got["sums"][0] / n), float(np.sqrt(got["sums"][1] / n))
         self.trace.append(BlockEval(k=state.rank, mae=score, seconds=time.perf_counter() - self._start))
         if score < self.best_mae - self.min_improvement:
             self._stale = 0

@@ -435,7 +435,7 @@ __global__ void k_pairs_reduce(int npairs, int nparts, const double* __restrict_
 // runs.  R^-1 is built in the strict lower triangle of G (column c by
 // thread c).  Whole CTA; G, dinv, bad in shared memory.
 __device__ void chol_inv_smem(int b, double (*G)[65], double* dinv, int* bad, double* __restrict__ Rinv,
-                              uint32_t* __restrict__ flag) {
+                              uint32_t* __restrict__ flag, uint32_t* __restrict__ zero_flag = nullptr) {
   if (threadIdx.x == 0) *bad = 0;
   __syncthreads();
   double dmax = 0.0, dmin = 1e300;
@@ -460,6 +460,7 @@ __device__ void chol_inv_smem(int b, double (*G)[65], double* dinv, int* bad, do
     dmin = fmin(dmin, rjj);
   }
   if (threadIdx.x == 0 && (*bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
+  if (threadIdx.x == 0 && zero_flag && *bad) atomicOr(zero_flag, 1u);
   const int c = threadIdx.x;
   if (c < b) {
     for (int i = c - 1; i >= 0; --i) {
@@ -521,7 +522,7 @@ __device__ __forceinline__ void dmma_cq(double (&d)[2], double a, double b) {
 //    barriers at all.
 // Same flag rule as chol_inv_smem.  G: upper triangle in, destroyed.
 __device__ void chol_inv_cta(int b, double (*G)[65], double* dinv, double* __restrict__ Rinv,
-                             uint32_t* __restrict__ flag) {
+                             uint32_t* __restrict__ flag, uint32_t* __restrict__ zero_flag = nullptr) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   bool bad = false;
@@ -552,6 +553,7 @@ __device__ void chol_inv_cta(int b, double (*G)[65], double* dinv, double* __res
     __syncthreads();
   }
   if (tid == 0 && (bad || dmin * dmin < 1e-12 * dmax * dmax)) atomicOr(flag, 1u);
+  if (tid == 0 && zero_flag && bad) atomicOr(zero_flag, 1u);  // every thread saw the same pivots
   // X = R^-1, column c: x_c = 1/R_cc, x_i = -(sum_{t=i+1..c} R_it x_t) / R_ii
   for (int c = warp; c < b; c += nwarps) {
     double xl = lane == c ? dinv[c] : 0.0;  // x_lane
@@ -569,7 +571,7 @@ template <int NT>
 __global__ void __launch_bounds__(kCqrThreads) k_cqr_gram(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
                                                           double* __restrict__ part, double* __restrict__ gpart,
                                                           unsigned* __restrict__ tickets, double* __restrict__ Rinv,
-                                                          uint32_t* __restrict__ flag) {
+                                                          uint32_t* __restrict__ flag, double* __restrict__ Gout) {
   constexpr int BP = 8 * NT, E = BP * BP;  // padded width, entries per partial
   __shared__ double red[NT * NT * 2 * 32];
   __shared__ double G[64][65];
@@ -669,6 +671,13 @@ __global__ void __launch_bounds__(kCqrThreads) k_cqr_gram(int64_t r, int b, cons
   }
   if (threadIdx.x == 0) tickets[0] = 0u;
   __syncthreads();
+  if (Gout) {  // Gram only (row-sharded CholeskyQR: the caller all-reduces it)
+    for (int t = threadIdx.x; t < b * b; t += kCqrThreads) {
+      const int i = t / b, j = t - i * b;
+      Gout[t] = i <= j ? G[i][j] : G[j][i];
+    }
+    return;
+  }
   chol_inv_cta(b, G, dinv, Rinv, flag);
 }
 
@@ -825,7 +834,7 @@ int cqr_pass_nt(int64_t r, int b, const double* Y, int64_t ldy, double* out, int
   double* part = reinterpret_cast<double*>(w + L.off_cqr);
   double* gpart = part + nc * (8 * NT) * (8 * NT);
   unsigned* tickets = reinterpret_cast<unsigned*>(w + L.off_tickets);
-  k_cqr_gram<NT><<<(unsigned)nc, kCqrThreads, 0, s>>>(r, b, Y, ldy, part, gpart, tickets, rinv, flag);
+  k_cqr_gram<NT><<<(unsigned)nc, kCqrThreads, 0, s>>>(r, b, Y, ldy, part, gpart, tickets, rinv, flag, nullptr);
   const int64_t tiles = (r + 15) / 16;
   int64_t grid = (tiles + 7) / 8;
   const int64_t cap = (int64_t)sm_count() * 8;
@@ -863,6 +872,108 @@ int cholqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int
   k_trapply<<<(unsigned)((r + kApplyRows - 1) / kApplyRows), kApplyRows, smem, s>>>(r, b, Y, ldy, rinv, out, ldo,
                                                                                      flag, only_if_clear);
   return check_launch("cholqr_pass", 4);
+}
+
+
+// ---- Row-sharded CholeskyQR building blocks --------------------------------
+// A rank holding rows [r0, r1) of a tall block Y computes its Gram partial
+// (svdrec_gram), the caller all-reduces the b x b partials, and every rank
+// factors the same G and applies R^-1 to its own rows (svdrec_chol_apply).
+
+// pairs (upper triangle, packed) -> full symmetric b x b
+__global__ void k_pairs_full(int b, const double* __restrict__ pairs, double* __restrict__ G) {
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+    int i = t / b, j = t - i * b;
+    if (i > j) { const int x = i; i = j; j = x; }
+    G[t] = pairs[i * b - i * (i - 1) / 2 + (j - i)];
+  }
+}
+
+// R = chol(G + shift_rel * trace(G) * I) (upper), Rinv = R^-1; one CTA.
+// flag |= 1 as in the CholeskyQR2 path (kappa > 1e6 or a bad pivot);
+// zero_flag |= 1 on a non-positive pivot (the caller's status word).
+__global__ void __launch_bounds__(kCqrThreads) k_chol_full(int b, const double* __restrict__ G, int64_t ldg,
+                                                           double shift_rel, double* __restrict__ Rinv,
+                                                           uint32_t* __restrict__ flag,
+                                                           uint32_t* __restrict__ zero_flag) {
+  __shared__ double Gs[64][65];
+  __shared__ double dinv[64];
+  __shared__ int bad;
+  __shared__ double shift;
+  if (threadIdx.x < 32) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < b; i += 32) t += G[i * ldg + i];
+    t = warp_sum(t);
+    if (threadIdx.x == 0) shift = shift_rel * t;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+    const int i = t / b, j = t - i * b;
+    if (i <= j) Gs[i][j] = G[i * ldg + j] + (i == j ? shift : 0.0);
+  }
+  __syncthreads();
+  if (b <= 32)
+    chol_inv_cta(b, Gs, dinv, Rinv, flag, zero_flag);
+  else
+    chol_inv_smem(b, Gs, dinv, &bad, Rinv, flag, zero_flag);
+}
+
+struct GramLayout {
+  size_t off_tickets, off_part, off_pairs, total;
+  int nparts;
+  int64_t rows_per;
+};
+
+GramLayout gram_layout(int64_t r, int b) {
+  GramLayout L{};
+  size_t o = 0;
+  L.off_tickets = o;
+  o = align_up(o + (size_t)(2 + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 4);
+  L.nparts = 2 * sm_count();
+  L.rows_per = (r + L.nparts - 1) / L.nparts;
+  if (L.rows_per < kGramRows) {
+    L.rows_per = kGramRows;
+    L.nparts = (int)((r + kGramRows - 1) / kGramRows);
+  }
+  L.off_part = o;
+  const size_t dmma = (size_t)(cqr_ctas(r) + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 32 * 32 * 8;
+  const size_t pairs = (size_t)L.nparts * (b * (b + 1) / 2) * 8;
+  o = align_up(o + (b <= 32 ? dmma : pairs));
+  L.off_pairs = o;
+  o = align_up(o + (size_t)b * (b + 1) / 2 * 8);
+  L.total = o;
+  return L;
+}
+
+template <int NT>
+void gram_nt(int64_t r, int b, const double* Y, int64_t ldy, double* G, const GramLayout& L, char* w, cudaStream_t s) {
+  const int64_t nc = cqr_ctas(r);
+  double* part = reinterpret_cast<double*>(w + L.off_part);
+  double* gpart = part + nc * (8 * NT) * (8 * NT);
+  unsigned* tickets = reinterpret_cast<unsigned*>(w + L.off_tickets);
+  k_cqr_gram<NT><<<(unsigned)nc, kCqrThreads, 0, s>>>(r, b, Y, ldy, part, gpart, tickets, nullptr, nullptr, G);
+}
+
+void trapply_launch(int64_t r, int b, const double* Y, int64_t ldy, const double* rinv, double* out, int64_t ldo,
+                    const uint32_t* flag, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_trapply, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    attr = true;
+  }
+  const size_t smem = ((size_t)kApplyRows * (b | 1) + (size_t)b * b) * 8;
+  k_trapply<<<(unsigned)((r + kApplyRows - 1) / kApplyRows), kApplyRows, smem, s>>>(r, b, Y, ldy, rinv, out, ldo,
+                                                                                   flag, 0);
+}
+
+template <int NT>
+void cqr_apply_launch(int64_t r, int b, const double* Y, int64_t ldy, const double* rinv, double* out, int64_t ldo,
+                      const uint32_t* flag, cudaStream_t s) {
+  const int64_t tiles = (r + 15) / 16;
+  int64_t grid = (tiles + 7) / 8;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (grid > cap) grid = cap;
+  k_cqr_apply<NT><<<(unsigned)grid, 256, 0, s>>>(r, b, Y, ldy, rinv, out, ldo, flag, 0);
 }
 
 }  // namespace
@@ -920,4 +1031,78 @@ extern "C" int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda,
   // fallback: Householder TSQR from the untouched input, only if flagged
   double* dummy_r = reinterpret_cast<double*>(w + L.off_rinv);
   return run_tsqr_gated(make_plan(r, b), r, b, d_A, lda, d_Q, ldq, dummy_r, w + L.off_tsqr, flag, s);
+}
+
+extern "C" size_t svdrec_gram_workspace_bytes(int64_t r, int32_t b) {
+  if (b < 1 || b > 64 || r < 0) return 256;
+  return svdrec::gram_layout(r, b).total + 256;
+}
+
+extern "C" int svdrec_gram(int64_t r, int32_t b, const double* d_Y, int64_t ldy, double* d_G, void* d_work,
+                           size_t work_bytes, void* stream) {
+  using namespace svdrec;
+  SVDREC_ARG(b >= 1 && b <= 64, "gram: block width %d outside [1, 64]", b);
+  SVDREC_ARG(r >= 0 && (r == 0 || ldy >= b), "gram: bad shape or leading dimension");
+  cudaStream_t s = as_stream(stream);
+  if (r == 0) {
+    SVDREC_CUDA(cudaMemsetAsync(d_G, 0, (size_t)b * b * 8, s));
+    return 0;
+  }
+  const GramLayout L = gram_layout(r, b);
+  if (work_bytes < L.total) {
+    set_error("gram: workspace %zu < %zu", work_bytes, L.total);
+    return SVDREC_E_WORKSPACE;
+  }
+  char* w = static_cast<char*>(d_work);
+  if (b <= 32) {
+    SVDREC_CUDA(cudaMemsetAsync(w + L.off_tickets, 0, (size_t)(2 + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 4, s));
+    switch ((b + 7) / 8) {
+      case 1: gram_nt<1>(r, b, d_Y, ldy, d_G, L, w, s); break;
+      case 2: gram_nt<2>(r, b, d_Y, ldy, d_G, L, w, s); break;
+      case 3: gram_nt<3>(r, b, d_Y, ldy, d_G, L, w, s); break;
+      default: gram_nt<4>(r, b, d_Y, ldy, d_G, L, w, s); break;
+    }
+    return check_launch("gram", 1);
+  }
+  double* part = reinterpret_cast<double*>(w + L.off_part);
+  double* pairs = reinterpret_cast<double*>(w + L.off_pairs);
+  const int npairs = b * (b + 1) / 2;
+  k_gram_part<<<(unsigned)L.nparts, 256, 0, s>>>(r, b, d_Y, ldy, L.rows_per, part);
+  k_pairs_reduce<<<(unsigned)((npairs * 32 + 255) / 256), 256, 0, s>>>(npairs, L.nparts, part, pairs);
+  k_pairs_full<<<1, 256, 0, s>>>(b, pairs, d_G);
+  return check_launch("gram", 3);
+}
+
+extern "C" size_t svdrec_chol_apply_workspace_bytes(int32_t b) {
+  if (b < 1 || b > 64) return 256;
+  return svdrec::align_up(16) + svdrec::align_up((size_t)b * b * 8) + 256;
+}
+
+extern "C" int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_t ldg, double shift_rel,
+                                 const double* d_Y, int64_t ldy, double* d_Q, int64_t ldq, uint32_t* d_status,
+                                 void* d_work, size_t work_bytes, void* stream) {
+  using namespace svdrec;
+  SVDREC_ARG(b >= 1 && b <= 64, "chol_apply: block width %d outside [1, 64]", b);
+  SVDREC_ARG(r >= 0 && ldg >= b && (r == 0 || (ldy >= b && ldq >= b)), "chol_apply: bad shape or leading dimension");
+  SVDREC_ARG(shift_rel >= 0.0, "chol_apply: negative shift");
+  const size_t need = align_up(16) + align_up((size_t)b * b * 8);
+  if (work_bytes < need) {
+    set_error("chol_apply: workspace %zu < %zu", work_bytes, need);
+    return SVDREC_E_WORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  char* w = static_cast<char*>(d_work);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(w);
+  double* rinv = reinterpret_cast<double*>(w + align_up(16));
+  SVDREC_CUDA(cudaMemsetAsync(flag, 0, 16, s));
+  k_chol_full<<<1, kCqrThreads, 0, s>>>(b, d_G, ldg, shift_rel, rinv, flag, d_status);
+  if (r == 0) return check_launch("chol_apply", 1);
+  switch ((b + 7) / 8) {
+    case 1: cqr_apply_launch<1>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
+    case 2: cqr_apply_launch<2>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
+    case 3: cqr_apply_launch<3>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
+    case 4: cqr_apply_launch<4>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
+    default: trapply_launch(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
+  }
+  return check_launch("chol_apply", 2);
 }

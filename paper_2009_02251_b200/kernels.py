@@ -222,6 +222,49 @@ def orth(A: torch.Tensor, Q: torch.Tensor | None = None) -> torch.Tensor:
     return Q
 
 
+def gram(Y: torch.Tensor, G: torch.Tensor | None = None) -> torch.Tensor:
+    """Full symmetric b x b Gram Y.T Y of (this rank's rows of) Y."""
+    r, b = Y.shape
+    ldy = _mat(Y, "gram.Y") if r else b
+    if G is None:
+        G = torch.empty(b, b, dtype=F64, device=Y.device)
+    ws, nb = scratch(Y.device).get(query("svdrec_gram_workspace_bytes", r, b))
+    with _span("gram", r * b * 8):
+        call("svdrec_gram", r, b, ptr(Y) if r else None, ldy, ptr(G), ws, nb, stream_handle())
+    return G
+
+
+def chol_apply(G: torch.Tensor, Y: torch.Tensor, Q: torch.Tensor | None = None, shift_rel: float = 0.0,
+               status: torch.Tensor | None = None) -> torch.Tensor:
+    """Q = Y R^-1 with R = chol(G + shift_rel trace(G) I); Q may alias Y."""
+    r, b = Y.shape
+    if Q is None:
+        Q = torch.empty(r, b, dtype=F64, device=Y.device)
+    ldy = _mat(Y, "chol_apply.Y") if r else b
+    ldq = _mat(Q, "chol_apply.Q") if r else b
+    ldg = _mat(G, "chol_apply.G")
+    if status is None:
+        status = _orth_status(Y.device)
+    ws, nb = scratch(Y.device).get(query("svdrec_chol_apply_workspace_bytes", b))
+    with _span("chol_apply", 2 * r * b * 8):
+        call("svdrec_chol_apply", r, b, ptr(G), ldg, float(shift_rel), ptr(Y) if r else None, ldy,
+             ptr(Q) if r else None, ldq, ptr(status), ws, nb, stream_handle())
+    return Q
+
+
+_ORTH_STATUS: dict = {}
+
+
+def _orth_status(device) -> torch.Tensor:
+    """Discarded status word for orthonormalisation calls (Householder QR
+    in the reference never fails on rank deficiency)."""
+    key = torch.device(device).index
+    st = _ORTH_STATUS.get(key)
+    if st is None:
+        st = _ORTH_STATUS[key] = new_status(device)
+    return st
+
+
 def lu_lower(A: torch.Tensor, status: torch.Tensor, udiag: torch.Tensor | None = None) -> torch.Tensor:
     """In-place P.L of partial-pivoting LU; returns U's diagonal (device)."""
     lda = _mat(A, "lu.A")

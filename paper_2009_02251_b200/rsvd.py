@@ -25,6 +25,7 @@ from . import kernels as K
 from ._lib import STATUS_NEAR_SINGULAR, STATUS_STREAM_SHORT, STATUS_ZERO_PIVOT
 from .linalg import (EIG_FLOOR, GaussianStream, NearSingularError, RankDeficientError, SvdTriplet, _check_rank,
                      sparse_dense_mul)
+from .parallel import ShardedRatings, sharded_orth
 from .sparse import SparseRatings
 
 F64 = torch.float64
@@ -133,14 +134,22 @@ TerminationCriterion = Callable[[QbState], bool]
 class _QbEngine:
     """Device state of one growing QB factorization."""
 
-    def __init__(self, A: SparseRatings, b: int, stream: GaussianStream, cap: int):
+    @staticmethod
+    def create(A, b: int, stream: GaussianStream, cap: int) -> "_QbEngine":
+        if isinstance(A, ShardedRatings) and A.world > 1:
+            return _ShardedQbEngine(A, b, stream, cap)
+        return _QbEngine(A.local if isinstance(A, ShardedRatings) else A, b, stream, cap)
+
+    def __init__(self, A: SparseRatings, b: int, stream: GaussianStream, cap: int, global_m: int | None = None,
+                 frob_sq: float | None = None):
         self.A = A
         self.dev = stream.device
         self.d = A.device(self.dev)
-        self.m, self.n = A.shape
+        self.m, self.n = A.shape  # rows held here (all of them unless sharded)
+        self.gm = self.m if global_m is None else int(global_m)
         self.b = b
         self.stream = stream
-        cap = max(b, min(cap, min(self.m, self.n)))
+        cap = max(b, min(cap, min(self.gm, self.n)))
         self.cap = cap
         self.Q = torch.empty(self.m, self._alloc_cols(0), dtype=F64, device=self.dev)
         self.Bt = torch.empty(self.n, self._alloc_cols(0), dtype=F64, device=self.dev)
@@ -152,7 +161,7 @@ class _QbEngine:
         # flags of the block's LU / sketch draws), copied back asynchronously
         # and parsed only when someone needs err / row energies / errors
         self._new_mailbox()
-        self.frob = self.d.frob_sq if A.nnz else 0.0
+        self.frob = (self.d.frob_sq if A.nnz else 0.0) if frob_sq is None else float(frob_sq)
         self.err = self.frob
         self.errs: list[float] = []
         self.blocks = 0
@@ -249,13 +258,54 @@ class _QbEngine:
                        None, engine=self)
 
 
+class _ShardedQbEngine(_QbEngine):
+    """QB engine over a row-sharded matrix (parallel.py): this rank holds
+    rows [row0, row1) of A and Q; the item side (sketches of n rows, B.T)
+    is replicated.  Exchanges: all-reduce of A.T products (n x b), of
+    Q.T Y (k x b) and of the b x b Grams of the sharded CholeskyQR."""
+
+    def __init__(self, A: ShardedRatings, b: int, stream: GaussianStream, cap: int):
+        super().__init__(A.local, b, stream, cap, global_m=A.m, frob_sq=A.frob_sq)
+        self.shard = A
+        self.comm = A.comm
+
+    def AT_mul(self, X, out):
+        sparse_dense_mul(self.A, X, True, out=out)
+        return self.comm.all_reduce_(out)
+
+    def minus_BtQtX(self, Y, X):
+        if self.K:
+            C = self.comm.all_reduce_(K.gemm_tn(self.Q[:, : self.K], X))
+            K.gemm_nn(self.Bt[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
+
+    def minus_QQtX(self, Y):
+        if self.K:
+            C = self.comm.all_reduce_(K.gemm_tn(self.Q[:, : self.K], Y))
+            K.gemm_nn(self.Q[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
+
+    def lu(self, Y):
+        # Y U^-1 with U upper triangular, like the reference's P.L: the
+        # block's final Q is the same up to column signs (parallel.py)
+        sharded_orth(Y, Y, self.comm, self.gm, passes=2, status=self.status)
+
+    def orth_into(self, Y, dst):
+        sharded_orth(Y, dst, self.comm, self.gm, passes=3)
+
+    def normal(self, rows: int, cols: int, out):
+        if out.shape[0] == rows:  # item-side draw: replicated
+            return self.stream.normal_device(rows, cols, out=out, status=self.status)
+        full = self.stream.normal_device(rows, cols, status=self.status)  # same stream on every rank
+        out.copy_(full[self.shard.row0: self.shard.row1])
+        return out
+
+
 def qb_power_blocks(A: SparseRatings, block_size: int, power: int, stream: GaussianStream,
                     max_rank: int | None = None) -> Iterator[QbState]:
     """Alg. 2 block generator with power iteration (rsvd.py:112-148)."""
     m, n = A.shape
     b = block_size
     cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
-    E = _QbEngine(A, b, stream, cap)
+    E = _QbEngine.create(A, b, stream, cap)
     while (E.blocks + 1) * b <= min(m, n):
         om = E.normal(n, b, E.yn)
         y = E.A_mul(om, E.ym)
@@ -280,7 +330,7 @@ def qb_pass_blocks(A: SparseRatings, block_size: int, passes: int, stream: Gauss
     if passes < 2:
         raise ValueError("passes must be at least 2")
     cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
-    E = _QbEngine(A, b, stream, cap)
+    E = _QbEngine.create(A, b, stream, cap)
     nsteps = (passes - 1) // 2
     while (E.blocks + 1) * b <= min(m, n) - b:
         if passes % 2 == 0:
@@ -357,9 +407,11 @@ def fixed_precision_qb(A: SparseRatings, tol: float, block_size: int = 20, power
         raise ValueError("power must be nonnegative")
     if block_size > min(A.shape):
         raise ValueError(f"block_size {block_size} exceeds min(m, n) = {min(A.shape)}")
-    if A.nnz == 0 or A.device().frob_sq == 0.0:
+    frob = A.frob_sq if isinstance(A, ShardedRatings) else (A.device().frob_sq if A.nnz else 0.0)
+    if A.nnz == 0 or frob == 0.0:
         dev = torch.device("cuda", torch.cuda.current_device())
-        return QbState(torch.empty(A.m, 0, dtype=F64, device=dev), torch.empty(A.n, 0, dtype=F64, device=dev),
+        rows = A.local.m if isinstance(A, ShardedRatings) else A.m
+        return QbState(torch.empty(rows, 0, dtype=F64, device=dev), torch.empty(A.n, 0, dtype=F64, device=dev),
                        0.0, 0, block_size, 0.0, np.empty(0))
     stream = GaussianStream(seed)
     last = None

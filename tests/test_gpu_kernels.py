@@ -172,3 +172,50 @@ def test_orth_cholqr2_and_fallback(gpu):
         # in place
         Q2 = K.orth(Md, Md).cpu().numpy()
         assert np.array_equal(Q2, Q)
+
+
+@pytest.mark.parametrize("r,b", [(0, 10), (5, 5), (1000, 10), (70001, 20), (3000, 32), (5000, 48), (9000, 64)])
+def test_gram_and_chol_apply(gpu, r, b):
+    """Row-sharded CholeskyQR blocks: Gram Y.T Y; Q = Y chol(G + s tr(G) I)^-1 (in place too)."""
+    import torch
+    from paper_2009_02251_b200 import kernels as K
+    rng = np.random.default_rng(r + b)
+    Yh = rng.standard_normal((r, b)) * np.logspace(0, -3, b)
+    Y = torch.from_numpy(Yh).cuda()
+    G = K.gram(Y)
+    Gh = Yh.T @ Yh
+    np.testing.assert_allclose(G.cpu().numpy(), Gh, rtol=1e-12, atol=1e-12 * max(np.trace(Gh), 1e-300))
+    if r == 0:
+        assert not G.abs().sum().item()
+        return
+    st = K.new_status(Y.device)
+    for shift in (0.0, 1e-10):
+        Q = K.chol_apply(G, Y, shift_rel=shift, status=st)
+        R = np.linalg.cholesky(Gh + shift * np.trace(Gh) * np.eye(b)).T
+        np.testing.assert_allclose(Q.cpu().numpy(), scipy.linalg.solve_triangular(R, Yh.T, trans="T").T,
+                                   rtol=1e-9, atol=1e-12)
+    Y2 = Y.clone()  # in place, strided destination
+    big = torch.zeros(r, b + 7, dtype=torch.float64, device=Y.device)
+    big[:, 3:3 + b] = Y
+    K.chol_apply(G, big[:, 3:3 + b], big[:, 3:3 + b])
+    K.chol_apply(G, Y2, Y2)
+    np.testing.assert_allclose(big[:, 3:3 + b].cpu().numpy(), Y2.cpu().numpy(), rtol=0, atol=0)
+    Qh = Y2.cpu().numpy()
+    assert np.linalg.norm(Qh.T @ Qh - np.eye(b)) < 1e-9
+    assert K.check_status(st) == 0
+    K.chol_apply(torch.zeros_like(G), Y, status=st)  # zero Gram: non-positive pivot flagged
+    assert K.check_status(st) & 1
+
+
+def test_sharded_orth_single_rank(gpu):
+    """shifted CholeskyQR3 on one rank: orthonormal, same span as Householder."""
+    import torch
+    from paper_2009_02251_b200 import kernels as K
+    from paper_2009_02251_b200.parallel import Comm, sharded_orth
+    rng = np.random.default_rng(3)
+    Yh = rng.standard_normal((20000, 20)) @ np.diag(np.logspace(0, -9, 20))
+    Y = torch.from_numpy(Yh).cuda()
+    Q = sharded_orth(Y, torch.empty_like(Y), Comm(), 20000).cpu().numpy()
+    assert np.linalg.norm(Q.T @ Q - np.eye(20)) < 1e-13
+    Qr = np.linalg.qr(Yh)[0]
+    np.testing.assert_allclose(np.abs(np.sum(Q * Qr, 0)), 1.0, atol=1e-6)
