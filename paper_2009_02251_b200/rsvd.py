@@ -235,13 +235,17 @@ class _QbEngine:
     def orth_into(self, Y, dst):
         K.orth(Y, dst)
 
+    def orth_final(self, Y, dst):
+        """Orthonormalisation of the block that is appended to Q."""
+        self.orth_into(Y, dst)
+
     def append(self, src):
         """Re-orthogonalise ``src`` against Q, append it and B_l = q.T A."""
         b, k0 = self.b, self.K
         self._ensure(k0 + b)
         self.minus_QQtX(src)
         qdst = self.Q[:, k0 : k0 + b]
-        self.orth_into(src, qdst)
+        self.orth_final(src, qdst)
         bdst = self.Bt[:, k0 : k0 + b]
         self.AT_mul(qdst, bdst)
         K.sumsq(bdst, self.mb["colsq"], self.mb["total"])
@@ -286,10 +290,16 @@ class _ShardedQbEngine(_QbEngine):
     def lu(self, Y):
         # Y U^-1 with U upper triangular, like the reference's P.L: the
         # block's final Q is the same up to column signs (parallel.py)
-        sharded_orth(Y, Y, self.comm, self.gm, passes=2, status=self.status)
+        # one shifted pass: a well-conditioned basis is all the next
+        # product needs
+        sharded_orth(Y, Y, self.comm, self.gm, passes=1, status=self.status)
 
     def orth_into(self, Y, dst):
-        sharded_orth(Y, dst, self.comm, self.gm, passes=3)
+        # intermediate bases (fed to a product, re-orthogonalised later)
+        sharded_orth(Y, dst, self.comm, self.gm, passes=2)
+
+    def orth_final(self, Y, dst):
+        sharded_orth(Y, dst, self.comm, self.gm, passes=3)  # shifted CholeskyQR3
 
     def normal(self, rows: int, cols: int, out):
         if out.shape[0] == rows:  # item-side draw: replicated
