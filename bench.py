@@ -232,6 +232,7 @@ def run_b200(args):
     import gc
     gc.collect()
     gc.freeze()
+    gc.disable()  # no collector pauses on the host while the GPU waits for it (re-enabled after timing)
     ck0 = clocks.mark()
     launches0 = lib.svdrec_launch_count()
     # the K steps are one timed region (total / K); per-step events inside
@@ -245,6 +246,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     times = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(args.steps)]
     launches = (lib.svdrec_launch_count() - launches0) // args.steps
+    gc.enable()
     ck = clocks.stop(ck0)
     t_step = ev[0].elapsed_time(ev[-1]) / 1e3 / args.steps
     # kernel breakdown from one extra, untimed step with per-call CUDA-event

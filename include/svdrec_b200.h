@@ -210,23 +210,28 @@ int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double
  *  svdrec_cf_normalize_pair: Xn = X / n, Yn = Y / n with n_l =
  *   sqrt(x_l.y_l) (zero rows where n_l = 0, the reference's skipped
  *   zero-norm items).
- *  svdrec_cf_predict: Alg. 4 (_predict, cf.py:108-143) for nsamp
- *   (user, item) pairs grouped by user: ``d_group_start`` (ngroups+1)
- *   offsets into the user-sorted samples.  Per user one warp forms
+ *  svdrec_cf_predict: Alg. 4 (_predict, cf.py:108-143) for held-out
+ *   (user, item) samples sorted by user.  Per user one warp forms
  *   P_u = sum_l A(u,l) Yn_l and S_u = sum_l Yn_l, then each sample's
  *   raw prediction is (Xn_j . P_u) / (Xn_j . S_u) with the |w| < 1e-9
  *   user-mean / global-mean fallback and clamping.  Writes clamped value,
- *   raw value and fallback flag per sample (in grouped order).  k <= 1024.
- *   d_hot_items (nullable) lists items by descending training degree and
- *   d_item_rank is its inverse; the first items whose Yn rows fit in
- *   ~200 KB of shared memory are staged on-chip in every CTA.  Warps fetch
- *   work items dynamically through d_counter (one device int32, reset
- *   here): d_work holds nwork (group, chunk) pairs, heaviest users first;
- *   d_ginfo holds per group (nchunks, first partial slot, done index).
- *   Users with more than ``chunk`` ratings are split across warps; each
- *   chunk stores (P, S, sum v) in d_partial ((2k+1) doubles per slot) and
- *   the warp completing the group (d_done counters, ndone of them, reset
- *   here) adds the slots in order and scores the group's samples.
+ *   raw value and fallback flag per sample (in sorted order).  k <= 1024.
+ *   The training CSR is passed RANKED: each item id replaced by its
+ *   popularity rank (svdrec_cf_relabel; 0 = most rated) and each row's
+ *   entries ordered by rank, with d_Yr the unit rows Yn in rank order
+ *   (Yr[rank(l)] = Yn[l]) plus one zero row at index n_items (the
+ *   padding target); d_Xn and d_norm stay indexed by item id, as do
+ *   the samples (d_items).  The first rows of Yr that fit in ~208 KB are
+ *   staged in every CTA's shared memory, so each user's hot ratings (a
+ *   prefix of the ranked row) read shared memory.  Work items -- a user,
+ *   or a <= 512-rating chunk of a heavy user -- are claimed dynamically
+ *   through d_counter (one device int32, reset here), heaviest first:
+ *   item w starts at CSR entry d_work_start[w] and d_work_meta[8w..8w+7]
+ *   = (length, user degree, first sample, end sample, chunks of the user,
+ *   partial slot or -1, completion counter, chunk index).  Chunks store
+ *   (P, S, sum v) in d_partial ((2k+1) doubles per slot) and the warp
+ *   completing the user (d_done counters, ndone of them, reset here) adds
+ *   the slots in order and scores the user's samples.
  *  svdrec_err_sum: fixed-order sum |pred - truth| and (pred-truth)^2.
  * ------------------------------------------------------------------- */
 int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int64_t ldt, double* d_Tn,
@@ -234,15 +239,18 @@ int svdrec_cf_normalize(int64_t n, int32_t k, const double* d_Tt, int64_t ldt, d
 int svdrec_cf_normalize_pair(int64_t n, int32_t k, const double* d_X, int64_t ldx,
                              const double* d_Y, int64_t ldy, double* d_Xn, double* d_Yn,
                              int64_t ldn, double* d_norm, void* stream);
-int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32_t* d_users,
-                      const int32_t* d_items, const int64_t* d_indptr,
-                      const int32_t* d_indices, const double* d_values, int32_t k,
-                      const double* d_Yn, const double* d_Xn, int64_t ldn, const double* d_norm,
-                      double global_mean, double rating_min, double rating_max,
-                      const int32_t* d_item_rank, const int32_t* d_hot_items, int32_t nhot_avail,
-                      int64_t nwork, const int32_t* d_work, const int32_t* d_ginfo, int32_t chunk,
-                      int32_t* d_done, int64_t ndone, double* d_partial, int32_t* d_counter,
-                      double* d_value, double* d_raw, uint8_t* d_fallback, void* stream);
+int svdrec_cf_predict(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
+                      const int32_t* d_items, const int32_t* d_ranked_indices,
+                      const double* d_ranked_values, int32_t k, const double* d_Yr, const double* d_Xn,
+                      int64_t ldn, const double* d_norm, double global_mean, double rating_min,
+                      double rating_max, int32_t n_items, int32_t* d_done, int64_t ndone,
+                      double* d_partial, int32_t* d_counter, double* d_value, double* d_raw,
+                      uint8_t* d_fallback, void* stream);
+/* Ranked CSR for svdrec_cf_predict: d_out[t] = d_rank[d_indices[t]] (item ->
+ * popularity rank, 0 = most rated); the caller then orders each row's
+ * entries by rank (ascending), so every user's hot items form a prefix. */
+int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,
+                      void* stream);
 
 /* G^(-1/2) of a k x k SPD Gram by coupled Newton-Schulz iteration (one
  * cooperative kernel, GEMM phases over the whole GPU).  Sets

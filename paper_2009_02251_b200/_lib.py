@@ -56,8 +56,9 @@ SIGNATURES = {
     "svdrec_gesvj": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _i64, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_cf_normalize": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p]),
     "svdrec_cf_normalize_pair": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p, _i64, _p, _p]),
-    "svdrec_cf_predict": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _i64, _p, _f64, _f64, _f64,
-                                    _p, _p, _i32, _i64, _p, _p, _i32, _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "svdrec_cf_predict": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p, _p, _i64, _p, _f64, _f64, _f64, _i32,
+                                    _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "svdrec_cf_relabel": (C.c_int, [_i64, _p, _p, _p, _p]),
     "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
     "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),
     "svdrec_err_sum_workspace_bytes": (_sz, [_i64]),

@@ -160,16 +160,25 @@ class WorkPlan:
 
     Groups (one per user with samples) are cut into chunks of at most
     ``CHUNK`` training ratings; items are ordered heaviest user first so the
-    dynamic scheduler never ends behind a long row.
+    dynamic scheduler never ends behind a long row.  Each item is described
+    up front (built on the device): ``start`` (its first CSR entry) and
+    ``meta`` = (length, user degree, first sample, end sample, chunks of the
+    user, partial slot, completion counter, chunk index) as int32.
     """
 
     CHUNK = 512
 
-    def __init__(self, group_deg: torch.Tensor, device):
-        """``group_deg``: training degree of each group's user (int64 tensor,
-        built and kept on ``device``)."""
+    def __init__(self, group_deg: torch.Tensor, device, group_start: torch.Tensor | None = None,
+                 row_start: torch.Tensor | None = None):
+        """``group_deg``: training degree of each group's user; ``group_start``
+        (ngroups + 1) sample offsets; ``row_start``: CSR offset of each
+        group's user row (all int64 tensors on ``device``)."""
         gd = torch.as_tensor(group_deg, device=device).to(torch.int64)
         ng = gd.numel()
+        if group_start is None:
+            group_start = torch.arange(ng + 1, device=device)
+        if row_start is None:
+            row_start = torch.cumsum(gd, 0) - gd
         nch = torch.clamp((gd + self.CHUNK - 1) // self.CHUNK, min=1)
         split = nch > 1
         cs = torch.cumsum(torch.where(split, nch, torch.zeros_like(nch)), 0)
@@ -181,10 +190,17 @@ class WorkPlan:
         first = torch.repeat_interleave(torch.cumsum(no, 0) - no, no)
         wc = torch.arange(wg.numel(), device=device) - first
         self.nwork = int(wg.numel())
-        self.work = torch.stack([wg, wc], 1).flatten().to(torch.int32) if self.nwork else \
-            torch.zeros(2, dtype=torch.int32, device=device)
-        self.ginfo = torch.stack([nch, slot0, done], 1).flatten().to(torch.int32) if ng else \
-            torch.zeros(3, dtype=torch.int32, device=device)
+        sp_w = split[wg]
+        deg_w = gd[wg]
+        off = torch.where(sp_w, wc * self.CHUNK, torch.zeros_like(wc))
+        self.start = (row_start.to(torch.int64)[wg] + off).contiguous() if self.nwork else \
+            torch.zeros(1, dtype=torch.int64, device=device)
+        length = torch.where(sp_w, torch.clamp(deg_w - off, max=self.CHUNK), deg_w)
+        gs = group_start.to(torch.int64)
+        meta = torch.stack([length, deg_w, gs[wg], gs[wg + 1], nch[wg],
+                            torch.where(sp_w, slot0[wg] + wc, torch.full_like(wc, -1)), done[wg], wc], 1)
+        self.meta = meta.to(torch.int32).flatten().contiguous() if self.nwork else \
+            torch.zeros(8, dtype=torch.int32, device=device)
         stats = torch.stack([split.sum(), torch.where(split, nch, torch.zeros_like(nch)).sum(), gd.sum()]).cpu() \
             if ng else torch.zeros(3, dtype=torch.int64)
         self.ndone = int(stats[0])
@@ -257,7 +273,8 @@ class _Samples:
         if hit is None:
             d = A.device(self.device)
             deg = d.A.indptr[1:] - d.A.indptr[:-1]
-            hit = self._plans[id(A)] = (A, WorkPlan(deg[self.group_users_dev], self.device))
+            gu = self.group_users_dev
+            hit = self._plans[id(A)] = (A, WorkPlan(deg[gu], self.device, self.groups, d.A.indptr[gu]))
         return hit[1]
 
     def check_bounds(self, A: SparseRatings) -> None:

@@ -12,13 +12,9 @@
 // item rows) plus one k-dot pair per held-out sample, instead of
 // deg(u) * k per sample.  One warp owns one user's group of samples and
 // keeps P_u, S_u in registers (k <= 1024).
-#include <cooperative_groups.h>
-
 #include <cstdlib>
 
 #include "common.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace svdrec {
 namespace {
@@ -62,180 +58,239 @@ __global__ void k_normalize_pair(int64_t n, int k, const double* __restrict__ X,
   if (lane == 0) norm[item] = nr;
 }
 
+// Threads per CTA of the scoring kernel (one persistent CTA per SM): the
+// register file caps the per-lane accumulators (2 * MAXR doubles plus four
+// rows of loads in flight), so wide k trades warps for registers.
 template <int MAXR>
-__global__ void __launch_bounds__(512, (MAXR <= 4 ? 2 : 1)) k_predict(int64_t ngroups,
-                                                                      const int64_t* __restrict__ gstart,
-                                                    const int32_t* __restrict__ users,
-                                                    const int32_t* __restrict__ items,
-                                                    const int64_t* __restrict__ indptr,
-                                                    const int32_t* __restrict__ indices,
-                                                    const double* __restrict__ values, int k,
-                                                    const double* __restrict__ Yn, const double* __restrict__ Xn,
-                                                    int64_t ldn, const double* __restrict__ norm, double gmean,
-                                                    double lo, double hi, const int32_t* __restrict__ rank,
-                                                    const int32_t* __restrict__ hot, int nhot,
-                                                    int64_t nwork, const int32_t* __restrict__ work,
-                                                    const int32_t* __restrict__ ginfo, int chunk,
-                                                    int* __restrict__ done, double* __restrict__ part,
-                                                    int* __restrict__ counter,
-                                                    double* __restrict__ out_val, double* __restrict__ out_raw,
-                                                    uint8_t* __restrict__ out_fb) {
-  // hot items (highest training degree) keep their unit rows in shared
-  // memory: under Zipf popularity they carry most of the gathers
-  // With a thread-block cluster the hot set is spread over the cluster's
-  // distributed shared memory: hot item h lives in CTA h % csize at slot
-  // h / csize, so a cluster of 8 stages 8x the rows one SM could hold, and
-  // remote rows are read over DSMEM (bandwidth additive to L2's).  ``nhot``
-  // is the cluster-wide count.
-  extern __shared__ double hs[];
-  __shared__ const double* peer[16];
-  cg::cluster_group cl = cg::this_cluster();
-  const int csize = (int)cl.num_blocks();
-  const int crank = (int)cl.block_rank();
-  const int nloc = (nhot - crank + csize - 1) / csize;  // slots this CTA holds
-  for (int64_t t = threadIdx.x; t < (int64_t)nloc * k; t += blockDim.x) {
-    const int64_t sl = t / k, e = t - sl * k;
-    hs[t] = Yn[(int64_t)hot[sl * csize + crank] * ldn + e];
+struct PredictShape {
+  static constexpr int kThreads = MAXR <= 4 ? 768 : (MAXR <= 8 ? 512 : 256);
+};
+
+// Ratings processed per step of the gather loops: every lane keeps
+// U * MAXR loads in flight, so narrow rows (small k) take more of them.
+template <int MAXR>
+struct PredictUnroll {
+  static constexpr int U = MAXR <= 2 ? 8 : 4;
+};
+
+// P += v * row, S += row for U rows (one per q), lane-strided; padding
+// entries point at a zero row.  The accumulation order is rating by rating.
+template <int MAXR, int U, bool SHARED>
+__device__ __forceinline__ void accum(double (&P)[MAXR], double (&S)[MAXR], const double* const (&rows)[U],
+                                      const double (&vv)[U], int lane, int k) {
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t) {
+    const int idx = lane + 32 * t;
+    if (idx < k) {
+      double x[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) x[q] = SHARED ? rows[q][idx] : __ldg(rows[q] + idx);
+#pragma unroll
+      for (int q = 0; q < U; ++q) P[t] = fma(vv[q], x[q], P[t]);
+#pragma unroll
+      for (int q = 0; q < U; ++q) S[t] += x[q];
+    }
   }
-  if (threadIdx.x < csize) peer[threadIdx.x] = cl.map_shared_rank(hs, threadIdx.x);
-  cl.sync();  // every CTA's slice is staged before anyone reads it
+}
+
+// Items are relabelled by popularity rank (0 = most rated) and every user's
+// ratings are stored in ascending rank order, so a user's hot items come
+// first: the unit rows of the ``nhot`` most popular items (Yr[0, nhot),
+// rank order) are staged once per CTA in shared memory and a 32-rating
+// batch splits into a shared-memory prefix (LDS, no long latency) and an
+// L2-gathered suffix (LDG, four rows in flight per lane).
+template <int MAXR>
+__global__ void __launch_bounds__(PredictShape<MAXR>::kThreads, 1)
+    k_predict(int64_t nwork, const int64_t* __restrict__ wstart, const int4* __restrict__ wmeta,
+              const int32_t* __restrict__ items, const int32_t* __restrict__ rindices,
+              const double* __restrict__ rvalues, int k, const double* __restrict__ Yr,
+              const double* __restrict__ Xn, int64_t ldn, const double* __restrict__ norm, double gmean, double lo,
+              double hi, int nhot, int zrow, int* __restrict__ done, double* __restrict__ part,
+              int* __restrict__ counter,
+              double* __restrict__ out_val, double* __restrict__ out_raw, uint8_t* __restrict__ out_fb) {
+  extern __shared__ double hs[];  // nhot rows + a zero row (padding target)
+  for (int64_t t = threadIdx.x; t < (int64_t)(nhot + 1) * k; t += blockDim.x) {
+    const int64_t sl = t / k, e = t - sl * k;
+    hs[t] = sl < nhot ? Yr[sl * ldn + e] : 0.0;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   // Work items are (group, chunk) pairs, heaviest users first.  Users with
   // more than ``chunk`` ratings are split across warps: each chunk leaves
   // (P, S, sum v) in its partial slot and the warp that completes the group
   // last adds the slots in order (deterministic) and scores the samples.
-  while (true) {
+  // Each work item's description is precomputed (one 8-B + two 16-B
+  // loads); the next item is claimed while this one is processed.
   int wi = 0;
   if (lane == 0) wi = atomicAdd(counter, 1);
   wi = __shfl_sync(0xffffffffu, wi, 0);
-  if (wi >= nwork) break;
-  const int64_t g = work[2 * (int64_t)wi];
-  const int c = work[2 * (int64_t)wi + 1];
-  const int nch = ginfo[3 * g];
-  const int64_t s0 = gstart[g], s1 = gstart[g + 1];
-  const int32_t u = users[s0];
-  const int64_t ra = indptr[u], re = indptr[u + 1];
-  const int64_t a = nch > 1 ? ra + (int64_t)c * chunk : ra;
-  const int64_t e = nch > 1 ? min64(re, a + chunk) : re;
-  double P[MAXR], S[MAXR];
-#pragma unroll
-  for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
-  double vsum = 0.0;
-  for (int64_t base = a; base < e; base += 32) {
-    const int64_t my = base + lane;
-    int32_t ci = 0, rk = 0x7fffffff;
-    double vi = 0.0;
-    if (my < e) {
-      ci = __ldg(indices + my);
-      vi = __ldg(values + my);
-      rk = rank ? __ldg(rank + ci) : 0x7fffffff;
-    }
-    const int nv = (int)min64(32, e - base);
-    // four nonzeros per step, branch-free (generic pointers into shared or
-    // global memory), so each lane keeps 4 * MAXR independent loads in
-    // flight; the accumulation order is still nonzero by nonzero
-    for (int j = 0; j < nv; j += 4) {
-      const double* rows[4];
-      double vv[4], mk[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int jj = (j + q) & 31;
-        const int32_t c = __shfl_sync(0xffffffffu, ci, jj);
-        const int32_t r = __shfl_sync(0xffffffffu, rk, jj);
-        const double v = __shfl_sync(0xffffffffu, vi, jj);
-        const bool ok = j + q < nv;
-        rows[q] = r >= nhot ? Yn + (int64_t)c * ldn
-                            : (csize == 1 ? hs + (int64_t)r * k : peer[r % csize] + (int64_t)(r / csize) * k);
-        vv[q] = ok ? v : 0.0;
-        mk[q] = ok ? 1.0 : 0.0;
-      }
-      vsum += vv[0];
-      vsum += vv[1];
-      vsum += vv[2];
-      vsum += vv[3];
-#pragma unroll
-      for (int t = 0; t < MAXR; ++t) {
-        const int idx = lane + 32 * t;
-        if (idx < k) {
-          const double x0 = rows[0][idx], x1 = rows[1][idx], x2 = rows[2][idx], x3 = rows[3][idx];
-          P[t] = fma(vv[0], x0, P[t]);
-          P[t] = fma(vv[1], x1, P[t]);
-          P[t] = fma(vv[2], x2, P[t]);
-          P[t] = fma(vv[3], x3, P[t]);
-          S[t] = fma(mk[0], x0, S[t]);
-          S[t] = fma(mk[1], x1, S[t]);
-          S[t] = fma(mk[2], x2, S[t]);
-          S[t] = fma(mk[3], x3, S[t]);
-        }
-      }
-    }
-  }
-  if (nch > 1) {
-    const int64_t slot0 = ginfo[3 * g + 1];
-    const int64_t pw = 2 * (int64_t)k + 1;
-    double* mine = part + (slot0 + c) * pw;
-#pragma unroll
-    for (int t = 0; t < MAXR; ++t) {
-      const int idx = lane + 32 * t;
-      if (idx < k) {
-        mine[idx] = P[t];
-        mine[k + idx] = S[t];
-      }
-    }
-    if (lane == 0) mine[2 * k] = vsum;
-    __threadfence();
-    int prev = 0;
-    if (lane == 0) prev = atomicAdd(done + ginfo[3 * g + 2], 1);
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev != nch - 1) continue;  // not the last chunk of this user
-    __threadfence();
+  while (wi < nwork) {
+    const int64_t a = __ldg(wstart + wi);
+    const int4 m0 = __ldg(wmeta + 2 * (int64_t)wi);      // len, deg, s0, s1
+    const int4 m1 = __ldg(wmeta + 2 * (int64_t)wi + 1);  // nch, slot, done, 0
+    int wn = 0;
+    if (lane == 0) wn = atomicAdd(counter, 1);
+    const int64_t e = a + m0.x;
+    const int64_t deg = m0.y;
+    const int64_t s0 = m0.z, s1 = m0.w;
+    const int nch = m1.x;
+    double P[MAXR], S[MAXR];
 #pragma unroll
     for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
-    vsum = 0.0;
-    for (int q = 0; q < nch; ++q) {
-      const double* ps = part + (slot0 + q) * pw;
+    double vsum = 0.0;
+    // the next 32-entry CSR batch is loaded while this one is processed
+    int32_t ci_next = 0x7fffffff;
+    double vi_next = 0.0;
+    if (a + lane < e) {
+      ci_next = __ldg(rindices + a + lane);
+      vi_next = __ldg(rvalues + a + lane);
+    }
+    for (int64_t base = a; base < e; base += 32) {
+      const int32_t ci = ci_next;
+      const double vi = vi_next;
+      const int64_t nx = base + 32 + lane;
+      ci_next = 0x7fffffff;
+      vi_next = 0.0;
+      if (nx < e) {
+        ci_next = __ldg(rindices + nx);
+        vi_next = __ldg(rvalues + nx);
+      }
+      const int nv = (int)min64(32, e - base);
+      vsum += vi;  // this lane's entry (0 past the end)
+      const int nh = __popc(__ballot_sync(0xffffffffu, ci < nhot));  // ascending ranks: a prefix
+      constexpr int U = PredictUnroll<MAXR>::U;
+      for (int j = 0; j < nh; j += U) {
+        const double* rows[U];
+        double vv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int jj = j + q;
+          const int32_t cq = __shfl_sync(0xffffffffu, ci, jj & 31);
+          vv[q] = __shfl_sync(0xffffffffu, vi, jj & 31);
+          rows[q] = hs + (int64_t)(jj < nh ? cq : nhot) * k;
+        }
+        accum<MAXR, U, true>(P, S, rows, vv, lane, k);
+      }
+      for (int j = nh; j < nv; j += U) {
+        const double* rows[U];
+        double vv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int jj = j + q;
+          const int32_t cq = __shfl_sync(0xffffffffu, ci, jj & 31);
+          vv[q] = __shfl_sync(0xffffffffu, vi, jj & 31);
+          rows[q] = Yr + (int64_t)(jj < nv ? cq : zrow) * ldn;
+        }
+        accum<MAXR, U, false>(P, S, rows, vv, lane, k);
+      }
+    }
+    vsum = warp_sum(vsum);
+    if (nch > 1) {
+      const int64_t pw = 2 * (int64_t)k + 1;
+      const int slot = m1.y, slot0 = slot - m1.w;  // m1.w: chunk index
+      double* mine = part + (int64_t)slot * pw;
 #pragma unroll
       for (int t = 0; t < MAXR; ++t) {
         const int idx = lane + 32 * t;
         if (idx < k) {
-          P[t] += __ldcg(ps + idx);
-          S[t] += __ldcg(ps + k + idx);
+          mine[idx] = P[t];
+          mine[k + idx] = S[t];
         }
       }
-      vsum += __ldcg(ps + 2 * k);
-    }
-  }
-  const int64_t deg = re - ra;
-  const double mean = deg > 0 ? vsum / (double)deg : gmean;
-  const double fb_val = fmin(fmax(mean, lo), hi);
-  for (int64_t sidx = s0; sidx < s1; ++sidx) {
-    const int32_t j = items[sidx];
-    const double nj = norm[j];
-    double num = 0.0, den = 0.0;
-    if (nj != 0.0 && deg > 0) {
-      const double* row = Xn + (int64_t)j * ldn;
+      if (lane == 0) mine[2 * k] = vsum;
+      __threadfence();
+      int prev = 0;
+      if (lane == 0) prev = atomicAdd(done + m1.z, 1);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev != nch - 1) {  // not the last chunk of this user
+        wi = __shfl_sync(0xffffffffu, wn, 0);
+        continue;
+      }
+      __threadfence();
 #pragma unroll
-      for (int t = 0; t < MAXR; ++t) {
-        const int idx = lane + 32 * t;
-        if (idx < k) {
-          const double x = __ldg(row + idx);
-          num = fma(x, P[t], num);
-          den = fma(x, S[t], den);
+      for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
+      vsum = 0.0;
+      for (int q = 0; q < nch; ++q) {
+        const double* ps = part + ((int64_t)slot0 + q) * pw;
+#pragma unroll
+        for (int t = 0; t < MAXR; ++t) {
+          const int idx = lane + 32 * t;
+          if (idx < k) {
+            P[t] += __ldcg(ps + idx);
+            S[t] += __ldcg(ps + k + idx);
+          }
+        }
+        vsum += __ldcg(ps + 2 * k);
+      }
+    }
+    const double mean = deg > 0 ? vsum / (double)deg : gmean;
+    const double fb_val = fmin(fmax(mean, lo), hi);
+    // score the group's samples: ids and norms of up to 32 samples are
+    // fetched by the lanes at once, then two samples' rows are in flight
+    // per step (the per-sample id -> norm -> row chain was latency-bound)
+    for (int64_t sb = s0; sb < s1; sb += 32) {
+      const int ns = (int)min64(32, s1 - sb);
+      int32_t jl = 0;
+      double nl = 0.0;
+      if (lane < ns) {
+        jl = items[sb + lane];
+        nl = norm[jl];
+      }
+      for (int q = 0; q < ns; q += 2) {
+        const int32_t j0 = __shfl_sync(0xffffffffu, jl, q);
+        const int32_t j1 = __shfl_sync(0xffffffffu, jl, (q + 1) & 31);
+        const double n0 = __shfl_sync(0xffffffffu, nl, q);
+        const double n1 = q + 1 < ns ? __shfl_sync(0xffffffffu, nl, (q + 1) & 31) : 0.0;
+        const bool ok0 = n0 != 0.0 && deg > 0, ok1 = n1 != 0.0 && deg > 0;
+        const double* row0 = Xn + (int64_t)j0 * ldn;
+        const double* row1 = Xn + (int64_t)j1 * ldn;
+        double num0 = 0.0, den0 = 0.0, num1 = 0.0, den1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXR; ++t) {
+          const int idx = lane + 32 * t;
+          if (idx < k) {
+            const double x0 = ok0 ? __ldg(row0 + idx) : 0.0;
+            const double x1 = ok1 ? __ldg(row1 + idx) : 0.0;
+            num0 = fma(x0, P[t], num0);
+            den0 = fma(x0, S[t], den0);
+            num1 = fma(x1, P[t], num1);
+            den1 = fma(x1, S[t], den1);
+          }
+        }
+        num0 = warp_sum(num0);
+        den0 = warp_sum(den0);
+        num1 = warp_sum(num1);
+        den1 = warp_sum(den1);
+        if (lane == 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (q + h >= ns) break;
+            const bool ok = h ? ok1 : ok0;
+            const double num = h ? num1 : num0, den = h ? den1 : den0;
+            const int64_t sidx = sb + q + h;
+            const bool fb = !ok || fabs(den) < kWeightFloor;
+            const double raw = fb ? mean : num / den;
+            out_raw[sidx] = raw;
+            out_val[sidx] = fb ? fb_val : fmin(fmax(raw, lo), hi);
+            out_fb[sidx] = fb ? 1 : 0;
+          }
         }
       }
-      num = warp_sum(num);
-      den = warp_sum(den);
     }
-    if (lane == 0) {
-      const bool fb = !(nj != 0.0 && deg > 0) || fabs(den) < kWeightFloor;
-      const double raw = fb ? mean : num / den;
-      out_raw[sidx] = raw;
-      out_val[sidx] = fb ? fb_val : fmin(fmax(raw, lo), hi);
-      out_fb[sidx] = fb ? 1 : 0;
-    }
-  }
-  }  // dynamic loop over user groups
-  cl.sync();  // peers may still be reading this CTA's slice
+    wi = __shfl_sync(0xffffffffu, wn, 0);
+  }  // dynamic loop over work items
+}
+
+// Ranked copy of a CSR for the scoring kernel: column j -> rank[j], each
+// row re-sorted ascending (stable within equal keys cannot occur: columns
+// are unique per row).  One segmented pass per row by a warp: rows are
+// short (<= a few thousand) and sorted by insertion into shared memory
+// would be quadratic, so the host sorts (row, rank) keys instead; this
+// kernel only relabels.
+__global__ void k_relabel(int64_t nnz, const int32_t* __restrict__ indices, const int32_t* __restrict__ rank,
+                          int32_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nnz) out[t] = rank[indices[t]];
 }
 
 __global__ void k_overlap(int64_t ns, const int32_t* __restrict__ users, const int32_t* __restrict__ items,
@@ -293,67 +348,47 @@ extern "C" int svdrec_cf_normalize_pair(int64_t n, int32_t k, const double* d_X,
   return check_launch("cf_normalize_pair");
 }
 
-extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, const int32_t* d_users,
-                                 const int32_t* d_items, const int64_t* d_indptr, const int32_t* d_indices,
-                                 const double* d_values, int32_t k, const double* d_Yn, const double* d_Xn,
-                                 int64_t ldn,
-                                 const double* d_norm, double global_mean, double rating_min, double rating_max,
-                                 const int32_t* d_item_rank, const int32_t* d_hot_items, int32_t nhot_avail,
-                                 int64_t nwork, const int32_t* d_work, const int32_t* d_ginfo, int32_t chunk,
-                                 int32_t* d_done, int64_t ndone, double* d_partial, int32_t* d_counter,
-                                 double* d_value, double* d_raw, uint8_t* d_fallback, void* stream) {
-  SVDREC_ARG(ngroups >= 0 && k >= 1 && ldn >= k, "cf_predict: bad arguments");
+extern "C" int svdrec_cf_predict(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
+                                 const int32_t* d_items, const int32_t* d_ranked_indices,
+                                 const double* d_ranked_values, int32_t k, const double* d_Yr, const double* d_Xn,
+                                 int64_t ldn, const double* d_norm, double global_mean, double rating_min,
+                                 double rating_max, int32_t n_items, int32_t* d_done, int64_t ndone,
+                                 double* d_partial, int32_t* d_counter, double* d_value, double* d_raw,
+                                 uint8_t* d_fallback, void* stream) {
+  SVDREC_ARG(nwork >= 0 && k >= 1 && ldn >= k && n_items >= 0, "cf_predict: bad arguments");
   if (k > 1024) {
     set_error("cf_predict: latent dimension %d > 1024 unsupported", k);
     return SVDREC_E_UNSUPPORTED;
   }
-  if (ngroups == 0) return 0;
-  SVDREC_ARG(d_counter && d_work && d_ginfo && nwork >= ngroups, "cf_predict: work plan required");
-  SVDREC_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), as_stream(stream)));
-  if (ndone > 0) SVDREC_CUDA(cudaMemsetAsync(d_done, 0, (size_t)ndone * sizeof(int32_t), as_stream(stream)));
+  if (nwork == 0) return 0;
+  SVDREC_ARG(d_counter && d_work_start && d_work_meta, "cf_predict: work plan required");
+  SVDREC_ARG(reinterpret_cast<uintptr_t>(d_work_meta) % 16 == 0, "cf_predict: work meta must be 16-B aligned");
   cudaStream_t s = as_stream(stream);
+  SVDREC_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), s));
+  if (ndone > 0) SVDREC_CUDA(cudaMemsetAsync(d_done, 0, (size_t)ndone * sizeof(int32_t), s));
   const int r = (k + 31) / 32;
-  // 16-warp CTAs, persistent: two per SM for k <= 128 (more gathers in
-  // flight), else one; each stages the hottest item rows in its shared
-  // memory.  SVDREC_CF_CLUSTER=c (2..8) spreads the hot set over a c-CTA
-  // cluster's distributed shared memory instead -- measured slower on B200
-  // (remote 8-byte reads cost more than the L2 hits they replace: cluster 1 /
-  // 2 / 4 / 8 -> 33.7 / 35.1 / 42.7 / 52.7 ms per bench step), so off.
-  static const int csize_env = getenv("SVDREC_CF_CLUSTER") ? atoi(getenv("SVDREC_CF_CLUSTER")) : 1;
-  int csize = csize_env >= 1 && csize_env <= 8 ? csize_env : 1;
-  const int per_sm = (csize == 1 && r <= 4) ? 2 : 1;
-  const size_t kHotBytes = per_sm == 2 ? 100 * 1024 : 200 * 1024;
-  int nhot = d_item_rank && d_hot_items ? (int)(kHotBytes / ((size_t)k * 8)) * csize : 0;
-  if (nhot > nhot_avail) nhot = nhot_avail;
+  // one persistent CTA per SM holding the hottest items' unit rows in
+  // shared memory (as many as fit in kHotBytes)
+  constexpr size_t kHotBytes = 208 * 1024;
+  int nhot = (int)(kHotBytes / ((size_t)k * 8));
+  if (nhot > n_items) nhot = n_items;
+  int nhot_fit = (int)(kHotBytes / ((size_t)k * 8)) - 1;  // + the zero row
+  if (nhot > nhot_fit) nhot = nhot_fit;
   if (nhot < 0) nhot = 0;
-  const size_t smem = (size_t)((nhot + csize - 1) / csize) * k * 8;
-  const int64_t want = (ngroups + 15) / 16;
-  int64_t grid = (int64_t)(per_sm * sm_count() / csize) * csize;
-  if (want < grid) grid = ((want + csize - 1) / csize) * csize;
-  if (grid < csize) grid = csize;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(512);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-#define SVDREC_PRED(R)                                                                                       \
-  do {                                                                                                       \
-    static bool attr_set = false;                                                                            \
-    if (!attr_set) {                                                                                         \
-      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024)); \
-      attr_set = true;                                                                                       \
-    }                                                                                                        \
-    SVDREC_CUDA(cudaLaunchKernelEx(&cfg, k_predict<R>, ngroups, d_group_start, d_users, d_items, d_indptr,   \
-                                   d_indices, d_values, k, d_Yn, d_Xn, ldn, d_norm, global_mean, rating_min, \
-                                   rating_max, d_item_rank, d_hot_items, nhot, nwork, d_work, d_ginfo, chunk, \
-                                   d_done, d_partial, d_counter, d_value, d_raw, d_fallback));                \
+  const size_t smem = (size_t)(nhot + 1) * k * 8;
+  const int64_t grid = sm_count();
+#define SVDREC_PRED(R)                                                                                        \
+  do {                                                                                                        \
+    static bool attr_set = false;                                                                             \
+    if (!attr_set) {                                                                                          \
+      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                       (int)kHotBytes));                                                      \
+      attr_set = true;                                                                                        \
+    }                                                                                                         \
+    k_predict<R><<<(unsigned)grid, PredictShape<R>::kThreads, smem, s>>>(                                     \
+        nwork, d_work_start, reinterpret_cast<const int4*>(d_work_meta), d_items, d_ranked_indices,           \
+        d_ranked_values, k, d_Yr, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, nhot, n_items,      \
+        d_done, d_partial, d_counter, d_value, d_raw, d_fallback);                                            \
   } while (0)
   if (r <= 1)
     SVDREC_PRED(1);
@@ -369,6 +404,14 @@ extern "C" int svdrec_cf_predict(int64_t ngroups, const int64_t* d_group_start, 
     SVDREC_PRED(32);
 #undef SVDREC_PRED
   return check_launch("cf_predict");
+}
+
+extern "C" int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,
+                                 void* stream) {
+  SVDREC_ARG(nnz >= 0, "cf_relabel: bad arguments");
+  if (nnz == 0) return 0;
+  k_relabel<<<(unsigned)((nnz + 255) / 256), 256, 0, as_stream(stream)>>>(nnz, d_indices, d_rank, d_out);
+  return check_launch("cf_relabel");
 }
 
 extern "C" int svdrec_count_overlap(int64_t nsamp, const int32_t* d_users, const int32_t* d_items,

@@ -341,11 +341,20 @@ def inv_sqrt(G: torch.Tensor, status: torch.Tensor, iters: torch.Tensor | None =
 
 def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Yn: torch.Tensor,
                Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float, plan):
-    """Alg. 4 over user-grouped samples.  ``plan`` is a cf.WorkPlan (work
-    items, per-group chunk info, completion counters, counter)."""
-    ldn = _mat(Yn, "cf.Yn")
-    if _mat(Xn, "cf.Xn") != ldn or Xn.shape != Yn.shape:
-        raise ValueError("cf_predict: Xn and Yn must share shape and leading dimension")
+    """Alg. 4 over user-grouped samples.  ``csr`` is a sparse.DeviceCSR (its
+    ranked copy is used); ``plan`` is a cf.WorkPlan (work items, per-group
+    chunk info, completion counters, counter)."""
+    ldn = _mat(Xn, "cf.Xn")
+    if Xn.shape != Yn.shape:
+        raise ValueError("cf_predict: Xn and Yn must share their shape")
+    rind, rval, order = csr.ranked()
+    n = Yn.shape[0]
+    Yr = torch.empty(n + 1, ldn, dtype=F64, device=Yn.device)  # rank order + a zero row
+    Yr[n].zero_()
+    if ldn == Yn.shape[1]:
+        torch.index_select(Yn, 0, order, out=Yr[:n])
+    else:
+        Yr[:n, : Yn.shape[1]].copy_(Yn.index_select(0, order))
     ns = users.shape[0]
     val = torch.empty(ns, dtype=F64, device=Yn.device)
     raw = torch.empty(ns, dtype=F64, device=Yn.device)
@@ -356,14 +365,18 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     # sample its ids, norm, Xn row and the three outputs
     nbytes = getattr(plan, "rated", 0) * (12 + 8 * k) + ns * (8 * k + 4 + 4 + 8 + 17)
     with _span("cf_predict", nbytes):
-        hot = getattr(csr, "hot_items", None)
-        rank = getattr(csr, "item_rank", None)
-        call("svdrec_cf_predict", groups.shape[0] - 1, ptr(groups), ptr(users), ptr(items), ptr(csr.indptr),
-             ptr(csr.indices), ptr(csr.values), Yn.shape[1], ptr(Yn), ptr(Xn), ldn, ptr(norm), float(gmean),
-             float(lo), float(hi), ptr(rank), ptr(hot), 0 if hot is None else hot.numel(), plan.nwork,
-             ptr(plan.work), ptr(plan.ginfo), plan.chunk, ptr(plan.done), plan.ndone,
-             ptr(plan.partial(Yn.shape[1])), ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
+        call("svdrec_cf_predict", plan.nwork, ptr(plan.start), ptr(plan.meta), ptr(items), ptr(rind), ptr(rval),
+             k, ptr(Yr), ptr(Xn), ldn, ptr(norm), float(gmean), float(lo), float(hi), n, ptr(plan.done),
+             plan.ndone, ptr(plan.partial(k)), ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
     return val, raw, fb
+
+
+def cf_relabel(indices: torch.Tensor, rank: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[t] = rank[indices[t]] (int32)."""
+    if out is None:
+        out = torch.empty_like(indices)
+    call("svdrec_cf_relabel", indices.numel(), ptr(indices), ptr(rank), ptr(out), stream_handle())
+    return out
 
 
 def err_sum(pred: torch.Tensor, truth: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

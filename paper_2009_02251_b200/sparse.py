@@ -235,6 +235,7 @@ class DeviceCSR:
         self.nwarp = int(max(1, min(self.nseg, sms * WARPS_PER_SM)))
         self.warp_seg = warp_plan_t(sb, se, self.nwarp)
         self._partial = {}
+        self._ranked = None
         self.h2d_bytes = h2d_bytes
 
     @classmethod
@@ -253,6 +254,20 @@ class DeviceCSR:
         indptr = torch.zeros(self.n + 1, dtype=torch.int64, device=self.device)
         torch.cumsum(counts, 0, out=indptr[1:])
         return DeviceCSR(indptr, rows[perm], self.values[perm], (self.n, self.m))
+
+    def ranked(self):
+        """(ranked indices, values, rank -> item order) for the CF scoring
+        kernel: item ids replaced by popularity rank, each row ordered by
+        rank (built once on the device, cached)."""
+        if self._ranked is None:
+            from . import kernels as K
+
+            rk = K.cf_relabel(self.indices, self.item_rank)
+            rows = torch.repeat_interleave(torch.arange(self.m, dtype=torch.int64, device=self.device),
+                                           self.indptr[1:] - self.indptr[:-1])
+            perm = torch.sort(rows * self.n + rk.to(torch.int64)).indices
+            self._ranked = (rk[perm].contiguous(), self.values[perm].contiguous(), self.hot_items.to(torch.int64))
+        return self._ranked
 
     def partial(self, b: int) -> torch.Tensor | None:
         if self.nslots == 0:

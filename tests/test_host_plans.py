@@ -60,12 +60,27 @@ def test_workplan_matches_numpy(chunk, monkeypatch):
     from paper_2009_02251_b200.cf import WorkPlan
     rng = np.random.default_rng(chunk)
     gd = rng.zipf(1.5, size=400).astype(np.int64) - 1
+    gs = np.r_[0, np.cumsum(rng.integers(1, 4, size=400))]  # samples per group
+    rs = np.r_[0, np.cumsum(gd)][:-1] + 7  # CSR offset of each group's row
     monkeypatch.setattr(WorkPlan, "CHUNK", chunk)
-    p = WorkPlan(torch.from_numpy(gd), torch.device("cpu"))
+    p = WorkPlan(torch.from_numpy(gd), torch.device("cpu"), torch.from_numpy(gs), torch.from_numpy(rs))
     work, ginfo, ndone, nslots = _np_workplan(gd, chunk)
-    np.testing.assert_array_equal(p.work.numpy(), work.astype(np.int32))
-    np.testing.assert_array_equal(p.ginfo.numpy(), ginfo.astype(np.int32))
-    assert (p.ndone, p.nslots, p.nwork) == (ndone, nslots, work.size // 2)
+    wg, wc = work[0::2], work[1::2]
+    nch, slot0, done = ginfo[0::3], ginfo[1::3], ginfo[2::3]
+    split = nch[wg] > 1
+    start = rs[wg] + np.where(split, wc * chunk, 0)
+    length = np.where(split, np.minimum(gd[wg] - wc * chunk, chunk), gd[wg])
+    meta = np.stack([length, gd[wg], gs[wg], gs[wg + 1], nch[wg], np.where(split, slot0[wg] + wc, -1), done[wg],
+                     wc], 1)
+    np.testing.assert_array_equal(p.start.numpy(), start)
+    np.testing.assert_array_equal(p.meta.numpy(), meta.ravel().astype(np.int32))
+    assert (p.ndone, p.nslots, p.nwork) == (ndone, nslots, wg.size)
+    # every rating of every user is covered exactly once by the items
+    cover = np.zeros(int(rs[-1] + gd[-1] + 8), dtype=np.int64)
+    for a, n in zip(start, length):
+        cover[a:a + n] += 1
+    for g in range(gd.size):
+        assert np.all(cover[rs[g]:rs[g] + gd[g]] == 1)
 
 
 def test_samples_grouping_on_host_device():
