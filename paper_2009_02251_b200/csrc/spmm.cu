@@ -144,25 +144,41 @@ struct TmaGeom {
   static constexpr int B = 2 * P;
   static constexpr int G4 = (4 * B * 8 + 127) / 128 * 16;  // doubles per gather4 block (128-B aligned)
   static constexpr int ROWS = 8 * G4;                       // 32 rows
-  static constexpr int STG = ROWS + 48;                     // + 32 values + 16 (meta, pad to 128 B)
+  static constexpr int STG = ROWS + 64;  // + 32 values + 16 (meta, pad) + 16 (32 column ids)
 };
 
-template <int P, int S>
-__global__ void __launch_bounds__(kPipeWarps * 32, 2) k_spmm_tma(
+// Hot rows (W = 16 warps, one CTA per SM): with ``nhot`` > 0 the first
+// nhot rows of X are staged once in shared memory after the rings, and the
+// CSR is "ranked" (columns < nhot form a prefix of every row, e.g. items
+// relabelled by popularity): a chunk's hot prefix is read from the staged
+// rows and only its cold entries are gathered by TMA (fully hot gather4
+// blocks are skipped, hot entries of mixed blocks use the zero-filled
+// coordinate -1), cutting the L2 row requests that bound this kernel.
+template <int P, int S, int W, bool HOT>
+__global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
     const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_seg,
     const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
     const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ indices, const double* __restrict__ values,
-    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial) {
+    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial, const double* __restrict__ X, int64_t ldx,
+    int nhot) {
   using Gm = TmaGeom<P>;
   constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWS, STG = Gm::STG;
   extern __shared__ __align__(128) double smd[];
-  __shared__ __align__(8) uint64_t bars[kPipeWarps * S];
+  __shared__ __align__(8) uint64_t bars[W * S];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   double* ring = smd + (size_t)wib * S * STG;
+  double* hot = smd + (size_t)W * S * STG;
   uint64_t* bar = bars + wib * S;
   if (lane < S) mbar_init(bar + lane, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (HOT && nhot > 0) {
+    for (int t = threadIdx.x; t < nhot * (B / 2); t += blockDim.x) {
+      const int r = t / (B / 2), c2 = t - r * (B / 2);
+      reinterpret_cast<double2*>(hot)[t] = __ldg(reinterpret_cast<const double2*>(X + (int64_t)r * ldx) + c2);
+    }
+    __syncthreads();
+  }
   __syncwarp();
   if (w >= nwarp) return;
   const int g = lane / P, pc = lane - (lane / P) * P;
@@ -226,23 +242,35 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) k_spmm_tma(
   auto issue = [&](int slot) {
     double* st = ring + slot * STG;
     st[ROWS + lane] = kvi;
-    if (lane == 0) *reinterpret_cast<int4*>(st + ROWS + 32) = km;
+    if (HOT) reinterpret_cast<int32_t*>(st + ROWS + 48)[lane] = kci;
+    // hot entries (column < nhot) form a prefix of the chunk
+    const int h = HOT ? __popc(__ballot_sync(0xffffffffu, kci >= 0 && kci < nhot)) : 0;
+    if (lane == 0) *reinterpret_cast<int4*>(st + ROWS + 32) = make_int4(km.x, km.y, km.z, km.w | (h << 2));
     const int ng = (km.z + 3) >> 2;
+    const int g0 = h >> 2;  // gather4 blocks [0, g0) are entirely hot
     const int t = lane & 7;
-    const int r0 = __shfl_sync(0xffffffffu, kci, 4 * t);
-    const int r1 = __shfl_sync(0xffffffffu, kci, 4 * t + 1);
-    const int r2 = __shfl_sync(0xffffffffu, kci, 4 * t + 2);
-    const int r3 = __shfl_sync(0xffffffffu, kci, 4 * t + 3);
-    if (ng > 0) {
-      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)(ng * 4 * B * 8));
+    int r0 = __shfl_sync(0xffffffffu, kci, 4 * t);
+    int r1 = __shfl_sync(0xffffffffu, kci, 4 * t + 1);
+    int r2 = __shfl_sync(0xffffffffu, kci, 4 * t + 2);
+    int r3 = __shfl_sync(0xffffffffu, kci, 4 * t + 3);
+    if (HOT) {
+      if (4 * t < h) r0 = -1;
+      if (4 * t + 1 < h) r1 = -1;
+      if (4 * t + 2 < h) r2 = -1;
+      if (4 * t + 3 < h) r3 = -1;
+    }
+    if (ng > g0) {
+      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)((ng - g0) * 4 * B * 8));
       __syncwarp();
-      if (lane < ng) tma_gather4(st + lane * G4, &tmX, 0, r0, r1, r2, r3, bar + slot);
+      if (lane >= g0 && lane < ng) tma_gather4(st + lane * G4, &tmX, 0, r0, r1, r2, r3, bar + slot);
     } else if (lane == 0) {
-      mbar_expect_tx(bar + slot, 0);  // empty segment: complete the phase
+      mbar_expect_tx(bar + slot, 0);  // empty or all-hot chunk: complete the phase
     }
   };
 
-  double2 acc = make_double2(0.0, 0.0);
+  // two accumulator pairs (even / odd steps of a chunk) halve the
+  // dependent DFMA chain; they are added at the end of each row
+  double2 acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
   int64_t issued = 0, consumed = 0;
   load_chunk();
 #pragma unroll
@@ -264,14 +292,17 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) k_spmm_tma(
     __syncwarp();
     const double* st = ring + slot * STG;
     const int4 m = *reinterpret_cast<const int4*>(st + ROWS + 32);
-    if (m.w & 1) acc = make_double2(0.0, 0.0);
+    if (m.w & 1) acc = acc1 = make_double2(0.0, 0.0);
     if (active) {
       // fully unrolled over the chunk's NS steps: unconditional loads at
       // constant smem offsets from one per-lane base (all in flight at
-      // once; rows past the chunk are stale but in-bounds), FMAs masked
+      // once; rows past the chunk are stale but in-bounds), FMAs masked;
+      // the chunk's hot prefix reads the staged hot rows instead
       constexpr int NS = (32 + G - 1) / G;
+      const int h = HOT ? m.w >> 2 : 0;
       const double* xr = st + ((g >> 2) * G4 + (g & 3) * B) + 2 * pc;
       const double* vr = st + ROWS + g;
+      const int32_t* ir = reinterpret_cast<const int32_t*>(st + ROWS + 48);
       double2 xs[NS];
       double vs[NS];
 #pragma unroll
@@ -279,19 +310,27 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) k_spmm_tma(
         const int j = q * G + g;
         const int jo = q * G;
         const int jc = j < 32 ? j : 31;
-        xs[q] = G4 == 4 * B ? *reinterpret_cast<const double2*>(xr + jo * B)
-                            : *reinterpret_cast<const double2*>(st + (jc >> 2) * G4 + (jc & 3) * B + 2 * pc);
+        const double* src = G4 == 4 * B ? xr + jo * B : st + (jc >> 2) * G4 + (jc & 3) * B + 2 * pc;
+        if (HOT && j < h) src = hot + ir[jc] * B + 2 * pc;
+        xs[q] = *reinterpret_cast<const double2*>(src);
         vs[q] = vr[jc - g];
       }
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
         if (q * G + g < m.z) {
-          acc.x = fma(vs[q], xs[q].x, acc.x);
-          acc.y = fma(vs[q], xs[q].y, acc.y);
+          if (q & 1) {
+            acc1.x = fma(vs[q], xs[q].x, acc1.x);
+            acc1.y = fma(vs[q], xs[q].y, acc1.y);
+          } else {
+            acc.x = fma(vs[q], xs[q].x, acc.x);
+            acc.y = fma(vs[q], xs[q].y, acc.y);
+          }
         }
       }
     }
     if (m.w & 2) {
+      acc.x += acc1.x;
+      acc.y += acc1.y;
       double2 tot = acc;
 #pragma unroll
       for (int h = 1; h < G; ++h) {
@@ -308,11 +347,11 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) k_spmm_tma(
   }
 }
 
-template <int P, int S>
+template <int P, int S, int W, bool HOT>
 int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
                const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
                const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
-               cudaStream_t s) {
+               int nhot, cudaStream_t s) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
     set_error("spmm: cuTensorMapEncodeTiled unavailable");
@@ -330,27 +369,38 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
     set_error("spmm: tensor map encode failed (%d)", (int)r);
     return SVDREC_E_UNSUPPORTED;
   }
-  constexpr size_t smem = (size_t)kPipeWarps * S * TmaGeom<P>::STG * sizeof(double);
+  constexpr size_t ring = (size_t)W * S * TmaGeom<P>::STG * sizeof(double);
+  constexpr size_t kMaxSmem = 226 * 1024;  // + the static mbarriers within the 227 KB opt-in
+  if constexpr (ring + 32 * 2 * P * sizeof(double) > kMaxSmem) {  // wide rows: no room for a hot set
+    return tma_launch<P, S, 8, false>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
+                               ldx, Y, ldy, partial, 0, s);
+  }
+  if (W <= 8) nhot = 0;  // two CTAs per SM: no room for a hot set
+  const int64_t fit = (int64_t)((kMaxSmem - ring) / (2 * P * sizeof(double)));
+  if (nhot > fit) nhot = (int)fit;
+  if (nhot > xrows) nhot = (int)xrows;
+  const size_t smem = ring + (size_t)nhot * 2 * P * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S, W, HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kMaxSmem));
     attr = true;
   }
-  const int64_t grid = (nwarp + kPipeWarps - 1) / kPipeWarps;
-  k_spmm_tma<P, S><<<(unsigned)grid, kPipeWarps * 32, smem, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
-                                                                seg_slot, indices, values, Y, ldy, partial);
+  const int64_t grid = (nwarp + W - 1) / W;
+  k_spmm_tma<P, S, W, HOT><<<(unsigned)grid, W * 32, smem, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
+                                                           seg_slot, indices, values, Y, ldy, partial, X, ldx, nhot);
   return check_launch("spmm_tma");
 }
 
-template <int S>
+template <int S, int W>
 int tma_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
                  const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
                  const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
-                 cudaStream_t s) {
-#define SVDREC_TMA(PP) \
-  case PP:             \
-    return tma_launch<PP, S>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X, ldx, \
-                             Y, ldy, partial, s);
+                 int nhot, cudaStream_t s) {
+#define SVDREC_TMA(PP)                                                                                              \
+  case PP:                                                                                                          \
+    return tma_launch<PP, S, W, (W > 8)>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,  \
+                                ldx, Y, ldy, partial, nhot, s);
   switch (b / 2) {
     SVDREC_TMA(1)
     SVDREC_TMA(2)
@@ -391,13 +441,12 @@ __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, con
 
 using namespace svdrec;
 
-extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
-                           const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_indices,
-                           const double* d_values, const double* d_X, int64_t ldx, int64_t xrows, double* d_Y,
-                           int64_t ldy,
-                           int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
-                           const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg, double* d_partial,
-                           void* stream) {
+namespace {
+int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin, const int64_t* d_seg_end,
+              const int32_t* d_seg_slot, const int32_t* d_indices, const double* d_values, const double* d_X,
+              int64_t ldx, int64_t xrows, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
+              const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
+              const int32_t* d_warp_seg, double* d_partial, int32_t nhot, void* stream) {
   SVDREC_ARG(b >= 1 && ldx >= b && ldy >= b && nseg >= 0 && nlong >= 0, "spmm: bad arguments b=%d", b);
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
@@ -410,8 +459,10 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
   // SVDREC_SPMM_KIND=0 forces the plain kernel (A/B measurements)
   static const int kind = getenv("SVDREC_SPMM_KIND") ? atoi(getenv("SVDREC_SPMM_KIND")) : 1;
   if (vec2 && b <= 32 && nwarp > 0 && d_warp_seg && kind != 0 && xrows < (1ll << 31)) {
-    rc = tma_dispatch<2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
-                         d_values, d_X, ldx, d_Y, ldy, d_partial, s);
+    rc = nhot > 0 ? tma_dispatch<2, 16>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
+                                        d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, nhot, s)
+                  : tma_dispatch<2, 8>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
+                                       d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, 0, s);
     if (rc) return rc;
     goto fixup;
   }
@@ -442,4 +493,26 @@ fixup:
     rc = check_launch("spmm_fixup");
   }
   return rc;
+}
+}  // namespace
+
+extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                           const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_indices,
+                           const double* d_values, const double* d_X, int64_t ldx, int64_t xrows, double* d_Y,
+                           int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
+                           const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
+                           const int32_t* d_warp_seg, double* d_partial, void* stream) {
+  return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
+                   ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, 0, stream);
+}
+
+extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                               const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_indices,
+                               const double* d_values, const double* d_X, int64_t ldx, int64_t xrows, double* d_Y,
+                               int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
+                               const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
+                               const int32_t* d_warp_seg, double* d_partial, int32_t nhot, void* stream) {
+  SVDREC_ARG(nhot >= 0, "spmm_hot: negative nhot");
+  return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
+                   ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, nhot, stream);
 }
