@@ -96,6 +96,12 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
                 int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                 const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
                 double* d_partial, void* stream);
+/* Warps per SM of the schedule (nwarp = SMs x this, warp_seg from
+ * svdrec_spmm_warp_plan) that the fast path for width b expects: 16 for even
+ * b <= 32 (two 8-warp CTAs, 2 doubles per lane), fewer for 32 < b <= 64 with
+ * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
+ * fall back to the plain kernel. */
+int svdrec_spmm_warps_per_sm(int32_t b);
 /* Same product with the first nhot rows of X staged in shared memory: the
  * CSR must be "ranked" -- in every row the entries with column < nhot come
  * first (e.g. columns relabelled by popularity and each row ordered by the

@@ -139,9 +139,9 @@ constexpr int kPipeWarps = 8;
 // mbarrier per stage, so the gathered bytes cross the L1 data pipe once
 // (the consumer's LDS).  Padding rows use coordinate -1: TMA zero-fills
 // out-of-bounds rows and still counts their bytes.
-template <int P>
+template <int P, int V = 2>
 struct TmaGeom {
-  static constexpr int B = 2 * P;
+  static constexpr int B = V * P;  // columns: P lanes x V doubles
   static constexpr int G4 = (4 * B * 8 + 127) / 128 * 16;  // doubles per gather4 block (128-B aligned)
   static constexpr int ROWS = 8 * G4;                       // 32 rows
   static constexpr int STG = ROWS + 64;  // + 32 values + 16 (meta, pad) + 16 (32 column ids)
@@ -154,14 +154,53 @@ struct TmaGeom {
 // rows and only its cold entries are gathered by TMA (fully hot gather4
 // blocks are skipped, hot entries of mixed blocks use the zero-filled
 // coordinate -1), cutting the L2 row requests that bound this kernel.
-template <int P, int S, int W, bool HOT>
-__global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
+// V doubles per lane (V = 2: b <= 32; V = 4: 32 < b <= 64, b % 4 == 0),
+// held as V/2 double2.
+template <int V>
+struct Acc {
+  double2 h[V / 2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) h[i] = make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ void load(const double* p) {
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) h[i] = reinterpret_cast<const double2*>(p)[i];
+  }
+  __device__ __forceinline__ void fma(double v, const Acc& x) {
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+      h[i].x = ::fma(v, x.h[i].x, h[i].x);
+      h[i].y = ::fma(v, x.h[i].y, h[i].y);
+    }
+  }
+  __device__ __forceinline__ void add(const Acc& o) {
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+      h[i].x += o.h[i].x;
+      h[i].y += o.h[i].y;
+    }
+  }
+  __device__ __forceinline__ Acc shfl(int src) const {
+    Acc r;
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) r.h[i] = shfl_v(h[i], src);
+    return r;
+  }
+  __device__ __forceinline__ void store(double* p) const {
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) reinterpret_cast<double2*>(p)[i] = h[i];
+  }
+};
+
+template <int P, int S, int W, bool HOT, int V>
+__global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma(
     const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_seg,
     const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
     const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ indices, const double* __restrict__ values,
     double* __restrict__ Y, int64_t ldy, double* __restrict__ partial, const double* __restrict__ X, int64_t ldx,
     int nhot) {
-  using Gm = TmaGeom<P>;
+  using Gm = TmaGeom<P, V>;
   constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWS, STG = Gm::STG;
   extern __shared__ __align__(128) double smd[];
   __shared__ __align__(8) uint64_t bars[W * S];
@@ -173,7 +212,7 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
   if (lane < S) mbar_init(bar + lane, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (HOT && nhot > 0) {
-    for (int t = threadIdx.x; t < nhot * (B / 2); t += blockDim.x) {
+    for (int t = threadIdx.x; t < nhot * (B / 2); t += blockDim.x) {  // B/2 double2 per row
       const int r = t / (B / 2), c2 = t - r * (B / 2);
       reinterpret_cast<double2*>(hot)[t] = __ldg(reinterpret_cast<const double2*>(X + (int64_t)r * ldx) + c2);
     }
@@ -270,7 +309,9 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
 
   // two accumulator pairs (even / odd steps of a chunk) halve the
   // dependent DFMA chain; they are added at the end of each row
-  double2 acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+  Acc<V> acc, acc1;
+  acc.zero();
+  acc1.zero();
   int64_t issued = 0, consumed = 0;
   load_chunk();
 #pragma unroll
@@ -292,7 +333,10 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
     __syncwarp();
     const double* st = ring + slot * STG;
     const int4 m = *reinterpret_cast<const int4*>(st + ROWS + 32);
-    if (m.w & 1) acc = acc1 = make_double2(0.0, 0.0);
+    if (m.w & 1) {
+      acc.zero();
+      acc1.zero();
+    }
     if (active) {
       // fully unrolled over the chunk's NS steps: unconditional loads at
       // constant smem offsets from one per-lane base (all in flight at
@@ -300,46 +344,42 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
       // the chunk's hot prefix reads the staged hot rows instead
       constexpr int NS = (32 + G - 1) / G;
       const int h = HOT ? m.w >> 2 : 0;
-      const double* xr = st + ((g >> 2) * G4 + (g & 3) * B) + 2 * pc;
+      const double* xr = st + ((g >> 2) * G4 + (g & 3) * B) + V * pc;
       const double* vr = st + ROWS + g;
       const int32_t* ir = reinterpret_cast<const int32_t*>(st + ROWS + 48);
-      double2 xs[NS];
+      Acc<V> xs[NS];
       double vs[NS];
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
         const int j = q * G + g;
         const int jo = q * G;
         const int jc = j < 32 ? j : 31;
-        const double* src = G4 == 4 * B ? xr + jo * B : st + (jc >> 2) * G4 + (jc & 3) * B + 2 * pc;
-        if (HOT && j < h) src = hot + ir[jc] * B + 2 * pc;
-        xs[q] = *reinterpret_cast<const double2*>(src);
+        const double* src = G4 == 4 * B ? xr + jo * B : st + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
+        if (HOT && j < h) src = hot + ir[jc] * B + V * pc;
+        xs[q].load(src);
         vs[q] = vr[jc - g];
       }
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
         if (q * G + g < m.z) {
-          if (q & 1) {
-            acc1.x = fma(vs[q], xs[q].x, acc1.x);
-            acc1.y = fma(vs[q], xs[q].y, acc1.y);
-          } else {
-            acc.x = fma(vs[q], xs[q].x, acc.x);
-            acc.y = fma(vs[q], xs[q].y, acc.y);
-          }
+          if (q & 1)
+            acc1.fma(vs[q], xs[q]);
+          else
+            acc.fma(vs[q], xs[q]);
         }
       }
     }
     if (m.w & 2) {
-      acc.x += acc1.x;
-      acc.y += acc1.y;
-      double2 tot = acc;
+      acc.add(acc1);
+      Acc<V> tot = acc;
 #pragma unroll
       for (int h = 1; h < G; ++h) {
-        const double2 o = shfl_v(acc, (lane + h * P) & 31);
-        if (g == 0) add_v(tot, o);
+        const Acc<V> o = acc.shfl((lane + h * P) & 31);
+        if (g == 0) tot.add(o);
       }
       if (g == 0) {
-        double* dst = m.y < 0 ? (Y + (int64_t)m.x * ldy + 2 * pc) : (partial + (int64_t)m.y * B + 2 * pc);
-        *reinterpret_cast<double2*>(dst) = tot;
+        double* dst = m.y < 0 ? (Y + (int64_t)m.x * ldy + V * pc) : (partial + (int64_t)m.y * B + V * pc);
+        tot.store(dst);
       }
     }
     ++consumed;
@@ -347,7 +387,7 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1)) k_spmm_tma(
   }
 }
 
-template <int P, int S, int W, bool HOT>
+template <int P, int S, int W, bool HOT, int V = 2>
 int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
                const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
                const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
@@ -358,9 +398,9 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
     return SVDREC_E_UNSUPPORTED;
   }
   CUtensorMap tm;
-  const cuuint64_t dims[2] = {(cuuint64_t)(2 * P), (cuuint64_t)xrows};
+  const cuuint64_t dims[2] = {(cuuint64_t)(V * P), (cuuint64_t)xrows};
   const cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
-  const cuuint32_t box[2] = {(cuuint32_t)(2 * P), 1};
+  const cuuint32_t box[2] = {(cuuint32_t)(V * P), 1};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -369,25 +409,25 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
     set_error("spmm: tensor map encode failed (%d)", (int)r);
     return SVDREC_E_UNSUPPORTED;
   }
-  constexpr size_t ring = (size_t)W * S * TmaGeom<P>::STG * sizeof(double);
+  constexpr size_t ring = (size_t)W * S * TmaGeom<P, V>::STG * sizeof(double);
   constexpr size_t kMaxSmem = 226 * 1024;  // + the static mbarriers within the 227 KB opt-in
-  if constexpr (ring + 32 * 2 * P * sizeof(double) > kMaxSmem) {  // wide rows: no room for a hot set
-    return tma_launch<P, S, 8, false>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
+  if constexpr (V == 2 && ring + 32 * 2 * P * sizeof(double) > kMaxSmem) {  // wide rows: no room for a hot set
+    return tma_launch<P, S, 8, false, V>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
                                ldx, Y, ldy, partial, 0, s);
   }
   if (W <= 8) nhot = 0;  // two CTAs per SM: no room for a hot set
-  const int64_t fit = (int64_t)((kMaxSmem - ring) / (2 * P * sizeof(double)));
+  const int64_t fit = (int64_t)((kMaxSmem - ring) / (V * P * sizeof(double)));
   if (nhot > fit) nhot = (int)fit;
   if (nhot > xrows) nhot = (int)xrows;
-  const size_t smem = ring + (size_t)nhot * 2 * P * sizeof(double);
+  const size_t smem = ring + (size_t)nhot * V * P * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S, W, HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S, W, HOT, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kMaxSmem));
     attr = true;
   }
   const int64_t grid = (nwarp + W - 1) / W;
-  k_spmm_tma<P, S, W, HOT><<<(unsigned)grid, W * 32, smem, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
+  k_spmm_tma<P, S, W, HOT, V><<<(unsigned)grid, W * 32, smem, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
                                                            seg_slot, indices, values, Y, ldy, partial, X, ldx, nhot);
   return check_launch("spmm_tma");
 }
@@ -424,6 +464,39 @@ int tma_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, c
 #undef SVDREC_TMA
 }
 
+// Wide blocks (32 < b <= 64, b % 4 == 0): four doubles per lane, P = b / 4
+// lanes per row, one CTA of w4_warps(P) warps per SM (the rings of 4-row
+// gathers of b-wide rows are twice as large).
+constexpr int w4_warps(int P) {
+  // two stages of TmaGeom<P, 4> per warp within the 226 KB budget, <= 8 warps
+  return (226 * 1024) / (2 * (8 * ((4 * 4 * P * 8 + 127) / 128 * 16) + 64) * 8) < 8
+             ? (226 * 1024) / (2 * (8 * ((4 * 4 * P * 8 + 127) / 128 * 16) + 64) * 8)
+             : 8;
+}
+
+int tma_dispatch4(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
+                  const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
+                  const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
+                  cudaStream_t s) {
+#define SVDREC_TMA4(PP)                                                                                          \
+  case PP:                                                                                                       \
+    return tma_launch<PP, 2, w4_warps(PP), false, 4>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end,       \
+                                                     seg_slot, indices, values, X, ldx, Y, ldy, partial, 0, s);
+  switch (b / 4) {
+    SVDREC_TMA4(9)
+    SVDREC_TMA4(10)
+    SVDREC_TMA4(11)
+    SVDREC_TMA4(12)
+    SVDREC_TMA4(13)
+    SVDREC_TMA4(14)
+    SVDREC_TMA4(15)
+    SVDREC_TMA4(16)
+    default:
+      return SVDREC_E_ARG;
+  }
+#undef SVDREC_TMA4
+}
+
 __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, const int32_t* __restrict__ s0,
                         const int32_t* __restrict__ s1, const double* __restrict__ partial, double* __restrict__ Y,
                         int64_t ldy, int b) {
@@ -440,6 +513,23 @@ __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, con
 }  // namespace svdrec
 
 using namespace svdrec;
+
+extern "C" int svdrec_spmm_warps_per_sm(int32_t b) {
+  if (b >= 1 && b <= 32 && b % 2 == 0) return 16;  // two CTAs of 8 warps
+  if (b > 32 && b <= 64 && b % 4 == 0) {
+    switch (b / 4) {
+      case 9: return w4_warps(9);
+      case 10: return w4_warps(10);
+      case 11: return w4_warps(11);
+      case 12: return w4_warps(12);
+      case 13: return w4_warps(13);
+      case 14: return w4_warps(14);
+      case 15: return w4_warps(15);
+      default: return w4_warps(16);
+    }
+  }
+  return 16;  // plain kernel: the schedule is not used
+}
 
 namespace {
 int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin, const int64_t* d_seg_end,
@@ -463,6 +553,13 @@ int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin
                                         d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, nhot, s)
                   : tma_dispatch<2, 8>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
                                        d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, 0, s);
+    if (rc) return rc;
+    goto fixup;
+  }
+  if (vec2 && b > 32 && b <= 64 && b % 4 == 0 && ldx % 4 == 0 && nwarp > 0 && d_warp_seg && kind != 0 &&
+      xrows < (1ll << 31) && nwarp == (int64_t)sm_count() * svdrec_spmm_warps_per_sm(b)) {
+    rc = tma_dispatch4(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                       d_values, d_X, ldx, d_Y, ldy, d_partial, s);
     if (rc) return rc;
     goto fixup;
   }

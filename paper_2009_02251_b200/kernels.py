@@ -156,10 +156,11 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
                  ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), plan.nwarp, ptr(plan.warp_seg), ptr(part),
                  plan.n, stream_handle())
         return Y
+    nwarp, wseg = plan.schedule(query("svdrec_spmm_warps_per_sm", b))
     with _span("spmm", nbytes):
         call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
              ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
-             ptr(plan.long_s0), ptr(plan.long_s1), plan.nwarp, ptr(plan.warp_seg), ptr(part), stream_handle())
+             ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(part), stream_handle())
     return Y
 
 

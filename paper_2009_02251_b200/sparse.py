@@ -236,6 +236,7 @@ class DeviceCSR:
         self.warp_seg = warp_plan_t(sb, se, self.nwarp)
         self._partial = {}
         self._ranked = None
+        self._sched = {}
         self.h2d_bytes = h2d_bytes
 
     @classmethod
@@ -254,6 +255,18 @@ class DeviceCSR:
         indptr = torch.zeros(self.n + 1, dtype=torch.int64, device=self.device)
         torch.cumsum(counts, 0, out=indptr[1:])
         return DeviceCSR(indptr, rows[perm], self.values[perm], (self.n, self.m))
+
+    def schedule(self, warps_per_sm: int) -> tuple[int, torch.Tensor]:
+        """(nwarp, warp_seg) for a kernel running ``warps_per_sm`` warps per SM."""
+        if warps_per_sm == WARPS_PER_SM:
+            return self.nwarp, self.warp_seg
+        hit = self._sched.get(warps_per_sm)
+        if hit is None:
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count \
+                if self.device.type == "cuda" else 148
+            nw = int(max(1, min(self.nseg, sms * warps_per_sm)))
+            hit = self._sched[warps_per_sm] = (nw, warp_plan_t(self.seg_begin, self.seg_end, nw))
+        return hit
 
     def ranked(self):
         """(ranked indices, values, rank -> item order) for the CF scoring

@@ -41,7 +41,7 @@ def test_spmm_matches_scipy(gpu):
     M = synth.generate(synth.CONFIGS["c0_100k"])
     A = P.SparseRatings(M, 1.0, 5.0)
     rng = np.random.default_rng(0)
-    for b in (1, 3, 10, 20, 64, 70):
+    for b in (1, 3, 10, 20, 36, 40, 48, 64, 70):  # 2-wide TMA, 4-wide TMA (36-64), plain kernel
         X = rng.standard_normal((A.n, b))
         Y = P.sparse_dense_mul(A, X)
         np.testing.assert_allclose(Y, M @ X, rtol=1e-12, atol=1e-11)
@@ -62,8 +62,9 @@ def test_spmm_long_rows_split(gpu):
     dense[3] = 0.0  # an empty row
     M = sp.csr_matrix(dense)
     A = P.SparseRatings(M, 0.5, 5.0)
-    X = rng.standard_normal((9000, 20))
-    np.testing.assert_allclose(P.sparse_dense_mul(A, X), dense @ X, rtol=1e-12, atol=1e-10)
+    for b in (20, 40):
+        X = rng.standard_normal((9000, b))
+        np.testing.assert_allclose(P.sparse_dense_mul(A, X), dense @ X, rtol=1e-12, atol=1e-10)
 
 
 def test_tsqr_orthonormal_and_spans(gpu):

@@ -42,3 +42,18 @@ a = K.spmm(d.A, X, out_m).clone()
 K.SPMM_HOT = True
 b = K.spmm(d.A, X, out_m).clone()
 print("hot vs plain max rel diff", float(((a - b).abs().max() / a.abs().max())))
+
+# one 40-column product vs two 20-column ones (the lookahead engine's fusion)
+X40 = torch.randn(A.n, 40, dtype=torch.float64, device=dev)
+Y40 = torch.randn(A.m, 40, dtype=torch.float64, device=dev)
+o40m = torch.empty(A.m, 40, dtype=torch.float64, device=dev)
+o40n = torch.empty(A.n, 40, dtype=torch.float64, device=dev)
+K.SPMM_HOT = False
+print(f"b=40: A@X {t(lambda: K.spmm(d.A, X40, o40m)):.1f} us   A.T@Y {t(lambda: K.spmm(d.AT, Y40, o40n)):.1f} us",
+      flush=True)
+ref = torch.cat([K.spmm(d.A, X40[:, :20].contiguous(), out_m).clone(), K.spmm(d.A, X40[:, 20:].contiguous(), out_m).clone()], 1)
+got = K.spmm(d.A, X40, o40m)
+print("b=40 vs 2 x b=20 max rel diff", float((got - ref).abs().max() / ref.abs().max()))
+X64 = torch.randn(A.n, 64, dtype=torch.float64, device=dev)
+o64 = torch.empty(A.m, 64, dtype=torch.float64, device=dev)
+print(f"b=64: A@X {t(lambda: K.spmm(d.A, X64, o64)):.1f} us")
