@@ -213,10 +213,11 @@ def run_b200(args):
     d = A.device(dev)
     torch.cuda.synchronize()
 
-    def step():
+    def step(precision="fp64"):
         f, trace = P.auto_latent_factors(A, vs, block_size=BLOCK, passes=PASSES, patience=PATIENCE,
-                                         min_improvement=MIN_IMPROVEMENT, seed=SEED, max_rank=K_CAP)
-        mae, rmse = P.evaluate_errors(A, f, ts)
+                                         min_improvement=MIN_IMPROVEMENT, seed=SEED, max_rank=K_CAP,
+                                         precision=precision)
+        mae, rmse = P.evaluate_errors(A, f, ts, precision=precision)
         return f, trace, mae, rmse
 
     clocks = Clocks(local) if not os.environ.get("BENCH_NO_CLOCKS") else Clocks.disabled()
@@ -251,14 +252,39 @@ def run_b200(args):
     t_step = ev[0].elapsed_time(ev[-1]) / 1e3 / args.steps
     # kernel breakdown from one extra, untimed step with per-call CUDA-event
     # spans (their host cost stays out of the timed region)
+    # (scoring on the caller's stream, so each span holds one kernel alone)
+    from paper_2009_02251_b200 import cf as _cf
+    pipe, _cf.PIPELINE = _cf.PIPELINE, False
     K.PROFILE = []
     step()
     torch.cuda.synchronize()
     prof = K.profile_summary(K.PROFILE)
     K.PROFILE = None
+    _cf.PIPELINE = pipe
     psteps = 1
     if ws > 1:  # the slowest rank's time per step
         t_step = max_over_ranks(t_step, dev)
+
+    # fp32 variant (BASELINE configs 2 / 4): float storage of the gathered
+    # operands, fp64 accumulation; same protocol, fewer steps
+    variants = {}
+    if not args.no_variants:
+        for _ in range(2):
+            step("fp32")
+        torch.cuda.synchronize()
+        nv = max(2, min(args.steps, 5))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(nv):
+            f32, tr32, mae32, rmse32 = step("fp32")
+        e1.record()
+        torch.cuda.synchronize()
+        t32 = max_over_ranks(e0.elapsed_time(e1) / 1e3 / nv, dev)
+        variants["fp32"] = {"value": round(t32, 6), "unit": "s", "steps": nv, "k": int(f32.k), "blocks": len(tr32),
+                            "test_mae": mae32, "test_rmse": rmse32,
+                            "test_rmse_rel_err_vs_f64": abs(rmse32 - rmse) / rmse,
+                            "storage": "float copies of the SpMM dense operand and of the CF item rows; "
+                                       "fp64 accumulation, QB algebra and outputs"}
 
     # e2e: the public API from host buffers, upload + results read inside
     e2e_times, h2d = [], 0
@@ -319,6 +345,7 @@ def run_b200(args):
         "e2e": {"value": round(statistics.median(e2e_times), 6), "unit": "s", "runs_s": [round(t, 4) for t in e2e_times], "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
+        "variants": variants,
         "clocks": ck,
         "setup": {"generate_split_s": round(gen_s, 2)},
     }
@@ -339,6 +366,7 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--blocks", type=int, default=None, help="reference arm: block count to extrapolate to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the fp32-variant timing")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

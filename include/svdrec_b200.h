@@ -102,6 +102,16 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
  * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
  * fall back to the plain kernel. */
 int svdrec_spmm_warps_per_sm(int32_t b);
+/* fp32 variant: X stored as float (half the gathered bytes), values,
+ * accumulation and Y in double.  b in {4, 8, ..., 32}, 16-B aligned rows,
+ * the 16-warps-per-SM schedule. */
+int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                    const int64_t* d_seg_end, const int32_t* d_seg_slot,
+                    const int32_t* d_indices, const double* d_values,
+                    const float* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
+                    int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
+                    const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
+                    double* d_partial, void* stream);
 /* Same product with the first nhot rows of X staged in shared memory: the
  * CSR must be "ranked" -- in every row the entries with column < nhot come
  * first (e.g. columns relabelled by popularity and each row ordered by the
@@ -239,7 +249,9 @@ int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double
  *   popularity rank (svdrec_cf_relabel; 0 = most rated) and each row's
  *   entries ordered by rank, with d_Yr the unit rows Yn in rank order
  *   (Yr[rank(l)] = Yn[l]) plus one zero row at index n_items (the
- *   padding target); d_Xn and d_norm stay indexed by item id, as do
+ *   padding target), rows 16-B aligned (ldy even; float: ldy % 4 == 0) and
+ *   zero-padded to that width (16-B vector loads);
+ *   d_Xn and d_norm stay indexed by item id, as do
  *   the samples (d_items).  The first rows of Yr that fit in ~208 KB are
  *   staged in every CTA's shared memory, so each user's hot ratings (a
  *   prefix of the ranked row) read shared memory.  Work items -- a user,
@@ -260,11 +272,21 @@ int svdrec_cf_normalize_pair(int64_t n, int32_t k, const double* d_X, int64_t ld
                              int64_t ldn, double* d_norm, void* stream);
 int svdrec_cf_predict(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
                       const int32_t* d_items, const int32_t* d_ranked_indices,
-                      const double* d_ranked_values, int32_t k, const double* d_Yr, const double* d_Xn,
-                      int64_t ldn, const double* d_norm, double global_mean, double rating_min,
-                      double rating_max, int32_t n_items, int32_t* d_done, int64_t ndone,
-                      double* d_partial, int32_t* d_counter, double* d_value, double* d_raw,
-                      uint8_t* d_fallback, void* stream);
+                      const double* d_ranked_values, int32_t k, const double* d_Yr, int64_t ldy,
+                      const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
+                      double rating_min, double rating_max, int32_t n_items, int32_t* d_done,
+                      int64_t ndone, double* d_partial, int32_t* d_counter, double* d_value,
+                      double* d_raw, uint8_t* d_fallback, void* stream);
+/* fp32 variant: d_Yr (leading dimension ldy) stored as float -- half the
+ * gathered bytes and twice the rows staged on chip; accumulation, the
+ * sample rows d_Xn and all outputs stay double. */
+int svdrec_cf_predict_f32(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
+                          const int32_t* d_items, const int32_t* d_ranked_indices,
+                          const double* d_ranked_values, int32_t k, const float* d_Yr, int64_t ldy,
+                          const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
+                          double rating_min, double rating_max, int32_t n_items, int32_t* d_done,
+                          int64_t ndone, double* d_partial, int32_t* d_counter, double* d_value,
+                          double* d_raw, uint8_t* d_fallback, void* stream);
 /* Ranked CSR for svdrec_cf_predict: d_out[t] = d_rank[d_indices[t]] (item ->
  * popularity rank, 0 = most rated); the caller then orders each row's
  * entries by rank (ascending), so every user's hot items form a prefix. */

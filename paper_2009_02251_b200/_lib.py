@@ -34,6 +34,7 @@ SIGNATURES = {
     "svdrec_normal_fill": (C.c_int, [_u64, _u64, _p, _i64, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_warps_per_sm": (C.c_int, [_i32]),
+    "svdrec_spmm_x32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_hot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _i32, _p]),
     "svdrec_gemm_tn_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "svdrec_gemm_tn": (C.c_int, [_i64, _i64, _i64, _f64, _p, _i64, _p, _i64, _f64, _p, _i64, _p, _sz, _p]),
@@ -58,8 +59,10 @@ SIGNATURES = {
     "svdrec_gesvj": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _i64, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_cf_normalize": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p]),
     "svdrec_cf_normalize_pair": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _p, _i64, _p, _p]),
-    "svdrec_cf_predict": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p, _p, _i64, _p, _f64, _f64, _f64, _i32,
-                                    _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "svdrec_cf_predict": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p, _i64, _p, _i64, _p, _f64, _f64, _f64,
+                                    _i32, _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "svdrec_cf_predict_f32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p, _i64, _p, _i64, _p, _f64, _f64, _f64,
+                                        _i32, _p, _i64, _p, _p, _p, _p, _p, _p]),
     "svdrec_cf_relabel": (C.c_int, [_i64, _p, _p, _p, _p]),
     "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
     "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),

@@ -31,9 +31,10 @@ from .sparse import SparseRatings
 
 WEIGHT_FLOOR = 1e-9  # cf.py:23
 F64 = torch.float64
-# Score block l on a side stream while block l+1 is factored (SVDREC_PIPELINE=1).
-# Off by default: measured slower on B200 (the two streams thrash L2).
-PIPELINE = os.environ.get("SVDREC_PIPELINE", "0") == "1"
+# Score block l on a side stream while block l+1 is factored (on by default:
+# 47.5 vs 48.1 ms per bench step with the ranked CF kernel; SVDREC_PIPELINE=0
+# scores on the caller's stream).
+PIPELINE = os.environ.get("SVDREC_PIPELINE", "1") == "1"
 SPECULATE = os.environ.get("SVDREC_SPECULATE", "0") == "1"  # measured: no gain
 _SIDE: dict = {}
 
@@ -291,10 +292,10 @@ class _Samples:
         self._checked.add(A.shape)
 
 
-def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float):
+def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float, precision: str = "fp64"):
     d = A.device(factors.Xn.device)
     return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Yn, factors.Xn, factors.norm_device, gmean,
-                        A.rating_min, A.rating_max, s.plan_for(A))
+                        A.rating_min, A.rating_max, s.plan_for(A), precision)
 
 
 def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: int) -> Prediction:
@@ -338,14 +339,14 @@ def mae(predictions: Sequence[float], truths: Sequence[float]) -> float:
     return float(np.abs(p - t).mean())
 
 
-def _errors(A, factors, s: _Samples):
+def _errors(A, factors, s: _Samples, precision: str = "fp64"):
     if A.nnz == 0:
         raise ValueError("cannot take the mean of a matrix with no ratings")
     if isinstance(A, ShardedRatings):
-        return _sharded_errors(A, factors, s)
+        return _sharded_errors(A, factors, s, precision)
     if s.n == 0:
         raise ValueError("cannot average zero errors")
-    val, _, _ = _predict_device(A, factors, s, A.device(factors.Xn.device).global_mean)
+    val, _, _ = _predict_device(A, factors, s, A.device(factors.Xn.device).global_mean, precision)
     e = K.err_sum(val, s.truth).cpu().numpy()
     return float(e[0] / s.n), float(np.sqrt(e[1] / s.n))
 
@@ -375,40 +376,42 @@ def _count(samples) -> int:
     return len(list(samples))
 
 
-def _local_err_sums(A: ShardedRatings, factors, s: _Samples, out: torch.Tensor) -> torch.Tensor:
+def _local_err_sums(A: ShardedRatings, factors, s: _Samples, out: torch.Tensor, precision: str = "fp64") -> torch.Tensor:
     """(sum |e|, sum e^2) over this rank's samples, then all-reduced."""
     if s.n:
-        val, _, _ = _predict_device(A.local, factors, s, A.global_mean)
+        val, _, _ = _predict_device(A.local, factors, s, A.global_mean, precision)
         K.err_sum(val, s.truth, out=out)
     else:
         out.zero_()
     return A.comm.all_reduce_(out)
 
 
-def _sharded_errors(A: ShardedRatings, factors, s):
+def _sharded_errors(A: ShardedRatings, factors, s, precision: str = "fp64"):
     dev = factors.Xn.device
     if not isinstance(s, _Samples) or not hasattr(s, "n_total"):
         s = _shard_samples(A, s, dev)
     if s.n_total == 0:
         raise ValueError("cannot average zero errors")
-    e = _local_err_sums(A, factors, s, torch.zeros(2, dtype=F64, device=dev)).cpu().numpy()
+    e = _local_err_sums(A, factors, s, torch.zeros(2, dtype=F64, device=dev), precision).cpu().numpy()
     return float(e[0] / s.n_total), float(np.sqrt(e[1] / s.n_total))
 
 
-def evaluate_mae(A: SparseRatings, factors: LatentFactors, samples: Iterable) -> float:
-    """MAE of clamped predictions over held-out triples (cf.py:178-190)."""
+def evaluate_mae(A: SparseRatings, factors: LatentFactors, samples: Iterable, precision: str = "fp64") -> float:
+    """MAE of clamped predictions over held-out triples (cf.py:178-190).
+    ``precision="fp32"`` (not in the reference) stores the gathered item
+    rows as float, accumulating in double."""
     if isinstance(A, ShardedRatings):
-        return _errors(A, factors, samples)[0]
+        return _errors(A, factors, samples, precision)[0]
     s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Xn.device)
-    return _errors(A, factors, s)[0]
+    return _errors(A, factors, s, precision)[0]
 
 
-def evaluate_errors(A: SparseRatings, factors: LatentFactors, samples) -> tuple[float, float]:
+def evaluate_errors(A: SparseRatings, factors: LatentFactors, samples, precision: str = "fp64") -> tuple[float, float]:
     """(MAE, RMSE) of clamped Alg. 4 predictions (RMSE: BASELINE metric)."""
     if isinstance(A, ShardedRatings):
-        return _errors(A, factors, samples)
+        return _errors(A, factors, samples, precision)
     s = samples if isinstance(samples, _Samples) else _Samples(samples, factors.Xn.device)
-    return _errors(A, factors, s)
+    return _errors(A, factors, s, precision)
 
 
 class ValidationMae:
@@ -422,7 +425,11 @@ class ValidationMae:
     block costs one small host read (error sums + status word).
     """
 
-    def __init__(self, train: SparseRatings, validation, patience: int = 2, min_improvement: float = 1e-4) -> None:
+    def __init__(self, train: SparseRatings, validation, patience: int = 2, min_improvement: float = 1e-4,
+                 precision: str = "fp64") -> None:
+        if precision not in ("fp64", "fp32"):
+            raise ValueError(f"precision must be 'fp64' or 'fp32', not {precision!r}")
+        self.precision = precision
         if patience < 1:
             raise ValueError("patience must be at least 1")
         if min_improvement < 0.0:
@@ -512,9 +519,9 @@ class ValidationMae:
             factors = LatentFactors.from_qb_metric(Bt, G, Z)
             s = self.samples
             if self.shard is not None:
-                _local_err_sums(self.shard, factors, s, mb["sums"])
+                _local_err_sums(self.shard, factors, s, mb["sums"], self.precision)
             else:
-                val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+                val, _, _ = _predict_device(self.train, factors, s, self._gmean, self.precision)
                 K.err_sum(val, s.truth, out=mb["sums"])
             mb.read_async()
         return state, factors
@@ -539,9 +546,10 @@ class ValidationMae:
             with torch.cuda.stream(self._stream):
                 factors = LatentFactors(_eig_T(state.Bt_device, factors._G))
                 if self.shard is not None:
-                    sums = _local_err_sums(self.shard, factors, s, torch.zeros(2, dtype=F64, device=s.device))
+                    sums = _local_err_sums(self.shard, factors, s, torch.zeros(2, dtype=F64, device=s.device),
+                                           self.precision)
                 else:
-                    val, _, _ = _predict_device(self.train, factors, s, self._gmean)
+                    val, _, _ = _predict_device(self.train, factors, s, self._gmean, self.precision)
                     sums = K.err_sum(val, s.truth)
                 got = {"sums": sums.cpu().numpy()}
         n = self.n_total
@@ -574,19 +582,22 @@ class ValidationMae:
 
 def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, passes: int = 10, patience: int = 2,
                         min_improvement: float = 1e-4, seed: int = 0,
-                        max_rank: int | None = None) -> tuple[LatentFactors, list[BlockEval]]:
+                        max_rank: int | None = None, precision: str = "fp64") -> tuple[LatentFactors, list[BlockEval]]:
     """Alg. 5: grow item factors until validation MAE stops improving
     (cf.py:257-294).  ``max_rank`` (not in the reference) ends the scan once
-    that many factors are held and keeps the best block so far."""
+    that many factors are held and keeps the best block so far.
+    ``precision="fp32"`` (not in the reference) is the fp32 variant: the
+    gathered operands of the SpMMs and of the CF scoring are stored as float
+    (accumulation, the QB algebra and all returned values stay double)."""
     if passes <= 2:
         raise ValueError("passes must exceed 2")
     if block_size < 1:
         raise ValueError("block_size must be positive")
     if 2 * block_size > min(A.shape):
         raise ValueError(f"block_size {block_size} too large for min(m, n) = {min(A.shape)}")
-    criterion = ValidationMae(A, validation, patience=patience, min_improvement=min_improvement)
+    criterion = ValidationMae(A, validation, patience=patience, min_improvement=min_improvement, precision=precision)
     stream = GaussianStream(seed)
-    gen = qb_pass_blocks(A, block_size, passes, stream, max_rank=max_rank)
+    gen = qb_pass_blocks(A, block_size, passes, stream, max_rank=max_rank, precision=precision)
     # Same criterion sequence as the reference's ``for state in ...: if
     # criterion(state): break``, pipelined: block l is scored on the
     # criterion's stream while block l+1 is factored on this one (a block

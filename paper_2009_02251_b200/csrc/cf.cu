@@ -58,37 +58,83 @@ __global__ void k_normalize_pair(int64_t n, int k, const double* __restrict__ X,
   if (lane == 0) norm[item] = nr;
 }
 
+// Row storage of the scoring kernel: 16-B vector loads, VE elements each
+// (double2 or float4), so a row of k values costs k / VE loads per lane
+// group instead of k -- the gathers are bound by load requests, not bytes.
+template <typename TY, int VE>
+struct RowVec;
+template <typename TY>
+struct RowVec<TY, 1> {
+  using T = TY;
+  __device__ __forceinline__ static void get(const T& x, double (&o)[1]) { o[0] = (double)x; }
+};
+template <>
+struct RowVec<double, 2> {
+  using T = double2;
+  __device__ __forceinline__ static void get(const T& x, double (&o)[2]) {
+    o[0] = x.x;
+    o[1] = x.y;
+  }
+};
+template <>
+struct RowVec<float, 2> {
+  using T = float2;
+  __device__ __forceinline__ static void get(const T& x, double (&o)[2]) {
+    o[0] = x.x;
+    o[1] = x.y;
+  }
+};
+template <>
+struct RowVec<float, 4> {
+  using T = float4;
+  __device__ __forceinline__ static void get(const T& x, double (&o)[4]) {
+    o[0] = x.x;
+    o[1] = x.y;
+    o[2] = x.z;
+    o[3] = x.w;
+  }
+};
+
 // Threads per CTA of the scoring kernel (one persistent CTA per SM): the
-// register file caps the per-lane accumulators (2 * MAXR doubles plus four
+// register file caps the per-lane accumulators (2 * NT * VE doubles plus U
 // rows of loads in flight), so wide k trades warps for registers.
-template <int MAXR>
+template <int NA>  // accumulators per lane (NT * VE)
 struct PredictShape {
-  static constexpr int kThreads = MAXR <= 4 ? 768 : (MAXR <= 8 ? 512 : 256);
+  static constexpr int kThreads = NA <= 4 ? 768 : (NA <= 6 ? 640 : (NA <= 8 ? 512 : 256));
 };
 
-// Ratings processed per step of the gather loops: every lane keeps
-// U * MAXR loads in flight, so narrow rows (small k) take more of them.
-template <int MAXR>
-struct PredictUnroll {
-  static constexpr int U = MAXR <= 2 ? 8 : 4;
+// Ratings processed per step of the gather loops: every lane keeps U * NT
+// vector loads in flight, so narrow rows (small k) take more of them.
+template <int NT, int VE>
+struct PredictUnroll {  // narrow rows in flight cost fewer registers: take more of them
+  static constexpr int U = (NT <= 1 || (VE == 4 && NT <= 2)) ? 8 : 4;
 };
 
-// P += v * row, S += row for U rows (one per q), lane-strided; padding
-// entries point at a zero row.  The accumulation order is rating by rating.
-template <int MAXR, int U, bool SHARED>
-__device__ __forceinline__ void accum(double (&P)[MAXR], double (&S)[MAXR], const double* const (&rows)[U],
-                                      const double (&vv)[U], int lane, int k) {
+// P += v * row, S += row for U rows (one per q), lane-strided in VE-wide
+// vectors (element (t * 32 + lane) * VE + i); padding entries point at a
+// zero row.  The accumulation order is rating by rating.
+template <int NT, int U, bool SHARED, typename TY, int VE>
+__device__ __forceinline__ void accum(double (&P)[NT * VE], double (&S)[NT * VE], const TY* const (&rows)[U],
+                                      const double (&vv)[U], int lane, int kp) {
+  using V = typename RowVec<TY, VE>::T;
 #pragma unroll
-  for (int t = 0; t < MAXR; ++t) {
-    const int idx = lane + 32 * t;
-    if (idx < k) {
-      double x[U];
+  for (int t = 0; t < NT; ++t) {
+    const int base = (t * 32 + lane) * VE;
+    if (base < kp) {
+      V x[U];
 #pragma unroll
-      for (int q = 0; q < U; ++q) x[q] = SHARED ? rows[q][idx] : __ldg(rows[q] + idx);
+      for (int q = 0; q < U; ++q)
+        x[q] = SHARED ? *reinterpret_cast<const V*>(rows[q] + base) : __ldg(reinterpret_cast<const V*>(rows[q] + base));
 #pragma unroll
-      for (int q = 0; q < U; ++q) P[t] = fma(vv[q], x[q], P[t]);
+      for (int q = 0; q < U; ++q) {
+        double xe[VE];
+        RowVec<TY, VE>::get(x[q], xe);
 #pragma unroll
-      for (int q = 0; q < U; ++q) S[t] += x[q];
+        for (int i = 0; i < VE; ++i) {
+          P[t * VE + i] = fma(vv[q], xe[i], P[t * VE + i]);
+          S[t * VE + i] += xe[i];
+        }
+      }
     }
   }
 }
@@ -98,20 +144,26 @@ __device__ __forceinline__ void accum(double (&P)[MAXR], double (&S)[MAXR], cons
 // first: the unit rows of the ``nhot`` most popular items (Yr[0, nhot),
 // rank order) are staged once per CTA in shared memory and a 32-rating
 // batch splits into a shared-memory prefix (LDS, no long latency) and an
-// L2-gathered suffix (LDG, four rows in flight per lane).
-template <int MAXR>
-__global__ void __launch_bounds__(PredictShape<MAXR>::kThreads, 1)
+// L2-gathered suffix (LDG, U rows in flight per lane).
+// TY: storage type of the gathered unit rows (double; float for the fp32
+// variant); rows are padded to kp (a multiple of VE) with zeros, ldy % VE
+// == 0; accumulation stays double.
+template <int NT, typename TY, int VE>
+__global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
     k_predict(int64_t nwork, const int64_t* __restrict__ wstart, const int4* __restrict__ wmeta,
               const int32_t* __restrict__ items, const int32_t* __restrict__ rindices,
-              const double* __restrict__ rvalues, int k, const double* __restrict__ Yr,
-              const double* __restrict__ Xn, int64_t ldn, const double* __restrict__ norm, double gmean, double lo,
-              double hi, int nhot, int zrow, int* __restrict__ done, double* __restrict__ part,
+              const double* __restrict__ rvalues, int k, const TY* __restrict__ Yr,
+              const double* __restrict__ Xn, int64_t ldn, int64_t ldy, const double* __restrict__ norm, double gmean,
+              double lo, double hi, int nhot, int zrow, int* __restrict__ done, double* __restrict__ part,
               int* __restrict__ counter,
               double* __restrict__ out_val, double* __restrict__ out_raw, uint8_t* __restrict__ out_fb) {
-  extern __shared__ double hs[];  // nhot rows + a zero row (padding target)
-  for (int64_t t = threadIdx.x; t < (int64_t)(nhot + 1) * k; t += blockDim.x) {
-    const int64_t sl = t / k, e = t - sl * k;
-    hs[t] = sl < nhot ? Yr[sl * ldn + e] : 0.0;
+  constexpr int NA = NT * VE;
+  const int kp = (k + VE - 1) / VE * VE;
+  extern __shared__ __align__(16) unsigned char hs_raw[];
+  TY* hs = reinterpret_cast<TY*>(hs_raw);  // nhot rows + a zero row (padding target), stride kp
+  for (int64_t t = threadIdx.x; t < (int64_t)(nhot + 1) * kp; t += blockDim.x) {
+    const int64_t sl = t / kp, e = t - sl * kp;
+    hs[t] = sl < nhot ? Yr[sl * ldy + e] : TY(0);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -127,16 +179,16 @@ __global__ void __launch_bounds__(PredictShape<MAXR>::kThreads, 1)
   while (wi < nwork) {
     const int64_t a = __ldg(wstart + wi);
     const int4 m0 = __ldg(wmeta + 2 * (int64_t)wi);      // len, deg, s0, s1
-    const int4 m1 = __ldg(wmeta + 2 * (int64_t)wi + 1);  // nch, slot, done, 0
+    const int4 m1 = __ldg(wmeta + 2 * (int64_t)wi + 1);  // nch, slot, done, chunk index
     int wn = 0;
     if (lane == 0) wn = atomicAdd(counter, 1);
     const int64_t e = a + m0.x;
     const int64_t deg = m0.y;
     const int64_t s0 = m0.z, s1 = m0.w;
     const int nch = m1.x;
-    double P[MAXR], S[MAXR];
+    double P[NA], S[NA];
 #pragma unroll
-    for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
+    for (int t = 0; t < NA; ++t) P[t] = S[t] = 0.0;
     double vsum = 0.0;
     // the next 32-entry CSR batch is loaded while this one is processed
     int32_t ci_next = 0x7fffffff;
@@ -158,45 +210,47 @@ __global__ void __launch_bounds__(PredictShape<MAXR>::kThreads, 1)
       const int nv = (int)min64(32, e - base);
       vsum += vi;  // this lane's entry (0 past the end)
       const int nh = __popc(__ballot_sync(0xffffffffu, ci < nhot));  // ascending ranks: a prefix
-      constexpr int U = PredictUnroll<MAXR>::U;
+      constexpr int U = PredictUnroll<NT, VE>::U;
       for (int j = 0; j < nh; j += U) {
-        const double* rows[U];
+        const TY* rows[U];
         double vv[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
           const int jj = j + q;
           const int32_t cq = __shfl_sync(0xffffffffu, ci, jj & 31);
           vv[q] = __shfl_sync(0xffffffffu, vi, jj & 31);
-          rows[q] = hs + (int64_t)(jj < nh ? cq : nhot) * k;
+          rows[q] = hs + (int64_t)(jj < nh ? cq : nhot) * kp;
         }
-        accum<MAXR, U, true>(P, S, rows, vv, lane, k);
+        accum<NT, U, true, TY, VE>(P, S, rows, vv, lane, kp);
       }
       for (int j = nh; j < nv; j += U) {
-        const double* rows[U];
+        const TY* rows[U];
         double vv[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
           const int jj = j + q;
           const int32_t cq = __shfl_sync(0xffffffffu, ci, jj & 31);
           vv[q] = __shfl_sync(0xffffffffu, vi, jj & 31);
-          rows[q] = Yr + (int64_t)(jj < nv ? cq : zrow) * ldn;
+          rows[q] = Yr + (int64_t)(jj < nv ? cq : zrow) * ldy;
         }
-        accum<MAXR, U, false>(P, S, rows, vv, lane, k);
+        accum<NT, U, false, TY, VE>(P, S, rows, vv, lane, kp);
       }
     }
     vsum = warp_sum(vsum);
     if (nch > 1) {
       const int64_t pw = 2 * (int64_t)k + 1;
-      const int slot = m1.y, slot0 = slot - m1.w;  // m1.w: chunk index
+      const int slot = m1.y, slot0 = slot - m1.w;
       double* mine = part + (int64_t)slot * pw;
 #pragma unroll
-      for (int t = 0; t < MAXR; ++t) {
-        const int idx = lane + 32 * t;
-        if (idx < k) {
-          mine[idx] = P[t];
-          mine[k + idx] = S[t];
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+          const int idx = (t * 32 + lane) * VE + i;
+          if (idx < k) {
+            mine[idx] = P[t * VE + i];
+            mine[k + idx] = S[t * VE + i];
+          }
         }
-      }
       if (lane == 0) mine[2 * k] = vsum;
       __threadfence();
       int prev = 0;
@@ -208,18 +262,20 @@ __global__ void __launch_bounds__(PredictShape<MAXR>::kThreads, 1)
       }
       __threadfence();
 #pragma unroll
-      for (int t = 0; t < MAXR; ++t) P[t] = S[t] = 0.0;
+      for (int t = 0; t < NA; ++t) P[t] = S[t] = 0.0;
       vsum = 0.0;
       for (int q = 0; q < nch; ++q) {
         const double* ps = part + ((int64_t)slot0 + q) * pw;
 #pragma unroll
-        for (int t = 0; t < MAXR; ++t) {
-          const int idx = lane + 32 * t;
-          if (idx < k) {
-            P[t] += __ldcg(ps + idx);
-            S[t] += __ldcg(ps + k + idx);
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int i = 0; i < VE; ++i) {
+            const int idx = (t * 32 + lane) * VE + i;
+            if (idx < k) {
+              P[t * VE + i] += __ldcg(ps + idx);
+              S[t * VE + i] += __ldcg(ps + k + idx);
+            }
           }
-        }
         vsum += __ldcg(ps + 2 * k);
       }
     }
@@ -246,17 +302,19 @@ __global__ void __launch_bounds__(PredictShape<MAXR>::kThreads, 1)
         const double* row1 = Xn + (int64_t)j1 * ldn;
         double num0 = 0.0, den0 = 0.0, num1 = 0.0, den1 = 0.0;
 #pragma unroll
-        for (int t = 0; t < MAXR; ++t) {
-          const int idx = lane + 32 * t;
-          if (idx < k) {
-            const double x0 = ok0 ? __ldg(row0 + idx) : 0.0;
-            const double x1 = ok1 ? __ldg(row1 + idx) : 0.0;
-            num0 = fma(x0, P[t], num0);
-            den0 = fma(x0, S[t], den0);
-            num1 = fma(x1, P[t], num1);
-            den1 = fma(x1, S[t], den1);
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int i = 0; i < VE; ++i) {
+            const int idx = (t * 32 + lane) * VE + i;
+            if (idx < k) {
+              const double x0 = ok0 ? __ldg(row0 + idx) : 0.0;
+              const double x1 = ok1 ? __ldg(row1 + idx) : 0.0;
+              num0 = fma(x0, P[t * VE + i], num0);
+              den0 = fma(x0, S[t * VE + i], den0);
+              num1 = fma(x1, P[t * VE + i], num1);
+              den1 = fma(x1, S[t * VE + i], den1);
+            }
           }
-        }
         num0 = warp_sum(num0);
         den0 = warp_sum(den0);
         num1 = warp_sum(num1);
@@ -348,14 +406,15 @@ extern "C" int svdrec_cf_normalize_pair(int64_t n, int32_t k, const double* d_X,
   return check_launch("cf_normalize_pair");
 }
 
-extern "C" int svdrec_cf_predict(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
-                                 const int32_t* d_items, const int32_t* d_ranked_indices,
-                                 const double* d_ranked_values, int32_t k, const double* d_Yr, const double* d_Xn,
-                                 int64_t ldn, const double* d_norm, double global_mean, double rating_min,
-                                 double rating_max, int32_t n_items, int32_t* d_done, int64_t ndone,
-                                 double* d_partial, int32_t* d_counter, double* d_value, double* d_raw,
-                                 uint8_t* d_fallback, void* stream) {
-  SVDREC_ARG(nwork >= 0 && k >= 1 && ldn >= k && n_items >= 0, "cf_predict: bad arguments");
+namespace {
+template <typename TY>
+int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta, const int32_t* d_items,
+                    const int32_t* d_ranked_indices, const double* d_ranked_values, int32_t k, const TY* d_Yr,
+                    int64_t ldy, const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
+                    double rating_min, double rating_max, int32_t n_items, int32_t* d_done, int64_t ndone,
+                    double* d_partial, int32_t* d_counter, double* d_value, double* d_raw, uint8_t* d_fallback,
+                    void* stream) {
+  SVDREC_ARG(nwork >= 0 && k >= 1 && ldn >= k && ldy >= k && n_items >= 0, "cf_predict: bad arguments");
   if (k > 1024) {
     set_error("cf_predict: latent dimension %d > 1024 unsupported", k);
     return SVDREC_E_UNSUPPORTED;
@@ -366,44 +425,87 @@ extern "C" int svdrec_cf_predict(int64_t nwork, const int64_t* d_work_start, con
   cudaStream_t s = as_stream(stream);
   SVDREC_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), s));
   if (ndone > 0) SVDREC_CUDA(cudaMemsetAsync(d_done, 0, (size_t)ndone * sizeof(int32_t), s));
-  const int r = (k + 31) / 32;
+  // elements per lane and load: 16-B vectors for wide rows, narrower ones
+  // for short rows (more lanes busy per rating)
+  constexpr int VMAX = (int)(16 / sizeof(TY));
+  const int ve = k <= 32 ? 1 : (k <= 64 || VMAX == 2 ? 2 : 4);
+  SVDREC_ARG(ldy % VMAX == 0 && reinterpret_cast<uintptr_t>(d_Yr) % 16 == 0,
+             "cf_predict: Yr rows must be 16-B aligned (ldy %% %d == 0)", VMAX);
+  const int kp = (k + ve - 1) / ve * ve;
+  const int nt = (kp / ve + 31) / 32;  // vector steps per lane
   // one persistent CTA per SM holding the hottest items' unit rows in
-  // shared memory (as many as fit in kHotBytes)
+  // shared memory (as many as fit in kHotBytes, plus the zero row)
   constexpr size_t kHotBytes = 208 * 1024;
-  int nhot = (int)(kHotBytes / ((size_t)k * 8));
+  int nhot = (int)(kHotBytes / ((size_t)kp * sizeof(TY))) - 1;
   if (nhot > n_items) nhot = n_items;
-  int nhot_fit = (int)(kHotBytes / ((size_t)k * 8)) - 1;  // + the zero row
-  if (nhot > nhot_fit) nhot = nhot_fit;
   if (nhot < 0) nhot = 0;
-  const size_t smem = (size_t)(nhot + 1) * k * 8;
+  const size_t smem = (size_t)(nhot + 1) * kp * sizeof(TY);
   const int64_t grid = sm_count();
-#define SVDREC_PRED(R)                                                                                        \
+#define SVDREC_PRED(NT, VE)                                                                                   \
   do {                                                                                                        \
     static bool attr_set = false;                                                                             \
     if (!attr_set) {                                                                                          \
-      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<NT, TY, VE>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                        (int)kHotBytes));                                                      \
       attr_set = true;                                                                                        \
     }                                                                                                         \
-    k_predict<R><<<(unsigned)grid, PredictShape<R>::kThreads, smem, s>>>(                                     \
+    k_predict<NT, TY, VE><<<(unsigned)grid, PredictShape<NT * VE>::kThreads, smem, s>>>(                      \
         nwork, d_work_start, reinterpret_cast<const int4*>(d_work_meta), d_items, d_ranked_indices,           \
-        d_ranked_values, k, d_Yr, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, nhot, n_items,      \
+        d_ranked_values, k, d_Yr, d_Xn, ldn, ldy, d_norm, global_mean, rating_min, rating_max, nhot, n_items, \
         d_done, d_partial, d_counter, d_value, d_raw, d_fallback);                                            \
   } while (0)
-  if (r <= 1)
-    SVDREC_PRED(1);
-  else if (r <= 2)
-    SVDREC_PRED(2);
-  else if (r <= 4)
-    SVDREC_PRED(4);
-  else if (r <= 8)
-    SVDREC_PRED(8);
-  else if (r <= 16)
-    SVDREC_PRED(16);
-  else
-    SVDREC_PRED(32);
+  if (ve == 1)
+    SVDREC_PRED(1, 1);
+  else if (ve == 2 && nt <= 1)
+    SVDREC_PRED(1, 2);
+  else if (VMAX == 4) {
+    if (nt <= 1)
+      SVDREC_PRED(1, VMAX);
+    else if (nt <= 2)
+      SVDREC_PRED(2, VMAX);
+    else if (nt <= 4)
+      SVDREC_PRED(4, VMAX);
+    else
+      SVDREC_PRED(8, VMAX);
+  } else {
+    if (nt <= 2)
+      SVDREC_PRED(2, VMAX);
+    else if (nt <= 3)
+      SVDREC_PRED(3, VMAX);
+    else if (nt <= 4)
+      SVDREC_PRED(4, VMAX);
+    else if (nt <= 8)
+      SVDREC_PRED(8, VMAX);
+    else
+      SVDREC_PRED(16, VMAX);
+  }
 #undef SVDREC_PRED
   return check_launch("cf_predict");
+}
+}  // namespace
+
+extern "C" int svdrec_cf_predict(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
+                                 const int32_t* d_items, const int32_t* d_ranked_indices,
+                                 const double* d_ranked_values, int32_t k, const double* d_Yr, int64_t ldy,
+                                 const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
+                                 double rating_min, double rating_max, int32_t n_items, int32_t* d_done,
+                                 int64_t ndone, double* d_partial, int32_t* d_counter, double* d_value,
+                                 double* d_raw, uint8_t* d_fallback, void* stream) {
+  return cf_predict_impl<double>(nwork, d_work_start, d_work_meta, d_items, d_ranked_indices, d_ranked_values, k,
+                                 d_Yr, ldy, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, n_items, d_done,
+                                 ndone, d_partial, d_counter, d_value, d_raw, d_fallback, stream);
+}
+
+extern "C" int svdrec_cf_predict_f32(int64_t nwork, const int64_t* d_work_start, const int32_t* d_work_meta,
+                                     const int32_t* d_items, const int32_t* d_ranked_indices,
+                                     const double* d_ranked_values, int32_t k, const float* d_Yr, int64_t ldy,
+                                     const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
+                                     double rating_min, double rating_max, int32_t n_items, int32_t* d_done,
+                                     int64_t ndone, double* d_partial, int32_t* d_counter, double* d_value,
+                                     double* d_raw, uint8_t* d_fallback, void* stream) {
+  return cf_predict_impl<float>(nwork, d_work_start, d_work_meta, d_items, d_ranked_indices, d_ranked_values, k,
+                                d_Yr, ldy, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, n_items, d_done,
+                                ndone, d_partial, d_counter, d_value, d_raw, d_fallback, stream);
 }
 
 extern "C" int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,

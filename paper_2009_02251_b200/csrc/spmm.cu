@@ -139,12 +139,16 @@ constexpr int kPipeWarps = 8;
 // mbarrier per stage, so the gathered bytes cross the L1 data pipe once
 // (the consumer's LDS).  Padding rows use coordinate -1: TMA zero-fills
 // out-of-bounds rows and still counts their bytes.
-template <int P, int V = 2>
+// TX: element type of X (double, or float for the fp32 variant).  G4 and
+// ROWS count TX elements; STG (the stage size) and ROWSD count doubles.
+template <int P, int V = 2, typename TX = double>
 struct TmaGeom {
-  static constexpr int B = V * P;  // columns: P lanes x V doubles
-  static constexpr int G4 = (4 * B * 8 + 127) / 128 * 16;  // doubles per gather4 block (128-B aligned)
-  static constexpr int ROWS = 8 * G4;                       // 32 rows
-  static constexpr int STG = ROWS + 64;  // + 32 values + 16 (meta, pad) + 16 (32 column ids)
+  static constexpr int ES = (int)sizeof(TX);
+  static constexpr int B = V * P;  // columns: P lanes x V values
+  static constexpr int G4 = (4 * B * ES + 127) / 128 * 128 / ES;  // elements per gather4 block (128-B aligned)
+  static constexpr int ROWS = 8 * G4;                              // 32 rows
+  static constexpr int ROWSD = ROWS * ES / 8;
+  static constexpr int STG = ROWSD + 64;  // + 32 values + 16 (meta, pad) + 16 (32 column ids)
 };
 
 // Hot rows (W = 16 warps, one CTA per SM): with ``nhot`` > 0 the first
@@ -166,6 +170,13 @@ struct Acc {
   __device__ __forceinline__ void load(const double* p) {
 #pragma unroll
     for (int i = 0; i < V / 2; ++i) h[i] = reinterpret_cast<const double2*>(p)[i];
+  }
+  __device__ __forceinline__ void load(const float* p) {
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+      const float2 f = reinterpret_cast<const float2*>(p)[i];
+      h[i] = make_double2((double)f.x, (double)f.y);
+    }
   }
   __device__ __forceinline__ void fma(double v, const Acc& x) {
 #pragma unroll
@@ -193,15 +204,16 @@ struct Acc {
   }
 };
 
-template <int P, int S, int W, bool HOT, int V>
+template <int P, int S, int W, bool HOT, int V, typename TX = double>
 __global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma(
     const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_seg,
     const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
     const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ indices, const double* __restrict__ values,
     double* __restrict__ Y, int64_t ldy, double* __restrict__ partial, const double* __restrict__ X, int64_t ldx,
     int nhot) {
-  using Gm = TmaGeom<P, V>;
-  constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWS, STG = Gm::STG;
+  using Gm = TmaGeom<P, V, TX>;
+  static_assert(!HOT || sizeof(TX) == 8, "hot rows are staged as double");
+  constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWSD, STG = Gm::STG;
   extern __shared__ __align__(128) double smd[];
   __shared__ __align__(8) uint64_t bars[W * S];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -299,9 +311,10 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma
       if (4 * t + 3 < h) r3 = -1;
     }
     if (ng > g0) {
-      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)((ng - g0) * 4 * B * 8));
+      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)((ng - g0) * 4 * B * sizeof(TX)));
       __syncwarp();
-      if (lane >= g0 && lane < ng) tma_gather4(st + lane * G4, &tmX, 0, r0, r1, r2, r3, bar + slot);
+      if (lane >= g0 && lane < ng)
+        tma_gather4(reinterpret_cast<TX*>(st) + lane * G4, &tmX, 0, r0, r1, r2, r3, bar + slot);
     } else if (lane == 0) {
       mbar_expect_tx(bar + slot, 0);  // empty or all-hot chunk: complete the phase
     }
@@ -344,7 +357,8 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma
       // the chunk's hot prefix reads the staged hot rows instead
       constexpr int NS = (32 + G - 1) / G;
       const int h = HOT ? m.w >> 2 : 0;
-      const double* xr = st + ((g >> 2) * G4 + (g & 3) * B) + V * pc;
+      const TX* sx = reinterpret_cast<const TX*>(st);
+      const TX* xr = sx + ((g >> 2) * G4 + (g & 3) * B) + V * pc;
       const double* vr = st + ROWS + g;
       const int32_t* ir = reinterpret_cast<const int32_t*>(st + ROWS + 48);
       Acc<V> xs[NS];
@@ -354,8 +368,10 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma
         const int j = q * G + g;
         const int jo = q * G;
         const int jc = j < 32 ? j : 31;
-        const double* src = G4 == 4 * B ? xr + jo * B : st + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
-        if (HOT && j < h) src = hot + ir[jc] * B + V * pc;
+        const TX* src = G4 == 4 * B ? xr + jo * B : sx + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
+        if constexpr (HOT) {
+          if (j < h) src = hot + ir[jc] * B + V * pc;
+        }
         xs[q].load(src);
         vs[q] = vr[jc - g];
       }
@@ -387,10 +403,10 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma
   }
 }
 
-template <int P, int S, int W, bool HOT, int V = 2>
+template <int P, int S, int W, bool HOT, int V = 2, typename TX = double>
 int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
                const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
-               const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
+               const double* values, const TX* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
                int nhot, cudaStream_t s) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
@@ -399,20 +415,21 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
   }
   CUtensorMap tm;
   const cuuint64_t dims[2] = {(cuuint64_t)(V * P), (cuuint64_t)xrows};
-  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(TX)};
   const cuuint32_t box[2] = {(cuuint32_t)(V * P), 1};
   const cuuint32_t es[2] = {1, 1};
-  const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+  const CUtensorMapDataType dt = sizeof(TX) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUresult r = enc(&tm, dt, 2, const_cast<TX*>(X), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("spmm: tensor map encode failed (%d)", (int)r);
     return SVDREC_E_UNSUPPORTED;
   }
-  constexpr size_t ring = (size_t)W * S * TmaGeom<P, V>::STG * sizeof(double);
+  constexpr size_t ring = (size_t)W * S * TmaGeom<P, V, TX>::STG * sizeof(double);
   constexpr size_t kMaxSmem = 226 * 1024;  // + the static mbarriers within the 227 KB opt-in
-  if constexpr (V == 2 && ring + 32 * 2 * P * sizeof(double) > kMaxSmem) {  // wide rows: no room for a hot set
-    return tma_launch<P, S, 8, false, V>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
+  if constexpr (HOT && (sizeof(TX) != 8 || ring + 32 * 2 * P * sizeof(double) > kMaxSmem)) {  // no hot set
+    return tma_launch<P, S, 8, false, V, TX>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
                                ldx, Y, ldy, partial, 0, s);
   }
   if (W <= 8) nhot = 0;  // two CTAs per SM: no room for a hot set
@@ -422,13 +439,14 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
   const size_t smem = ring + (size_t)nhot * V * P * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S, W, HOT, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S, W, HOT, V, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kMaxSmem));
     attr = true;
   }
   const int64_t grid = (nwarp + W - 1) / W;
-  k_spmm_tma<P, S, W, HOT, V><<<(unsigned)grid, W * 32, smem, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
-                                                           seg_slot, indices, values, Y, ldy, partial, X, ldx, nhot);
+  k_spmm_tma<P, S, W, HOT, V, TX><<<(unsigned)grid, W * 32, smem, s>>>(
+      tm, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, Y, ldy, partial,
+      reinterpret_cast<const double*>(X), ldx, nhot);
   return check_launch("spmm_tma");
 }
 
@@ -497,6 +515,31 @@ int tma_dispatch4(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, 
 #undef SVDREC_TMA4
 }
 
+// fp32 X (the fp32 variant): same kernels with float rows (half the gathered
+// bytes); b % 4 == 0 so every TMA row is a multiple of 16 B.
+int tma_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
+                     const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot,
+                     const int32_t* indices, const double* values, const float* X, int64_t ldx, double* Y,
+                     int64_t ldy, double* partial, cudaStream_t s) {
+#define SVDREC_TMAF(PP)                                                                                             \
+  case PP:                                                                                                          \
+    return tma_launch<PP, 2, 8, false, 2, float>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot,     \
+                                                 indices, values, X, ldx, Y, ldy, partial, 0, s);
+  switch (b / 2) {
+    SVDREC_TMAF(2)
+    SVDREC_TMAF(4)
+    SVDREC_TMAF(6)
+    SVDREC_TMAF(8)
+    SVDREC_TMAF(10)
+    SVDREC_TMAF(12)
+    SVDREC_TMAF(14)
+    SVDREC_TMAF(16)
+    default:
+      return SVDREC_E_ARG;
+  }
+#undef SVDREC_TMAF
+}
+
 __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, const int32_t* __restrict__ s0,
                         const int32_t* __restrict__ s1, const double* __restrict__ partial, double* __restrict__ Y,
                         int64_t ldy, int b) {
@@ -557,7 +600,7 @@ int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin
     goto fixup;
   }
   if (vec2 && b > 32 && b <= 64 && b % 4 == 0 && ldx % 4 == 0 && nwarp > 0 && d_warp_seg && kind != 0 &&
-      xrows < (1ll << 31) && nwarp == (int64_t)sm_count() * svdrec_spmm_warps_per_sm(b)) {
+      xrows < (1ll << 31)) {
     rc = tma_dispatch4(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
                        d_values, d_X, ldx, d_Y, ldy, d_partial, s);
     if (rc) return rc;
@@ -612,4 +655,31 @@ extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int
   SVDREC_ARG(nhot >= 0, "spmm_hot: negative nhot");
   return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
                    ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, nhot, stream);
+}
+
+extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                               const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_indices,
+                               const double* d_values, const float* d_X, int64_t ldx, int64_t xrows, double* d_Y,
+                               int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
+                               const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
+                               const int32_t* d_warp_seg, double* d_partial, void* stream) {
+  SVDREC_ARG(b >= 4 && b <= 32 && b % 4 == 0 && ldx >= b && ldx % 4 == 0 && ldy >= b && ldy % 2 == 0 && nseg >= 0 &&
+                 nlong >= 0,
+             "spmm_x32: needs b in {4, 8, ..., 32} and 16-B aligned rows (b=%d)", b);
+  SVDREC_ARG(nwarp > 0 && d_warp_seg, "spmm_x32: needs a warp schedule");
+  SVDREC_ARG(((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
+               reinterpret_cast<uintptr_t>(d_partial)) % 16) == 0,
+             "spmm_x32: operands must be 16-B aligned");
+  if (nseg == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  int rc = tma_dispatch_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                            d_values, d_X, ldx, d_Y, ldy, d_partial, s);
+  if (rc) return rc;
+  if (nlong > 0) {
+    const int64_t tot = nlong * b;
+    k_fixup<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial,
+                                                          d_Y, ldy, b);
+    rc = check_launch("spmm_fixup");
+  }
+  return rc;
 }

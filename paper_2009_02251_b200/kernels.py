@@ -131,7 +131,7 @@ def normal_fill(key: tuple[int, int], pos: torch.Tensor, rows: int, cols: int, o
 SPMM_HOT = __import__("os").environ.get("SVDREC_SPMM_HOT", "0") == "1"
 
 
-def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
+def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> torch.Tensor:
     """Y = A @ X for the CSR described by ``plan`` (a sparse.DeviceCSR).
 
     When the CSR carries an item popularity order (the CSR of A: its columns
@@ -145,6 +145,16 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
     # algorithmic bytes: per nonzero its CSR entry (12 B) and the gathered
     # row of X (8b, L2 / shared-memory resident); per output row 8b written
     nbytes = plan.nnz * (12 + 8 * b) + plan.m * b * 8
+    if precision == "fp32" and b % 4 == 0 and b <= 32 and ldy % 2 == 0 and plan.nnz:
+        # fp32 variant: X stored as float (a rounded copy), fp64 values / accumulation / Y
+        X32 = torch.empty(X.shape[0], b, dtype=torch.float32, device=X.device)
+        X32.copy_(X)
+        with _span("spmm", plan.nnz * (12 + 4 * b) + plan.m * b * 8):
+            call("svdrec_spmm_x32", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end),
+                 ptr(plan.seg_slot), ptr(plan.indices), ptr(plan.values), ptr(X32), b, plan.n, ptr(Y), ldy, b,
+                 plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), plan.nwarp, ptr(plan.warp_seg),
+                 ptr(part), stream_handle())
+        return Y
     hot = SPMM_HOT and getattr(plan, "hot_items", None) is not None and b % 2 == 0 and b <= 32 and plan.nnz
     if hot:
         rind, rval, order = plan.ranked()
@@ -362,34 +372,46 @@ def inv_sqrt(G: torch.Tensor, status: torch.Tensor, iters: torch.Tensor | None =
 
 
 def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Yn: torch.Tensor,
-               Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float, plan):
+               Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float, plan,
+               precision: str = "fp64"):
     """Alg. 4 over user-grouped samples.  ``csr`` is a sparse.DeviceCSR (its
     ranked copy is used); ``plan`` is a cf.WorkPlan (work items, per-group
-    chunk info, completion counters, counter)."""
+    chunk info, completion counters, counter).  ``precision="fp32"`` stores
+    the gathered item rows as float (fp64 accumulation)."""
     ldn = _mat(Xn, "cf.Xn")
     if Xn.shape != Yn.shape:
         raise ValueError("cf_predict: Xn and Yn must share their shape")
+    if precision not in ("fp64", "fp32"):
+        raise ValueError(f"precision must be 'fp64' or 'fp32', not {precision!r}")
     rind, rval, order = csr.ranked()
-    n = Yn.shape[0]
-    Yr = torch.empty(n + 1, ldn, dtype=F64, device=Yn.device)  # rank order + a zero row
+    n, k = Yn.shape
+    f32 = precision == "fp32"
+    # rank order + a zero row; rows zero-padded to a 16-B multiple (vector loads)
+    ldy = (k + 3) // 4 * 4 if f32 else (k + 1) // 2 * 2
+    Yr = torch.empty(n + 1, ldy, dtype=torch.float32 if f32 else F64, device=Yn.device)
     Yr[n].zero_()
-    if ldn == Yn.shape[1]:
+    if ldy > k:
+        Yr[:, k:].zero_()
+    if not f32 and ldy == k and Yn.is_contiguous():
         torch.index_select(Yn, 0, order, out=Yr[:n])
     else:
-        Yr[:n, : Yn.shape[1]].copy_(Yn.index_select(0, order))
+        Yr[:n, :k].copy_(Yn.index_select(0, order))
     ns = users.shape[0]
     val = torch.empty(ns, dtype=F64, device=Yn.device)
     raw = torch.empty(ns, dtype=F64, device=Yn.device)
     fb = torch.empty(ns, dtype=torch.uint8, device=Yn.device)
-    k = Yn.shape[1]
     # algorithmic bytes: per streamed rating its CSR entry (12 B) and the
-    # rated item's unit row (k doubles, L2/shared-memory resident); per
+    # rated item's unit row (k values, L2/shared-memory resident); per
     # sample its ids, norm, Xn row and the three outputs
-    nbytes = getattr(plan, "rated", 0) * (12 + 8 * k) + ns * (8 * k + 4 + 4 + 8 + 17)
+    nbytes = getattr(plan, "rated", 0) * (12 + (4 if f32 else 8) * k) + ns * (8 * k + 4 + 4 + 8 + 17)
+    common = (plan.nwork, ptr(plan.start), ptr(plan.meta), ptr(items), ptr(rind), ptr(rval), k)
+    tail = (ptr(norm), float(gmean), float(lo), float(hi), n, ptr(plan.done), plan.ndone, ptr(plan.partial(k)),
+            ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
     with _span("cf_predict", nbytes):
-        call("svdrec_cf_predict", plan.nwork, ptr(plan.start), ptr(plan.meta), ptr(items), ptr(rind), ptr(rval),
-             k, ptr(Yr), ptr(Xn), ldn, ptr(norm), float(gmean), float(lo), float(hi), n, ptr(plan.done),
-             plan.ndone, ptr(plan.partial(k)), ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
+        if f32:
+            call("svdrec_cf_predict_f32", *common, ptr(Yr), ldy, ptr(Xn), ldn, *tail)
+        else:
+            call("svdrec_cf_predict", *common, ptr(Yr), ldy, ptr(Xn), ldn, *tail)
     return val, raw, fb
 
 

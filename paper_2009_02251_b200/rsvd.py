@@ -135,10 +135,15 @@ class _QbEngine:
     """Device state of one growing QB factorization."""
 
     @staticmethod
-    def create(A, b: int, stream: GaussianStream, cap: int) -> "_QbEngine":
+    def create(A, b: int, stream: GaussianStream, cap: int, precision: str = "fp64") -> "_QbEngine":
+        if precision not in ("fp64", "fp32"):
+            raise ValueError(f"precision must be 'fp64' or 'fp32', not {precision!r}")
         if isinstance(A, ShardedRatings) and A.world > 1:
-            return _ShardedQbEngine(A, b, stream, cap)
-        return _QbEngine(A.local if isinstance(A, ShardedRatings) else A, b, stream, cap)
+            E = _ShardedQbEngine(A, b, stream, cap)
+        else:
+            E = _QbEngine(A.local if isinstance(A, ShardedRatings) else A, b, stream, cap)
+        E.precision = precision
+        return E
 
     def __init__(self, A: SparseRatings, b: int, stream: GaussianStream, cap: int, global_m: int | None = None,
                  frob_sq: float | None = None):
@@ -203,11 +208,17 @@ class _QbEngine:
             Bt[:, : self.K].copy_(self.Bt[:, : self.K])
         self.Q, self.Bt = Q, Bt
 
+    precision = "fp64"  # "fp32": the SpMMs gather float copies of their dense operand
+
     # -- products through the (monkeypatchable) sparse_dense_mul -----------
     def A_mul(self, X, out):
+        if self.precision == "fp32":
+            return K.spmm(self.d.A, X, out, "fp32")
         return sparse_dense_mul(self.A, X, False, out=out)
 
     def AT_mul(self, X, out):
+        if self.precision == "fp32":
+            return K.spmm(self.d.AT, X, out, "fp32")
         return sparse_dense_mul(self.A, X, True, out=out)
 
     # -- deflations ----------------------------------------------------------
@@ -274,7 +285,10 @@ class _ShardedQbEngine(_QbEngine):
         self.comm = A.comm
 
     def AT_mul(self, X, out):
-        sparse_dense_mul(self.A, X, True, out=out)
+        if self.precision == "fp32":
+            K.spmm(self.d.AT, X, out, "fp32")
+        else:
+            sparse_dense_mul(self.A, X, True, out=out)
         return self.comm.all_reduce_(out)
 
     def minus_BtQtX(self, Y, X):
@@ -310,12 +324,12 @@ class _ShardedQbEngine(_QbEngine):
 
 
 def qb_power_blocks(A: SparseRatings, block_size: int, power: int, stream: GaussianStream,
-                    max_rank: int | None = None) -> Iterator[QbState]:
+                    max_rank: int | None = None, precision: str = "fp64") -> Iterator[QbState]:
     """Alg. 2 block generator with power iteration (rsvd.py:112-148)."""
     m, n = A.shape
     b = block_size
     cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
-    E = _QbEngine.create(A, b, stream, cap)
+    E = _QbEngine.create(A, b, stream, cap, precision)
     while (E.blocks + 1) * b <= min(m, n):
         om = E.normal(n, b, E.yn)
         y = E.A_mul(om, E.ym)
@@ -333,14 +347,14 @@ def qb_power_blocks(A: SparseRatings, block_size: int, power: int, stream: Gauss
 
 
 def qb_pass_blocks(A: SparseRatings, block_size: int, passes: int, stream: GaussianStream,
-                   max_rank: int | None = None) -> Iterator[QbState]:
+                   max_rank: int | None = None, precision: str = "fp64") -> Iterator[QbState]:
     """Alg. 3 pass-capped block generator (rsvd.py:151-199)."""
     m, n = A.shape
     b = block_size
     if passes < 2:
         raise ValueError("passes must be at least 2")
     cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
-    E = _QbEngine.create(A, b, stream, cap)
+    E = _QbEngine.create(A, b, stream, cap, precision)
     nsteps = (passes - 1) // 2
     while (E.blocks + 1) * b <= min(m, n) - b:
         if passes % 2 == 0:

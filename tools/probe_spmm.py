@@ -57,3 +57,9 @@ print("b=40 vs 2 x b=20 max rel diff", float((got - ref).abs().max() / ref.abs()
 X64 = torch.randn(A.n, 64, dtype=torch.float64, device=dev)
 o64 = torch.empty(A.m, 64, dtype=torch.float64, device=dev)
 print(f"b=64: A@X {t(lambda: K.spmm(d.A, X64, o64)):.1f} us")
+
+# fp32 variant: float copy of X (the conversion is part of the call)
+for name, plan, src, dst in (("A@X", d.A, X, out_m), ("A.T@Y", d.AT, Yu, out_n)):
+    print(f"fp32 {name} {t(lambda: K.spmm(plan, src, dst, 'fp32')):.1f} us", flush=True)
+X32 = X.float()
+Y32 = torch.empty(A.m, 20, dtype=torch.float64, device=dev)
