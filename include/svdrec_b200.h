@@ -202,6 +202,12 @@ int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_t ldg, doub
  * kernel, one grid barrier per column.
  * ------------------------------------------------------------------- */
 size_t svdrec_lu_workspace_bytes(int64_t r, int32_t b);
+/* 1 if the r x b factorization takes the panel-resident (shared-memory)
+ * path -- every CTA's rows on chip, ~0.1 ms at 138k x 20 -- else 0 (the
+ * global-memory path: one grid barrier per column over r rows, slow for
+ * tall blocks; the QB engines then use a CholeskyQR basis instead, which
+ * spans the same columns, see rsvd.py). */
+int svdrec_lu_fast_path(int64_t r, int32_t b);
 int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag,
                     void* d_work, size_t work_bytes, uint32_t* d_status, void* stream);
 

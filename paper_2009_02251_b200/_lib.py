@@ -52,6 +52,7 @@ SIGNATURES = {
     "svdrec_chol_apply_workspace_bytes": (_sz, [_i32]),
     "svdrec_chol_apply": (C.c_int, [_i64, _i32, _p, _i64, _f64, _p, _i64, _p, _i64, _p, _p, _sz, _p]),
     "svdrec_lu_workspace_bytes": (_sz, [_i64, _i32]),
+    "svdrec_lu_fast_path": (C.c_int, [_i64, _i32]),
     "svdrec_lu_lower": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _sz, _p, _p]),
     "svdrec_syev_workspace_bytes": (_sz, [_i32]),
     "svdrec_syev": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _p, _i64, _p, _sz, _p, _p]),

@@ -340,6 +340,13 @@ int try_lu_smem(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag,
 }
 }  // namespace
 
+extern "C" int svdrec_lu_fast_path(int64_t r, int32_t b) {
+  if (b < 1 || b > 128 || r < b) return 0;
+  const int nblk = 2 * sm_count();
+  const int64_t rpc = (r + nblk - 1) / nblk;
+  return (size_t)rpc * (b | 1) * 8 + (size_t)rpc * 4 + 64 <= kLuSmemMax ? 1 : 0;
+}
+
 extern "C" int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag, void* d_work,
                                size_t work_bytes, uint32_t* d_status, void* stream) {
   SVDREC_ARG(b >= 1 && r >= b && lda >= b, "lu_lower: needs rows >= cols >= 1");

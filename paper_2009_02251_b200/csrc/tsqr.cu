@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) k_buildq(int64_t rows, int64_t nc, i
 // launch, gated on a device flag: the CholeskyQR2 fallback costs a single
 // launch that returns at once when the flag is clear (it was 2 x levels
 // launches, ~20 us per orth call).
-constexpr int kMaxLevels = 12;
+constexpr int kMaxLevels = 24;  // halving tree: rows up to ~2^23 x (chunk rows) at b = 64
 struct CoopLevels {
   int nl;
   int64_t rows[kMaxLevels], nc[kMaxLevels];

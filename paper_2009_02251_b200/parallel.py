@@ -71,6 +71,13 @@ class Comm:
         self.rank = dist.get_rank(group) if on else 0
         self.backend = dist.get_backend(group) if on else None
 
+    @classmethod
+    def local(cls) -> "Comm":
+        """A one-rank communicator regardless of any process group."""
+        c = object.__new__(cls)
+        c.group, c.world, c.rank, c.backend = None, 1, 0, None
+        return c
+
     def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
             if t.is_contiguous():

@@ -25,7 +25,7 @@ from . import kernels as K
 from ._lib import STATUS_NEAR_SINGULAR, STATUS_STREAM_SHORT, STATUS_ZERO_PIVOT
 from .linalg import (EIG_FLOOR, GaussianStream, NearSingularError, RankDeficientError, SvdTriplet, _check_rank,
                      sparse_dense_mul)
-from .parallel import ShardedRatings, sharded_orth
+from .parallel import Comm, ShardedRatings, sharded_orth
 from .sparse import SparseRatings
 
 F64 = torch.float64
@@ -241,7 +241,16 @@ class _QbEngine:
             K.gemm_nn(self.Q[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
 
     def lu(self, Y):
-        K.lu_lower(Y, self.status)
+        """lu_lower_basis of a power step (rsvd.py:183-190).  Tall blocks
+        whose rows do not fit the on-chip LU get a one-pass shifted
+        CholeskyQR basis instead: both are Y times an upper-triangular
+        matrix, so the block's final Q is the same up to column signs
+        (parallel.py), and an all-zero Y still flags a zero pivot."""
+        r, b = Y.shape
+        if K.query("svdrec_lu_fast_path", r, b):
+            K.lu_lower(Y, self.status)
+        else:
+            sharded_orth(Y, Y, _LOCAL, r, passes=1, status=self.status)
 
     def orth_into(self, Y, dst):
         K.orth(Y, dst)
@@ -271,6 +280,9 @@ class _QbEngine:
     def state(self) -> QbState:
         return QbState(self.Q[:, : self.K], self.Bt[:, : self.K], None, self.blocks, self.b, self.frob,
                        None, engine=self)
+
+
+_LOCAL = Comm.local()  # one-rank communicator: every all-reduce is a no-op
 
 
 class _ShardedQbEngine(_QbEngine):

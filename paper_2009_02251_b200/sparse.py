@@ -299,11 +299,15 @@ class DeviceRatings:
     """A and A.T in HBM (both row-major CSRs) + scalar summaries."""
 
     def __init__(self, ratings: SparseRatings, device: torch.device):
+        A = DeviceCSR.upload(ratings.matrix, device)
+        self._init_from(A, device, ratings.m, ratings.n, ratings.nnz, ratings.rating_min, ratings.rating_max)
+
+    def _init_from(self, A: "DeviceCSR", device, m, n, nnz, rating_min, rating_max) -> None:
         self.device = device
-        self.m, self.n = ratings.shape
-        self.nnz = ratings.nnz
-        self.rating_min, self.rating_max = ratings.rating_min, ratings.rating_max
-        self.A = DeviceCSR.upload(ratings.matrix, device)
+        self.m, self.n = m, n
+        self.nnz = nnz
+        self.rating_min, self.rating_max = rating_min, rating_max
+        self.A = A
         self.AT = self.A.transposed()
         # item popularity order (column degree, descending) for on-chip
         # staging of the hottest items' rows in the CF scoring kernel
@@ -325,6 +329,14 @@ class DeviceRatings:
         s = stats.cpu().numpy()
         self.frob_sq = float(s[0])
         self.global_mean = float(s[1] / self.nnz) if self.nnz else float("nan")
+
+    @classmethod
+    def from_csr(cls, csr: DeviceCSR, rating_min: float, rating_max: float) -> "DeviceRatings":
+        """Wrap a CSR already in HBM (no host copy): A.T, popularity order
+        and the scalar summaries are built on the device."""
+        self = object.__new__(cls)
+        self._init_from(csr, csr.device, csr.m, csr.n, csr.nnz, rating_min, rating_max)
+        return self
 
     def check(self):
         """(any row not strictly increasing, all values finite, min, max) of
@@ -352,3 +364,37 @@ class DeviceRatings:
         v.m, v.n = self.n, self.m
         v.A, v.AT = self.AT, self.A
         return v
+
+
+class DeviceSparseRatings:
+    """A rating matrix that lives only in HBM (e.g. generated on the device).
+
+    The subset of the SparseRatings interface the QB engines and the SpMM
+    use: shape / m / n / nnz, the rating bounds and ``device()`` (the CSR of
+    A, the CSR of A.T built on the device, ||A||_F^2).  ``to_host()``
+    copies it to a SparseRatings (e.g. for an oracle check of a row range).
+    """
+
+    def __init__(self, csr: DeviceCSR, rating_min: float, rating_max: float):
+        self.rating_min, self.rating_max = float(rating_min), float(rating_max)
+        self._d = DeviceRatings.from_csr(csr, self.rating_min, self.rating_max)
+
+    shape = property(lambda self: (self._d.m, self._d.n))
+    m = property(lambda self: self._d.m)
+    n = property(lambda self: self._d.n)
+    nnz = property(lambda self: self._d.nnz)
+
+    def device(self, device=None) -> "DeviceRatings":
+        if device is not None and torch.device(device) != self._d.device:
+            raise ValueError("a DeviceSparseRatings lives on one device")
+        return self._d
+
+    def to_host(self, row0: int = 0, row1: int | None = None) -> SparseRatings:
+        """Rows [row0, row1) as a host SparseRatings."""
+        A = self._d.A
+        row1 = A.m if row1 is None else row1
+        ip = A.indptr[row0: row1 + 1].cpu().numpy()
+        a, b = int(ip[0]), int(ip[-1])
+        csr = sp.csr_matrix((A.values[a:b].cpu().numpy(), A.indices[a:b].cpu().numpy(), ip - a),
+                            shape=(row1 - row0, A.n))
+        return SparseRatings(csr, self.rating_min, self.rating_max)

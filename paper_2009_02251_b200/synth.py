@@ -51,6 +51,8 @@ CONFIGS = {
     "c1_1m": SynthConfig("c1_1m", 6040, 3706, 1_000_209, 20, 1.0, False),
     "c2_10m": SynthConfig("c2_10m", 69_878, 10_677, 10_000_054, 30, 1.1, True),
     "c3_20m": SynthConfig("c3_20m", 138_493, 26_744, 20_000_263, 40, 1.2, True),
+    # scale-out: generated on the device (generate_device), fp32-range values
+    "c4_2b": SynthConfig("c4_2b", 8_000_000, 1_000_000, 2_000_000_000, 64, 1.2, True),
 }
 
 
@@ -193,3 +195,105 @@ def split_holdout(mat: sp.csr_matrix, fractions=(0.9, 0.05, 0.05), seed: int = 0
     train = sp.coo_matrix((vals[tr], (rows[tr], cols[tr])), shape=mat.shape).tocsr()
     train.sort_indices()
     return train, (rows[va], cols[va], vals[va]), (rows[te], cols[te], vals[te])
+
+
+def generate_device(cfg: SynthConfig, device=None, scale: float = 1.0, chunk_nnz: int = 1 << 27):
+    """The same rating model drawn on the GPU (for the scale-out config,
+    whose 2e9 ratings the host generator cannot build in reasonable time).
+
+    ``scale`` shrinks the users and the rating count together (items stay:
+    the dense item-side operands keep their size, so the SpMM gathers stay
+    out of L2).  Degrees come from the host rule (_degrees); each user's
+    items are drawn ~ Zipf over a seeded permutation, with replacement and
+    re-drawn until ``deg`` distinct ones are held (heavy users by Gumbel
+    top-k), values as in :func:`generate`.  A different random stream than
+    :func:`generate` (torch's device Philox), so the matrix differs from a
+    host-generated one of the same config.  Returns a
+    :class:`sparse.DeviceSparseRatings` whose CSR never leaves the device.
+    """
+    import torch
+
+    from .sparse import DeviceCSR, DeviceSparseRatings
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    m = max(1, int(round(cfg.users * scale)))
+    nnz = max(m, int(round(cfg.nnz * scale)))
+    n = cfg.items
+    sub = SynthConfig(cfg.name, m, n, nnz, cfg.rank, cfg.zipf, cfg.half_stars, cfg.lognorm_mu, cfg.lognorm_sigma,
+                      cfg.min_per_user, cfg.noise, cfg.seed)
+    rng = np.random.default_rng(np.random.SeedSequence([cfg.seed, m, n, nnz, 4]))
+    deg_h = _degrees(sub, rng)
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(rng.integers(1 << 62)))
+    deg = torch.from_numpy(deg_h).to(dev)
+    ranks_w = torch.arange(1, n + 1, dtype=torch.float64, device=dev).pow_(-cfg.zipf)
+    cdf = torch.cumsum(ranks_w, 0)
+    cdf /= cdf[-1].clone()
+    logw = torch.log(ranks_w)
+    perm = torch.randperm(n, generator=g, device=dev)
+    indptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(deg, 0, out=indptr[1:])
+    total = int(indptr[-1].item())
+    indices = torch.empty(total, dtype=torch.int32, device=dev)
+    heavy_cut = max(64, n // 16)
+    # user chunks of ~chunk_nnz ratings
+    bounds = np.searchsorted(np.cumsum(deg_h), np.arange(chunk_nnz, total + chunk_nnz, chunk_nnz), side="right")
+    starts = np.concatenate([[0], np.minimum(bounds + 1, m)])
+    starts = np.unique(np.minimum(starts, m))
+    if starts[-1] != m:
+        starts = np.append(starts, m)
+    for u0, u1 in zip(starts[:-1], starts[1:]):
+        u0, u1 = int(u0), int(u1)
+        dchunk = deg[u0:u1]
+        heavy = torch.nonzero(dchunk > heavy_cut).flatten()
+        light_need = torch.where(dchunk > heavy_cut, torch.zeros_like(dchunk), dchunk)
+        keys = torch.empty(0, dtype=torch.int64, device=dev)
+        need = light_need.clone()
+        for _ in range(64):
+            users = torch.nonzero(need > 0).flatten()
+            if users.numel() == 0:
+                break
+            cnt = 2 * need[users] + 2
+            rows = torch.repeat_interleave(users, cnt)
+            r = torch.searchsorted(cdf, torch.rand(rows.numel(), generator=g, device=dev, dtype=torch.float64),
+                                   right=True).clamp_(max=n - 1)
+            cand = rows * n + perm[r]
+            keys = torch.unique(torch.cat([keys, cand]))  # sorted, distinct
+            have = torch.bincount(keys // n, minlength=u1 - u0)
+            need = torch.clamp(light_need - have, min=0)
+        # keep a random subset of deg distinct items for over-full users
+        ku = keys // n
+        pri = torch.rand(keys.numel(), generator=g, device=dev)
+        order = torch.argsort(ku * 2.0 + pri)  # by user, random within user (pri < 1)
+        keys, ku = keys[order], ku[order]
+        first = torch.searchsorted(ku, ku, right=False)
+        keys = keys[(torch.arange(keys.numel(), device=dev) - first) < light_need[ku]]
+        parts = [keys]
+        for h in heavy.tolist():
+            gum = logw - torch.log(-torch.log(torch.rand(n, generator=g, device=dev, dtype=torch.float64)))
+            top = torch.topk(gum, int(dchunk[h].item())).indices
+            parts.append(h * n + perm[top])
+        keys = torch.sort(torch.cat(parts)).values
+        a, b = int(indptr[u0].item()), int(indptr[u1].item())
+        if keys.numel() != b - a:
+            raise RuntimeError(f"generator: {keys.numel()} ratings for users [{u0}, {u1}), expected {b - a}")
+        indices[a:b] = (keys % n).to(torch.int32)
+        del keys
+    sd = (1.0 / np.sqrt(cfg.rank)) ** 0.5
+    U = torch.randn(m, cfg.rank, generator=g, device=dev, dtype=torch.float64).mul_(sd)
+    V = torch.randn(n, cfg.rank, generator=g, device=dev, dtype=torch.float64).mul_(sd)
+    values = torch.empty(total, dtype=torch.float64, device=dev)
+    rows_all = None
+    step = 1 << 22
+    lo, hi = cfg.bounds
+    for s0 in range(0, total, step):
+        s1 = min(total, s0 + step)
+        rows_all = torch.searchsorted(indptr, torch.arange(s0, s1, device=dev), right=True) - 1
+        cols = indices[s0:s1].to(torch.int64)
+        v = (U[rows_all] * V[cols]).sum(1)
+        v += 3.5 + cfg.noise * torch.randn(s1 - s0, generator=g, device=dev, dtype=torch.float64)
+        v = torch.round(v * 2.0) / 2.0 if cfg.half_stars else torch.round(v)
+        values[s0:s1] = v.clamp_(lo, hi)
+    del U, V, rows_all
+    csr = DeviceCSR(indptr, indices, values, (m, n))
+    return DeviceSparseRatings(csr, lo, hi)
