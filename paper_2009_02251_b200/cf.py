@@ -23,6 +23,7 @@ import numpy as np
 import torch
 
 from . import kernels as K
+from .hostio import to_device
 from ._lib import STATUS_NEAR_SINGULAR, STATUS_NS_CHECK
 from .linalg import EIG_FLOOR, GaussianStream, NearSingularError
 from .parallel import ShardedRatings, local_samples
@@ -239,9 +240,9 @@ class _Samples:
         self.n = int(u.size)
         self.users_np, self.items_np, self.truth_np = u, i, r
         # grouped by user on the device: stable sort of the raw arrays
-        ud = torch.from_numpy(u).to(device)
-        idev = torch.from_numpy(i).to(device)
-        rd = torch.from_numpy(r).to(device)
+        ud = to_device(u, np.int64, device)
+        idev = to_device(i, np.int64, device)
+        rd = to_device(r, np.float64, device)
         self.h2d_bytes = self.n * 24
         order = torch.sort(ud, stable=True).indices if self.n else torch.zeros(0, dtype=torch.int64, device=device)
         us = ud[order]

@@ -241,7 +241,9 @@ class DeviceCSR:
 
     @classmethod
     def upload(cls, csr: sp.csr_matrix, device: torch.device) -> "DeviceCSR":
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).astype(dt, copy=False)).to(device)  # noqa: E731
+        from .hostio import to_device
+
+        t = lambda a, dt: to_device(a, dt, device)  # noqa: E731
         return cls(t(csr.indptr, np.int64), t(csr.indices, np.int32), t(csr.data, np.float64), csr.shape,
                    h2d_bytes=(csr.shape[0] + 1) * 8 + csr.nnz * 12)
 
