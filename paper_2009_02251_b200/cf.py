@@ -77,6 +77,7 @@ def _eig_T(Bt: torch.Tensor, G: torch.Tensor | None = None, status: torch.Tensor
 
 
 _DEBUG_NS = bool(os.environ.get("SVDREC_DEBUG_NS"))
+_HOST_TRACE: list | None = None  # (rank, submit s, next block s, collect s) per block when a list
 
 
 class LatentFactors:
@@ -609,11 +610,17 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
     pipeline = PIPELINE or SPECULATE
     state = next(gen, None)
     while state is not None:
+        t0 = time.perf_counter() if _HOST_TRACE is not None else 0.0
         pending = criterion.submit(state)
         capped = max_rank is not None and state.rank >= max_rank
         if pipeline:
+            t1 = time.perf_counter() if _HOST_TRACE is not None else 0.0
             nxt = None if capped else next(gen, None)
-            if criterion.collect(pending) or capped:
+            t2 = time.perf_counter() if _HOST_TRACE is not None else 0.0
+            stop = criterion.collect(pending) or capped
+            if _HOST_TRACE is not None:
+                _HOST_TRACE.append((state.rank, t1 - t0, t2 - t1, time.perf_counter() - t2))
+            if stop:
                 break
         else:
             if criterion.collect(pending) or capped:
