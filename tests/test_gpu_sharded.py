@@ -101,10 +101,10 @@ def _worker(rank, world, port, outdir, case, arg):
         dist.destroy_process_group()
 
 
-def _run(tmp_path, case, arg=None):
+def _run(tmp_path, case, arg=None, world=WORLD):
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(WORLD, _free_port(), str(tmp_path), case, arg), nprocs=WORLD, join=True)
-    return [dict(np.load(tmp_path / f"r{r}.npz")) for r in range(WORLD)]
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), case, arg), nprocs=world, join=True)
+    return [dict(np.load(tmp_path / f"r{r}.npz")) for r in range(world)]
 
 
 def _same_up_to_sign(a, b, axis, tol):
@@ -133,13 +133,15 @@ def test_sharded_engine_matches_single_gpu(gpu, tmp_path, case, arg):
         assert np.array_equal(r0[f"B2_{blk}"], r1[f"B2_{blk}"])
 
 
-def test_sharded_cf_pipeline_matches_single_gpu(gpu, tmp_path):
-    res = _run(tmp_path, "cf")
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cf_pipeline_matches_single_gpu(gpu, tmp_path, world):
+    res = _run(tmp_path, "cf", world=world)
     for r in res:
         assert int(r["k2"]) == int(r["k1"])
         np.testing.assert_allclose(r["mae2"], r["mae1"], rtol=1e-9)
         np.testing.assert_allclose(r["test2"], r["test1"], rtol=1e-9)
         # item factors equal up to sign per latent column (B rows up to sign)
         _same_up_to_sign(r["Xn1"], r["Xn2"], axis=0, tol=1e-9)
-    assert np.array_equal(res[0]["Yn2"], res[1]["Yn2"])
-    assert np.array_equal(res[0]["mae2"], res[1]["mae2"])
+    for r in res[1:]:
+        assert np.array_equal(res[0]["Yn2"], r["Yn2"])
+        assert np.array_equal(res[0]["mae2"], r["mae2"])
