@@ -186,6 +186,10 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
     const int64_t deg = m0.y;
     const int64_t s0 = m0.z, s1 = m0.w;
     const int nch = m1.x;
+    // the first 32 samples' item ids, loaded now and used after the rating
+    // loop (one dependent load less at the end of the item)
+    int32_t jl_first = 0;
+    if (lane < s1 - s0) jl_first = __ldg(items + s0 + lane);
     double P[NA], S[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) P[t] = S[t] = 0.0;
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
       int32_t jl = 0;
       double nl = 0.0;
       if (lane < ns) {
-        jl = items[sb + lane];
+        jl = sb == s0 ? jl_first : items[sb + lane];
         nl = norm[jl];
       }
       for (int q = 0; q < ns; q += 2) {

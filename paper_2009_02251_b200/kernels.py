@@ -8,6 +8,8 @@ copies.  Nothing here synchronises the device.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -128,7 +130,7 @@ def normal_fill(key: tuple[int, int], pos: torch.Tensor, rows: int, cols: int, o
 # SpMM with a shared-memory hot set (A @ X on the popularity-ranked CSR);
 # off by default: measured slower on the c3 bench (17.8 vs 16.9 ms per step),
 # SVDREC_SPMM_HOT=1 turns it on (A/B measurements)
-SPMM_HOT = __import__("os").environ.get("SVDREC_SPMM_HOT", "0") == "1"
+SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "0") == "1"
 
 
 def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> torch.Tensor:
