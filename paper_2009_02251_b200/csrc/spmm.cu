@@ -205,7 +205,7 @@ struct Acc {
 };
 
 template <int P, int S, int W, bool HOT, int V, typename TX = double>
-__global__ void __launch_bounds__(W * 32, (W <= 8 && V == 2 ? 2 : 1)) k_spmm_tma(
+__global__ void __launch_bounds__(W * 32, (!HOT && V == 2 ? 2 : 1)) k_spmm_tma(
     const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_seg,
     const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
     const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ indices, const double* __restrict__ values,
@@ -432,7 +432,7 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
     return tma_launch<P, S, 8, false, V, TX>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
                                ldx, Y, ldy, partial, 0, s);
   }
-  if (W <= 8) nhot = 0;  // two CTAs per SM: no room for a hot set
+  if (!HOT) nhot = 0;  // two CTAs per SM: no room for a hot set
   const int64_t fit = (int64_t)((kMaxSmem - ring) / (V * P * sizeof(double)));
   if (nhot > fit) nhot = (int)fit;
   if (nhot > xrows) nhot = (int)xrows;
@@ -457,7 +457,7 @@ int tma_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, c
                  int nhot, cudaStream_t s) {
 #define SVDREC_TMA(PP)                                                                                              \
   case PP:                                                                                                          \
-    return tma_launch<PP, S, W, (W > 8)>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,  \
+    return tma_launch<PP, S, W, (W == 16)>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,  \
                                 ldx, Y, ldy, partial, nhot, s);
   switch (b / 2) {
     SVDREC_TMA(1)
@@ -515,6 +515,13 @@ int tma_dispatch4(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, 
 #undef SVDREC_TMA4
 }
 
+#ifndef SVDREC_SPMM_W2
+#define SVDREC_SPMM_W2 8
+#endif
+// warps per CTA of the 2-CTA-per-SM variant (rings: 2 stages x ~5.6 KB per
+// warp at b = 20)
+constexpr int kW2 = SVDREC_SPMM_W2;
+
 // fp32 X (the fp32 variant): same kernels with float rows (half the gathered
 // bytes); b % 4 == 0 so every TMA row is a multiple of 16 B.
 int tma_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
@@ -558,7 +565,7 @@ __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, con
 using namespace svdrec;
 
 extern "C" int svdrec_spmm_warps_per_sm(int32_t b) {
-  if (b >= 1 && b <= 32 && b % 2 == 0) return 16;  // two CTAs of 8 warps
+  if (b >= 1 && b <= 32 && b % 2 == 0) return 2 * kW2;  // two CTAs of kW2 warps
   if (b > 32 && b <= 64 && b % 4 == 0) {
     switch (b / 4) {
       case 9: return w4_warps(9);
@@ -594,7 +601,7 @@ int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin
   if (vec2 && b <= 32 && nwarp > 0 && d_warp_seg && kind != 0 && xrows < (1ll << 31)) {
     rc = nhot > 0 ? tma_dispatch<2, 16>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
                                         d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, nhot, s)
-                  : tma_dispatch<2, 8>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
+                  : tma_dispatch<2, kW2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
                                        d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, 0, s);
     if (rc) return rc;
     goto fixup;
