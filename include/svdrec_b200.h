@@ -103,8 +103,9 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
  * fall back to the plain kernel. */
 int svdrec_spmm_warps_per_sm(int32_t b);
 /* fp32 variant: X stored as float (half the gathered bytes), values,
- * accumulation and Y in double.  b in {4, 8, ..., 32}, 16-B aligned rows,
- * the 16-warps-per-SM schedule. */
+ * accumulation and Y in double.  b in {4, 8, ..., 64}, 16-B aligned rows,
+ * a schedule of svdrec_spmm_x32_warps_per_sm(b) warps per SM. */
+int svdrec_spmm_x32_warps_per_sm(int32_t b);
 int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
                     const int64_t* d_seg_end, const int32_t* d_seg_slot,
                     const int32_t* d_indices, const double* d_values,
@@ -189,7 +190,7 @@ int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_
 size_t svdrec_gram_workspace_bytes(int64_t r, int32_t b);
 int svdrec_gram(int64_t r, int32_t b, const double* d_Y, int64_t ldy, double* d_G, void* d_work,
                 size_t work_bytes, void* stream);
-size_t svdrec_chol_apply_workspace_bytes(int32_t b);
+size_t svdrec_chol_apply_workspace_bytes(int64_t r, int32_t b);
 int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_t ldg, double shift_rel,
                       const double* d_Y, int64_t ldy, double* d_Q, int64_t ldq, uint32_t* d_status,
                       void* d_work, size_t work_bytes, void* stream);

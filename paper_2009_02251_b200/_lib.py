@@ -34,6 +34,7 @@ SIGNATURES = {
     "svdrec_normal_fill": (C.c_int, [_u64, _u64, _p, _i64, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_warps_per_sm": (C.c_int, [_i32]),
+    "svdrec_spmm_x32_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_x32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_hot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _i32, _p]),
     "svdrec_gemm_tn_workspace_bytes": (_sz, [_i64, _i64, _i64]),
@@ -49,7 +50,7 @@ SIGNATURES = {
     "svdrec_orth": (C.c_int, [_i64, _i32, _p, _i64, _p, _i64, _p, _sz, _p]),
     "svdrec_gram_workspace_bytes": (_sz, [_i64, _i32]),
     "svdrec_gram": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _sz, _p]),
-    "svdrec_chol_apply_workspace_bytes": (_sz, [_i32]),
+    "svdrec_chol_apply_workspace_bytes": (_sz, [_i64, _i32]),
     "svdrec_chol_apply": (C.c_int, [_i64, _i32, _p, _i64, _f64, _p, _i64, _p, _i64, _p, _p, _sz, _p]),
     "svdrec_lu_workspace_bytes": (_sz, [_i64, _i32]),
     "svdrec_lu_fast_path": (C.c_int, [_i64, _i32]),

@@ -547,6 +547,38 @@ int tma_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_se
 #undef SVDREC_TMAF
 }
 
+// fp32 X, 32 < b <= 64 (b % 4 == 0): four floats per lane; the rings are
+// half as wide as the double ones, so twice the warps fit (<= 12 per SM).
+constexpr int w4f_warps(int P) {
+  return (226 * 1024) / (2 * (8 * ((4 * 4 * P * 4 + 127) / 128 * 128) + 512)) < 12
+             ? (226 * 1024) / (2 * (8 * ((4 * 4 * P * 4 + 127) / 128 * 128) + 512))
+             : 12;
+}
+
+int tma_dispatch4_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
+                      const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot,
+                      const int32_t* indices, const double* values, const float* X, int64_t ldx, double* Y,
+                      int64_t ldy, double* partial, cudaStream_t s) {
+#define SVDREC_TMA4F(PP)                                                                                         \
+  case PP:                                                                                                       \
+    return tma_launch<PP, 2, w4f_warps(PP), false, 4, float>(xrows, nwarp, warp_seg, seg_row, seg_begin,         \
+                                                              seg_end, seg_slot, indices, values, X, ldx, Y, ldy, \
+                                                              partial, 0, s);
+  switch (b / 4) {
+    SVDREC_TMA4F(9)
+    SVDREC_TMA4F(10)
+    SVDREC_TMA4F(11)
+    SVDREC_TMA4F(12)
+    SVDREC_TMA4F(13)
+    SVDREC_TMA4F(14)
+    SVDREC_TMA4F(15)
+    SVDREC_TMA4F(16)
+    default:
+      return SVDREC_E_ARG;
+  }
+#undef SVDREC_TMA4F
+}
+
 __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, const int32_t* __restrict__ s0,
                         const int32_t* __restrict__ s1, const double* __restrict__ partial, double* __restrict__ Y,
                         int64_t ldy, int b) {
@@ -670,17 +702,19 @@ extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int
                                int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
                                const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
                                const int32_t* d_warp_seg, double* d_partial, void* stream) {
-  SVDREC_ARG(b >= 4 && b <= 32 && b % 4 == 0 && ldx >= b && ldx % 4 == 0 && ldy >= b && ldy % 2 == 0 && nseg >= 0 &&
-                 nlong >= 0,
-             "spmm_x32: needs b in {4, 8, ..., 32} and 16-B aligned rows (b=%d)", b);
+  SVDREC_ARG(b >= 4 && b <= 64 && b % 4 == 0 && ldx >= b && ldx % 4 == 0 && ldy >= b && ldy % 2 == 0 && nseg >= 0 &&
+                 nlong >= 0 && (b <= 32 || ldy % 4 == 0),
+             "spmm_x32: needs b in {4, 8, ..., 64} and 16-B aligned rows (b=%d)", b);
   SVDREC_ARG(nwarp > 0 && d_warp_seg, "spmm_x32: needs a warp schedule");
   SVDREC_ARG(((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
                reinterpret_cast<uintptr_t>(d_partial)) % 16) == 0,
              "spmm_x32: operands must be 16-B aligned");
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
-  int rc = tma_dispatch_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
-                            d_values, d_X, ldx, d_Y, ldy, d_partial, s);
+  int rc = b <= 32 ? tma_dispatch_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
+                                     d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, s)
+                   : tma_dispatch4_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
+                                       d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, s);
   if (rc) return rc;
   if (nlong > 0) {
     const int64_t tot = nlong * b;
@@ -689,4 +723,20 @@ extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int
     rc = check_launch("spmm_fixup");
   }
   return rc;
+}
+
+extern "C" int svdrec_spmm_x32_warps_per_sm(int32_t b) {
+  if (b > 32 && b <= 64 && b % 4 == 0) {
+    switch (b / 4) {
+      case 9: return w4f_warps(9);
+      case 10: return w4f_warps(10);
+      case 11: return w4f_warps(11);
+      case 12: return w4f_warps(12);
+      case 13: return w4f_warps(13);
+      case 14: return w4f_warps(14);
+      case 15: return w4f_warps(15);
+      default: return w4f_warps(16);
+    }
+  }
+  return 16;  // two CTAs of 8 warps
 }

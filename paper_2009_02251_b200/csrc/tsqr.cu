@@ -24,6 +24,13 @@
 
 namespace cg = cooperative_groups;
 
+extern "C" size_t svdrec_gemm_tn_workspace_bytes(int64_t r, int64_t p, int64_t q);
+extern "C" int svdrec_gemm_tn(int64_t r, int64_t p, int64_t q, double alpha, const double* d_X, int64_t ldx,
+                              const double* d_Y, int64_t ldy, double beta, double* d_C, int64_t ldc, void* d_work,
+                              size_t work_bytes, void* stream);
+extern "C" int svdrec_gemm_nn(int64_t r, int64_t p, int64_t q, double alpha, const double* d_X, int64_t ldx,
+                              const double* d_C, int64_t ldc, double beta, double* d_Y, int64_t ldy, void* stream);
+
 namespace svdrec {
 namespace {
 
@@ -361,67 +368,6 @@ int run_tsqr_gated(const Plan& p, int64_t r, int32_t b, const double* d_A, int64
 // ---- CholeskyQR2 fast path -------------------------------------------------
 // G = Y.T Y over a row range per CTA (upper triangle pairs), fixed-order sum.
 constexpr int kGramRows = 64;
-constexpr int kApplyRows = 128;
-
-// G = Y.T Y partial per CTA row slab.  Rows are staged 64 at a time in
-// shared memory; each thread owns up to 12 (i <= j) pairs whose indices are
-// computed once, then accumulates over the slab.
-__global__ void __launch_bounds__(256) k_gram_part(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
-                                                   int64_t rows_per, double* __restrict__ part) {
-  __shared__ double ys[kGramRows][65];
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min64(r, r0 + rows_per);
-  const int npairs = b * (b + 1) / 2;
-  int pi[12], pj[12];
-  double acc[12];
-#pragma unroll
-  for (int q = 0; q < 12; ++q) {
-    const int pidx = threadIdx.x + q * 256;
-    acc[q] = 0.0;
-    pi[q] = -1;
-    pj[q] = 0;
-    if (pidx < npairs) {
-      int i = 0, off = 0;
-      while (off + (b - i) <= pidx) {
-        off += b - i;
-        ++i;
-      }
-      pi[q] = i;
-      pj[q] = i + (pidx - off);
-    }
-  }
-  for (int64_t base = r0; base < r1; base += kGramRows) {
-    for (int t = threadIdx.x; t < kGramRows * b; t += blockDim.x) {
-      const int rr = t / b, c = t - rr * b;
-      const int64_t gr = base + rr;
-      ys[rr][c] = gr < r1 ? Y[gr * ldy + c] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 12; ++q) {
-      if (pi[q] >= 0) {
-        const int i = pi[q], j = pj[q];
-        double a = acc[q];
-#pragma unroll 8
-        for (int rr = 0; rr < kGramRows; ++rr) a = fma(ys[rr][i], ys[rr][j], a);
-        acc[q] = a;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < 12; ++q) {
-    const int pidx = threadIdx.x + q * 256;
-    if (pidx < npairs) part[(int64_t)blockIdx.x * npairs + pidx] = acc[q];
-  }
-}
-
-// Fixed-order sum of the per-CTA Gram partials, one warp per pair.
-__global__ void k_pairs_reduce(int npairs, int nparts, const double* __restrict__ part, double* __restrict__ out) {
-  const int t = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= npairs) return;
-  const double s = warp_strided_sum(part + t, nparts, npairs);
-  if ((threadIdx.x & 31) == 0) out[t] = s;
-}
 
 // Cholesky G = R.T R (upper R) of the reduced Gram pairs, then R^-1.
 // flag |= 1 when a pivot is non-positive or (min R_jj / max R_jj)^2 < 1e-12
@@ -474,24 +420,6 @@ __device__ void chol_inv_smem(int b, double (*G)[65], double* dinv, int* bad, do
     const int i = t / b, cc = t - i * b;
     Rinv[t] = i == cc ? dinv[cc] : (i < cc ? G[cc][i] : 0.0);
   }
-}
-
-__global__ void __launch_bounds__(256) k_chol_inv(int b, const double* __restrict__ pairs, double* __restrict__ Rinv,
-                                                  uint32_t* __restrict__ flag) {
-  __shared__ double G[64][65];
-  __shared__ double dinv[64];
-  __shared__ int bad;
-  const int npairs = b * (b + 1) / 2;
-  for (int pidx = threadIdx.x; pidx < npairs; pidx += blockDim.x) {
-    int i = 0, off = 0;
-    while (off + (b - i) <= pidx) {
-      off += b - i;
-      ++i;
-    }
-    const int j = i + (pidx - off);
-    G[i][j] = pairs[pidx];
-  }
-  chol_inv_smem(b, G, dinv, &bad, Rinv, flag);
 }
 
 // ---------------------------------------------------------------------------
@@ -753,44 +681,9 @@ __global__ void __launch_bounds__(256) k_cqr_apply(int64_t r, int b, const doubl
   }
 }
 
-// out = Y @ Rinv (upper triangular), one thread per row over a 128-row
-// tile staged (and written back) through shared memory for coalescing;
-// with ``only_if_clear`` nothing is stored when the flag is set (the TSQR
-// fallback owns the output then).
-__global__ void __launch_bounds__(kApplyRows) k_trapply(int64_t r, int b, const double* __restrict__ Y, int64_t ldy,
-                                                        const double* __restrict__ Rinv, double* __restrict__ out,
-                                                        int64_t ldo, const uint32_t* __restrict__ flag,
-                                                        int only_if_clear) {
-  extern __shared__ double sm[];
-  if (only_if_clear && *flag) return;
-  const int ldp = b | 1;
-  double* Ys = sm;
-  double* Rs = sm + kApplyRows * ldp;
-  for (int t = threadIdx.x; t < b * b; t += blockDim.x) Rs[t] = Rinv[t];
-  const int64_t r0 = (int64_t)blockIdx.x * kApplyRows;
-  const int nr = (int)min64(kApplyRows, r - r0);
-  for (int t = threadIdx.x; t < nr * b; t += blockDim.x) {
-    const int rr = t / b, c = t - rr * b;
-    Ys[rr * ldp + c] = Y[(r0 + rr) * ldy + c];
-  }
-  __syncthreads();
-  if (threadIdx.x < nr) {
-    double* yr = Ys + threadIdx.x * ldp;
-    for (int j = b - 1; j >= 0; --j) {  // descending: in-place overwrite is safe
-      double a = 0.0;
-      for (int q = 0; q <= j; ++q) a = fma(yr[q], Rs[q * b + j], a);
-      yr[j] = a;
-    }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < nr * b; t += blockDim.x) {
-    const int rr = t / b, c = t - rr * b;
-    out[(r0 + rr) * ldo + c] = Ys[rr * ldp + c];
-  }
-}
-
 struct OrthLayout {
-  size_t off_flag, off_rinv, off_red, off_part, off_tmp, off_tsqr, off_cqr, off_tickets, total;
+  size_t off_flag, off_rinv, off_red, off_part, off_tmp, off_tsqr, off_cqr, off_tickets, off_g, off_gemm, off_tmp2,
+      gemm_bytes, total;
   int nparts;
   int64_t rows_per;
 };
@@ -821,6 +714,15 @@ OrthLayout orth_layout(int64_t r, int b) {
   o = align_up(o + make_plan(r, b).total);
   L.off_cqr = o;  // DMMA path: CTA partials + group partials (BP x BP each, BP <= 32) + tickets
   o = align_up(o + (size_t)(cqr_ctas(r) + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 32 * 32 * 8);
+  if (b > 32) {  // wide blocks: Gram / apply on the DMMA GEMMs, second pass into tmp2
+    L.off_g = o;
+    o = align_up(o + (size_t)b * b * 8);
+    L.gemm_bytes = svdrec_gemm_tn_workspace_bytes(r, b, b);
+    L.off_gemm = o;
+    o = align_up(o + L.gemm_bytes);
+    L.off_tmp2 = o;
+    o = align_up(o + (size_t)r * b * 8);
+  }
   L.total = o;
   return L;
 }
@@ -853,41 +755,12 @@ int cqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_
   }
 }
 
-int cholqr_pass(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_t ldo, const OrthLayout& L,
-                char* w, int only_if_clear, cudaStream_t s) {
-  double* part = reinterpret_cast<double*>(w + L.off_part);
-  double* rinv = reinterpret_cast<double*>(w + L.off_rinv);
-  uint32_t* flag = reinterpret_cast<uint32_t*>(w + L.off_flag);
-  k_gram_part<<<(unsigned)L.nparts, 256, 0, s>>>(r, b, Y, ldy, L.rows_per, part);
-  double* red = reinterpret_cast<double*>(w + L.off_red);
-  const int npairs = b * (b + 1) / 2;
-  k_pairs_reduce<<<(unsigned)((npairs * 32 + 255) / 256), 256, 0, s>>>(npairs, L.nparts, part, red);
-  k_chol_inv<<<1, 256, 0, s>>>(b, red, rinv, flag);
-  const size_t smem = ((size_t)kApplyRows * (b | 1) + (size_t)b * b) * 8;
-  static bool attr = false;
-  if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_trapply, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    attr = true;
-  }
-  k_trapply<<<(unsigned)((r + kApplyRows - 1) / kApplyRows), kApplyRows, smem, s>>>(r, b, Y, ldy, rinv, out, ldo,
-                                                                                     flag, only_if_clear);
-  return check_launch("cholqr_pass", 4);
-}
 
 
 // ---- Row-sharded CholeskyQR building blocks --------------------------------
 // A rank holding rows [r0, r1) of a tall block Y computes its Gram partial
 // (svdrec_gram), the caller all-reduces the b x b partials, and every rank
 // factors the same G and applies R^-1 to its own rows (svdrec_chol_apply).
-
-// pairs (upper triangle, packed) -> full symmetric b x b
-__global__ void k_pairs_full(int b, const double* __restrict__ pairs, double* __restrict__ G) {
-  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
-    int i = t / b, j = t - i * b;
-    if (i > j) { const int x = i; i = j; j = x; }
-    G[t] = pairs[i * b - i * (i - 1) / 2 + (j - i)];
-  }
-}
 
 // R = chol(G + shift_rel * trace(G) * I) (upper), Rinv = R^-1; one CTA.
 // flag |= 1 as in the CholeskyQR2 path (kappa > 1e6 or a bad pivot);
@@ -918,6 +791,32 @@ __global__ void __launch_bounds__(kCqrThreads) k_chol_full(int b, const double* 
     chol_inv_smem(b, Gs, dinv, &bad, Rinv, flag, zero_flag);
 }
 
+// One CholeskyQR pass for 32 < b <= 64 on the DMMA GEMMs (TMA-staged
+// tall-skinny kernels of skinny.cu): G = Y.T Y, R = chol(G + shift tr(G) I),
+// out = Y R^-1.  out must not alias Y.
+int cholqr_pass_wide(int64_t r, int b, const double* Y, int64_t ldy, double* out, int64_t ldo, double* G,
+                     void* gw, size_t gwb, double* rinv, uint32_t* flag, uint32_t* zero_flag, double shift_rel,
+                     cudaStream_t s) {
+  int rc = svdrec_gemm_tn(r, b, b, 1.0, Y, ldy, Y, ldy, 0.0, G, b, gw, gwb, s);
+  if (rc) return rc;
+  k_chol_full<<<1, kCqrThreads, 0, s>>>(b, G, b, shift_rel, rinv, flag, zero_flag);
+  rc = check_launch("cholqr_wide");
+  if (rc) return rc;
+  return svdrec_gemm_nn(r, b, b, 1.0, Y, ldy, rinv, b, 0.0, out, ldo, s);
+}
+
+// dst = src (r x b) unless the flag is set (the TSQR fallback owns dst then)
+__global__ void k_gated_copy(int64_t r, int b, const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                             int64_t ldd, const uint32_t* __restrict__ flag) {
+  if (*flag) return;
+  const int64_t n = r * b;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / b;
+    const int j = (int)(t - i * b);
+    dst[i * ldd + j] = src[i * lds + j];
+  }
+}
+
 struct GramLayout {
   size_t off_tickets, off_part, off_pairs, total;
   int nparts;
@@ -937,8 +836,8 @@ GramLayout gram_layout(int64_t r, int b) {
   }
   L.off_part = o;
   const size_t dmma = (size_t)(cqr_ctas(r) + (cqr_ctas(r) + kCqrGroup - 1) / kCqrGroup) * 32 * 32 * 8;
-  const size_t pairs = (size_t)L.nparts * (b * (b + 1) / 2) * 8;
-  o = align_up(o + (b <= 32 ? dmma : pairs));
+  const size_t gemm = svdrec_gemm_tn_workspace_bytes(r, b, b);  // b > 32: the DMMA GEMM
+  o = align_up(o + (b <= 32 ? dmma : gemm));
   L.off_pairs = o;
   o = align_up(o + (size_t)b * (b + 1) / 2 * 8);
   L.total = o;
@@ -952,18 +851,6 @@ void gram_nt(int64_t r, int b, const double* Y, int64_t ldy, double* G, const Gr
   double* gpart = part + nc * (8 * NT) * (8 * NT);
   unsigned* tickets = reinterpret_cast<unsigned*>(w + L.off_tickets);
   k_cqr_gram<NT><<<(unsigned)nc, kCqrThreads, 0, s>>>(r, b, Y, ldy, part, gpart, tickets, nullptr, nullptr, G);
-}
-
-void trapply_launch(int64_t r, int b, const double* Y, int64_t ldy, const double* rinv, double* out, int64_t ldo,
-                    const uint32_t* flag, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_trapply, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    attr = true;
-  }
-  const size_t smem = ((size_t)kApplyRows * (b | 1) + (size_t)b * b) * 8;
-  k_trapply<<<(unsigned)((r + kApplyRows - 1) / kApplyRows), kApplyRows, smem, s>>>(r, b, Y, ldy, rinv, out, ldo,
-                                                                                   flag, 0);
 }
 
 template <int NT>
@@ -1022,10 +909,19 @@ extern "C" int svdrec_orth(int64_t r, int32_t b, const double* d_A, int64_t lda,
     rc = cqr_pass(r, b, d_A, lda, tmp, b, L, w, 0, s);  // Q1 = A R1^-1
     if (rc) return rc;
     rc = cqr_pass(r, b, tmp, b, d_Q, ldq, L, w, 1, s);  // Q = Q1 R2^-1 (if both passes are sound)
-  } else {
-    rc = cholqr_pass(r, b, d_A, lda, tmp, b, L, w, 0, s);
+  } else {  // 32 < b <= 64: DMMA GEMM passes; pass 2 into tmp2, copied to Q unless flagged
+    double* G = reinterpret_cast<double*>(w + L.off_g);
+    double* rinv = reinterpret_cast<double*>(w + L.off_rinv);
+    double* tmp2 = reinterpret_cast<double*>(w + L.off_tmp2);
+    rc = cholqr_pass_wide(r, b, d_A, lda, tmp, b, G, w + L.off_gemm, L.gemm_bytes, rinv, flag, nullptr, 0.0, s);
     if (rc) return rc;
-    rc = cholqr_pass(r, b, tmp, b, d_Q, ldq, L, w, 1, s);
+    rc = cholqr_pass_wide(r, b, tmp, b, tmp2, b, G, w + L.off_gemm, L.gemm_bytes, rinv, flag, nullptr, 0.0, s);
+    if (rc) return rc;
+    const int64_t n = r * b;
+    int64_t grid = (n + 255) / 256;
+    if (grid > (int64_t)sm_count() * 16) grid = (int64_t)sm_count() * 16;
+    k_gated_copy<<<(unsigned)grid, 256, 0, s>>>(r, b, tmp2, b, d_Q, ldq, flag);
+    rc = check_launch("orth_copy");
   }
   if (rc) return rc;
   // fallback: Householder TSQR from the untouched input, only if flagged
@@ -1064,18 +960,15 @@ extern "C" int svdrec_gram(int64_t r, int32_t b, const double* d_Y, int64_t ldy,
     }
     return check_launch("gram", 1);
   }
-  double* part = reinterpret_cast<double*>(w + L.off_part);
-  double* pairs = reinterpret_cast<double*>(w + L.off_pairs);
-  const int npairs = b * (b + 1) / 2;
-  k_gram_part<<<(unsigned)L.nparts, 256, 0, s>>>(r, b, d_Y, ldy, L.rows_per, part);
-  k_pairs_reduce<<<(unsigned)((npairs * 32 + 255) / 256), 256, 0, s>>>(npairs, L.nparts, part, pairs);
-  k_pairs_full<<<1, 256, 0, s>>>(b, pairs, d_G);
-  return check_launch("gram", 3);
+  return svdrec_gemm_tn(r, b, b, 1.0, d_Y, ldy, d_Y, ldy, 0.0, d_G, b, w + L.off_part,
+                        L.off_pairs - L.off_part, s);
 }
 
-extern "C" size_t svdrec_chol_apply_workspace_bytes(int32_t b) {
-  if (b < 1 || b > 64) return 256;
-  return svdrec::align_up(16) + svdrec::align_up((size_t)b * b * 8) + 256;
+extern "C" size_t svdrec_chol_apply_workspace_bytes(int64_t r, int32_t b) {
+  if (b < 1 || b > 64 || r < 0) return 256;
+  // b > 32: the apply is a DMMA GEMM, through a temporary when Q aliases Y
+  return svdrec::align_up(16) + svdrec::align_up((size_t)b * b * 8) +
+         (b > 32 ? svdrec::align_up((size_t)r * b * 8) : 0) + 256;
 }
 
 extern "C" int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_t ldg, double shift_rel,
@@ -1085,7 +978,7 @@ extern "C" int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_
   SVDREC_ARG(b >= 1 && b <= 64, "chol_apply: block width %d outside [1, 64]", b);
   SVDREC_ARG(r >= 0 && ldg >= b && (r == 0 || (ldy >= b && ldq >= b)), "chol_apply: bad shape or leading dimension");
   SVDREC_ARG(shift_rel >= 0.0, "chol_apply: negative shift");
-  const size_t need = align_up(16) + align_up((size_t)b * b * 8);
+  const size_t need = align_up(16) + align_up((size_t)b * b * 8) + (b > 32 ? align_up((size_t)r * b * 8) : 0);
   if (work_bytes < need) {
     set_error("chol_apply: workspace %zu < %zu", work_bytes, need);
     return SVDREC_E_WORKSPACE;
@@ -1102,7 +995,15 @@ extern "C" int svdrec_chol_apply(int64_t r, int32_t b, const double* d_G, int64_
     case 2: cqr_apply_launch<2>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
     case 3: cqr_apply_launch<3>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
     case 4: cqr_apply_launch<4>(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
-    default: trapply_launch(r, b, d_Y, ldy, rinv, d_Q, ldq, flag, s); break;
+    default: {
+      const bool alias = d_Q == d_Y;
+      double* dst = alias ? reinterpret_cast<double*>(w + align_up(16) + align_up((size_t)b * b * 8)) : d_Q;
+      const int64_t ldd = alias ? b : ldq;
+      int rc = svdrec_gemm_nn(r, b, b, 1.0, d_Y, ldy, rinv, b, 0.0, dst, ldd, s);
+      if (rc) return rc;
+      if (alias) SVDREC_CUDA(cudaMemcpy2DAsync(d_Q, ldq * 8, dst, ldd * 8, (size_t)b * 8, r, cudaMemcpyDeviceToDevice, s));
+      return check_launch("chol_apply", 1);
+    }
   }
   return check_launch("chol_apply", 2);
 }

@@ -147,15 +147,17 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
     # algorithmic bytes: per nonzero its CSR entry (12 B) and the gathered
     # row of X (8b, L2 / shared-memory resident); per output row 8b written
     nbytes = plan.nnz * (12 + 8 * b) + plan.m * b * 8
-    if precision == "fp32" and b % 4 == 0 and b <= 32 and ldy % 2 == 0 and plan.nnz:
+    if precision == "fp32" and b % 4 == 0 and b <= 64 and ldy % (2 if b <= 32 else 4) == 0 and plan.nnz:
         # fp32 variant: X stored as float (a rounded copy), fp64 values / accumulation / Y
         X32 = torch.empty(X.shape[0], b, dtype=torch.float32, device=X.device)
         X32.copy_(X)
+        nw, ws = plan.schedule(query("svdrec_spmm_x32_warps_per_sm", b))
+        sched = (nw, ptr(ws))
         with _span("spmm", plan.nnz * (12 + 4 * b) + plan.m * b * 8):
             call("svdrec_spmm_x32", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end),
                  ptr(plan.seg_slot), ptr(plan.indices), ptr(plan.values), ptr(X32), b, plan.n, ptr(Y), ldy, b,
-                 plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), plan.nwarp, ptr(plan.warp_seg),
-                 ptr(part), stream_handle())
+                 plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), *sched, ptr(part),
+                 stream_handle())
         return Y
     hot = SPMM_HOT and getattr(plan, "hot_items", None) is not None and b % 2 == 0 and b <= 32 and plan.nnz
     if hot:
@@ -279,7 +281,7 @@ def chol_apply(G: torch.Tensor, Y: torch.Tensor, Q: torch.Tensor | None = None, 
     ldg = _mat(G, "chol_apply.G")
     if status is None:
         status = _orth_status(Y.device)
-    ws, nb = scratch(Y.device).get(query("svdrec_chol_apply_workspace_bytes", b))
+    ws, nb = scratch(Y.device).get(query("svdrec_chol_apply_workspace_bytes", r, b))
     with _span("chol_apply", 2 * r * b * 8):
         call("svdrec_chol_apply", r, b, ptr(G), ldg, float(shift_rel), ptr(Y) if r else None, ldy,
              ptr(Q) if r else None, ldq, ptr(status), ws, nb, stream_handle())

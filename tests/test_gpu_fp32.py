@@ -23,7 +23,7 @@ def test_spmm_fp32_operand(gpu):
     A = P.SparseRatings(M, 1.0, 5.0)
     d = A.device()
     rng = np.random.default_rng(1)
-    for b in (4, 20, 32):
+    for b in (4, 20, 32, 40, 64):
         X = torch.from_numpy(rng.standard_normal((A.n, b))).cuda()
         Y = torch.empty(A.m, b, dtype=torch.float64, device="cuda")
         K.spmm(d.A, X, Y, "fp32")

@@ -162,6 +162,10 @@ def test_orth_cholqr2_and_fallback(gpu):
     base = rng.standard_normal((3000, 4))
     cases.append(np.hstack([base, base[:, :2], np.zeros((3000, 2))]))  # rank deficient -> fallback
     cases.append(rng.standard_normal((70, 64)))
+    cases.append(rng.standard_normal((200000, 64)) @ np.diag(np.geomspace(1, 1e-4, 64)))  # wide: DMMA GEMM passes
+    cases.append(rng.standard_normal((9000, 40)))
+    Uw = np.linalg.qr(rng.standard_normal((6000, 48)))[0]
+    cases.append(Uw * np.geomspace(1, 1e-10, 48))  # wide, kappa 1e10 -> fallback
     for M in cases:
         Md = torch.from_numpy(M).cuda()
         Q = K.orth(Md.clone()).cpu().numpy()

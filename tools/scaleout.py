@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--sub", type=int, default=64, help="oracle row subsample 1/sub")
+    ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp64",
+                    help="fp32: the SpMMs gather float copies of their dense operand")
     args = ap.parse_args()
     dev = torch.device("cuda")
     cfg = synth.CONFIGS["c4_2b"]
@@ -52,7 +54,7 @@ def main():
     torch.cuda.reset_peak_memory_stats()
     m, n = A.shape
     # QB to k = 512 (warm-up: one block on a fresh stream, then the timed run)
-    g = P.qb_pass_blocks(A, B, PASSES, P.GaussianStream(1), max_rank=K_CAP)
+    g = P.qb_pass_blocks(A, B, PASSES, P.GaussianStream(1), max_rank=K_CAP, precision=args.precision)
     next(g).err
     del g
     torch.cuda.synchronize()
@@ -60,7 +62,7 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True)]
     ev[0].record()
     errs, ranks = [], []
-    for s in P.qb_pass_blocks(A, B, PASSES, P.GaussianStream(0), max_rank=K_CAP):
+    for s in P.qb_pass_blocks(A, B, PASSES, P.GaussianStream(0), max_rank=K_CAP, precision=args.precision):
         e = torch.cuda.Event(enable_timing=True)
         e.record()
         ev.append(e)
@@ -82,11 +84,12 @@ def main():
     # through L2 (X is 512 MB, out of L2: the cold rows come from HBM)
     csr_b = A.nnz * 12
     alg = csr_b + (m + n) * B * 8
-    gathered = A.nnz * B * 8
+    gathered = A.nnz * B * (4 if args.precision == "fp32" else 8)
     per_call_ms = ms / max(c, 1)
     line = {
         "config": f"c4_2b x {args.scale:g}: {m} users x {n} items, {A.nnz} ratings, rank 64, Zipf(1.2), half stars "
                   f"(device-generated)",
+        "precision": args.precision,
         "qb": {"block_size": B, "passes": PASSES, "power": (PASSES - 2) // 2, "k_cap": K_CAP, "k": ranks[-1],
                "blocks": len(ranks)},
         "time_to_k_s": round(total_s, 4), "block_s": [round(x, 4) for x in block_s],
