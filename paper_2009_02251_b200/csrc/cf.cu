@@ -100,14 +100,14 @@ struct RowVec<float, 4> {
 // rows of loads in flight), so wide k trades warps for registers.
 template <int NA>  // accumulators per lane (NT * VE)
 struct PredictShape {
-  static constexpr int kThreads = NA <= 4 ? 768 : (NA <= 6 ? 640 : (NA <= 8 ? 512 : 256));
+  static constexpr int kThreads = NA <= 8 ? (NA <= 4 ? 768 : 640) : 256;
 };
 
 // Ratings processed per step of the gather loops: every lane keeps U * NT
 // vector loads in flight, so narrow rows (small k) take more of them.
 template <int NT, int VE>
 struct PredictUnroll {  // narrow rows in flight cost fewer registers: take more of them
-  static constexpr int U = (NT <= 1 || (VE == 4 && NT <= 2)) ? 8 : 4;
+  static constexpr int U = (NT <= 1 || (VE == 4 && NT <= 2)) ? 8 : (NT == 4 && VE == 2 ? 3 : 4);
 };
 
 // P += v * row, S += row for U rows (one per q), lane-strided in VE-wide
