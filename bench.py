@@ -288,7 +288,7 @@ def run_b200(args):
 
     # e2e: the public API from host buffers, upload + results read inside
     e2e_times, h2d = [], 0
-    for _ in range(3):
+    for i in range(4):  # the first run is a warm-up (pinned staging buffers, first-call plans)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -298,7 +298,8 @@ def run_b200(args):
         mae2, rmse2 = P.evaluate_errors(A2, f2, te)
         e1.record()
         torch.cuda.synchronize()
-        e2e_times.append(max_over_ranks(e0.elapsed_time(e1) / 1e3, dev))
+        if i:
+            e2e_times.append(max_over_ranks(e0.elapsed_time(e1) / 1e3, dev))
         d2 = A2.device(dev)
         h2d = d2.h2d_bytes + 24 * (len(va[0]) + len(te[0]))  # CSR of A (this rank's rows) + (u, i, r) triples
     nb = len(trace)
