@@ -63,3 +63,23 @@ for name, plan, src, dst in (("A@X", d.A, X, out_m), ("A.T@Y", d.AT, Yu, out_n))
     print(f"fp32 {name} {t(lambda: K.spmm(plan, src, dst, 'fp32')):.1f} us", flush=True)
 X32 = X.float()
 Y32 = torch.empty(A.m, 20, dtype=torch.float64, device=dev)
+
+# hot/cold split through sparse_dense_mul (dense hot block on the tensor cores)
+from paper_2009_02251_b200 import linalg as L  # noqa: E402
+for h in (0, 128, 256, 512):
+    L.DENSE_HOT = h
+    ax = t(lambda: P.sparse_dense_mul(A, X, False, out=out_m))
+    aty = t(lambda: P.sparse_dense_mul(A, Yu, True, out=out_n))
+    a1 = P.sparse_dense_mul(A, X, False, out=out_m).clone()
+    a2 = P.sparse_dense_mul(A, Yu, True, out=out_n).clone()
+    if h == 0:
+        r1, r2 = a1, a2
+    print(f"dense-hot h={h}: A@X {ax:.1f} us  A.T@Y {aty:.1f} us  rel diff {float((a1 - r1).abs().max() / r1.abs().max()):.1e} "
+          f"{float((a2 - r2).abs().max() / r2.abs().max()):.1e}", flush=True)
+
+L.DENSE_HOT = 256
+sp = d.hybrid(256)
+print("hot share of nnz", sp.hot_nnz / A.nnz)
+xh = X.index_select(0, sp.hot_items)
+print(f"parts: cold A@X {t(lambda: K.spmm(sp.A, X, out_m)):.1f} us, dense A_hot@X {t(lambda: K.gemm_nn(sp.dense, xh, out_m, alpha=1.0, beta=1.0)):.1f} us, "
+      f"cold A.T@Y {t(lambda: K.spmm(sp.AT, Yu, out_n)):.1f} us, dense A_hot.T@Y {t(lambda: K.gemm_tn(sp.dense, Yu)):.1f} us", flush=True)
