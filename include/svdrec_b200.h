@@ -75,9 +75,13 @@ int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_pos,
  * Sparse x dense.  Replaces sparse_dense_mul (linalg.py:141-158):
  * Y = A @ X with A in CSR (int64 indptr, int32 indices, float64 values).
  * A.T @ X is the same call on the CSR of A.T (the host keeps both).
- * Rows are cut into segments of <= seg_max nonzeros by the host plan
- * (svdrec_spmm_plan_*); long rows go through a deterministic fix-up, so
- * results are bitwise reproducible run to run.
+ * Rows are described by segments (row, [begin, end) of the CSR arrays);
+ * the simplest valid plan is one segment per row (seg_row[i] = i,
+ * seg_begin/end = indptr[i]/indptr[i+1], seg_slot = -1, nlong = 0,
+ * nwarp = 0).  The Python host cuts long rows into <= 2048-nonzero segments
+ * whose partial sums a deterministic fix-up adds in slot order
+ * (paper_2009_02251_b200/sparse.py: segment_plan), so results are bitwise
+ * reproducible run to run; tests/c_abi/spmm_smoke.c is a plain-C caller.
  *   seg_row/seg_begin/seg_end : nseg segments, row-ordered
  *   seg_slot                  : -1 = segment covers its whole row (direct
  *                               store), else partial slot index
@@ -86,7 +90,8 @@ int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_pos,
  *   nwarp/warp_seg            : optional balanced schedule (nwarp = 0:
  *                               none): warp w owns segments
  *                               [warp_seg[w], warp_seg[w+1]) -- contiguous,
- *                               ~equal nonzeros (svdrec_spmm_warp_plan)
+ *                               ~equal nonzeros (sparse.py: warp_plan),
+ *                               nwarp = SMs x svdrec_spmm_warps_per_sm(b)
  *   d_partial                 : (nslots x b) scratch
  * ------------------------------------------------------------------- */
 int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
@@ -96,8 +101,8 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
                 int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                 const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
                 double* d_partial, void* stream);
-/* Warps per SM of the schedule (nwarp = SMs x this, warp_seg from
- * svdrec_spmm_warp_plan) that the fast path for width b expects: 16 for even
+/* Warps per SM of the schedule (nwarp = SMs x this, warp_seg as above)
+ * that the fast path for width b expects: 16 for even
  * b <= 32 (two 8-warp CTAs, 2 doubles per lane), fewer for 32 < b <= 64 with
  * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
  * fall back to the plain kernel. */
