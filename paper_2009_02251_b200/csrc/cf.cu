@@ -343,12 +343,9 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
   }  // dynamic loop over work items
 }
 
-// Ranked copy of a CSR for the scoring kernel: column j -> rank[j], each
-// row re-sorted ascending (stable within equal keys cannot occur: columns
-// are unique per row).  One segmented pass per row by a warp: rows are
-// short (<= a few thousand) and sorted by insertion into shared memory
-// would be quadratic, so the host sorts (row, rank) keys instead; this
-// kernel only relabels.
+// Ranked copy of a CSR for the scoring kernel, step 1: column j -> rank[j].
+// Step 2 (the caller: sparse.DeviceCSR.ranked) orders every row by rank
+// with one device radix sort of (row, rank) keys; ranks are unique per row.
 __global__ void k_relabel(int64_t nnz, const int32_t* __restrict__ indices, const int32_t* __restrict__ rank,
                           int32_t* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
