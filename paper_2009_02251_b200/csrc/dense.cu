@@ -230,8 +230,10 @@ int64_t tn_splits(int64_t r, int64_t tiles) {
 }
 
 int64_t sumsq_blocks(int64_t r) {
-  int64_t nb = (r + 1023) / 1024;
-  const int64_t cap = (int64_t)sm_count() * 2;
+  // short per-thread chains (<= ~128 rows per CTA): the partial sums are
+  // latency-bound, not bandwidth-bound, at the QB engine's n x b blocks
+  int64_t nb = (r + 127) / 128;
+  const int64_t cap = (int64_t)sm_count() * 4;
   return nb > cap ? cap : (nb < 1 ? 1 : nb);
 }
 
