@@ -17,7 +17,7 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 import torch
 
-CHUNK_BYTES = 8 << 20
+CHUNK_BYTES = int(os.environ.get("SVDREC_H2D_CHUNK_MB", "8")) << 20
 MIN_BYTES = 32 << 20  # smaller arrays: plain copy (a single chunk gains nothing)
 _POOL: ThreadPoolExecutor | None = None
 
@@ -25,7 +25,8 @@ _POOL: ThreadPoolExecutor | None = None
 def _pool() -> ThreadPoolExecutor:
     global _POOL
     if _POOL is None:
-        _POOL = ThreadPoolExecutor(max_workers=max(2, min(8, (os.cpu_count() or 4) // 2)),
+        workers = int(os.environ.get("SVDREC_H2D_THREADS", "0")) or max(2, min(8, (os.cpu_count() or 4) // 2))
+        _POOL = ThreadPoolExecutor(max_workers=workers,
                                    thread_name_prefix="svdrec-h2d")
     return _POOL
 
