@@ -198,12 +198,18 @@ __global__ void __launch_bounds__(kTnWarps * 32, 2) k_tn_mma(int64_t r, int64_t 
 // of a fragment load in distinct bank quarters (halves)).
 constexpr int kNnRT = 128, kNnKP = 20, kNnS = 4;  // rows per tile, k per stage, stages
 
+// kNnW warps per CTA, each on kNnRT / kNnW rows of the 128-row tile
+#ifndef SVDREC_NN_WARPS
+#define SVDREC_NN_WARPS 8
+#endif
+constexpr int kNnW = SVDREC_NN_WARPS;
+
 template <int NT>
-__global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensorMap tmX,
+__global__ void __launch_bounds__(kNnW * 32) k_nn_tma(const __grid_constant__ CUtensorMap tmX,
                                                 const __grid_constant__ CUtensorMap tmC, int64_t r, int64_t p, int q,
                                                 double alpha, double beta, double* __restrict__ Y, int64_t ldy,
                                                 int64_t ntiles, int tpc, int qb) {
-  constexpr int MT = 4;  // 32 rows per warp
+  constexpr int MT = kNnRT / (8 * kNnW);  // 8 * MT rows per warp
   const int col0 = 32 * blockIdx.y;  // column block (q > 32: several, C box qb = 32 wide)
   const bool vec2 = (ldy % 2 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
   extern __shared__ __align__(128) double sm[];
@@ -242,7 +248,7 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
   for (int64_t n = 0; n < total; ++n) {
     const int slot = (int)(n % kNnS);
     mbar_wait(bar + slot, (unsigned)((n / kNnS) & 1));
-    const double* xs = sm + slot * stage + (32 * warp + g) * kNnKP + tq;
+    const double* xs = sm + slot * stage + (8 * MT * warp + g) * kNnKP + tq;
     const double* cs_ = sm + slot * stage + xstage + tq * qb + g;
 #pragma unroll
     for (int kk = 0; kk < kNnKP / 4; ++kk) {
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(128) k_nn_tma(const __grid_constant__ CUtensor
         for (int j = 0; j < NT; ++j) dmma(acc[i][j], a[i], b[j]);
     }
     if (++cs == nks) {
-      const int64_t rbase = (t0 + ct) * kNnRT + 32 * warp + g;
+      const int64_t rbase = (t0 + ct) * kNnRT + 8 * MT * warp + g;
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         const int64_t row = rbase + 8 * i;
@@ -408,14 +414,14 @@ int nn_tma_launch(int64_t r, int64_t p, int64_t q, double alpha, const double* X
   const int64_t gy = (q + 31) / 32;
   static int per_sm = 0, per_qb = -1;  // smem depends on qb: re-query when it changes
   if (per_qb != qb) {
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<NT>, 128, smem));
+    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<NT>, kNnW * 32, smem));
     per_qb = qb;
   }
   const int64_t slots = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
   const int64_t per_col = (slots + gy - 1) / gy;  // CTAs per column block
   const int tpc = (int)((ntiles + per_col - 1) / per_col);
   const int64_t grid = (ntiles + tpc - 1) / tpc;
-  k_nn_tma<NT><<<dim3((unsigned)grid, (unsigned)gy), 128, smem, s>>>(tx, tc, r, p, (int)q, alpha, beta, Y, ldy,
+  k_nn_tma<NT><<<dim3((unsigned)grid, (unsigned)gy), kNnW * 32, smem, s>>>(tx, tc, r, p, (int)q, alpha, beta, Y, ldy,
                                                                      ntiles, tpc, qb);
   return check_launch("gemm_nn_tma");
 }
