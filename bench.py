@@ -288,7 +288,7 @@ def run_b200(args):
 
     # e2e: the public API from host buffers, upload + results read inside
     e2e_times, h2d = [], 0
-    for i in range(4):  # the first run is a warm-up (pinned staging buffers, first-call plans)
+    for i in range(6):  # the first run is a warm-up (pinned staging buffers, first-call plans); median of 5
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
