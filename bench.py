@@ -288,6 +288,7 @@ def run_b200(args):
 
     # e2e: the public API from host buffers, upload + results read inside
     e2e_times, h2d = [], 0
+    gc.disable()  # as in the timed region: no collector pauses inside the runs
     for i in range(6):  # the first run is a warm-up (pinned staging buffers, first-call plans); median of 5
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -302,6 +303,7 @@ def run_b200(args):
             e2e_times.append(max_over_ranks(e0.elapsed_time(e1) / 1e3, dev))
         d2 = A2.device(dev)
         h2d = d2.h2d_bytes + 24 * (len(va[0]) + len(te[0]))  # CSR of A (this rank's rows) + (u, i, r) triples
+    gc.enable()
     nb = len(trace)
     d2h = nb * ((BLOCK + 1) * 8 + 4 * 3 + 16) + 16
 

@@ -46,5 +46,5 @@ def run(verbose):
         print(" | ".join(f"{k} {v:.1f} ms" for k, v in T.items()), f"total {sum(T.values()):.1f} ms")
 
 
-for i in range(3):
-    run(i == 2)
+for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
+    run(i >= 1)
