@@ -312,11 +312,19 @@ def run_b200(args):
     if peaks_p.is_file():
         peak, peak_src = float(json.loads(peaks_p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
 
+    # DRAM bytes per launch from the committed ncu --set full captures
+    # (tools/traffic.py -> profiles/traffic.json), or null
+    traffic_p = ROOT / "profiles" / "traffic.json"
+    traffic = json.loads(traffic_p.read_text()) if traffic_p.is_file() else {}
+
     def roof(name, kernel, l2_ceiling, l2_note):
         c, ms, nbytes = prof.get(name, (0, 0.0, 0))
         ach = (nbytes / (ms / 1e3)) / 1e9 if ms > 0 else None
+        tr_ = traffic.get(name, {}).get("dram_bytes_per_launch")
         return {"kernel": kernel, "bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
-                "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": None,
+                "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": tr_,
+                "traffic_source": f"ncu --set full, profiles/traffic.json ({traffic[name]['launches']} launches)"
+                if tr_ else None,
                 "peak_source": peak_src, "calls_per_step": c // psteps,
                 "algorithmic_bytes_per_call": int(nbytes / max(c, 1)), "ms_per_step": round(ms / psteps, 3),
                 "l2_gather": {"ceiling_GBps": l2_ceiling, "frac": round(ach / l2_ceiling, 4) if ach else None,
