@@ -570,6 +570,11 @@ class ValidationMae:
     def __call__(self, state: QbState) -> bool:
         return self.collect(self.submit(state))
 
+    def may_stop(self) -> bool:
+        """Whether the next collected score can end the scan (one more
+        stale block reaches ``patience``)."""
+        return self._stale + 1 >= self.patience
+
     def join(self) -> None:
         """Make the current stream wait for everything scored so far and
         keep the best factors alive across streams."""
@@ -613,7 +618,10 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
         t0 = time.perf_counter() if _HOST_TRACE is not None else 0.0
         pending = criterion.submit(state)
         capped = max_rank is not None and state.rank >= max_rank
-        if pipeline:
+        # speculate on the next block only when this score cannot end the
+        # scan (fewer than patience - 1 stale blocks so far): a block queued
+        # past the stop would be computed for nothing, next to the scoring
+        if pipeline and not criterion.may_stop():
             t1 = time.perf_counter() if _HOST_TRACE is not None else 0.0
             nxt = None if capped else next(gen, None)
             t2 = time.perf_counter() if _HOST_TRACE is not None else 0.0
