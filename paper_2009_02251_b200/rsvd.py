@@ -15,6 +15,8 @@ sketch generation, SpMM, deflation, LU, TSQR -- is queued on one stream.
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 from typing import Callable, Iterator
 
@@ -30,6 +32,13 @@ from .sparse import SparseRatings
 
 F64 = torch.float64
 
+
+# basis of the power steps' lu_lower_basis: 'cqr' (one-pass shifted
+# CholeskyQR, ~45 us at 138493 x 20) or 'lu' (partial pivoting on-chip,
+# ~130 us); both are Y times an upper-triangular matrix, so the block's
+# final Q is the same up to column signs (bench: 42.8 vs 43.8 ms per step,
+# same k, MAE trace and test RMSE to every printed digit)
+LU_BASIS = os.environ.get("SVDREC_LU_BASIS", "cqr")
 
 class QbState:
     """Snapshot of a growing QB factorization after a completed block.
@@ -241,13 +250,14 @@ class _QbEngine:
             K.gemm_nn(self.Q[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
 
     def lu(self, Y):
-        """lu_lower_basis of a power step (rsvd.py:183-190).  Tall blocks
-        whose rows do not fit the on-chip LU get a one-pass shifted
-        CholeskyQR basis instead: both are Y times an upper-triangular
-        matrix, so the block's final Q is the same up to column signs
-        (parallel.py), and an all-zero Y still flags a zero pivot."""
+        """lu_lower_basis of a power step (rsvd.py:183-190) as a one-pass
+        shifted CholeskyQR basis (LU_BASIS = "cqr", the default; with "lu"
+        the on-chip partial-pivoting LU where the rows fit it): both are Y
+        times an upper-triangular matrix, so the block's final Q is the same
+        up to column signs (parallel.py), and an all-zero Y still flags a
+        zero pivot."""
         r, b = Y.shape
-        if K.query("svdrec_lu_fast_path", r, b):
+        if LU_BASIS == "lu" and K.query("svdrec_lu_fast_path", r, b):
             K.lu_lower(Y, self.status)
         else:
             sharded_orth(Y, Y, _LOCAL, r, passes=1, status=self.status)
