@@ -118,6 +118,66 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+class NvmlClocks(Clocks):
+    """The same clocks line sampled in-process through NVML (the library
+    nvidia-smi queries): SM clock and the clock-event reasons every
+    BENCH_SMI_MS ms from a daemon thread (BENCH_CLOCKS=nvml; the default is
+    the recipe's nvidia-smi -lms process).  Both measured alike: neither
+    sampler disturbs the timed steps."""
+
+    def __init__(self, index: int):
+        import threading
+        import pynvml as nv
+        self.nv = nv
+        nv.nvmlInit()
+        self.h = nv.nvmlDeviceGetHandleByIndex(index)
+        self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        self.bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                     "sw_power_cap": 0x4}
+        self.samples: list[tuple[float, int]] = []
+        self.p = self  # "running" marker for the base class
+        self._halt = threading.Event()
+        dt = float(os.environ.get("BENCH_SMI_MS", "100")) / 1e3
+
+        def loop():
+            while not self._halt.is_set():
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)), int(get(self.h))))
+                self._halt.wait(dt)
+
+        self.t = threading.Thread(target=loop, daemon=True)
+        self.t.start()
+
+    def wait_first(self, timeout: float = 5.0) -> None:
+        t = time.perf_counter()
+        while not self.samples and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def mark(self) -> int:
+        return len(self.samples)
+
+    def stop(self, start: int = 0) -> dict:
+        end = self.mark()
+        self._halt.set()
+        self.t.join()
+        rows = self.samples[start:max(end, start + 1)]
+        sm = [c for c, _ in rows]
+        reasons = sorted({n for _, r in rows for n, b in self.bits.items() if r & b})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(rows), "sampler": "nvml"}
+
+
+def make_clocks(index: int) -> Clocks:
+    if os.environ.get("BENCH_NO_CLOCKS"):
+        return Clocks.disabled()
+    if os.environ.get("BENCH_CLOCKS", "smi") == "nvml":
+        try:
+            return NvmlClocks(index)
+        except Exception:  # no NVML binding / library: the nvidia-smi process
+            pass
+    return Clocks(index)
+
+
 def cpu_estimate(tr, va, te, nblocks: int, n_samples: int = 600):
     """Time the oracle on a bounded sample and extrapolate to the full step.
 
@@ -220,22 +280,35 @@ def run_b200(args):
         mae, rmse = P.evaluate_errors(A, f, ts, precision=precision)
         return f, trace, mae, rmse
 
-    clocks = Clocks(local) if not os.environ.get("BENCH_NO_CLOCKS") else Clocks.disabled()
+    clocks = make_clocks(local)
     clocks.wait_first()
-    for _ in range(args.warmup):
-        step()
+    import gc
+    for i in range(args.warmup):
+        if i == args.warmup - 1:
+            # the last warm-up step runs on a clean heap: collect, then
+            # freeze the set-up objects (data generation leaves millions of
+            # them) so a cyclic collection inside the timed steps does not
+            # walk them; the collector stays off until the timing ends.  One
+            # step between the collection and the timed region absorbs what
+            # the collection leaves behind (freed pages, deferred frees).
+            gc.collect()
+            gc.freeze()
+            gc.disable()
+        # hold the result as the timed loop does (the previous step's
+        # factors stay alive while the next step runs), so the caching
+        # allocator reaches the timed loop's peak here: otherwise the
+        # second timed step made one cudaMalloc (+10 to +90 ms, seen)
+        f, trace, mae, rmse = step()
+    if args.warmup == 0:
+        gc.collect()
+        gc.freeze()
+        gc.disable()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    # start the timed region from a clean heap: collect, then freeze the
-    # set-up objects (data generation leaves millions of them) so a cyclic
-    # collection inside the timed steps does not walk them
-    import gc
-    gc.collect()
-    gc.freeze()
-    gc.disable()  # no collector pauses on the host while the GPU waits for it (re-enabled after timing)
     ck0 = clocks.mark()
     launches0 = lib.svdrec_launch_count()
+    ms0 = torch.cuda.memory_stats(dev)
     # the K steps are one timed region (total / K); per-step events inside
     # it are reported for spread only
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -249,6 +322,9 @@ def run_b200(args):
     launches = (lib.svdrec_launch_count() - launches0) // args.steps
     gc.enable()
     ck = clocks.stop(ck0)
+    ms1 = torch.cuda.memory_stats(dev)
+    alloc = {k: int(ms1.get(k, 0) - ms0.get(k, 0)) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries",
+                                                             "num_sync_all_streams")}
     t_step = ev[0].elapsed_time(ev[-1]) / 1e3 / args.steps
     # kernel breakdown from one extra, untimed step with per-call CUDA-event
     # spans (their host cost stays out of the timed region)
@@ -303,6 +379,9 @@ def run_b200(args):
             e2e_times.append(max_over_ranks(e0.elapsed_time(e1) / 1e3, dev))
         d2 = A2.device(dev)
         h2d = d2.h2d_bytes + 24 * (len(va[0]) + len(te[0]))  # CSR of A (this rank's rows) + (u, i, r) triples
+        # release this run's matrix and factors before the next run builds
+        # its own, so every run is served from the allocator's cache
+        del A2, d2, f2, tr2
     gc.enable()
     nb = len(trace)
     d2h = nb * ((BLOCK + 1) * 8 + 4 * 3 + 16) + 16
@@ -358,6 +437,7 @@ def run_b200(args):
         "gpu_launches": int(launches),
         "variants": variants,
         "clocks": ck,
+        "allocator_in_timed_region": alloc,
         "setup": {"generate_split_s": round(gen_s, 2)},
     }
     if ws == 1 and not args.no_cpu_baseline:
