@@ -107,7 +107,10 @@ struct PredictShape {
 // vector loads in flight, so narrow rows (small k) take more of them.
 template <int NT, int VE>
 struct PredictUnroll {  // narrow rows in flight cost fewer registers: take more of them
-  static constexpr int U = (NT <= 1 || (VE == 4 && NT <= 2)) ? 8 : (NT == 4 && VE == 2 ? 3 : 4);
+#ifndef SVDREC_CF_U1
+#define SVDREC_CF_U1 8  // rows in flight per lane for the narrow (NT = 1) rows
+#endif
+  static constexpr int U = NT <= 1 ? SVDREC_CF_U1 : ((VE == 4 && NT <= 2) ? 8 : (NT == 4 && VE == 2 ? 3 : 4));
 };
 
 // P += v * row, S += row for U rows (one per q), lane-strided in VE-wide
