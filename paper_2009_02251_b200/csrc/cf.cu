@@ -168,8 +168,21 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
     const int64_t sl = t / kp, e = t - sl * kp;
     hs[t] = sl < nhot ? Yr[sl * ldy + e] : TY(0);
   }
+  // per-warp batch tables: a 32-rating batch's row ids (hot: shared-memory
+  // row or the zero row; cold: Yr row or the zero row) and values, read by
+  // every lane with broadcast LDS instead of three shuffles, a compare and a
+  // select per rating; U trailing slots are padding for the U-wide steps
+  constexpr int U = PredictUnroll<NT, VE>::U;
+  constexpr int NWARP = PredictShape<NA>::kThreads / 32, BS = 32 + U;
+  __shared__ int32_t s_hot[NWARP][BS], s_cold[NWARP][BS];
+  __shared__ double s_val[NWARP][BS];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane < U) {
+    s_hot[wid][32 + lane] = nhot;
+    s_cold[wid][32 + lane] = zrow;
+    s_val[wid][32 + lane] = 0.0;
+  }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   // Work items are (group, chunk) pairs, heaviest users first.  Users with
   // more than ``chunk`` ratings are split across warps: each chunk leaves
   // (P, S, sum v) in its partial slot and the warp that completes the group
@@ -216,17 +229,20 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
       }
       const int nv = (int)min64(32, e - base);
       vsum += vi;  // this lane's entry (0 past the end)
-      const int nh = __popc(__ballot_sync(0xffffffffu, ci < nhot));  // ascending ranks: a prefix
-      constexpr int U = PredictUnroll<NT, VE>::U;
+      const bool hot = ci < nhot;  // ascending ranks: the hot entries are a prefix
+      const int nh = __popc(__ballot_sync(0xffffffffu, hot));
+      __syncwarp();  // the previous batch's tables are read
+      s_hot[wid][lane] = hot ? ci : nhot;
+      s_cold[wid][lane] = (lane < nv && !hot) ? ci : zrow;
+      s_val[wid][lane] = vi;
+      __syncwarp();
       for (int j = 0; j < nh; j += U) {
         const TY* rows[U];
         double vv[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
-          const int jj = j + q;
-          const int32_t cq = __shfl_sync(0xffffffffu, ci, jj & 31);
-          vv[q] = __shfl_sync(0xffffffffu, vi, jj & 31);
-          rows[q] = hs + (int64_t)(jj < nh ? cq : nhot) * kp;
+          rows[q] = hs + (int64_t)s_hot[wid][j + q] * kp;
+          vv[q] = s_val[wid][j + q];
         }
         accum<NT, U, true, TY, VE>(P, S, rows, vv, lane, kp);
       }
@@ -235,10 +251,8 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
         double vv[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
-          const int jj = j + q;
-          const int32_t cq = __shfl_sync(0xffffffffu, ci, jj & 31);
-          vv[q] = __shfl_sync(0xffffffffu, vi, jj & 31);
-          rows[q] = Yr + (int64_t)(jj < nv ? cq : zrow) * ldy;
+          rows[q] = Yr + (int64_t)s_cold[wid][j + q] * ldy;
+          vv[q] = s_val[wid][j + q];
         }
         accum<NT, U, false, TY, VE>(P, S, rows, vv, lane, kp);
       }
