@@ -174,8 +174,9 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
   // select per rating; U trailing slots are padding for the U-wide steps
   constexpr int U = PredictUnroll<NT, VE>::U;
   constexpr int NWARP = PredictShape<NA>::kThreads / 32, BS = 32 + U;
-  __shared__ int32_t s_hot[NWARP][BS], s_cold[NWARP][BS];
-  __shared__ double s_val[NWARP][BS];
+  __shared__ __align__(16) int32_t s_hot[NWARP][BS];
+  __shared__ int32_t s_cold[NWARP][BS];
+  __shared__ __align__(16) double s_val[NWARP][BS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane < U) {
     s_hot[wid][32 + lane] = nhot;
@@ -236,13 +237,30 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
       s_cold[wid][lane] = (lane < nv && !hot) ? ci : zrow;
       s_val[wid][lane] = vi;
       __syncwarp();
-      for (int j = 0; j < nh; j += U) {
+      for (int j = 0; j < nh; j += U) {  // j % U == 0: 16-B table reads when U % 4 == 0
         const TY* rows[U];
         double vv[U];
+        if constexpr (U % 4 == 0) {
 #pragma unroll
-        for (int q = 0; q < U; ++q) {
-          rows[q] = hs + (int64_t)s_hot[wid][j + q] * kp;
-          vv[q] = s_val[wid][j + q];
+          for (int q = 0; q < U; q += 4) {
+            const int4 id = *reinterpret_cast<const int4*>(&s_hot[wid][j + q]);
+            const double2 v0 = *reinterpret_cast<const double2*>(&s_val[wid][j + q]);
+            const double2 v1 = *reinterpret_cast<const double2*>(&s_val[wid][j + q + 2]);
+            rows[q] = hs + (int64_t)id.x * kp;
+            rows[q + 1] = hs + (int64_t)id.y * kp;
+            rows[q + 2] = hs + (int64_t)id.z * kp;
+            rows[q + 3] = hs + (int64_t)id.w * kp;
+            vv[q] = v0.x;
+            vv[q + 1] = v0.y;
+            vv[q + 2] = v1.x;
+            vv[q + 3] = v1.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            rows[q] = hs + (int64_t)s_hot[wid][j + q] * kp;
+            vv[q] = s_val[wid][j + q];
+          }
         }
         accum<NT, U, true, TY, VE>(P, S, rows, vv, lane, kp);
       }
