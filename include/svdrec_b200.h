@@ -118,20 +118,6 @@ int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg
                     int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                     const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
                     double* d_partial, void* stream);
-/* Same product with the first nhot rows of X staged in shared memory: the
- * CSR must be "ranked" -- in every row the entries with column < nhot come
- * first (e.g. columns relabelled by popularity and each row ordered by the
- * new label, as svdrec_cf_relabel + a per-row sort produce) -- and X given
- * in the same labelling.  Only the cold entries are gathered from L2.
- * nwarp/warp_seg must be the 16-warps-per-SM schedule. */
-int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
-                    const int64_t* d_seg_end, const int32_t* d_seg_slot,
-                    const int32_t* d_indices, const double* d_values,
-                    const double* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
-                    int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
-                    const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
-                    double* d_partial, int32_t nhot, void* stream);
-
 /* ---------------------------------------------------------------------
  * Dense tall-skinny contractions (the deflation products of
  * rsvd.py:135-142, 179-194: Q @ (B @ X), Q @ (Q.T @ X), B.T @ (Q.T @ X)

@@ -36,7 +36,6 @@ SIGNATURES = {
     "svdrec_spmm_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_x32_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_x32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
-    "svdrec_spmm_hot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _i32, _p]),
     "svdrec_gemm_tn_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "svdrec_gemm_tn": (C.c_int, [_i64, _i64, _i64, _f64, _p, _i64, _p, _i64, _f64, _p, _i64, _p, _sz, _p]),
     "svdrec_gemm_nn": (C.c_int, [_i64, _i64, _i64, _f64, _p, _i64, _p, _i64, _f64, _p, _i64, _p]),

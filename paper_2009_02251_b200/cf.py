@@ -36,7 +36,6 @@ F64 = torch.float64
 # 47.5 vs 48.1 ms per bench step with the ranked CF kernel; SVDREC_PIPELINE=0
 # scores on the caller's stream).
 PIPELINE = os.environ.get("SVDREC_PIPELINE", "1") == "1"
-SPECULATE = os.environ.get("SVDREC_SPECULATE", "0") == "1"  # measured: no gain
 _SIDE: dict = {}
 
 
@@ -612,7 +611,7 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
     # the next block is enqueued before the host waits for this block's
     # score (same stream unless PIPELINE), so the GPU never idles on the
     # stop decision; a block computed past the stop is discarded
-    pipeline = PIPELINE or SPECULATE
+    pipeline = PIPELINE
     state = next(gen, None)
     while state is not None:
         t0 = time.perf_counter() if _HOST_TRACE is not None else 0.0

@@ -103,6 +103,9 @@ struct PredictShape {
   static constexpr int kThreads = NA <= 8 ? (NA <= 4 ? 768 : 640) : 256;
 };
 
+// dynamic shared memory of the scoring kernel: the hottest items' unit rows
+constexpr size_t kHotBytes = 208 * 1024;
+
 // Ratings processed per step of the gather loops: every lane keeps U * NT
 // vector loads in flight, so narrow rows (small k) take more of them.
 template <int NT, int VE>
@@ -177,6 +180,8 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
   __shared__ __align__(16) int32_t s_hot[NWARP][BS];
   __shared__ int32_t s_cold[NWARP][BS];
   __shared__ __align__(16) double s_val[NWARP][BS];
+  // the static tables and the dynamic hot rows share the 227 KB opt-in
+  static_assert((size_t)NWARP * BS * 16 + kHotBytes <= 232448, "cf_predict: shared memory over the opt-in limit");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane < U) {
     s_hot[wid][32 + lane] = nhot;
@@ -471,7 +476,6 @@ int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d
   const int nt = (kp / ve + 31) / 32;  // vector steps per lane
   // one persistent CTA per SM holding the hottest items' unit rows in
   // shared memory (as many as fit in kHotBytes, plus the zero row)
-  constexpr size_t kHotBytes = 208 * 1024;
   int nhot = (int)(kHotBytes / ((size_t)kp * sizeof(TY))) - 1;
   if (nhot > n_items) nhot = n_items;
   if (nhot < 0) nhot = 0;
@@ -479,12 +483,7 @@ int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d
   const int64_t grid = sm_count();
 #define SVDREC_PRED(NT, VE)                                                                                   \
   do {                                                                                                        \
-    static bool attr_set = false;                                                                             \
-    if (!attr_set) {                                                                                          \
-      SVDREC_CUDA(cudaFuncSetAttribute(k_predict<NT, TY, VE>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                       (int)kHotBytes));                                                      \
-      attr_set = true;                                                                                        \
-    }                                                                                                         \
+    SVDREC_CUDA(smem_attr_once(k_predict<NT, TY, VE>, (int)kHotBytes));                                     \
     k_predict<NT, TY, VE><<<(unsigned)grid, PredictShape<NT * VE>::kThreads, smem, s>>>(                      \
         nwork, d_work_start, reinterpret_cast<const int4*>(d_work_meta), d_items, d_ranked_indices,           \
         d_ranked_values, k, d_Yr, d_Xn, ldn, ldy, d_norm, global_mean, rating_min, rating_max, nhot, n_items, \

@@ -49,6 +49,23 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 int sm_count();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a process driving several GPUs sets it on
+// each of them (lib.cu keeps the set of (kernel, device) pairs done).
+bool smem_attr_done(const void* kernel, int dev);
+void smem_attr_mark(const void* kernel, int dev);
+template <class K>
+cudaError_t smem_attr_once(K* kernel, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  if (smem_attr_done(key, dev)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) smem_attr_mark(key, dev);
+  return e;
+}
+
 // skinny.cu: tall-skinny GEMMs for q <= 32 (see the file header)
 int64_t tn_skinny_slabs(int64_t r, int64_t p);
 int launch_nn_skinny(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C,

@@ -2,6 +2,8 @@
 #include <cstdarg>
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 
@@ -29,6 +31,19 @@ int sm_count() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
   });
   return n;
+}
+
+static std::mutex g_attr_mu;
+static std::set<std::pair<const void*, int>> g_attr_done;
+
+bool smem_attr_done(const void* kernel, int dev) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  return g_attr_done.count({kernel, dev}) != 0;
+}
+
+void smem_attr_mark(const void* kernel, int dev) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  g_attr_done.insert({kernel, dev});
 }
 
 }  // namespace svdrec

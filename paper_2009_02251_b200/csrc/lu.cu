@@ -321,11 +321,7 @@ int try_lu_smem(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag,
   const int64_t rpc = (r + nblk - 1) / nblk;
   const size_t smem = (size_t)rpc * (b | 1) * 8 + (size_t)rpc * 4 + 64;
   if (smem > kLuSmemMax) return 0;
-  static bool attr = false;
-  if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLuSmemMax));
-    attr = true;
-  }
+  SVDREC_CUDA(smem_attr_once(k_lu_smem, (int)kLuSmemMax));
   int per_sm = 0;
   SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu_smem, kLuThreads, smem));
   if (per_sm < 2) return 0;

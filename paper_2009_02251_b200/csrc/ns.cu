@@ -323,9 +323,9 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
   const size_t smem = use_tma ? kNsSmemT : kNsSmem;
   static int max_blocks_t[2] = {0, 0};
   int& max_blocks = max_blocks_t[use_tma];
+  SVDREC_CUDA(smem_attr_once(k_ns, (int)kNsSmemT));
   if (!max_blocks) {
     int per_sm = 0;
-    SVDREC_CUDA(cudaFuncSetAttribute(k_ns, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNsSmemT));
     SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, smem));
     max_blocks = per_sm * sm_count();
     if (max_blocks > 4 * sm_count()) max_blocks = 4 * sm_count();

@@ -405,11 +405,7 @@ int nn_tma_launch(int64_t r, int64_t p, int64_t q, double alpha, const double* X
   if (rc) return rc;
   const int stage = kNnRT * kNnKP + ((kNnKP * qb + 15) & ~15);
   const size_t smem = (size_t)kNnS * stage * 8;
-  static bool attr = false;
-  if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_nn_tma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    attr = true;
-  }
+  SVDREC_CUDA(smem_attr_once(k_nn_tma<NT>, 100 * 1024));
   const int64_t ntiles = (r + kNnRT - 1) / kNnRT;
   const int64_t gy = (q + 31) / 32;
   static int per_sm = 0, per_qb = -1;  // smem depends on qb: re-query when it changes
@@ -438,11 +434,7 @@ int tn_tma_launch(int64_t r, int64_t p, int64_t q, const double* X, int64_t ldx,
   size_t smem = (size_t)kTnS2 * stage * 8;
   const size_t red = (size_t)MT * NT * 2 * 32 * 8;
   if (smem < red) smem = red;
-  static bool attr = false;
-  if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_tn_tma<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    attr = true;
-  }
+  SVDREC_CUDA(smem_attr_once(k_tn_tma<MT, NT>, 100 * 1024));
   dim3 grid((unsigned)nslab, (unsigned)((p + 8 * MT - 1) / (8 * MT)), (unsigned)((q + 31) / 32));
   k_tn_tma<MT, NT><<<grid, 128, smem, s>>>(tx, ty, r, p, (int)q, part, rows_per, qb);
   return check_launch("gemm_tn_tma");

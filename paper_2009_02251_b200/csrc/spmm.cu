@@ -131,8 +131,6 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t nseg, const int32_t* __res
 // order.  Measured on the c3 bench (ms per step, 48 calls): k_spmm 25.4,
 // cp.async (LDGSTS) staging 20.1 (L1 data pipe 90% busy: the rows crossed
 // it twice), this kernel 16.8.
-constexpr int kPipeWarps = 8;
-
 // Rows are fetched with the sm_100 tensor-memory-accelerator gather
 // (cp.async.bulk.tensor.2d ... tile::gather4: four X rows of b doubles per
 // instruction, lanes 0..7 each issue one per chunk) completing on one
@@ -151,13 +149,6 @@ struct TmaGeom {
   static constexpr int STG = ROWSD + 64;  // + 32 values + 16 (meta, pad) + 16 (32 column ids)
 };
 
-// Hot rows (W = 16 warps, one CTA per SM): with ``nhot`` > 0 the first
-// nhot rows of X are staged once in shared memory after the rings, and the
-// CSR is "ranked" (columns < nhot form a prefix of every row, e.g. items
-// relabelled by popularity): a chunk's hot prefix is read from the staged
-// rows and only its cold entries are gathered by TMA (fully hot gather4
-// blocks are skipped, hot entries of mixed blocks use the zero-filled
-// coordinate -1), cutting the L2 row requests that bound this kernel.
 // V doubles per lane (V = 2: b <= 32; V = 4: 32 < b <= 64, b % 4 == 0),
 // held as V/2 double2.
 template <int V>
@@ -204,32 +195,22 @@ struct Acc {
   }
 };
 
-template <int P, int S, int W, bool HOT, int V, typename TX = double>
-__global__ void __launch_bounds__(W * 32, (!HOT && V == 2 ? 2 : 1)) k_spmm_tma(
+template <int P, int S, int W, int V, typename TX = double>
+__global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_tma(
     const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_seg,
     const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
     const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ indices, const double* __restrict__ values,
-    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial, const double* __restrict__ X, int64_t ldx,
-    int nhot) {
+    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial) {
   using Gm = TmaGeom<P, V, TX>;
-  static_assert(!HOT || sizeof(TX) == 8, "hot rows are staged as double");
   constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWSD, STG = Gm::STG;
   extern __shared__ __align__(128) double smd[];
   __shared__ __align__(8) uint64_t bars[W * S];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   double* ring = smd + (size_t)wib * S * STG;
-  double* hot = smd + (size_t)W * S * STG;
   uint64_t* bar = bars + wib * S;
   if (lane < S) mbar_init(bar + lane, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  if (HOT && nhot > 0) {
-    for (int t = threadIdx.x; t < nhot * (B / 2); t += blockDim.x) {  // B/2 double2 per row
-      const int r = t / (B / 2), c2 = t - r * (B / 2);
-      reinterpret_cast<double2*>(hot)[t] = __ldg(reinterpret_cast<const double2*>(X + (int64_t)r * ldx) + c2);
-    }
-    __syncthreads();
-  }
   __syncwarp();
   if (w >= nwarp) return;
   const int g = lane / P, pc = lane - (lane / P) * P;
@@ -293,27 +274,17 @@ __global__ void __launch_bounds__(W * 32, (!HOT && V == 2 ? 2 : 1)) k_spmm_tma(
   auto issue = [&](int slot) {
     double* st = ring + slot * STG;
     st[ROWS + lane] = kvi;
-    if (HOT) reinterpret_cast<int32_t*>(st + ROWS + 48)[lane] = kci;
-    // hot entries (column < nhot) form a prefix of the chunk
-    const int h = HOT ? __popc(__ballot_sync(0xffffffffu, kci >= 0 && kci < nhot)) : 0;
-    if (lane == 0) *reinterpret_cast<int4*>(st + ROWS + 32) = make_int4(km.x, km.y, km.z, km.w | (h << 2));
+    if (lane == 0) *reinterpret_cast<int4*>(st + ROWS + 32) = km;
     const int ng = (km.z + 3) >> 2;
-    const int g0 = h >> 2;  // gather4 blocks [0, g0) are entirely hot
     const int t = lane & 7;
-    int r0 = __shfl_sync(0xffffffffu, kci, 4 * t);
-    int r1 = __shfl_sync(0xffffffffu, kci, 4 * t + 1);
-    int r2 = __shfl_sync(0xffffffffu, kci, 4 * t + 2);
-    int r3 = __shfl_sync(0xffffffffu, kci, 4 * t + 3);
-    if (HOT) {
-      if (4 * t < h) r0 = -1;
-      if (4 * t + 1 < h) r1 = -1;
-      if (4 * t + 2 < h) r2 = -1;
-      if (4 * t + 3 < h) r3 = -1;
-    }
-    if (ng > g0) {
-      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)((ng - g0) * 4 * B * sizeof(TX)));
+    const int r0 = __shfl_sync(0xffffffffu, kci, 4 * t);
+    const int r1 = __shfl_sync(0xffffffffu, kci, 4 * t + 1);
+    const int r2 = __shfl_sync(0xffffffffu, kci, 4 * t + 2);
+    const int r3 = __shfl_sync(0xffffffffu, kci, 4 * t + 3);
+    if (ng > 0) {
+      if (lane == 0) mbar_expect_tx(bar + slot, (unsigned)(ng * 4 * B * sizeof(TX)));
       __syncwarp();
-      if (lane >= g0 && lane < ng)
+      if (lane < ng)
         tma_gather4(reinterpret_cast<TX*>(st) + lane * G4, &tmX, 0, r0, r1, r2, r3, bar + slot);
     } else if (lane == 0) {
       mbar_expect_tx(bar + slot, 0);  // empty or all-hot chunk: complete the phase
@@ -353,14 +324,11 @@ __global__ void __launch_bounds__(W * 32, (!HOT && V == 2 ? 2 : 1)) k_spmm_tma(
     if (active) {
       // fully unrolled over the chunk's NS steps: unconditional loads at
       // constant smem offsets from one per-lane base (all in flight at
-      // once; rows past the chunk are stale but in-bounds), FMAs masked;
-      // the chunk's hot prefix reads the staged hot rows instead
+      // once; rows past the chunk are stale but in-bounds), FMAs masked
       constexpr int NS = (32 + G - 1) / G;
-      const int h = HOT ? m.w >> 2 : 0;
       const TX* sx = reinterpret_cast<const TX*>(st);
       const TX* xr = sx + ((g >> 2) * G4 + (g & 3) * B) + V * pc;
       const double* vr = st + ROWS + g;
-      const int32_t* ir = reinterpret_cast<const int32_t*>(st + ROWS + 48);
       Acc<V> xs[NS];
       double vs[NS];
 #pragma unroll
@@ -369,9 +337,6 @@ __global__ void __launch_bounds__(W * 32, (!HOT && V == 2 ? 2 : 1)) k_spmm_tma(
         const int jo = q * G;
         const int jc = j < 32 ? j : 31;
         const TX* src = G4 == 4 * B ? xr + jo * B : sx + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
-        if constexpr (HOT) {
-          if (j < h) src = hot + ir[jc] * B + V * pc;
-        }
         xs[q].load(src);
         vs[q] = vr[jc - g];
       }
@@ -403,11 +368,11 @@ __global__ void __launch_bounds__(W * 32, (!HOT && V == 2 ? 2 : 1)) k_spmm_tma(
   }
 }
 
-template <int P, int S, int W, bool HOT, int V = 2, typename TX = double>
+template <int P, int S, int W, int V = 2, typename TX = double>
 int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
                const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
                const double* values, const TX* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
-               int nhot, cudaStream_t s) {
+               cudaStream_t s) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
     set_error("spmm: cuTensorMapEncodeTiled unavailable");
@@ -428,25 +393,11 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
   }
   constexpr size_t ring = (size_t)W * S * TmaGeom<P, V, TX>::STG * sizeof(double);
   constexpr size_t kMaxSmem = 226 * 1024;  // + the static mbarriers within the 227 KB opt-in
-  if constexpr (HOT && (sizeof(TX) != 8 || ring + 32 * 2 * P * sizeof(double) > kMaxSmem)) {  // no hot set
-    return tma_launch<P, S, 8, false, V, TX>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,
-                               ldx, Y, ldy, partial, 0, s);
-  }
-  if (!HOT) nhot = 0;  // two CTAs per SM: no room for a hot set
-  const int64_t fit = (int64_t)((kMaxSmem - ring) / (V * P * sizeof(double)));
-  if (nhot > fit) nhot = (int)fit;
-  if (nhot > xrows) nhot = (int)xrows;
-  const size_t smem = ring + (size_t)nhot * V * P * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_spmm_tma<P, S, W, HOT, V, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kMaxSmem));
-    attr = true;
-  }
+  static_assert(ring <= kMaxSmem, "spmm: gather rings exceed shared memory");
+  SVDREC_CUDA(smem_attr_once(k_spmm_tma<P, S, W, V, TX>, (int)kMaxSmem));
   const int64_t grid = (nwarp + W - 1) / W;
-  k_spmm_tma<P, S, W, HOT, V, TX><<<(unsigned)grid, W * 32, smem, s>>>(
-      tm, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, Y, ldy, partial,
-      reinterpret_cast<const double*>(X), ldx, nhot);
+  k_spmm_tma<P, S, W, V, TX><<<(unsigned)grid, W * 32, ring, s>>>(tm, nwarp, warp_seg, seg_row, seg_begin, seg_end,
+                                                                  seg_slot, indices, values, Y, ldy, partial);
   return check_launch("spmm_tma");
 }
 
@@ -454,11 +405,11 @@ template <int S, int W>
 int tma_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
                  const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
                  const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
-                 int nhot, cudaStream_t s) {
-#define SVDREC_TMA(PP)                                                                                              \
-  case PP:                                                                                                          \
-    return tma_launch<PP, S, W, (W == 16)>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, X,  \
-                                ldx, Y, ldy, partial, nhot, s);
+                 cudaStream_t s) {
+#define SVDREC_TMA(PP)                                                                                          \
+  case PP:                                                                                                      \
+    return tma_launch<PP, S, W>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, \
+                                X, ldx, Y, ldy, partial, s);
   switch (b / 2) {
     SVDREC_TMA(1)
     SVDREC_TMA(2)
@@ -498,8 +449,8 @@ int tma_dispatch4(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, 
                   cudaStream_t s) {
 #define SVDREC_TMA4(PP)                                                                                          \
   case PP:                                                                                                       \
-    return tma_launch<PP, 2, w4_warps(PP), false, 4>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end,       \
-                                                     seg_slot, indices, values, X, ldx, Y, ldy, partial, 0, s);
+    return tma_launch<PP, 2, w4_warps(PP), 4>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end,       \
+                                                     seg_slot, indices, values, X, ldx, Y, ldy, partial, s);
   switch (b / 4) {
     SVDREC_TMA4(9)
     SVDREC_TMA4(10)
@@ -530,8 +481,8 @@ int tma_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_se
                      int64_t ldy, double* partial, cudaStream_t s) {
 #define SVDREC_TMAF(PP)                                                                                             \
   case PP:                                                                                                          \
-    return tma_launch<PP, 2, 8, false, 2, float>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot,     \
-                                                 indices, values, X, ldx, Y, ldy, partial, 0, s);
+    return tma_launch<PP, 2, 8, 2, float>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot,     \
+                                                 indices, values, X, ldx, Y, ldy, partial, s);
   switch (b / 2) {
     SVDREC_TMAF(2)
     SVDREC_TMAF(4)
@@ -561,9 +512,9 @@ int tma_dispatch4_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_s
                       int64_t ldy, double* partial, cudaStream_t s) {
 #define SVDREC_TMA4F(PP)                                                                                         \
   case PP:                                                                                                       \
-    return tma_launch<PP, 2, w4f_warps(PP), false, 4, float>(xrows, nwarp, warp_seg, seg_row, seg_begin,         \
+    return tma_launch<PP, 2, w4f_warps(PP), 4, float>(xrows, nwarp, warp_seg, seg_row, seg_begin,         \
                                                               seg_end, seg_slot, indices, values, X, ldx, Y, ldy, \
-                                                              partial, 0, s);
+                                                              partial, s);
   switch (b / 4) {
     SVDREC_TMA4F(9)
     SVDREC_TMA4F(10)
@@ -618,7 +569,7 @@ int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin
               const int32_t* d_seg_slot, const int32_t* d_indices, const double* d_values, const double* d_X,
               int64_t ldx, int64_t xrows, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
               const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
-              const int32_t* d_warp_seg, double* d_partial, int32_t nhot, void* stream) {
+              const int32_t* d_warp_seg, double* d_partial, void* stream) {
   SVDREC_ARG(b >= 1 && ldx >= b && ldy >= b && nseg >= 0 && nlong >= 0, "spmm: bad arguments b=%d", b);
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
@@ -631,10 +582,8 @@ int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin
   // SVDREC_SPMM_KIND=0 forces the plain kernel (A/B measurements)
   static const int kind = getenv("SVDREC_SPMM_KIND") ? atoi(getenv("SVDREC_SPMM_KIND")) : 1;
   if (vec2 && b <= 32 && nwarp > 0 && d_warp_seg && kind != 0 && xrows < (1ll << 31)) {
-    rc = nhot > 0 ? tma_dispatch<2, 16>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
-                                        d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, nhot, s)
-                  : tma_dispatch<2, kW2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
-                                       d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, 0, s);
+    rc = tma_dispatch<2, kW2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                              d_values, d_X, ldx, d_Y, ldy, d_partial, s);
     if (rc) return rc;
     goto fixup;
   }
@@ -682,18 +631,7 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
                            const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
                            const int32_t* d_warp_seg, double* d_partial, void* stream) {
   return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
-                   ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, 0, stream);
-}
-
-extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
-                               const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_indices,
-                               const double* d_values, const double* d_X, int64_t ldx, int64_t xrows, double* d_Y,
-                               int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
-                               const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
-                               const int32_t* d_warp_seg, double* d_partial, int32_t nhot, void* stream) {
-  SVDREC_ARG(nhot >= 0, "spmm_hot: negative nhot");
-  return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
-                   ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, nhot, stream);
+                   ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, stream);
 }
 
 extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,

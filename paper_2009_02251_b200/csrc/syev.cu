@@ -324,8 +324,8 @@ int run_jacobi(int64_t rows, int k, const double* A, int64_t lda, double* W, dou
   if (k > 1 && rows <= kBRowsMax) {
     static int max_blocks_b = 0;
     const size_t smem = (size_t)2 * kBW * (kBRowsMax | 1) * 8;
+    SVDREC_CUDA(smem_attr_once(k_bjacobi, (int)smem));
     if (!max_blocks_b) {
-      SVDREC_CUDA(cudaFuncSetAttribute(k_bjacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
       SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, kBT, smem));
       max_blocks_b = per_sm * sm_count();

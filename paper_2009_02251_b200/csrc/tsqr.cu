@@ -290,14 +290,10 @@ namespace {
 // unless *gate != 0 (the CholeskyQR2 fast path flagged itself unreliable).
 int run_tsqr(const Plan& p, int64_t r, int32_t b, const double* d_A, int64_t lda, double* d_Q, int64_t ldq,
              double* d_R, char* w, const uint32_t* gate, cudaStream_t s) {
-  static bool attr_set = false;
   const size_t smem_f = (size_t)b * ((p.rcmax + 1) | 1) * 8;
   const size_t smem_q = 2 * smem_f;
-  if (!attr_set) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
-    SVDREC_CUDA(cudaFuncSetAttribute(k_buildq, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
-    attr_set = true;
-  }
+  SVDREC_CUDA(smem_attr_once(k_factor, 2 * kChunkBytes + 4096));
+  SVDREC_CUDA(smem_attr_once(k_buildq, 2 * kChunkBytes + 4096));
   const int nl = (int)p.lv.size();
   const double* in = d_A;
   int64_t ldin = lda;
@@ -336,11 +332,7 @@ int run_tsqr_gated(const Plan& p, int64_t r, int32_t b, const double* d_A, int64
     set_error("orth: TSQR tree deeper than %d levels", kMaxLevels);
     return SVDREC_E_UNSUPPORTED;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    SVDREC_CUDA(cudaFuncSetAttribute(k_tsqr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kChunkBytes + 4096));
-    attr_set = true;
-  }
+  SVDREC_CUDA(smem_attr_once(k_tsqr_coop, 2 * kChunkBytes + 4096));
   CoopLevels L{};
   L.nl = nl;
   int64_t maxnc = 1;

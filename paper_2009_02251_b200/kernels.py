@@ -8,8 +8,6 @@ copies.  Nothing here synchronises the device.
 """
 from __future__ import annotations
 
-import os
-
 import numpy as np
 import torch
 
@@ -127,18 +125,10 @@ def normal_fill(key: tuple[int, int], pos: torch.Tensor, rows: int, cols: int, o
     return out
 
 
-# SpMM with a shared-memory hot set (A @ X on the popularity-ranked CSR);
-# off by default: measured slower on the c3 bench (17.8 vs 16.9 ms per step),
-# SVDREC_SPMM_HOT=1 turns it on (A/B measurements)
-SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "0") == "1"
-
-
 def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> torch.Tensor:
-    """Y = A @ X for the CSR described by ``plan`` (a sparse.DeviceCSR).
-
-    When the CSR carries an item popularity order (the CSR of A: its columns
-    are items), the product runs on the ranked copy with X permuted to the
-    same order, the hottest rows of X staged in shared memory."""
+    """Y = A @ X for the CSR described by ``plan`` (a sparse.DeviceCSR):
+    the TMA-gather kernel of csrc/spmm.cu (``precision="fp32"``: its variant
+    gathering a float copy of X)."""
     ldx, ldy = _mat(X, "spmm.X"), _mat(Y, "spmm.Y")
     b = X.shape[1]
     if Y.shape[1] != b or X.shape[0] != plan.n or Y.shape[0] != plan.m:
@@ -159,23 +149,17 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
                  plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), *sched, ptr(part),
                  stream_handle())
         return Y
-    hot = SPMM_HOT and getattr(plan, "hot_items", None) is not None and b % 2 == 0 and b <= 32 and plan.nnz
-    if hot:
-        rind, rval, order = plan.ranked()
-        Xr = torch.empty(plan.n, b, dtype=F64, device=X.device)
-        torch.index_select(X, 0, order, out=Xr) if X.is_contiguous() else Xr.copy_(X.index_select(0, order))
-        with _span("spmm", nbytes):
-            call("svdrec_spmm_hot", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end),
-                 ptr(plan.seg_slot), ptr(rind), ptr(rval), ptr(Xr), b, plan.n, ptr(Y), ldy, b, plan.nlong,
-                 ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), plan.nwarp, ptr(plan.warp_seg), ptr(part),
-                 plan.n, stream_handle())
-        return Y
-    nwarp, wseg = plan.schedule(query("svdrec_spmm_warps_per_sm", b))
     with _span("spmm", nbytes):
-        call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
-             ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
-             ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(part), stream_handle())
+        _spmm_tma(plan, X, ldx, Y, ldy, b)
     return Y
+
+
+def _spmm_tma(plan, X, ldx, Y, ldy, b):
+    """The TMA-gather kernel (csrc/spmm.cu) on one CSR."""
+    nwarp, wseg = plan.schedule(query("svdrec_spmm_warps_per_sm", b))
+    call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
+         ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
+         ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(plan.partial(b)), stream_handle())
 
 
 def gemm_tn(X: torch.Tensor, Y: torch.Tensor, C: torch.Tensor | None = None, alpha: float = 1.0,

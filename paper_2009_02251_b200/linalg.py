@@ -9,7 +9,6 @@ libsvdrec_b200.so; without a CUDA device these raise
 """
 from __future__ import annotations
 
-import os
 from typing import NamedTuple
 
 import numpy as np
@@ -20,12 +19,6 @@ from ._lib import STATUS_NEAR_SINGULAR, STATUS_STREAM_SHORT, STATUS_ZERO_PIVOT, 
 from .sparse import SparseRatings
 
 ORTH_RANK_FLOOR = 1e-12  # linalg.py:16
-# hottest items handled as a dense block on the tensor cores in the SpMM
-# (sparse.HotColdSplit).  Off by default: at h = 256 (41 % of the headline's
-# ratings) A @ X 364 -> 351 us and A.T @ Y 338 -> 310 us, but the dense
-# products (86 / 77 us) cannot overlap the gather kernel, whose rings fill
-# every SM's shared memory, and the split's construction lands in e2e.
-DENSE_HOT = int(os.environ.get("SVDREC_SPMM_DENSE_HOT", "0"))
 EIG_FLOOR = 1e-14  # linalg.py:17
 MASK64 = (1 << 64) - 1
 
@@ -188,15 +181,7 @@ def sparse_dense_mul(A: SparseRatings, X, transpose_a: bool = False, out: torch.
     csr = d.AT if transpose_a else d.A
     if out is None:
         out = torch.empty(csr.m, t.shape[1], dtype=torch.float64, device=t.device)
-    split = d.hybrid(DENSE_HOT) if DENSE_HOT and t.shape[1] <= 32 else None
-    if split is None:
-        K.spmm(csr, t, out)
-    elif not transpose_a:  # A @ X = A_cold @ X + A_hot @ X[hot items]
-        K.spmm(split.A, t, out)
-        K.gemm_nn(split.dense, t.index_select(0, split.hot_items), out, alpha=1.0, beta=1.0)
-    else:  # A.T @ X: cold item rows by the SpMM, hot item rows = A_hot.T @ X
-        K.spmm(split.AT, t, out)
-        out.index_copy_(0, split.hot_items, K.gemm_tn(split.dense, t))
+    K.spmm(csr, t, out)
     return _out(out, host)
 
 

@@ -340,17 +340,6 @@ class DeviceRatings:
         self._init_from(csr, csr.device, csr.m, csr.n, csr.nnz, rating_min, rating_max)
         return self
 
-    def hybrid(self, h: int) -> "HotColdSplit | None":
-        """The split A = A_hot + A_cold by item popularity (built once, cached):
-        the ``h`` most rated items as a dense m x h block (products on the
-        FP64 tensor cores) and the rest as CSRs of A and A.T."""
-        if h <= 0 or self.n <= 2 * h or self.nnz == 0:
-            return None
-        hit = getattr(self, "_hybrid", None)
-        if hit is None or hit.h != h:
-            hit = self._hybrid = HotColdSplit(self, h)
-        return hit
-
     def check(self):
         """(any row not strictly increasing, all values finite, min, max) of
         the uploaded CSR -- the reference's constructor checks
@@ -412,32 +401,3 @@ class DeviceSparseRatings:
                             shape=(row1 - row0, A.n))
         return SparseRatings(csr, self.rating_min, self.rating_max)
 
-
-class HotColdSplit:
-    """A = A_hot + A_cold for the SpMM.  Under Zipf item popularity the few
-    hottest items carry a large share of the ratings (h = 256 of 26,744
-    items: ~42 % on the headline config): their columns form a dense m x h
-    block A_hot whose products A_hot @ X_hot and A_hot.T @ Y run on the FP64
-    tensor cores (svdrec_gemm_nn / svdrec_gemm_tn) at HBM speed, while the
-    gather-bound TMA SpMM only walks the cold ratings.  Columns keep their
-    item ids in the cold CSRs; ``hot_items`` maps the dense block's columns
-    to items."""
-
-    def __init__(self, d: "DeviceRatings", h: int):
-        A = d.A
-        dev = d.device
-        self.h = h
-        self.hot_items = A.hot_items[:h].to(torch.int64)
-        rank = A.item_rank
-        rows = torch.repeat_interleave(torch.arange(A.m, dtype=torch.int64, device=dev), A.indptr[1:] - A.indptr[:-1])
-        rk = rank[A.indices.to(torch.int64)].to(torch.int64)
-        hot = rk < h
-        self.dense = torch.zeros(A.m, h, dtype=torch.float64, device=dev)
-        self.dense[rows[hot], rk[hot]] = A.values[hot]
-        cold = ~hot
-        counts = torch.bincount(rows[cold], minlength=A.m)
-        indptr = torch.zeros(A.m + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(counts, 0, out=indptr[1:])
-        self.A = DeviceCSR(indptr, A.indices[cold], A.values[cold], (A.m, A.n))
-        self.AT = self.A.transposed()
-        self.hot_nnz = int(hot.sum().item())

@@ -150,3 +150,23 @@ def test_config0_cf_golden_and_split():
     np.testing.assert_allclose([t[1] for t in res.trace], g["c0_trace_mae"], rtol=1e-9)
     tp = O.predict_many(tr, res.T, 1.0, 5.0, te[0], te[1])
     np.testing.assert_allclose(tp[:, 0], g["c0_test_pred"], rtol=1e-9, atol=1e-9)
+
+
+def test_oracle_full_c1_pipeline_matches_reference():
+    """The oracle's Alg. 5 + Alg. 4 on BASELINE config 1 (6040 x 3706, 1M
+    ratings; 90/5/5 split) against the reference's own full run
+    (tests/golden/full_c1_1m.npz): same k and blocks, MAE trace 1e-9,
+    test MAE/RMSE 1e-9."""
+    from oracle import svdrec_oracle as O
+    from paper_2009_02251_b200 import synth
+
+    g = golden("full_c1_1m")
+    cfg = synth.CONFIGS["c1_1m"]
+    tr, va, te = synth.split_holdout(synth.generate(cfg), (0.9, 0.05, 0.05), seed=0)
+    lo, hi = cfg.bounds
+    res = O.auto_latent_factors(tr, va, lo, hi, block_size=20, passes=4, patience=2, min_improvement=1e-4, seed=0)
+    assert res.k == int(g["k"]) and len(res.trace) == int(g["blocks"])
+    np.testing.assert_allclose([t[1] for t in res.trace], g["trace_mae"], rtol=1e-9)
+    pred = O.predict_many(tr, res.T, lo, hi, te[0], te[1])[:, 0]
+    assert abs(np.abs(pred - te[2]).mean() - float(g["test_mae"])) <= 1e-9
+    assert abs(np.sqrt(np.mean((pred - te[2]) ** 2)) - float(g["test_rmse"])) <= 1e-9
