@@ -288,6 +288,17 @@ int svdrec_cf_predict_f32(int64_t nwork, const int64_t* d_work_start, const int3
 /* Ranked CSR for svdrec_cf_predict: d_out[t] = d_rank[d_indices[t]] (item ->
  * popularity rank, 0 = most rated); the caller then orders each row's
  * entries by rank (ascending), so every user's hot items form a prefix. */
+/* Alg. 4 for wide factors (k > 1024, which svdrec_cf_predict rejects): the
+ * same outputs, one CTA per user group.  Groups are runs of samples of one
+ * user: samples [group_offsets[g], group_offsets[g+1]) belong to user
+ * group_users[g]; d_indptr is the training CSR's row pointer (the ranked
+ * copy shares it); d_Yr the unit rows in rank order (n_items x ldy). */
+int svdrec_cf_predict_wide(int64_t ngroups, const int64_t* d_group_offsets, const int64_t* d_group_users,
+                           const int64_t* d_indptr, const int32_t* d_items, const int32_t* d_ranked_indices,
+                           const double* d_ranked_values, int32_t k, const double* d_Yr, int64_t ldy,
+                           const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
+                           double rating_min, double rating_max, double* d_value, double* d_raw,
+                           uint8_t* d_fallback, void* stream);
 int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,
                       void* stream);
 

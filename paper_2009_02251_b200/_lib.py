@@ -64,6 +64,8 @@ SIGNATURES = {
                                     _i32, _p, _i64, _p, _p, _p, _p, _p, _p]),
     "svdrec_cf_predict_f32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p, _i64, _p, _i64, _p, _f64, _f64, _f64,
                                         _i32, _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "svdrec_cf_predict_wide": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _i64, _p, _i64, _p, _f64, _f64,
+                                         _f64, _p, _p, _p, _p]),
     "svdrec_cf_relabel": (C.c_int, [_i64, _p, _p, _p, _p]),
     "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
     "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),

@@ -296,7 +296,7 @@ class _Samples:
 def _predict_device(A: SparseRatings, factors: LatentFactors, s: _Samples, gmean: float, precision: str = "fp64"):
     d = A.device(factors.Xn.device)
     return K.cf_predict(s.groups, s.users, s.items, d.A, factors.Yn, factors.Xn, factors.norm_device, gmean,
-                        A.rating_min, A.rating_max, s.plan_for(A), precision)
+                        A.rating_min, A.rating_max, s.plan_for(A), precision, group_users=s.group_users_dev)
 
 
 def predict_rating(A: SparseRatings, factors: LatentFactors, user: int, item: int) -> Prediction:

@@ -383,6 +383,90 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
   }  // dynamic loop over work items
 }
 
+// Wide factors (k > 1024, e.g. the factors of a fixed-precision QB at a
+// few thousand columns): one CTA per user group, the k columns in tiles of
+// kWideCols (4 per thread); per tile P_u, S_u are built in registers from
+// the user's rated unit rows and every sample's tile dot products are
+// block-reduced in a fixed order and accumulated in out_raw (numerator) and
+// out_val (denominator), finalised after the last tile.  Same arithmetic
+// and fallback rules as k_predict; deterministic.
+constexpr int kWideThreads = 256, kWideCols = 4 * kWideThreads;
+
+template <typename TY>
+__global__ void __launch_bounds__(kWideThreads) k_predict_wide(
+    int64_t ngroups, const int64_t* __restrict__ goff, const int64_t* __restrict__ guser,
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ items, const int32_t* __restrict__ rindices,
+    const double* __restrict__ rvalues, int k, const TY* __restrict__ Yr, int64_t ldy, const double* __restrict__ Xn,
+    int64_t ldn, const double* __restrict__ norm, double gmean, double lo, double hi, double* __restrict__ out_val,
+    double* __restrict__ out_raw, uint8_t* __restrict__ out_fb) {
+  __shared__ double red[2][kWideThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
+    const int64_t s0 = goff[gi], s1 = goff[gi + 1];
+    const int64_t u = guser[gi];
+    const int64_t r0 = indptr[u], deg = indptr[u + 1] - r0;
+    for (int c0 = 0; c0 < k; c0 += kWideCols) {
+      double P[4] = {0.0, 0.0, 0.0, 0.0}, S[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int64_t t = 0; t < deg; ++t) {
+        const double v = rvalues[r0 + t];
+        const TY* row = Yr + (int64_t)rindices[r0 + t] * ldy;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c = c0 + threadIdx.x + i * kWideThreads;
+          if (c < k) {
+            const double x = (double)row[c];
+            P[i] = fma(v, x, P[i]);
+            S[i] += x;
+          }
+        }
+      }
+      for (int64_t sidx = s0; sidx < s1; ++sidx) {
+        const double* xr = Xn + (int64_t)items[sidx] * ldn;
+        double num = 0.0, den = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c = c0 + threadIdx.x + i * kWideThreads;
+          if (c < k) {
+            num = fma(xr[c], P[i], num);
+            den = fma(xr[c], S[i], den);
+          }
+        }
+        num = warp_sum(num);
+        den = warp_sum(den);
+        if (lane == 0) {
+          red[0][wid] = num;
+          red[1][wid] = den;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double tn = 0.0, td = 0.0;
+          for (int w = 0; w < kWideThreads / 32; ++w) {
+            tn += red[0][w];
+            td += red[1][w];
+          }
+          out_raw[sidx] = c0 ? out_raw[sidx] + tn : tn;
+          out_val[sidx] = c0 ? out_val[sidx] + td : td;
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      double vsum = 0.0;
+      for (int64_t t = 0; t < deg; ++t) vsum += rvalues[r0 + t];
+      const double mean = deg > 0 ? vsum / (double)deg : gmean;
+      for (int64_t sidx = s0; sidx < s1; ++sidx) {
+        const double num = out_raw[sidx], den = out_val[sidx];
+        const bool fb = norm[items[sidx]] == 0.0 || deg == 0 || fabs(den) < kWeightFloor;
+        const double raw = fb ? mean : num / den;
+        out_raw[sidx] = raw;
+        out_val[sidx] = fmin(fmax(raw, lo), hi);
+        out_fb[sidx] = fb ? 1 : 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Ranked copy of a CSR for the scoring kernel, step 1: column j -> rank[j].
 // Step 2 (the caller: sparse.DeviceCSR.ranked) orders every row by rank
 // with one device radix sort of (row, rank) keys; ranks are unique per row.
@@ -457,7 +541,7 @@ int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d
                     void* stream) {
   SVDREC_ARG(nwork >= 0 && k >= 1 && ldn >= k && ldy >= k && n_items >= 0, "cf_predict: bad arguments");
   if (k > 1024) {
-    set_error("cf_predict: latent dimension %d > 1024 unsupported", k);
+    set_error("cf_predict: latent dimension %d > 1024: use svdrec_cf_predict_wide", k);
     return SVDREC_E_UNSUPPORTED;
   }
   if (nwork == 0) return 0;
@@ -541,6 +625,22 @@ extern "C" int svdrec_cf_predict_f32(int64_t nwork, const int64_t* d_work_start,
   return cf_predict_impl<float>(nwork, d_work_start, d_work_meta, d_items, d_ranked_indices, d_ranked_values, k,
                                 d_Yr, ldy, d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, n_items, d_done,
                                 ndone, d_partial, d_counter, d_value, d_raw, d_fallback, stream);
+}
+
+extern "C" int svdrec_cf_predict_wide(int64_t ngroups, const int64_t* d_group_offsets, const int64_t* d_group_users,
+                                      const int64_t* d_indptr, const int32_t* d_items,
+                                      const int32_t* d_ranked_indices, const double* d_ranked_values, int32_t k,
+                                      const double* d_Yr, int64_t ldy, const double* d_Xn, int64_t ldn,
+                                      const double* d_norm, double global_mean, double rating_min, double rating_max,
+                                      double* d_value, double* d_raw, uint8_t* d_fallback, void* stream) {
+  SVDREC_ARG(ngroups >= 0 && k >= 1 && ldn >= k && ldy >= k, "cf_predict_wide: bad arguments");
+  if (ngroups == 0) return 0;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  const unsigned grid = (unsigned)(ngroups < cap ? ngroups : cap);
+  k_predict_wide<double><<<grid, kWideThreads, 0, as_stream(stream)>>>(
+      ngroups, d_group_offsets, d_group_users, d_indptr, d_items, d_ranked_indices, d_ranked_values, k, d_Yr, ldy,
+      d_Xn, ldn, d_norm, global_mean, rating_min, rating_max, d_value, d_raw, d_fallback);
+  return check_launch("cf_predict_wide");
 }
 
 extern "C" int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,

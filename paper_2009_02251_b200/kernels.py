@@ -361,7 +361,7 @@ def inv_sqrt(G: torch.Tensor, status: torch.Tensor, iters: torch.Tensor | None =
 
 def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, csr, Yn: torch.Tensor,
                Xn: torch.Tensor, norm: torch.Tensor, gmean: float, lo: float, hi: float, plan,
-               precision: str = "fp64"):
+               precision: str = "fp64", group_users: torch.Tensor | None = None):
     """Alg. 4 over user-grouped samples.  ``csr`` is a sparse.DeviceCSR (its
     ranked copy is used); ``plan`` is a cf.WorkPlan (work items, per-group
     chunk info, completion counters, counter).  ``precision="fp32"`` stores
@@ -373,7 +373,7 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
         raise ValueError(f"precision must be 'fp64' or 'fp32', not {precision!r}")
     rind, rval, order = csr.ranked()
     n, k = Yn.shape
-    f32 = precision == "fp32"
+    f32 = precision == "fp32" and k <= 1024  # the wide kernel gathers fp64 rows
     # rank order + a zero row; rows zero-padded to a 16-B multiple (vector loads)
     ldy = (k + 3) // 4 * 4 if f32 else (k + 1) // 2 * 2
     Yr = torch.empty(n + 1, ldy, dtype=torch.float32 if f32 else F64, device=Yn.device)
@@ -392,6 +392,12 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     # rated item's unit row (k values, L2/shared-memory resident); per
     # sample its ids, norm, Xn row and the three outputs
     nbytes = getattr(plan, "rated", 0) * (12 + (4 if f32 else 8) * k) + ns * (8 * k + 4 + 4 + 8 + 17)
+    if k > 1024:  # wide factors: the k-tiled kernel (fp64 rows)
+        with _span("cf_predict", nbytes):
+            call("svdrec_cf_predict_wide", groups.numel() - 1, ptr(groups), ptr(group_users), ptr(csr.indptr),
+                 ptr(items), ptr(rind), ptr(rval), k, ptr(Yr), ldy, ptr(Xn), ldn, ptr(norm), float(gmean), float(lo),
+                 float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
+        return val, raw, fb
     common = (plan.nwork, ptr(plan.start), ptr(plan.meta), ptr(items), ptr(rind), ptr(rval), k)
     tail = (ptr(norm), float(gmean), float(lo), float(hi), n, ptr(plan.done), plan.ndone, ptr(plan.partial(k)),
             ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
