@@ -12,10 +12,18 @@ device-timed seconds of one step (lower is better).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
---impl reference times the CPU oracle (a numpy restatement of the
-reference, oracle/svdrec_oracle.py) on a bounded sample of the same
-workload and extrapolates to the full step (the reference's per-sample
-Python scoring loop makes a full run take hours).
+--impl reference times the CPU port of the reference (the oracle,
+oracle/svdrec_oracle.py: numpy/scipy orchestration statement by statement,
+with the reference's CSR products and its per-sample Alg. 4 loop in
+threaded C, oracle/cpu_port.c + cf_score.c) on the host cores: full runs
+of the same job, as many as fit a time budget (BENCH_REF_BUDGET_S, default
+240 s; at least one).  Nothing is extrapolated.  The unmodified reference
+package itself (single-threaded Python scoring loop) took 1,568.6 s on
+this workload in the build container (profiles/r2_reference_c3_20m.json);
+that recorded figure is carried in the line as ``reference_package_recorded``.
+
+--gpus N without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (one GPU each, NCCL).
 """
 from __future__ import annotations
 
@@ -38,9 +46,6 @@ CONFIG = "c3_20m"
 BLOCK, PASSES, PATIENCE, MIN_IMPROVEMENT, SEED, K_CAP = 20, 4, 2, 1e-4, 0, 400
 SPLIT = (0.9, 0.05, 0.05)
 METRIC = "time-to-converged-k (s), adaptive-PCA CF pipeline, 138k x 27k / 20M nnz"
-# blocks the pipeline runs on this workload (deterministic; measured by the
-# b200 arm, used by the reference arm's extrapolation)
-REF_BLOCKS = 12
 
 
 def _dist():
@@ -62,7 +67,7 @@ def _workload():
 
 def _config_dict(cfg, tr):
     return {
-        "workload": f"{CONFIG}: ML-20M-shaped synthetic {cfg.users}x{cfg.items}, {cfg.nnz} ratings "
+        "workload": f"{CONFIG}: synthetic {cfg.users}x{cfg.items}, {cfg.nnz} ratings "
                     f"(train {tr.nnz}), rank {cfg.rank}, Zipf({cfg.zipf}) items, half stars",
         "pipeline": "auto_latent_factors (Alg. 5, ValidationMae stop) + test MAE/RMSE",
         "block_size": BLOCK, "passes": PASSES, "power": (PASSES - 2) // 2, "patience": PATIENCE,
@@ -178,68 +183,81 @@ def make_clocks(index: int) -> Clocks:
     return Clocks(index)
 
 
-def cpu_estimate(tr, va, te, nblocks: int, n_samples: int = 600):
-    """Time the oracle on a bounded sample and extrapolate to the full step.
-
-    Measured: the oracle's first two QB blocks (K = 20, 40) on the full
-    train matrix, latent_T at K = 20 / 40, and Alg. 4 scoring of
-    ``n_samples`` validation samples at K = 20 / 40.  Each cost is
-    extrapolated linearly in K to the nblocks of the real run; scoring cost
-    is scaled to the full validation (per block) and test (once) sets.
-    """
+def cpu_port_run(tr, va, te, lo, hi, threads: int | None = None):
+    """One full run of the job on the CPU port of the reference: the
+    oracle's Alg. 5 pipeline (auto_latent_factors with the bench settings)
+    + test scoring, with its CSR products and per-sample Alg. 4 loop on
+    ``threads`` host threads (all of this process's CPUs by default) and
+    BLAS single-threaded (its spinning workers would otherwise contend with
+    the C kernels' threads: 3.5x slower measured on c1).  Returns (seconds,
+    threads, summary)."""
     from oracle import svdrec_oracle as O
     import threadpoolctl
 
-    t_qb, t_lat, t_ps = [], [], []
-    gen = O.pass_blocks(tr, BLOCK, PASSES, O.Stream(SEED))
-    sub = (va[0][:n_samples], va[1][:n_samples])
-    t_all = time.perf_counter()
-    for _ in range(2):
-        t = time.perf_counter()
-        s = next(gen)
-        t_qb.append(time.perf_counter() - t)
-        t = time.perf_counter()
-        T = O.latent_T(s.B)
-        t_lat.append(time.perf_counter() - t)
-        t = time.perf_counter()
-        O.predict_many(tr, T, 0.5, 5.0, *sub)
-        t_ps.append((time.perf_counter() - t) / n_samples)
-    measured = time.perf_counter() - t_all
+    with threadpoolctl.threadpool_limits(1):
+        nt = O.use_c_backend(threads)
+        try:
+            t = time.perf_counter()
+            res = O.auto_latent_factors(tr, va, lo, hi, block_size=BLOCK, passes=PASSES, patience=PATIENCE,
+                                        min_improvement=MIN_IMPROVEMENT, seed=SEED, max_rank=K_CAP)
+            p = O.predict_many(tr, res.T, lo, hi, te[0], te[1])
+            dt = time.perf_counter() - t
+        finally:
+            O.use_c_backend(0)
+    e = p[:, 0] - te[2]
+    return dt, nt, {"k": int(res.k), "blocks": len(res.trace), "test_mae": float(np.abs(e).mean()),
+                    "test_rmse": float(np.sqrt((e * e).mean()))}
 
-    def at(vals, k):  # linear in K through the two measured points (K = 20, 40)
-        return max(vals[0] + (vals[1] - vals[0]) * (k - BLOCK) / BLOCK, vals[0])
 
-    nv, nt = len(va[0]), len(te[0])
-    total = 0.0
-    for l in range(1, nblocks + 1):
-        k = l * BLOCK
-        total += at(t_qb, k) + at(t_lat, k) + nv * at(t_ps, k)
-    total += nt * at(t_ps, nblocks * BLOCK)
-    info = threadpoolctl.threadpool_info()
-    cores = max([i.get("num_threads", 1) for i in info] + [1])
-    sample = (f"oracle: 2 QB blocks on the full train matrix + latent_T + Alg. 4 scoring of {n_samples} "
-              f"validation samples at K=20,40 ({measured:.1f} s measured); extrapolated linearly in K to "
-              f"{nblocks} blocks x {nv} validation + {nt} test samples")
-    return total, cores, sample, measured
+def _cpu_sample_text(nt, nv, nte, blocks):
+    return (f"one full run of the job (not extrapolated): {blocks} QB blocks + {blocks} validation scorings of {nv} "
+            f"samples + test scoring of {nte} samples, by the oracle port (numpy/scipy orchestration, CSR products "
+            f"and the per-sample Alg. 4 loop in C on {nt} threads, BLAS 1 thread)")
+
+
+def _recorded_reference():
+    p = ROOT / "profiles" / f"r2_reference_{CONFIG}.json"
+    if not p.is_file():
+        return None
+    r = json.loads(p.read_text())
+    return {"value": r.get("total_s"), "unit": "s", "host_cpus": r.get("host_cpus"), "k": r.get("k"),
+            "test_rmse": r.get("test_rmse"), "source": f"profiles/{p.name}",
+            "note": "the unmodified reference package (per-sample Python scoring loop), run once in the build "
+                    "container; it cannot run on the GPU box (no /root/reference there)"}
 
 
 def run_reference(args):
-    ws, rank, _ = _dist()
-    if rank != 0:
+    _, rank, _ = _dist()
+    if rank != 0:  # rank 0 alone runs the CPU reference arm
         return
-    cfg, M, tr, va, te, _ = _workload()
-    nblocks = args.blocks or REF_BLOCKS or 6
-    vals = []
-    for i in range(args.warmup + args.steps):
-        total, cores, sample, _ = cpu_estimate(tr, va, te, nblocks, n_samples=300 if i < args.warmup else 600)
-        if i >= args.warmup:
-            vals.append(total)
-    v = float(np.median(vals))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+    cfg, M, tr, va, te, gen_s = _workload()
+    lo, hi = cfg.bounds
+    # warm-up: the same pipeline on config 0's small workload (pages in the
+    # code paths and libraries; nothing is cached across runs)
+    from paper_2009_02251_b200 import synth
+    c0 = synth.CONFIGS["c0_100k"]
+    s_tr, s_va, s_te = synth.split_holdout(synth.generate(c0), SPLIT, seed=0)
+    for _ in range(args.warmup):
+        cpu_port_run(s_tr, s_va, s_te, *c0.bounds)
+    budget = float(os.environ.get("BENCH_REF_BUDGET_S", "240"))
+    runs, info, nt = [], {}, 1
+    while len(runs) < args.steps:
+        dt, nt, info = cpu_port_run(tr, va, te, lo, hi)
+        runs.append(dt)
+        if sum(runs) + dt > budget:
+            break
+    v = float(statistics.median(runs))
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": args.gpus,
+            "steps": len(runs), "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config_dict(cfg, tr),
-            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample},
-            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "runs_s": [round(x, 3) for x in runs], "result": info,
+            "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": nt, "kind": "port",
+                             "sample": _cpu_sample_text(nt, len(va[0]), len(te[0]), info.get("blocks"))
+                                       + f"; median of {len(runs)} run(s) within a {budget:.0f} s budget"},
+            "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_package_recorded": _recorded_reference(),
+            "setup": {"generate_split_s": round(gen_s, 2)}}
     print(json.dumps(line), flush=True)
 
 
@@ -397,25 +415,38 @@ def run_b200(args):
     traffic = json.loads(traffic_p.read_text()) if traffic_p.is_file() else {}
 
     def roof(name, kernel, l2_ceiling, l2_note):
-        c, ms, nbytes = prof.get(name, (0, 0.0, 0))
-        ach = (nbytes / (ms / 1e3)) / 1e9 if ms > 0 else None
+        """HBM roofline of one kernel: achieved = its compulsory HBM bytes
+        (inputs read once, outputs written once; kernels.py spans) over its
+        CUDA-event time in the profiled step.  The gathered bytes (every
+        fetched row, wherever it is served from) are reported beside it,
+        against the measured L2 random-gather ceiling."""
+        c, ms, hbm_b, gath_b = prof.get(name, (0, 0.0, 0, 0))
+        sec = ms / 1e3
+        ach = hbm_b / sec / 1e9 if sec > 0 else None
+        g_rate = (hbm_b + gath_b) / sec / 1e9 if sec > 0 else None
         tr_ = traffic.get(name, {}).get("dram_bytes_per_launch")
         return {"kernel": kernel, "bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
                 "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": tr_,
                 "traffic_source": f"ncu --set full, profiles/traffic.json ({traffic[name]['launches']} launches)"
-                if tr_ else None,
-                "peak_source": peak_src, "calls_per_step": c // psteps,
-                "algorithmic_bytes_per_call": int(nbytes / max(c, 1)), "ms_per_step": round(ms / psteps, 3),
-                "l2_gather": {"ceiling_GBps": l2_ceiling, "frac": round(ach / l2_ceiling, 4) if ach else None,
-                              "note": l2_note}}
+                if tr_ else None, "peak_source": peak_src,
+                "algorithmic_bytes_per_call": int(hbm_b / max(c, 1)),
+                "algorithmic_bytes": "compulsory HBM bytes: CSR once, dense operands once, outputs once",
+                "calls_per_step": c // psteps, "ms_per_step": round(ms / psteps, 3),
+                "us_per_call": round(ms * 1e3 / max(c, 1), 1),
+                "gathered": {"bytes_per_call": int(gath_b / max(c, 1)), "GBps": round(g_rate, 1) if g_rate else None,
+                             "l2_gather_ceiling_GBps": l2_ceiling,
+                             "frac_of_l2_ceiling": round(g_rate / l2_ceiling, 4) if g_rate else None,
+                             "note": l2_note}}
 
-    # dominant kernel: the CF scoring pass (its gathers are served by L2 /
-    # shared memory, so the HBM fraction exceeds 1; the L2 gather ceiling
-    # measured by tools/probe_l2bw.cu is the meaningful bound)
     roof_cf = roof("cf_predict", "svdrec_cf_predict (k_predict<R>)", 18904.6,
-                   "random 1920-B row gathers from L2, 32 warps/SM (tools/probe_l2bw.cu on B200)")
+                   "CSR stream + every gathered item row; ceiling: random 1920-B row gathers from L2, 32 warps/SM "
+                   "(tools/probe_l2bw.cu on B200)")
     roof_spmm = roof("spmm", "svdrec_spmm (k_spmm_tma: TMA gather4 pipeline)", 7799.0,
-                     "random 160-B row gathers from L2, 64 warps/SM (tools/probe_l2bw.cu on B200)")
+                     "CSR stream + every gathered row of X; ceiling: random 160-B row gathers from L2, 64 warps/SM "
+                     "(tools/probe_l2bw.cu on B200)")
+    # the line's roofline is the kernel with the larger share of the step
+    dominant, other = (roof_cf, roof_spmm) if roof_cf["ms_per_step"] >= roof_spmm["ms_per_step"] else \
+        (roof_spmm, roof_cf)
     breakdown = {k: {"calls": v[0] // psteps, "ms": round(v[1] / psteps, 3),
                      "share": round(v[1] / (sum(x[1] for x in prof.values()) or 1), 4)} for k, v in prof.items()}
 
@@ -429,8 +460,9 @@ def run_b200(args):
         "config": _config_dict(cfg, tr),
         "k": int(f.k), "blocks": nb, "test_mae": mae, "test_rmse": rmse, "val_mae": min(e.mae for e in trace),
         "step_times_s": [round(t, 6) for t in times],
-        "roofline": roof_cf,
-        "roofline_spmm": roof_spmm,
+        "roofline": dominant,
+        "roofline_other": other,
+        "spmm_hbm_GBps": roof_spmm["achieved"],
         "kernel_breakdown": breakdown,
         "e2e": {"value": round(statistics.median(e2e_times), 6), "unit": "s", "runs_s": [round(t, 4) for t in e2e_times], "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
@@ -441,24 +473,44 @@ def run_b200(args):
         "setup": {"generate_split_s": round(gen_s, 2)},
     }
     if ws == 1 and not args.no_cpu_baseline:
-        total, cores, sample, _ = cpu_estimate(tr, va, te, nb)
+        total, cores, info = cpu_port_run(tr, va, te, lo, hi)
         line["cpu_baseline"] = {"value": round(total, 3), "unit": "s", "cores": cores, "kind": "port",
-                                "sample": sample}
+                                "sample": _cpu_sample_text(cores, len(va[0]), len(te[0]), info["blocks"]),
+                                "result": info, "reference_package_recorded": _recorded_reference()}
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
 
 
+def _spawn(nproc: int) -> int:
+    """Re-launch this command under torch.distributed.run with ``nproc``
+    ranks on 127.0.0.1 (one GPU per rank); returns its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
+    global CONFIG
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--config", default=CONFIG, help="workload (default: the headline c3_20m; smaller ones for tests)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--blocks", type=int, default=None, help="reference arm: block count to extrapolate to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the fp32-variant timing")
     args = ap.parse_args()
+    CONFIG = args.config
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args.gpus))
+    ws = _dist()[0]
+    if ws != args.gpus and args.impl != "reference":
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args)
     else:

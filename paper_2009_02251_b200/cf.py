@@ -378,13 +378,15 @@ def _count(samples) -> int:
 
 
 def _local_err_sums(A: ShardedRatings, factors, s: _Samples, out: torch.Tensor, precision: str = "fp64") -> torch.Tensor:
-    """(sum |e|, sum e^2) over this rank's samples, then all-reduced."""
+    """(sum |e|, sum e^2) over this rank's samples, then all-reduced on the
+    scoring communicator (A.score_comm: scoring may run on a side stream,
+    apart from the QB chain's collectives on A.comm)."""
     if s.n:
         val, _, _ = _predict_device(A.local, factors, s, A.global_mean, precision)
         K.err_sum(val, s.truth, out=out)
     else:
         out.zero_()
-    return A.comm.all_reduce_(out)
+    return A.score_comm.all_reduce_(out)
 
 
 def _sharded_errors(A: ShardedRatings, factors, s, precision: str = "fp64"):

@@ -17,16 +17,20 @@ from ._lib import call, ptr, query, scratch, stream_handle
 F64 = torch.float64
 
 # Optional live instrumentation: when ``PROFILE`` is a list, every wrapper
-# below appends (name, start_event, end_event, algorithmic_bytes) recorded
-# on the launching stream.  bench.py uses it for the roofline numbers.
+# below appends (name, start_event, end_event, hbm_bytes, gathered_bytes)
+# recorded on the launching stream.  ``hbm_bytes`` are the launch's
+# compulsory HBM bytes (every input byte read once, every output byte
+# written once); ``gathered_bytes`` (gather kernels only) count each
+# gathered row every time it is fetched, whether L2, L1 or shared memory
+# serves it.  bench.py uses them for the roofline numbers.
 PROFILE: list | None = None
 
 
 class _span:
-    __slots__ = ("name", "nbytes", "e0")
+    __slots__ = ("name", "nbytes", "gathered", "e0")
 
-    def __init__(self, name: str, nbytes: int = 0):
-        self.name, self.nbytes, self.e0 = name, nbytes, None
+    def __init__(self, name: str, nbytes: int = 0, gathered: int = 0):
+        self.name, self.nbytes, self.gathered, self.e0 = name, nbytes, gathered, None
 
     def __enter__(self):
         if PROFILE is not None:
@@ -38,16 +42,16 @@ class _span:
         if self.e0 is not None and exc[0] is None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
-            PROFILE.append((self.name, self.e0, e1, self.nbytes))
+            PROFILE.append((self.name, self.e0, e1, self.nbytes, self.gathered))
         return False
 
 
 def profile_summary(records) -> dict:
-    """{name: (calls, total_ms, total_algorithmic_bytes)} after a sync."""
+    """{name: (calls, total_ms, total_hbm_bytes, total_gathered_bytes)} after a sync."""
     out: dict = {}
-    for name, e0, e1, nb in records:
-        c, t, b = out.get(name, (0, 0.0, 0))
-        out[name] = (c + 1, t + e0.elapsed_time(e1), b + nb)
+    for name, e0, e1, nb, ng in records:
+        c, t, b, g = out.get(name, (0, 0.0, 0, 0))
+        out[name] = (c + 1, t + e0.elapsed_time(e1), b + nb, g + ng)
     return out
 
 
@@ -134,22 +138,23 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
     if Y.shape[1] != b or X.shape[0] != plan.n or Y.shape[0] != plan.m:
         raise ValueError(f"spmm: shape mismatch A{(plan.m, plan.n)} X{tuple(X.shape)} Y{tuple(Y.shape)}")
     part = plan.partial(b)
-    # algorithmic bytes: per nonzero its CSR entry (12 B) and the gathered
-    # row of X (8b, L2 / shared-memory resident); per output row 8b written
-    nbytes = plan.nnz * (12 + 8 * b) + plan.m * b * 8
+    # compulsory HBM bytes: the CSR once (12 B per nonzero + row pointers),
+    # X once, Y written once; gathered: one X row (8b B) per nonzero
+    nbytes = plan.nnz * 12 + (plan.m + 1) * 8 + plan.n * b * 8 + plan.m * b * 8
+    gathered = plan.nnz * 8 * b
     if precision == "fp32" and b % 4 == 0 and b <= 64 and ldy % (2 if b <= 32 else 4) == 0 and plan.nnz:
         # fp32 variant: X stored as float (a rounded copy), fp64 values / accumulation / Y
         X32 = torch.empty(X.shape[0], b, dtype=torch.float32, device=X.device)
         X32.copy_(X)
         nw, ws = plan.schedule(query("svdrec_spmm_x32_warps_per_sm", b))
         sched = (nw, ptr(ws))
-        with _span("spmm", plan.nnz * (12 + 4 * b) + plan.m * b * 8):
+        with _span("spmm", plan.nnz * 12 + (plan.m + 1) * 8 + plan.n * b * 4 + plan.m * b * 8, plan.nnz * 4 * b):
             call("svdrec_spmm_x32", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end),
                  ptr(plan.seg_slot), ptr(plan.indices), ptr(plan.values), ptr(X32), b, plan.n, ptr(Y), ldy, b,
                  plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), *sched, ptr(part),
                  stream_handle())
         return Y
-    with _span("spmm", nbytes):
+    with _span("spmm", nbytes, gathered):
         _spmm_tma(plan, X, ldx, Y, ldy, b)
     return Y
 
@@ -388,12 +393,16 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     val = torch.empty(ns, dtype=F64, device=Yn.device)
     raw = torch.empty(ns, dtype=F64, device=Yn.device)
     fb = torch.empty(ns, dtype=torch.uint8, device=Yn.device)
-    # algorithmic bytes: per streamed rating its CSR entry (12 B) and the
-    # rated item's unit row (k values, L2/shared-memory resident); per
-    # sample its ids, norm, Xn row and the three outputs
-    nbytes = getattr(plan, "rated", 0) * (12 + (4 if f32 else 8) * k) + ns * (8 * k + 4 + 4 + 8 + 17)
+    # compulsory HBM bytes: the scored users' ranked CSR rows once (12 B per
+    # rating), the two n x k item tables once, per sample its item id, norm
+    # and the three outputs; gathered: one item row per streamed rating and
+    # one Xn row per sample
+    es = 4 if f32 else 8
+    rated = getattr(plan, "rated", 0)
+    nbytes = rated * 12 + n * k * (es + 8) + ns * (4 + 8 + 17)
+    gathered = rated * es * k + ns * 8 * k
     if k > 1024:  # wide factors: the k-tiled kernel (fp64 rows)
-        with _span("cf_predict", nbytes):
+        with _span("cf_predict", nbytes, gathered):
             call("svdrec_cf_predict_wide", groups.numel() - 1, ptr(groups), ptr(group_users), ptr(csr.indptr),
                  ptr(items), ptr(rind), ptr(rval), k, ptr(Yr), ldy, ptr(Xn), ldn, ptr(norm), float(gmean), float(lo),
                  float(hi), ptr(val), ptr(raw), ptr(fb), stream_handle())
@@ -401,7 +410,7 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     common = (plan.nwork, ptr(plan.start), ptr(plan.meta), ptr(items), ptr(rind), ptr(rval), k)
     tail = (ptr(norm), float(gmean), float(lo), float(hi), n, ptr(plan.done), plan.ndone, ptr(plan.partial(k)),
             ptr(plan.counter), ptr(val), ptr(raw), ptr(fb), stream_handle())
-    with _span("cf_predict", nbytes):
+    with _span("cf_predict", nbytes, gathered):
         if f32:
             call("svdrec_cf_predict_f32", *common, ptr(Yr), ldy, ptr(Xn), ldn, *tail)
         else:

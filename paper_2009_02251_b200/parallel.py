@@ -56,6 +56,9 @@ def max_over_ranks(value: float, device: torch.device | None = None) -> float:
     return float(t.item())
 
 
+_SIBLINGS: dict = {}
+
+
 class Comm:
     """The process group the shards of one matrix live on.
 
@@ -87,6 +90,23 @@ class Comm:
                 dist.all_reduce(c, group=self.group)
                 t.copy_(c)
         return t
+
+    def sibling(self) -> "Comm":
+        """A second communicator over the same ranks (its own process group,
+        hence its own NCCL communicator), for collectives issued from
+        another CUDA stream: the CF scoring's error sums run on the scoring
+        side stream while the QB chain's all-reduces run on the main one,
+        and two streams must not share one NCCL communicator.  Created
+        collectively on first use (every rank constructs its shards in the
+        same order) and cached per parent group."""
+        if self.world == 1:
+            return self
+        key = id(self.group) if self.group is not None else 0
+        hit = _SIBLINGS.get(key)
+        if hit is None:
+            ranks = dist.get_process_group_ranks(self.group) if self.group is not None else None
+            hit = _SIBLINGS[key] = Comm(dist.new_group(ranks=ranks, backend=self.backend))
+        return hit
 
     def all_gather(self, t: torch.Tensor) -> list[torch.Tensor]:
         if self.world == 1:
@@ -139,6 +159,7 @@ class ShardedRatings:
     def __init__(self, local: SparseRatings, row0: int, m: int, comm: Comm | None = None,
                  offsets: np.ndarray | None = None) -> None:
         self.comm = comm or Comm()
+        self.score_comm = self.comm.sibling()  # CF scoring collectives (side stream)
         self.local = local
         self.row0 = int(row0)
         self.row1 = self.row0 + local.m
@@ -200,8 +221,42 @@ class ShardedRatings:
         """HBM image of the LOCAL rows (A_r and A_r.T)."""
         return self.local.device(device)
 
-    def transposed(self):
-        raise NotImplementedError("a row-sharded matrix transposes to a column-sharded one; shard A.T instead")
+    def transposed(self) -> "ColumnShardedView":
+        """A.T, column-sharded: the same shards seen through their device
+        transposes (no data moves)."""
+        return ColumnShardedView(self)
+
+
+class ColumnShardedView:
+    """A.T of a row-sharded A: n x m with the m columns sharded (this rank
+    holds columns [row0, row1), i.e. A_r.T from the local HBM image).  The
+    QB engine over it (rsvd._ColShardedQbEngine) keeps the n-side (Q, the
+    sketches A.T Omega) replicated and the m-side (B.T = A Q) sharded; its
+    exchanges are the all-reduces of A_r.T X_r (n x b), of B.T X (k x b),
+    of the m-side Grams (b x b) and of B_l's row energies."""
+
+    def __init__(self, base: ShardedRatings) -> None:
+        from .sparse import TransposedRatings
+
+        self.base = base
+        self.local = TransposedRatings(base.local)  # n x m_r
+        self.comm = base.comm
+        self.frob_sq = base.frob_sq
+        self.rating_min, self.rating_max = base.rating_min, base.rating_max
+
+    shape = property(lambda self: (self.base.n, self.base.m))
+    m = property(lambda self: self.base.n)
+    n = property(lambda self: self.base.m)
+    nnz = property(lambda self: self.base.nnz)
+    world = property(lambda self: self.base.world)
+    row0 = property(lambda self: self.base.row0)
+    row1 = property(lambda self: self.base.row1)
+
+    def device(self, device=None):
+        return self.local.device(device)
+
+    def transposed(self) -> ShardedRatings:
+        return self.base
 
 
 def sharded_orth(Y: torch.Tensor, dst: torch.Tensor, comm: Comm, m_global: int, passes: int = 3,
@@ -238,5 +293,5 @@ def local_samples(samples, row0: int, row1: int):
     return u[keep] - row0, i[keep], r[keep]
 
 
-__all__ = ["Comm", "ShardedRatings", "env_ranks", "local_samples", "max_over_ranks", "row_partition",
+__all__ = ["ColumnShardedView", "Comm", "ShardedRatings", "env_ranks", "local_samples", "max_over_ranks", "row_partition",
            "sharded_orth"]

@@ -27,8 +27,8 @@ from . import kernels as K
 from ._lib import STATUS_NEAR_SINGULAR, STATUS_STREAM_SHORT, STATUS_ZERO_PIVOT
 from .linalg import (EIG_FLOOR, GaussianStream, NearSingularError, RankDeficientError, SvdTriplet, _check_rank,
                      sparse_dense_mul)
-from .parallel import Comm, ShardedRatings, sharded_orth
-from .sparse import SparseRatings
+from .parallel import ColumnShardedView, Comm, ShardedRatings, sharded_orth
+from .sparse import SparseRatings, TransposedRatings
 
 F64 = torch.float64
 
@@ -149,21 +149,24 @@ class _QbEngine:
             raise ValueError(f"precision must be 'fp64' or 'fp32', not {precision!r}")
         if isinstance(A, ShardedRatings) and A.world > 1:
             E = _ShardedQbEngine(A, b, stream, cap)
+        elif isinstance(A, ColumnShardedView) and A.world > 1:
+            E = _ColShardedQbEngine(A, b, stream, cap)
         else:
-            E = _QbEngine(A.local if isinstance(A, ShardedRatings) else A, b, stream, cap)
+            E = _QbEngine(A.local if isinstance(A, (ShardedRatings, ColumnShardedView)) else A, b, stream, cap)
         E.precision = precision
         return E
 
     def __init__(self, A: SparseRatings, b: int, stream: GaussianStream, cap: int, global_m: int | None = None,
-                 frob_sq: float | None = None):
+                 frob_sq: float | None = None, global_n: int | None = None):
         self.A = A
         self.dev = stream.device
         self.d = A.device(self.dev)
         self.m, self.n = A.shape  # rows held here (all of them unless sharded)
         self.gm = self.m if global_m is None else int(global_m)
+        self.gn = self.n if global_n is None else int(global_n)
         self.b = b
         self.stream = stream
-        cap = max(b, min(cap, min(self.gm, self.n)))
+        cap = max(b, min(cap, min(self.gm, self.gn)))
         self.cap = cap
         self.Q = torch.empty(self.m, self._alloc_cols(0), dtype=F64, device=self.dev)
         self.Bt = torch.empty(self.n, self._alloc_cols(0), dtype=F64, device=self.dev)
@@ -279,10 +282,14 @@ class _QbEngine:
         bdst = self.Bt[:, k0 : k0 + b]
         self.AT_mul(qdst, bdst)
         K.sumsq(bdst, self.mb["colsq"], self.mb["total"])
+        self._reduce_energy()
         self._pending.append(self.mb.read_async())  # parsed lazily by flush()
         self._new_mailbox()
         self.K = k0 + b
         self.blocks += 1
+
+    def _reduce_energy(self) -> None:
+        """B_l's row energies are complete on this rank (B.T replicated)."""
 
     def normal(self, rows: int, cols: int, out):
         return self.stream.normal_device(rows, cols, out=out, status=self.status)
@@ -339,6 +346,48 @@ class _ShardedQbEngine(_QbEngine):
 
     def normal(self, rows: int, cols: int, out):
         if out.shape[0] == rows:  # item-side draw: replicated
+            return self.stream.normal_device(rows, cols, out=out, status=self.status)
+        full = self.stream.normal_device(rows, cols, status=self.status)  # same stream on every rank
+        out.copy_(full[self.shard.row0: self.shard.row1])
+        return out
+
+
+class _ColShardedQbEngine(_QbEngine):
+    """QB engine over A.T of a row-sharded A (parallel.ColumnShardedView;
+    adaptive_pca of a tall matrix, reference rsvd.py:359).  The n rows of
+    A.T (items) are replicated -- Q, the sketches A.T Omega and their
+    orthonormalisations are computed identically on every rank -- and its
+    m columns (users) are sharded: B.T = A Q holds this rank's rows.
+    Exchanges: all-reduce of A_r.T X_r (n x b) and of B.T X (k x b), the
+    b x b Grams of m-side orthonormalisations (power steps of Alg. 2), and
+    B_l's row energies."""
+
+    def __init__(self, A: ColumnShardedView, b: int, stream: GaussianStream, cap: int):
+        super().__init__(A.local, b, stream, cap, frob_sq=A.frob_sq, global_n=A.n)
+        self.shard = A
+        self.comm = A.comm
+
+    def A_mul(self, X, out):
+        super().A_mul(X, out)  # A_r.T X_r
+        return self.comm.all_reduce_(out)
+
+    def minus_QBX(self, Y, X):
+        if self.K:
+            C = self.comm.all_reduce_(K.gemm_tn(self.Bt[:, : self.K], X))
+            K.gemm_nn(self.Q[:, : self.K], C, Y, alpha=-1.0, beta=1.0)
+
+    def orth_into(self, Y, dst):
+        if Y.shape[0] == self.m:  # replicated n-side block
+            K.orth(Y, dst)
+        else:  # sharded m-side block (Alg. 2 power steps)
+            sharded_orth(Y, dst, self.comm, self.gn, passes=2)
+
+    def _reduce_energy(self) -> None:
+        self.comm.all_reduce_(self.mb["colsq"])
+        self.comm.all_reduce_(self.mb["total"])
+
+    def normal(self, rows: int, cols: int, out):
+        if out.shape[0] == rows:  # n-side draw: replicated
             return self.stream.normal_device(rows, cols, out=out, status=self.status)
         full = self.stream.normal_device(rows, cols, status=self.status)  # same stream on every rank
         out.copy_(full[self.shard.row0: self.shard.row1])
@@ -472,10 +521,13 @@ def fixed_precision_qb(A: SparseRatings, tol: float, block_size: int = 20, power
     raise RankExhaustedError(f"residual target {tol:.3e} unmet at rank cap", state=last)
 
 
-def _svd_from_qb(Qm: torch.Tensor, Btm: torch.Tensor, k: int):
-    """Top-k singular triplets of Q B through eig_svd(B.T) (rsvd.py:384-389)."""
+def _svd_from_qb(Qm: torch.Tensor, Btm: torch.Tensor, k: int, comm: Comm | None = None):
+    """Top-k singular triplets of Q B through eig_svd(B.T) (rsvd.py:384-389).
+    ``comm``: B.T's rows are sharded over it (the Gram is all-reduced)."""
     st = K.new_status(Qm.device)
     G = K.gemm_tn(Btm, Btm)  # B B.T
+    if comm is not None:
+        comm.all_reduce_(G)
     w, V = K.syev(G, st)
     if K.check_status(st) & STATUS_NEAR_SINGULAR:
         raise NearSingularError(f"Gram eigenvalue {float(w[0].item()):.3e} below floor "
@@ -499,7 +551,12 @@ def adaptive_pca(A: SparseRatings, criterion: TerminationCriterion, block_size: 
     if block_size < 1:
         raise ValueError("block_size must be positive")
     m, n = A.shape
-    work = A.transposed() if m > n else A
+    # the transpose is a view of the HBM image (its CSR of A.T), not a host
+    # transpose and a second upload
+    if m > n:
+        work = A.transposed() if isinstance(A, ShardedRatings) else TransposedRatings(A)
+    else:
+        work = A
     b = block_size
     if isinstance(criterion, FixedRank):
         b = min(b, criterion.k)
@@ -527,8 +584,9 @@ def adaptive_pca(A: SparseRatings, criterion: TerminationCriterion, block_size: 
     else:
         k = met.rank
         Qm, Btm = met.Q_device, met.Bt_device
-    u, s, v = _svd_from_qb(Qm, Btm, k)
-    if m > n:
+    col_sharded = isinstance(work, ColumnShardedView) and work.world > 1
+    u, s, v = _svd_from_qb(Qm, Btm, k, work.comm if col_sharded else None)
+    if m > n:  # u: this rank's rows when A is row-sharded (as for m <= n)
         u, v = v, u
     if device_output:
         return SvdTriplet(u, s, v, int(k))

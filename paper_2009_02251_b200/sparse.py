@@ -368,6 +368,39 @@ class DeviceRatings:
         return v
 
 
+class TransposedRatings:
+    """A.T of a matrix whose HBM image is (or will be) built: the image
+    already holds the CSR of A.T (DeviceRatings.AT, built on the device), so
+    the transpose is the two CSRs swapped -- no host transpose and no second
+    upload.  What adaptive_pca works on when m > n (reference rsvd.py:359,
+    ``A.transposed()``); the QB engines need only shape / nnz / bounds and
+    ``device()``.  ``matrix`` (the host CSR of A.T) is built only if asked."""
+
+    def __init__(self, base) -> None:
+        self.base = base
+        self.rating_min, self.rating_max = base.rating_min, base.rating_max
+        self._views: dict = {}
+
+    shape = property(lambda self: (self.base.n, self.base.m))
+    m = property(lambda self: self.base.n)
+    n = property(lambda self: self.base.m)
+    nnz = property(lambda self: self.base.nnz)
+
+    def device(self, device=None) -> "DeviceRatings":
+        d = self.base.device(device)
+        v = self._views.get(id(d))
+        if v is None:
+            v = self._views[id(d)] = (d, d.swapped())
+        return v[1]
+
+    @property
+    def matrix(self) -> sp.csr_matrix:
+        return self.base.matrix.transpose().tocsr()
+
+    def transposed(self):
+        return self.base
+
+
 class DeviceSparseRatings:
     """A rating matrix that lives only in HBM (e.g. generated on the device).
 

@@ -75,6 +75,35 @@ def _cf_case(P, rank, comm):
             "Xn1": f1.Xn.cpu().numpy()}
 
 
+def _apca_case(P, rank, comm, passes):
+    """adaptive_pca of a TALL matrix (m > n: the reference transposes,
+    rsvd.py:359) on row shards -> the column-sharded engine over A.T."""
+    import inputs
+    from paper_2009_02251_b200.parallel import ShardedRatings
+    from paper_2009_02251_b200.sparse import TransposedRatings
+    _, M = inputs.rand_sparse(420, 150, 0.1, seed=17)
+    A = P.SparseRatings(M, 0.5, 5.0)
+    S = ShardedRatings.from_full(A, comm)
+    out = {"row0": S.row0, "row1": S.row1}
+    for name, crit in (("tol", P.FrobTolerance(0.5)), ("fixed", P.FixedRank(23))):
+        r1 = P.adaptive_pca(A, crit, block_size=8, passes=passes, seed=4)
+        r2 = P.adaptive_pca(S, crit, block_size=8, passes=passes, seed=4)
+        out[f"{name}_k1"], out[f"{name}_k2"] = r1.k, r2.k
+        out[f"{name}_s1"], out[f"{name}_s2"] = r1.s, r2.s
+        out[f"{name}_u1"], out[f"{name}_u2"] = r1.u[S.row0:S.row1], r2.u
+        out[f"{name}_v1"], out[f"{name}_v2"] = r1.v, r2.v
+    # Alg. 2 power steps on the column-sharded view (sharded m-side orth)
+    g1 = P.qb_power_blocks(TransposedRatings(A), 8, 1, P.GaussianStream(6))
+    g2 = P.qb_power_blocks(S.transposed(), 8, 1, P.GaussianStream(6))
+    for blk, (s1, s2) in enumerate(zip(g1, g2), 1):
+        out[f"pw_err1_{blk}"], out[f"pw_err2_{blk}"] = s1.err, s2.err
+        out[f"pw_Q1_{blk}"], out[f"pw_Q2_{blk}"] = s1.Q, s2.Q
+        if blk == 3:
+            break
+    out["frob"] = S.frob_sq
+    return out
+
+
 def _worker(rank, world, port, outdir, case, arg):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world), RANK=str(rank),
                       LOCAL_RANK=str(rank))
@@ -93,6 +122,8 @@ def _worker(rank, world, port, outdir, case, arg):
         comm = Comm()
         if case == "cf":
             res = _cf_case(P, rank, comm)
+        elif case == "apca":
+            res = _apca_case(P, rank, comm, arg)
         else:
             res = _engine_case(P, rank, comm, case, arg)
         torch.cuda.synchronize()
@@ -145,3 +176,20 @@ def test_sharded_cf_pipeline_matches_single_gpu(gpu, tmp_path, world):
     for r in res[1:]:
         assert np.array_equal(res[0]["Yn2"], r["Yn2"])
         assert np.array_equal(res[0]["mae2"], r["mae2"])
+
+
+@pytest.mark.parametrize("passes", [4, 5])
+def test_sharded_adaptive_pca_tall_matrix(gpu, tmp_path, passes):
+    res = _run(tmp_path, "apca", passes)
+    fro = float(res[0]["frob"])
+    for r in res:
+        for name in ("tol", "fixed"):
+            assert int(r[f"{name}_k2"]) == int(r[f"{name}_k1"])
+            np.testing.assert_allclose(r[f"{name}_s2"], r[f"{name}_s1"], rtol=1e-9)
+            _same_up_to_sign(r[f"{name}_v1"], r[f"{name}_v2"], axis=0, tol=1e-8)
+            _same_up_to_sign(r[f"{name}_u1"], r[f"{name}_u2"], axis=0, tol=1e-8)
+        for blk in range(1, 4):
+            assert abs(float(r[f"pw_err2_{blk}"]) - float(r[f"pw_err1_{blk}"])) <= 1e-10 * fro
+            _same_up_to_sign(r[f"pw_Q1_{blk}"], r[f"pw_Q2_{blk}"], axis=0, tol=1e-9)
+    # the n-side (items) is replicated: bitwise equal on both ranks
+    assert np.array_equal(res[0]["tol_v2"], res[1]["tol_v2"])

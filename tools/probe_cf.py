@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 K.PROFILE = []
 P.auto_latent_factors(A, vs, precision=prec, **kw)
 torch.cuda.synchronize()
-rec = [(n, e0.elapsed_time(e1), nb) for n, e0, e1, nb in K.PROFILE if n == "cf_predict"]
+rec = [(n, e0.elapsed_time(e1), nb) for n, e0, e1, nb, _g in K.PROFILE if n == "cf_predict"]
 K.PROFILE = None
 d = A.device()
 rk = d.A.ranked()[0].cpu().numpy()

@@ -78,7 +78,7 @@ def main():
     errs = [float(x) for x in s._engine.errs]
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").is_file() else {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    c, ms, _ = prof.get("spmm", (0, 0.0, 0))
+    c, ms, _, _ = prof.get("spmm", (0, 0.0, 0, 0))
     # per SpMM call: CSR stream + one pass over X + Y (algorithmic HBM bytes);
     # the gathered row bytes (nnz x 8b) are what the kernel actually moves
     # through L2 (X is 512 MB, out of L2: the cold rows come from HBM)
