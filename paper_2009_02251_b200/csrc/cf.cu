@@ -216,12 +216,14 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
 #pragma unroll
     for (int t = 0; t < NA; ++t) P[t] = S[t] = 0.0;
     double vsum = 0.0;
-    // the next 32-entry CSR batch is loaded while this one is processed
+    // the next 32-entry CSR batch is loaded while this one is processed;
+    // the CSR is streamed once per call, so its loads are evict-first
+    // (__ldcs) and do not push the gathered item rows out of L2
     int32_t ci_next = 0x7fffffff;
     double vi_next = 0.0;
     if (a + lane < e) {
-      ci_next = __ldg(rindices + a + lane);
-      vi_next = __ldg(rvalues + a + lane);
+      ci_next = __ldcs(rindices + a + lane);
+      vi_next = __ldcs(rvalues + a + lane);
     }
     for (int64_t base = a; base < e; base += 32) {
       const int32_t ci = ci_next;
@@ -230,8 +232,8 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
       ci_next = 0x7fffffff;
       vi_next = 0.0;
       if (nx < e) {
-        ci_next = __ldg(rindices + nx);
-        vi_next = __ldg(rvalues + nx);
+        ci_next = __ldcs(rindices + nx);
+        vi_next = __ldcs(rvalues + nx);
       }
       const int nv = (int)min64(32, e - base);
       vsum += vi;  // this lane's entry (0 past the end)
@@ -565,6 +567,8 @@ int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d
   if (nhot < 0) nhot = 0;
   const size_t smem = (size_t)(nhot + 1) * kp * sizeof(TY);
   const int64_t grid = sm_count();
+  // the gathered (cold) item rows: optionally a persisting L2 window
+  const L2Window win(s, d_Yr + (size_t)nhot * ldy, (size_t)(n_items + 1 - nhot) * ldy * sizeof(TY));
 #define SVDREC_PRED(NT, VE)                                                                                   \
   do {                                                                                                        \
     SVDREC_CUDA(smem_attr_once(k_predict<NT, TY, VE>, (int)kHotBytes));                                     \

@@ -37,7 +37,14 @@ def to_device(a: np.ndarray, dtype, device) -> torch.Tensor:
     if a.dtype != dtype:
         a = a.astype(dtype)
     src = torch.from_numpy(a)
-    if a.nbytes < MIN_BYTES or not torch.cuda.is_available():
+    if not torch.cuda.is_available():
+        return src.to(device)
+    if src.is_pinned():
+        # already page-locked (e.g. a view of a pinned torch tensor): one
+        # DMA straight from the caller's buffer, stream-ordered; the caller
+        # keeps the buffer alive (SparseRatings holds its matrix)
+        return src.to(device, non_blocking=True)
+    if a.nbytes < MIN_BYTES:
         return src.to(device)
     flat = src.reshape(-1)
     out = torch.empty(flat.shape, dtype=flat.dtype, device=device)
