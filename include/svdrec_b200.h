@@ -244,7 +244,8 @@ int svdrec_gesvj(int64_t rows, int32_t k, const double* d_A, int64_t lda, double
  *   user-mean / global-mean fallback and clamping.  Writes clamped value,
  *   raw value and fallback flag per sample (in sorted order).  k <= 1024.
  *   The training CSR is passed RANKED: each item id replaced by its
- *   popularity rank (svdrec_cf_relabel; 0 = most rated) and each row's
+ *   popularity rank (0 = most rated; svdrec_csr_transpose of A.T taken
+ *   in popularity order builds it) and each row's
  *   entries ordered by rank, with d_Yr the unit rows Yn in rank order
  *   (Yr[rank(l)] = Yn[l]) plus one zero row at index n_items (the
  *   padding target), rows 16-B aligned (ldy even; float: ldy % 4 == 0) and
@@ -299,8 +300,41 @@ int svdrec_cf_predict_wide(int64_t ngroups, const int64_t* d_group_offsets, cons
                            const double* d_Xn, int64_t ldn, const double* d_norm, double global_mean,
                            double rating_min, double rating_max, double* d_value, double* d_raw,
                            uint8_t* d_fallback, void* stream);
-int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,
-                      void* stream);
+/* The scoring kernel's work plan (see svdrec_cf_predict) on the device:
+ * groups with degree d_group_deg (int64, ngroups), heaviest-first order
+ * d_order (a stable sort of -degree).  plan_scan writes d_first (first
+ * work item of the j-th group in that order), d_slot0 / d_done_idx (per
+ * group: first partial slot / completion counter of a split group, -1
+ * otherwise) and d_stats = (work items, split groups, partial slots,
+ * ratings streamed); plan_emit writes d_work_start / d_work_meta
+ * (d_stats[0] items; d_group_start: ngroups + 1 sample offsets,
+ * d_row_start: CSR offset of each group's user row). */
+int svdrec_cf_plan_scan(int64_t ngroups, const int64_t* d_group_deg, const int64_t* d_order, int32_t chunk,
+                        int64_t* d_first, int32_t* d_slot0, int32_t* d_done_idx, int64_t* d_stats,
+                        void* stream);
+int svdrec_cf_plan_emit(int64_t ngroups, const int64_t* d_group_deg, const int64_t* d_order,
+                        const int64_t* d_first, const int32_t* d_slot0, const int32_t* d_done_idx,
+                        const int64_t* d_group_start, const int64_t* d_row_start, int32_t chunk,
+                        int64_t* d_work_start, int32_t* d_work_meta, void* stream);
+
+/* Stable counting-sort transpose of a CSR, on the device (ingest; replaces
+ * the reference's scipy transpose behind ``A.T @ X``, linalg.py:141-158,
+ * and SparseRatings.transposed, sparse.py).  The nrows input rows are
+ * taken in processing order d_perm (nullable: identity) with d_pptr[q] =
+ * sum of the lengths of the first q rows in that order (nrows + 1
+ * entries; total = d_pptr[nrows], passed by the caller: no device read).  Output row c (c < n_out) lists, in processing order, every
+ * input row holding column c: its entries carry the input row's index
+ * (relabel = 0) or its processing position (relabel = 1) and the value.
+ * Writes d_out_indptr (n_out + 1), d_out_indices / d_out_values (one per
+ * entry).  Deterministic; no sort.  Fewer than 2^31 entries.  Scratch:
+ * svdrec_csr_transpose_scratch(n_out) + 2 x (entries x 4 B, rounded up to
+ * 256 B). */
+int64_t svdrec_csr_transpose_scratch(int64_t n_out);
+int svdrec_csr_transpose(int64_t nrows, int64_t n_out, int64_t total, const int64_t* d_indptr,
+                         const int32_t* d_indices, const double* d_values, const int32_t* d_perm,
+                         const int64_t* d_pptr, int32_t relabel,
+                         int64_t* d_out_indptr, int32_t* d_out_indices, double* d_out_values, void* d_scratch,
+                         int64_t scratch_bytes, void* stream);
 
 /* G^(-1/2) of a k x k SPD Gram by coupled Newton-Schulz iteration (one
  * cooperative kernel, GEMM phases over the whole GPU).  Sets
@@ -320,13 +354,6 @@ int svdrec_err_sum(int64_t nsamp, const double* d_pred, const double* d_truth,
 int svdrec_count_overlap(int64_t nsamp, const int32_t* d_users, const int32_t* d_items,
                          const int64_t* d_indptr, const int32_t* d_indices,
                          int32_t* d_count, void* stream);
-
-/* North-star extension (not in the reference): model-based prediction
- * mu + U_k S_k V_k^T at sampled (i, j), pred[t] = mu + sum_l U[i,l] s[l] V[j,l]. */
-int svdrec_lowrank_predict(int64_t nsamp, const int32_t* d_users, const int32_t* d_items,
-                           int32_t k, const double* d_U, int64_t ldu, const double* d_s,
-                           const double* d_V, int64_t ldv, double mu, double* d_pred,
-                           void* stream);
 
 #ifdef __cplusplus
 }

@@ -66,13 +66,15 @@ SIGNATURES = {
                                         _i32, _p, _i64, _p, _p, _p, _p, _p, _p]),
     "svdrec_cf_predict_wide": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _i64, _p, _i64, _p, _f64, _f64,
                                          _f64, _p, _p, _p, _p]),
-    "svdrec_cf_relabel": (C.c_int, [_i64, _p, _p, _p, _p]),
+    "svdrec_cf_plan_scan": (C.c_int, [_i64, _p, _p, _i32, _p, _p, _p, _p, _p]),
+    "svdrec_cf_plan_emit": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p]),
+    "svdrec_csr_transpose_scratch": (_i64, [_i64]),
+    "svdrec_csr_transpose": (C.c_int, [_i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _i64, _p]),
     "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
     "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),
     "svdrec_err_sum_workspace_bytes": (_sz, [_i64]),
     "svdrec_err_sum": (C.c_int, [_i64, _p, _p, _p, _p, _sz, _p]),
     "svdrec_count_overlap": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p]),
-    "svdrec_lowrank_predict": (C.c_int, [_i64, _p, _p, _i32, _p, _i64, _p, _p, _i64, _f64, _p, _p]),
 }
 
 

@@ -175,39 +175,27 @@ class WorkPlan:
         """``group_deg``: training degree of each group's user; ``group_start``
         (ngroups + 1) sample offsets; ``row_start``: CSR offset of each
         group's user row (all int64 tensors on ``device``)."""
-        gd = torch.as_tensor(group_deg, device=device).to(torch.int64)
+        gd = torch.as_tensor(group_deg, device=device).to(torch.int64).contiguous()
         ng = gd.numel()
         if group_start is None:
             group_start = torch.arange(ng + 1, device=device)
         if row_start is None:
             row_start = torch.cumsum(gd, 0) - gd
-        nch = torch.clamp((gd + self.CHUNK - 1) // self.CHUNK, min=1)
-        split = nch > 1
-        cs = torch.cumsum(torch.where(split, nch, torch.zeros_like(nch)), 0)
-        slot0 = torch.where(split, cs - nch, torch.full_like(nch, -1))
-        done = torch.where(split, torch.cumsum(split.to(torch.int64), 0) - 1, torch.full_like(nch, -1))
-        order = torch.sort(-gd, stable=True).indices
-        no = nch[order]
-        wg = torch.repeat_interleave(order, no)
-        first = torch.repeat_interleave(torch.cumsum(no, 0) - no, no)
-        wc = torch.arange(wg.numel(), device=device) - first
-        self.nwork = int(wg.numel())
-        sp_w = split[wg]
-        deg_w = gd[wg]
-        off = torch.where(sp_w, wc * self.CHUNK, torch.zeros_like(wc))
-        self.start = (row_start.to(torch.int64)[wg] + off).contiguous() if self.nwork else \
-            torch.zeros(1, dtype=torch.int64, device=device)
-        length = torch.where(sp_w, torch.clamp(deg_w - off, max=self.CHUNK), deg_w)
-        gs = group_start.to(torch.int64)
-        meta = torch.stack([length, deg_w, gs[wg], gs[wg + 1], nch[wg],
-                            torch.where(sp_w, slot0[wg] + wc, torch.full_like(wc, -1)), done[wg], wc], 1)
-        self.meta = meta.to(torch.int32).flatten().contiguous() if self.nwork else \
-            torch.zeros(8, dtype=torch.int32, device=device)
-        stats = torch.stack([split.sum(), torch.where(split, nch, torch.zeros_like(nch)).sum(), gd.sum()]).cpu() \
-            if ng else torch.zeros(3, dtype=torch.int64)
-        self.ndone = int(stats[0])
-        self.nslots = int(stats[1])
-        self.rated = int(stats[2])  # training ratings streamed per scoring pass
+        gs = group_start.to(torch.int64).contiguous()
+        rs = row_start.to(torch.int64).contiguous()
+        # heaviest user first (ties: group order), then two kernels: chunk
+        # counts / slot bases / first items (one CTA), then the records
+        order = torch.sort(-gd, stable=True).indices if ng else torch.zeros(0, dtype=torch.int64, device=device)
+        first = torch.empty(max(ng, 1), dtype=torch.int64, device=device)
+        slot0 = torch.empty(max(ng, 1), dtype=torch.int32, device=device)
+        done_idx = torch.empty(max(ng, 1), dtype=torch.int32, device=device)
+        stats = torch.empty(4, dtype=torch.int64, device=device)
+        K.cf_plan_scan(gd, order, self.CHUNK, first, slot0, done_idx, stats)
+        st = stats.cpu().numpy()  # the plan's sizes (one small read)
+        self.nwork, self.ndone, self.nslots, self.rated = int(st[0]), int(st[1]), int(st[2]), int(st[3])
+        self.start = torch.zeros(max(self.nwork, 1), dtype=torch.int64, device=device)
+        self.meta = torch.zeros(8 * max(self.nwork, 1), dtype=torch.int32, device=device)
+        K.cf_plan_emit(gd, order, first, slot0, done_idx, gs, rs, self.CHUNK, self.start, self.meta)
         self.done = torch.zeros(max(self.ndone, 1), dtype=torch.int32, device=device)
         self.counter = torch.zeros(1, dtype=torch.int32, device=device)
         self.chunk = self.CHUNK
@@ -603,9 +591,14 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
         raise ValueError("block_size must be positive")
     if 2 * block_size > min(A.shape):
         raise ValueError(f"block_size {block_size} too large for min(m, n) = {min(A.shape)}")
-    criterion = ValidationMae(A, validation, patience=patience, min_improvement=min_improvement, precision=precision)
     stream = GaussianStream(seed)
     gen = qb_pass_blocks(A, block_size, passes, stream, max_rank=max_rank, precision=precision)
+    # block 1 is queued before the validation samples are ingested (upload,
+    # grouping, bounds and disjointness checks -- host work with a few
+    # small reads), so that ingest overlaps the block on the GPU; a
+    # criterion error still surfaces before any result exists
+    state = next(gen, None)
+    criterion = ValidationMae(A, validation, patience=patience, min_improvement=min_improvement, precision=precision)
     # Same criterion sequence as the reference's ``for state in ...: if
     # criterion(state): break``, pipelined: block l is scored on the
     # criterion's stream while block l+1 is factored on this one (a block
@@ -614,7 +607,6 @@ def auto_latent_factors(A: SparseRatings, validation, block_size: int = 20, pass
     # score (same stream unless PIPELINE), so the GPU never idles on the
     # stop decision; a block computed past the stop is discarded
     pipeline = PIPELINE
-    state = next(gen, None)
     while state is not None:
         t0 = time.perf_counter() if _HOST_TRACE is not None else 0.0
         pending = criterion.submit(state)

@@ -469,15 +469,6 @@ __global__ void __launch_bounds__(kWideThreads) k_predict_wide(
   }
 }
 
-// Ranked copy of a CSR for the scoring kernel, step 1: column j -> rank[j].
-// Step 2 (the caller: sparse.DeviceCSR.ranked) orders every row by rank
-// with one device radix sort of (row, rank) keys; ranks are unique per row.
-__global__ void k_relabel(int64_t nnz, const int32_t* __restrict__ indices, const int32_t* __restrict__ rank,
-                          int32_t* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < nnz) out[t] = rank[indices[t]];
-}
-
 __global__ void k_overlap(int64_t ns, const int32_t* __restrict__ users, const int32_t* __restrict__ items,
                           const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int32_t* count) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -494,18 +485,96 @@ __global__ void k_overlap(int64_t ns, const int32_t* __restrict__ users, const i
   if (lo < indptr[users[t] + 1] && indices[lo] == it) atomicAdd(count, 1);
 }
 
-__global__ void k_lowrank(int64_t ns, const int32_t* __restrict__ users, const int32_t* __restrict__ items, int k,
-                          const double* __restrict__ U, int64_t ldu, const double* __restrict__ s,
-                          const double* __restrict__ V, int64_t ldv, double mu, double* __restrict__ pred) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (t >= ns) return;
-  const double* ur = U + (int64_t)users[t] * ldu;
-  const double* vr = V + (int64_t)items[t] * ldv;
-  double acc = 0.0;
-  for (int e = lane; e < k; e += 32) acc = fma(ur[e] * s[e], vr[e], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) pred[t] = mu + acc;
+// Scoring work plan (the WorkPlan of cf.py) in two launches: k_plan_scan
+// (one CTA) turns the per-group degrees into chunk counts, partial-slot and
+// completion-counter bases (group order) and the first work item of each
+// group in heaviest-first order; k_plan_emit writes every item's start and
+// 8-int meta record.  Same arrays as the torch restatement it replaces.
+__global__ void __launch_bounds__(1024) k_plan_scan(int64_t ng, const int64_t* __restrict__ gd,
+                                                    const int64_t* __restrict__ order, int chunk,
+                                                    int64_t* __restrict__ first, int32_t* __restrict__ slot0,
+                                                    int32_t* __restrict__ done_idx, int64_t* __restrict__ stats) {
+  __shared__ int64_t sh[3][1024];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int64_t per = (ng + T - 1) / T;
+  const int64_t a = min64(ng, per * t), b = min64(ng, a + per);
+  auto nch_of = [&](int64_t d) -> int64_t { return d <= chunk ? 1 : (d + chunk - 1) / chunk; };
+  int64_t sl = 0, dn = 0, it = 0, rated = 0;
+  for (int64_t g = a; g < b; ++g) {
+    const int64_t n = nch_of(gd[g]);
+    if (n > 1) {
+      sl += n;
+      dn += 1;
+    }
+    it += nch_of(gd[order[g]]);
+    rated += gd[g];
+  }
+  sh[0][t] = sl;
+  sh[1][t] = dn;
+  sh[2][t] = it;
+  __syncthreads();
+  for (int off = 1; off < T; off <<= 1) {
+    int64_t v0 = 0, v1 = 0, v2 = 0;
+    if (t >= off) {
+      v0 = sh[0][t - off];
+      v1 = sh[1][t - off];
+      v2 = sh[2][t - off];
+    }
+    __syncthreads();
+    sh[0][t] += v0;
+    sh[1][t] += v1;
+    sh[2][t] += v2;
+    __syncthreads();
+  }
+  int64_t s0 = sh[0][t] - sl, d0 = sh[1][t] - dn, i0 = sh[2][t] - it;
+  const int64_t nslots = sh[0][T - 1];
+  for (int64_t g = a; g < b; ++g) {
+    const int64_t n = nch_of(gd[g]);
+    slot0[g] = n > 1 ? (int32_t)s0 : -1;
+    done_idx[g] = n > 1 ? (int32_t)d0 : -1;
+    if (n > 1) {
+      s0 += n;
+      d0 += 1;
+    }
+    first[g] = i0;
+    i0 += nch_of(gd[order[g]]);
+  }
+  // rated: a block reduction of the per-thread sums (reuse sh[0])
+  __syncthreads();
+  sh[0][t] = rated;
+  __syncthreads();
+  for (int off = T / 2; off > 0; off >>= 1) {
+    if (t < off) sh[0][t] += sh[0][t + off];
+    __syncthreads();
+  }
+  if (t == T - 1) {
+    stats[0] = sh[2][T - 1];  // work items (sh[1], sh[2] keep their scans)
+    stats[1] = sh[1][T - 1];  // split groups (completion counters)
+    stats[2] = nslots;        // partial slots
+  }
+  if (t == 0) stats[3] = sh[0][0];  // training ratings streamed per pass
+}
+
+// j: position in heaviest-first order
+__global__ void k_plan_emit(int64_t ng, const int64_t* __restrict__ gd, const int64_t* __restrict__ order,
+                            const int64_t* __restrict__ first, const int32_t* __restrict__ slot0,
+                            const int32_t* __restrict__ done_idx, const int64_t* __restrict__ gs,
+                            const int64_t* __restrict__ row_start, int chunk, int64_t* __restrict__ start,
+                            int4* __restrict__ meta) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ng) return;
+  const int64_t g = order[j];
+  const int64_t deg = gd[g];
+  const int64_t nch = deg <= chunk ? 1 : (deg + chunk - 1) / chunk;
+  const bool split = nch > 1;
+  const int64_t w0 = first[j];
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t off = split ? c * chunk : 0;
+    const int64_t len = split ? min64(chunk, deg - off) : deg;
+    start[w0 + c] = row_start[g] + off;
+    meta[2 * (w0 + c)] = make_int4((int)len, (int)deg, (int)gs[g], (int)gs[g + 1]);
+    meta[2 * (w0 + c) + 1] = make_int4((int)nch, split ? slot0[g] + (int)c : -1, done_idx[g], (int)c);
+  }
 }
 
 }  // namespace
@@ -567,8 +636,6 @@ int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d
   if (nhot < 0) nhot = 0;
   const size_t smem = (size_t)(nhot + 1) * kp * sizeof(TY);
   const int64_t grid = sm_count();
-  // the gathered (cold) item rows: optionally a persisting L2 window
-  const L2Window win(s, d_Yr + (size_t)nhot * ldy, (size_t)(n_items + 1 - nhot) * ldy * sizeof(TY));
 #define SVDREC_PRED(NT, VE)                                                                                   \
   do {                                                                                                        \
     SVDREC_CUDA(smem_attr_once(k_predict<NT, TY, VE>, (int)kHotBytes));                                     \
@@ -647,14 +714,6 @@ extern "C" int svdrec_cf_predict_wide(int64_t ngroups, const int64_t* d_group_of
   return check_launch("cf_predict_wide");
 }
 
-extern "C" int svdrec_cf_relabel(int64_t nnz, const int32_t* d_indices, const int32_t* d_rank, int32_t* d_out,
-                                 void* stream) {
-  SVDREC_ARG(nnz >= 0, "cf_relabel: bad arguments");
-  if (nnz == 0) return 0;
-  k_relabel<<<(unsigned)((nnz + 255) / 256), 256, 0, as_stream(stream)>>>(nnz, d_indices, d_rank, d_out);
-  return check_launch("cf_relabel");
-}
-
 extern "C" int svdrec_count_overlap(int64_t nsamp, const int32_t* d_users, const int32_t* d_items,
                                     const int64_t* d_indptr, const int32_t* d_indices, int32_t* d_count,
                                     void* stream) {
@@ -666,13 +725,26 @@ extern "C" int svdrec_count_overlap(int64_t nsamp, const int32_t* d_users, const
   return check_launch("count_overlap");
 }
 
-extern "C" int svdrec_lowrank_predict(int64_t nsamp, const int32_t* d_users, const int32_t* d_items, int32_t k,
-                                      const double* d_U, int64_t ldu, const double* d_s, const double* d_V,
-                                      int64_t ldv, double mu, double* d_pred, void* stream) {
-  SVDREC_ARG(nsamp >= 0 && k >= 1 && ldu >= k && ldv >= k, "lowrank_predict: bad arguments");
-  if (nsamp == 0) return 0;
-  const int64_t thr = nsamp * 32;
-  k_lowrank<<<(unsigned)((thr + 255) / 256), 256, 0, as_stream(stream)>>>(nsamp, d_users, d_items, k, d_U, ldu, d_s,
-                                                                          d_V, ldv, mu, d_pred);
-  return check_launch("lowrank_predict");
+extern "C" int svdrec_cf_plan_scan(int64_t ngroups, const int64_t* d_group_deg, const int64_t* d_order,
+                                   int32_t chunk, int64_t* d_first, int32_t* d_slot0, int32_t* d_done_idx,
+                                   int64_t* d_stats, void* stream) {
+  SVDREC_ARG(ngroups >= 0 && chunk >= 1, "cf_plan_scan: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  SVDREC_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(int64_t), s));
+  if (ngroups == 0) return 0;
+  k_plan_scan<<<1, 1024, 0, s>>>(ngroups, d_group_deg, d_order, chunk, d_first, d_slot0, d_done_idx, d_stats);
+  return check_launch("cf_plan_scan");
+}
+
+extern "C" int svdrec_cf_plan_emit(int64_t ngroups, const int64_t* d_group_deg, const int64_t* d_order,
+                                   const int64_t* d_first, const int32_t* d_slot0, const int32_t* d_done_idx,
+                                   const int64_t* d_group_start, const int64_t* d_row_start, int32_t chunk,
+                                   int64_t* d_work_start, int32_t* d_work_meta, void* stream) {
+  SVDREC_ARG(ngroups >= 0 && chunk >= 1, "cf_plan_emit: bad arguments");
+  SVDREC_ARG(reinterpret_cast<uintptr_t>(d_work_meta) % 16 == 0, "cf_plan_emit: work meta must be 16-B aligned");
+  if (ngroups == 0) return 0;
+  k_plan_emit<<<(unsigned)((ngroups + 255) / 256), 256, 0, as_stream(stream)>>>(
+      ngroups, d_group_deg, d_order, d_first, d_slot0, d_done_idx, d_group_start, d_row_start, chunk, d_work_start,
+      reinterpret_cast<int4*>(d_work_meta));
+  return check_launch("cf_plan_emit");
 }

@@ -67,46 +67,6 @@ cudaError_t smem_attr_once(K* kernel, int bytes) {
   return e;
 }
 
-// Persisting L2 access-policy window over [base, base + bytes) for the
-// kernels launched on ``s`` while the object lives (SVDREC_L2WIN=1; off by
-// default): the gathered rows stay in the set-aside part of L2 while a
-// streamed operand passes through.  The window is removed on destruction
-// (kernels keep the policy they were launched with).
-struct L2Window {
-  cudaStream_t s = nullptr;
-  bool on = false;
-  L2Window(cudaStream_t st, const void* base, size_t bytes) : s(st) {
-    static const int enabled = getenv("SVDREC_L2WIN") ? atoi(getenv("SVDREC_L2WIN")) : 0;
-    if (!enabled || bytes == 0) return;
-    int dev = 0, maxp = 0, maxw = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    if (maxp <= 0 || maxw <= 0) return;
-    size_t cur = 0;
-    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    if (cur < (size_t)maxp && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess) {
-      cudaGetLastError();
-      return;
-    }
-    cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-    v.accessPolicyWindow.num_bytes = bytes < (size_t)maxw ? bytes : (size_t)maxw;
-    const double ratio = (double)maxp / (double)v.accessPolicyWindow.num_bytes;
-    v.accessPolicyWindow.hitRatio = (float)(ratio < 1.0 ? ratio : 1.0);
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    on = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
-    if (!on) cudaGetLastError();
-  }
-  ~L2Window() {
-    if (!on) return;
-    cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.num_bytes = 0;
-    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
-  }
-};
-
 // skinny.cu: tall-skinny GEMMs for q <= 32 (see the file header)
 int64_t tn_skinny_slabs(int64_t r, int64_t p);
 int launch_nn_skinny(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C,

@@ -1,0 +1,269 @@
+// Device-side ingest: stable counting-sort transpose of a CSR.
+//
+// Builds the two derived layouts the hot path needs from the uploaded CSR
+// of A (reference sparse.py keeps only A; its ``A.T @ X`` is scipy's
+// transposed product, linalg.py:141-158):
+//   * the CSR of A.T (item rows, users ascending) for A.T @ X;
+//   * the popularity-ranked CSR for the CF scoring kernel (user rows, items
+//     relabelled by popularity rank and stored in rank order) -- the
+//     transpose of A.T with its rows taken in rank order.
+// Both are "transpose the rows of a CSR, taken in a given order": output
+// row c lists, in processing order, every input row r holding column c.
+//
+// No sort.  k_tr_expand lays out, per processing position, the input row
+// (in processing order) and the entry's index (one warp per row, coalesced
+// writes).  Then, per range of at most kBins output rows (columns of the
+// input):
+//   k_tr_hist    one CTA per contiguous slice of the processing positions:
+//                column histogram in shared memory -> hist[c][cta];
+//   k_tr_offsets one thread per column: off[c][cta] = out_indptr[c] + the
+//                column's count in the slices before cta (fixed order);
+//   k_tr_scatter each CTA re-walks its slice with its offsets in shared
+//                memory.  An input row's columns are distinct, so entries
+//                of one input row never collide: each 1024-entry tile is
+//                processed input row by input row (one CTA barrier per
+//                row), which keeps the output stable (processing order)
+//                and deterministic.  The next tile's loads are in flight
+//                while a tile is scattered (two-deep register pipeline).
+// Traffic: the entries are read twice and written once (scattered); the
+// per-(column, slice) tables are n x slices int32 (transient).
+#include "common.cuh"
+
+namespace svdrec {
+namespace {
+
+constexpr int kTrThreads = 1024;
+constexpr int kBins = 50 * 1024;  // output rows per range (int32 bins, 200 KB of shared memory)
+
+__device__ __forceinline__ void slice(int64_t total, int64_t& t0, int64_t& t1) {
+  t0 = total * (int64_t)blockIdx.x / gridDim.x;
+  t1 = total * ((int64_t)blockIdx.x + 1) / gridDim.x;
+}
+
+// row_p[p] = processing row of position p; src_e[p] = its entry index
+__global__ void k_tr_expand(int64_t nrows, const int64_t* __restrict__ pptr, const int64_t* __restrict__ indptr,
+                            const int32_t* __restrict__ perm, int32_t* __restrict__ row_p,
+                            int32_t* __restrict__ src_e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = w0; q < nrows; q += nw) {
+    const int64_t a = pptr[q], b = pptr[q + 1];
+    const int64_t e0 = indptr[perm ? (int64_t)perm[q] : q];
+    for (int64_t p = a + lane; p < b; p += 32) {
+      row_p[p] = (int32_t)q;
+      src_e[p] = (int32_t)(e0 + (p - a));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTrThreads) k_tr_hist(const int32_t* __restrict__ src_e,
+                                                         const int32_t* __restrict__ indices, int64_t total,
+                                                         int32_t c0, int32_t nb, int32_t* __restrict__ hist) {
+  extern __shared__ int32_t bins[];
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) bins[c] = 0;
+  __syncthreads();
+  int64_t t0, t1;
+  slice(total, t0, t1);
+#pragma unroll 4
+  for (int64_t p = t0 + threadIdx.x; p < t1; p += blockDim.x) {
+    const int32_t c = indices[__ldcs(src_e + p)] - c0;
+    if ((uint32_t)c < (uint32_t)nb) atomicAdd(&bins[c], 1);
+  }
+  __syncthreads();
+  const int64_t g = gridDim.x;
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) hist[(int64_t)c * g + blockIdx.x] = bins[c];
+}
+
+// per column: running sum over the slices, from the column's output start
+__global__ void k_tr_offsets(int32_t nb, int32_t g, const int64_t* __restrict__ out_indptr, int32_t c0,
+                             int32_t* __restrict__ hist) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nb) return;
+  int64_t run = out_indptr[c0 + c];
+  int32_t* h = hist + c * g;
+  for (int i = 0; i < g; ++i) {
+    const int32_t n = h[i];
+    h[i] = (int32_t)run;
+    run += n;
+  }
+}
+
+// column totals of the histogram (for the output row pointers)
+__global__ void k_tr_totals(int32_t nb, int32_t g, const int32_t* __restrict__ hist, int64_t* __restrict__ counts) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nb) return;
+  int64_t s = 0;
+  for (int i = 0; i < g; ++i) s += hist[c * g + i];
+  counts[c] = s;
+}
+
+// exclusive scan of counts[0, n) into indptr[0, n] (one CTA; n is a column
+// count, up to a few hundred thousand)
+__global__ void __launch_bounds__(1024) k_scan_counts(int64_t n, const int64_t* __restrict__ counts,
+                                                      int64_t* __restrict__ indptr) {
+  __shared__ int64_t part[1024];
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t a = min64(n, per * threadIdx.x), b = min64(n, a + per);
+  int64_t s = 0;
+#pragma unroll 8
+  for (int64_t i = a; i < b; ++i) s += counts[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const int64_t v = threadIdx.x >= (unsigned)off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = part[threadIdx.x] - s;
+#pragma unroll 8
+  for (int64_t i = a; i < b; ++i) {
+    const int64_t c = counts[i];
+    indptr[i] = run;
+    run += c;
+  }
+  if (threadIdx.x == blockDim.x - 1) indptr[n] = part[threadIdx.x];
+}
+
+// relabel: output column id = the input row's processing position (rank)
+// instead of its index
+template <bool RELABEL>
+__global__ void __launch_bounds__(kTrThreads) k_tr_scatter(const int32_t* __restrict__ row_p,
+                                                            const int32_t* __restrict__ src_e,
+                                                            const int32_t* __restrict__ perm,
+                                                            const int32_t* __restrict__ indices,
+                                                            const double* __restrict__ values, int64_t total,
+                                                            int32_t c0, int32_t nb, const int32_t* __restrict__ hist,
+                                                            int32_t* __restrict__ out_idx,
+                                                            double* __restrict__ out_val) {
+  extern __shared__ int32_t off[];
+  __shared__ int32_t s_rows[2][2];
+  const int64_t g = gridDim.x;
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) off[c] = hist[(int64_t)c * g + blockIdx.x];
+  int64_t t0, t1;
+  slice(total, t0, t1);
+  const int T = blockDim.x;
+  // two-deep pipeline: (row, entry) of tile i+2 and (column, value) of
+  // tile i+1 are loading while tile i is scattered
+  auto load_re = [&](int64_t p0, int32_t& r, int32_t& e) {
+    const int64_t p = p0 + threadIdx.x;
+    r = -1;
+    e = -1;
+    if (p < t1) {
+      r = __ldcs(row_p + p);
+      e = __ldcs(src_e + p);
+    }
+  };
+  auto load_cv = [&](int32_t e, int32_t& c, double& v) {
+    c = -1;
+    v = 0.0;
+    if (e >= 0) {
+      c = __ldcs(indices + e) - c0;
+      v = __ldcs(values + e);
+    }
+  };
+  int32_t r_cur, e_cur, r_nx, e_nx, c_cur;
+  double v_cur;
+  load_re(t0, r_cur, e_cur);
+  load_re(t0 + T, r_nx, e_nx);
+  load_cv(e_cur, c_cur, v_cur);
+  __syncthreads();  // offsets staged
+  int par = 0;
+  for (int64_t p0 = t0; p0 < t1; p0 += T) {
+    // the tile's first and last rows
+    if (threadIdx.x == 0) s_rows[par][0] = r_cur;
+    if (p0 + threadIdx.x == min64(p0 + T, t1) - 1) s_rows[par][1] = r_cur;
+    int32_t c_nx;
+    double v_nx;
+    load_cv(e_nx, c_nx, v_nx);  // tile i+1's columns / values
+    int32_t r_nx2, e_nx2;
+    load_re(p0 + 2 * T, r_nx2, e_nx2);  // tile i+2's rows / entries
+    __syncthreads();
+    const int32_t q = s_rows[par][0], ql = s_rows[par][1];
+    for (int32_t rr = q; rr <= ql; ++rr) {
+      if (r_cur == rr && (uint32_t)c_cur < (uint32_t)nb) {
+        const int32_t pos = off[c_cur];
+        off[c_cur] = pos + 1;
+        out_idx[pos] = RELABEL ? rr : (perm ? perm[rr] : rr);
+        out_val[pos] = v_cur;
+      }
+      __syncthreads();
+    }
+    r_cur = r_nx;
+    c_cur = c_nx;
+    v_cur = v_nx;
+    r_nx = r_nx2;
+    e_nx = e_nx2;
+    par ^= 1;
+  }
+}
+
+}  // namespace
+}  // namespace svdrec
+
+using namespace svdrec;
+
+extern "C" int64_t svdrec_csr_transpose_scratch(int64_t n_out) {
+  // hist tables (int32, n_out x slices) + column totals (int64); the
+  // per-position row / entry arrays are allocated by the caller's scratch
+  // too: see svdrec_csr_transpose (2 x entries x int32 after these)
+  const int64_t nb = n_out < kBins ? n_out : kBins;
+  return (int64_t)align_up((size_t)nb * sm_count() * sizeof(int32_t)) + (int64_t)align_up((size_t)(n_out + 1) * 8);
+}
+
+extern "C" int svdrec_csr_transpose(int64_t nrows, int64_t n_out, int64_t total, const int64_t* d_indptr,
+                                    const int32_t* d_indices, const double* d_values, const int32_t* d_perm,
+                                    const int64_t* d_pptr, int32_t relabel, int64_t* d_out_indptr, int32_t* d_out_indices,
+                                    double* d_out_values, void* d_scratch, int64_t scratch_bytes, void* stream) {
+  SVDREC_ARG(nrows >= 0 && n_out >= 0 && d_pptr && d_indptr && d_out_indptr, "csr_transpose: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  SVDREC_ARG(total >= 0 && total < (1ll << 31), "csr_transpose: %lld entries exceed int32 positions", (long long)total);
+  const int64_t base = svdrec_csr_transpose_scratch(n_out);
+  SVDREC_ARG(scratch_bytes >= base + 2 * (int64_t)align_up((size_t)total * 4),
+             "csr_transpose: scratch too small (%lld < %lld)", (long long)scratch_bytes,
+             (long long)(base + 2 * (int64_t)align_up((size_t)total * 4)));
+  const int g = sm_count();
+  char* ws = reinterpret_cast<char*>(d_scratch);
+  int32_t* hist = reinterpret_cast<int32_t*>(ws);
+  const int64_t nbmax = n_out < kBins ? n_out : kBins;
+  int64_t* counts = reinterpret_cast<int64_t*>(ws + align_up((size_t)nbmax * g * sizeof(int32_t)));
+  int32_t* row_p = reinterpret_cast<int32_t*>(ws + base);
+  int32_t* src_e = reinterpret_cast<int32_t*>(ws + base + align_up((size_t)total * 4));
+  const size_t smem = (size_t)nbmax * sizeof(int32_t);
+  SVDREC_CUDA(smem_attr_once(k_tr_hist, (int)(kBins * sizeof(int32_t))));
+  SVDREC_CUDA(smem_attr_once(k_tr_scatter<true>, (int)(kBins * sizeof(int32_t))));
+  SVDREC_CUDA(smem_attr_once(k_tr_scatter<false>, (int)(kBins * sizeof(int32_t))));
+  int launches = 0;
+  if (total > 0) {
+    k_tr_expand<<<g * 8, 256, 0, s>>>(nrows, d_pptr, d_indptr, d_perm, row_p, src_e);
+    launches += 1;
+  }
+  // pass 1: column totals -> output row pointers
+  for (int64_t c0 = 0; c0 < n_out; c0 += kBins) {
+    const int32_t nb = (int32_t)min64(kBins, n_out - c0);
+    k_tr_hist<<<g, kTrThreads, smem, s>>>(src_e, d_indices, total, (int32_t)c0, nb, hist);
+    k_tr_totals<<<(nb + 255) / 256, 256, 0, s>>>(nb, g, hist, counts + c0);
+    launches += 2;
+  }
+  k_scan_counts<<<1, 1024, 0, s>>>(n_out, counts, d_out_indptr);
+  launches += 1;
+  // pass 2: per range, histogram (kept from pass 1 for a single range) ->
+  // offsets -> stable scatter
+  for (int64_t c0 = 0; c0 < n_out && total > 0; c0 += kBins) {
+    const int32_t nb = (int32_t)min64(kBins, n_out - c0);
+    if (n_out > kBins) {
+      k_tr_hist<<<g, kTrThreads, smem, s>>>(src_e, d_indices, total, (int32_t)c0, nb, hist);
+      launches += 1;
+    }
+    k_tr_offsets<<<(nb + 255) / 256, 256, 0, s>>>(nb, g, d_out_indptr, (int32_t)c0, hist);
+    if (relabel)
+      k_tr_scatter<true><<<g, kTrThreads, smem, s>>>(row_p, src_e, d_perm, d_indices, d_values, total, (int32_t)c0,
+                                                      nb, hist, d_out_indices, d_out_values);
+    else
+      k_tr_scatter<false><<<g, kTrThreads, smem, s>>>(row_p, src_e, d_perm, d_indices, d_values, total,
+                                                       (int32_t)c0, nb, hist, d_out_indices, d_out_values);
+    launches += 2;
+  }
+  return check_launch("csr_transpose", launches);
+}

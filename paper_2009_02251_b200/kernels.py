@@ -418,12 +418,47 @@ def cf_predict(groups: torch.Tensor, users: torch.Tensor, items: torch.Tensor, c
     return val, raw, fb
 
 
-def cf_relabel(indices: torch.Tensor, rank: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """out[t] = rank[indices[t]] (int32)."""
-    if out is None:
-        out = torch.empty_like(indices)
-    call("svdrec_cf_relabel", indices.numel(), ptr(indices), ptr(rank), ptr(out), stream_handle())
-    return out
+def cf_plan_scan(gd, order, chunk, first, slot0, done_idx, stats):
+    """Scoring work plan, step 1 (csrc/cf.cu k_plan_scan)."""
+    call("svdrec_cf_plan_scan", gd.numel(), ptr(gd), ptr(order), int(chunk), ptr(first), ptr(slot0),
+         ptr(done_idx), ptr(stats), stream_handle())
+
+
+def cf_plan_emit(gd, order, first, slot0, done_idx, group_start, row_start, chunk, start, meta):
+    """Scoring work plan, step 2 (csrc/cf.cu k_plan_emit): start / meta records."""
+    call("svdrec_cf_plan_emit", gd.numel(), ptr(gd), ptr(order), ptr(first), ptr(slot0), ptr(done_idx),
+         ptr(group_start), ptr(row_start), int(chunk), ptr(start), ptr(meta), stream_handle())
+
+
+def csr_transpose(indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, n_out: int,
+                  perm: torch.Tensor | None = None, relabel: bool = False):
+    """Stable counting-sort transpose (csrc/ingest.cu): returns (indptr,
+    indices, values) of the n_out-row transpose, the input rows taken in
+    the order ``perm`` (default: 0..m-1); entries carry the input row index,
+    or its position in ``perm`` when ``relabel``."""
+    dev = indptr.device
+    m = indptr.numel() - 1
+    if perm is None:
+        pptr = indptr
+    else:
+        pptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+        if m:
+            torch.cumsum((indptr[1:] - indptr[:-1])[perm], 0, out=pptr[1:])
+        perm = perm.to(torch.int32).contiguous()
+    nnz = int(indices.numel())
+    out_ptr = torch.empty(n_out + 1, dtype=torch.int64, device=dev)
+    out_idx = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    out_val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    if nnz == 0 or n_out == 0:
+        out_ptr.zero_()
+        return out_ptr, out_idx[:nnz], out_val[:nnz]
+    sb = int(query("svdrec_csr_transpose_scratch", n_out)) + 2 * ((nnz * 4 + 255) // 256 * 256)
+    ws = torch.empty(sb, dtype=torch.uint8, device=dev)  # transient (allocator-cached)
+    with _span("csr_transpose", nnz * (12 * 3 + 16)):
+        call("svdrec_csr_transpose", m, n_out, nnz, ptr(indptr), ptr(indices), ptr(values),
+             ptr(perm) if perm is not None else None, ptr(pptr), int(relabel), ptr(out_ptr), ptr(out_idx),
+             ptr(out_val), ptr(ws), sb, stream_handle())
+    return out_ptr, out_idx, out_val
 
 
 def err_sum(pred: torch.Tensor, truth: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -441,15 +476,6 @@ def count_overlap(users: torch.Tensor, items: torch.Tensor, csr) -> torch.Tensor
     call("svdrec_count_overlap", users.shape[0], ptr(users), ptr(items), ptr(csr.indptr), ptr(csr.indices),
          ptr(cnt), stream_handle())
     return cnt
-
-
-def lowrank_predict(users: torch.Tensor, items: torch.Tensor, U: torch.Tensor, s: torch.Tensor, V: torch.Tensor,
-                    mu: float) -> torch.Tensor:
-    ldu, ldv = _mat(U, "lowrank.U"), _mat(V, "lowrank.V")
-    pred = torch.empty(users.shape[0], dtype=F64, device=U.device)
-    call("svdrec_lowrank_predict", users.shape[0], ptr(users), ptr(items), U.shape[1], ptr(U), ldu, ptr(s),
-         ptr(V), ldv, float(mu), ptr(pred), stream_handle())
-    return pred
 
 
 def check_status(status: torch.Tensor) -> int:

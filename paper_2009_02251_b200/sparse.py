@@ -236,6 +236,7 @@ class DeviceCSR:
         self.warp_seg = warp_plan_t(sb, se, self.nwarp)
         self._partial = {}
         self._ranked = None
+        self._transpose = None
         self._sched = {}
         self.h2d_bytes = h2d_bytes
 
@@ -248,15 +249,15 @@ class DeviceCSR:
                    h2d_bytes=(csr.shape[0] + 1) * 8 + csr.nnz * 12)
 
     def transposed(self) -> "DeviceCSR":
-        """CSR of the transpose, built on the device: a stable sort of the
-        column indices (rows stay ascending within each column)."""
-        rows = torch.repeat_interleave(torch.arange(self.m, dtype=torch.int32, device=self.device),
-                                       self.indptr[1:] - self.indptr[:-1])
-        perm = torch.sort(self.indices, stable=True).indices
-        counts = torch.bincount(self.indices, minlength=self.n)
-        indptr = torch.zeros(self.n + 1, dtype=torch.int64, device=self.device)
-        torch.cumsum(counts, 0, out=indptr[1:])
-        return DeviceCSR(indptr, rows[perm], self.values[perm], (self.n, self.m))
+        """CSR of the transpose, built on the device: a stable counting-sort
+        transpose (csrc/ingest.cu, no sort; rows stay ascending within each
+        column)."""
+        from . import kernels as K
+
+        indptr, rows, vals = K.csr_transpose(self.indptr, self.indices, self.values, self.n)
+        t = DeviceCSR(indptr, rows, vals, (self.n, self.m))
+        self._transpose = t
+        return t
 
     def schedule(self, warps_per_sm: int) -> tuple[int, torch.Tensor]:
         """(nwarp, warp_seg) for a kernel running ``warps_per_sm`` warps per SM."""
@@ -273,16 +274,20 @@ class DeviceCSR:
     def ranked(self):
         """(ranked indices, values, rank -> item order) for the CF scoring
         kernel: item ids replaced by popularity rank, each row ordered by
-        rank (built once on the device, cached)."""
+        rank.  Built once on the device (cached) as the transpose of A.T
+        with A.T's rows taken in rank order (csrc/ingest.cu): every user's
+        row then lists its items hottest first, relabelled by rank."""
         if self._ranked is None:
             from . import kernels as K
 
-            rk = K.cf_relabel(self.indices, self.item_rank)
-            rows = torch.repeat_interleave(torch.arange(self.m, dtype=torch.int64, device=self.device),
-                                           self.indptr[1:] - self.indptr[:-1])
-            perm = torch.sort(rows * self.n + rk.to(torch.int64)).indices
-            self._ranked = (rk[perm].contiguous(), self.values[perm].contiguous(), self.hot_items.to(torch.int64))
+            AT = self._transpose_of_self()
+            _, rk, rv = K.csr_transpose(AT.indptr, AT.indices, AT.values, self.m, perm=self.hot_items,
+                                        relabel=True)
+            self._ranked = (rk, rv, self.hot_items.to(torch.int64))
         return self._ranked
+
+    def _transpose_of_self(self) -> "DeviceCSR":
+        return self._transpose if self._transpose is not None else self.transposed()
 
     def partial(self, b: int) -> torch.Tensor | None:
         if self.nslots == 0:

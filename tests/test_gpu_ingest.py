@@ -1,0 +1,116 @@
+"""Device ingest: the stable counting-sort transpose (csrc/ingest.cu)
+against scipy's transpose and against a sort-based restatement of the
+ranked CSR, bit for bit (integer / index work)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from scipy import sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand_csr(m, n, density, seed, empty_rows=(), empty_cols=()):
+    rng = np.random.default_rng(seed)
+    M = sp.random(m, n, density=density, format="csr", random_state=rng, dtype=np.float64)
+    M.data[:] = rng.integers(1, 11, M.nnz) * 0.5
+    M = M.tolil()
+    for r in empty_rows:
+        M[r, :] = 0
+    for c in empty_cols:
+        M[:, c] = 0
+    M = M.tocsr()
+    M.eliminate_zeros()
+    M.sort_indices()
+    return M
+
+
+def _dev(M, dev):
+    import torch
+    return (torch.as_tensor(M.indptr.astype(np.int64), device=dev), torch.as_tensor(M.indices.astype(np.int32), device=dev),
+            torch.as_tensor(M.data, device=dev))
+
+
+@pytest.mark.parametrize("m,n,density,seed", [(300, 200, 0.05, 0), (2000, 57000, 0.002, 1), (1, 5, 1.0, 2),
+                                              (5000, 300, 0.2, 3)])
+def test_transpose_matches_scipy(gpu, m, n, density, seed):
+    from paper_2009_02251_b200 import kernels as K
+    M = _rand_csr(m, n, density, seed, empty_rows=(0,) if m > 1 else (), empty_cols=(1,))
+    ip, ix, dv = _dev(M, gpu)
+    tp, ti, tv = K.csr_transpose(ip, ix, dv, n)
+    T = M.T.tocsr()
+    T.sort_indices()
+    assert np.array_equal(tp.cpu().numpy(), T.indptr)
+    assert np.array_equal(ti.cpu().numpy(), T.indices)
+    assert np.array_equal(tv.cpu().numpy(), T.data)
+
+
+@pytest.mark.parametrize("m,n,seed", [(800, 300, 4), (60000, 900, 5)])
+def test_ranked_csr_matches_sort(gpu, m, n, seed):
+    """Transpose of A.T taken in popularity order == each row of A relabelled
+    by rank and sorted by rank (the previous sort-based construction)."""
+    import torch
+    from paper_2009_02251_b200 import kernels as K
+    M = _rand_csr(m, n, 0.02, seed)
+    T = M.T.tocsr()
+    deg = np.diff(T.indptr)
+    order = np.argsort(-deg, kind="stable")
+    rank = np.empty(n, dtype=np.int64)
+    rank[order] = np.arange(n)
+    ip, ix, dv = _dev(T, gpu)
+    _, rk, rv = K.csr_transpose(ip, ix, dv, m, perm=torch.as_tensor(order, device=gpu), relabel=True)
+    rows = np.repeat(np.arange(m), np.diff(M.indptr))
+    key = rows * n + rank[M.indices]
+    perm = np.argsort(key, kind="stable")
+    assert np.array_equal(rk.cpu().numpy(), rank[M.indices][perm])
+    assert np.array_equal(rv.cpu().numpy(), M.data[perm])
+
+
+def test_empty_transpose(gpu):
+    from paper_2009_02251_b200 import kernels as K
+    M = sp.csr_matrix((4, 6))
+    ip, ix, dv = _dev(M, gpu)
+    tp, ti, tv = K.csr_transpose(ip, ix, dv, 6)
+    assert tp.cpu().numpy().tolist() == [0] * 7 and ti.numel() == 0
+
+
+def _plan_torch(gd, group_start, row_start, chunk):
+    """The work plan as plain torch ops (the restatement the kernels replaced)."""
+    import torch
+    nch = torch.clamp((gd + chunk - 1) // chunk, min=1)
+    split = nch > 1
+    cs = torch.cumsum(torch.where(split, nch, torch.zeros_like(nch)), 0)
+    slot0 = torch.where(split, cs - nch, torch.full_like(nch, -1))
+    done = torch.where(split, torch.cumsum(split.to(torch.int64), 0) - 1, torch.full_like(nch, -1))
+    order = torch.sort(-gd, stable=True).indices
+    no = nch[order]
+    wg = torch.repeat_interleave(order, no)
+    first = torch.repeat_interleave(torch.cumsum(no, 0) - no, no)
+    wc = torch.arange(wg.numel(), device=gd.device) - first
+    sp_w = split[wg]
+    deg_w = gd[wg]
+    off = torch.where(sp_w, wc * chunk, torch.zeros_like(wc))
+    start = row_start[wg] + off
+    length = torch.where(sp_w, torch.clamp(deg_w - off, max=chunk), deg_w)
+    meta = torch.stack([length, deg_w, group_start[wg], group_start[wg + 1], nch[wg],
+                        torch.where(sp_w, slot0[wg] + wc, torch.full_like(wc, -1)), done[wg], wc], 1)
+    stats = (int(wg.numel()), int(split.sum()), int(torch.where(split, nch, torch.zeros_like(nch)).sum()),
+             int(gd.sum()))
+    return start, meta.to(torch.int32).flatten(), stats
+
+
+@pytest.mark.parametrize("ng,seed", [(1, 0), (37, 1), (5000, 2), (130000, 3)])
+def test_work_plan_kernels_match_torch(gpu, ng, seed):
+    import torch
+    from paper_2009_02251_b200.cf import WorkPlan
+    rng = np.random.default_rng(seed)
+    deg = np.minimum(rng.lognormal(4, 1.5, ng).astype(np.int64), 40000)
+    deg[: min(ng, 4)] = [0, 512, 513, 1024][: min(ng, 4)]
+    gd = torch.as_tensor(deg, device=gpu)
+    gs = torch.as_tensor(np.concatenate([[0], np.cumsum(rng.integers(1, 9, ng))]), device=gpu)
+    rs = torch.cumsum(gd, 0) - gd + 7
+    p = WorkPlan(gd, gpu, gs, rs)
+    start, meta, stats = _plan_torch(gd, gs, rs, WorkPlan.CHUNK)
+    assert (p.nwork, p.ndone, p.nslots, p.rated) == stats
+    assert torch.equal(p.start[: p.nwork], start)
+    assert torch.equal(p.meta[: 8 * p.nwork], meta)

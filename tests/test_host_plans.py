@@ -1,5 +1,6 @@
-"""Host-side planning logic (no GPU): the torch plan builders that run next
-to the data on the device must reproduce the numpy definitions exactly."""
+"""Planning logic: the plan builders that run next to the data on the
+device must reproduce the numpy definitions exactly (torch-op builders on
+CPU tensors; the kernel-built ones, marked gpu, on the device)."""
 import numpy as np
 import pytest
 import torch
@@ -40,30 +41,34 @@ def test_segment_and_warp_plans_match_numpy(seed):
         np.testing.assert_array_equal(S.warp_plan(sb, se, nw), S.warp_plan_t(got[1], got[2], nw).numpy())
 
 
-def test_device_transpose_matches_scipy():
+@pytest.mark.gpu
+def test_device_transpose_matches_scipy(gpu):
+    """DeviceCSR.transposed runs the counting-sort kernel (csrc/ingest.cu)."""
     import scipy.sparse as sp
     rng = np.random.default_rng(5)
     M = sp.random(300, 170, density=0.05, random_state=rng, format="csr")
     M.data = np.round(M.data * 9) / 2 + 0.5
-    d = S.DeviceCSR(torch.from_numpy(M.indptr.astype(np.int64)), torch.from_numpy(M.indices.astype(np.int32)),
-                    torch.from_numpy(M.data), M.shape)
+    d = S.DeviceCSR(torch.from_numpy(M.indptr.astype(np.int64)).to(gpu),
+                    torch.from_numpy(M.indices.astype(np.int32)).to(gpu), torch.from_numpy(M.data).to(gpu), M.shape)
     t = d.transposed()
     ref = M.T.tocsr()
     ref.sort_indices()
-    np.testing.assert_array_equal(t.indptr.numpy(), ref.indptr)
-    np.testing.assert_array_equal(t.indices.numpy(), ref.indices)
-    np.testing.assert_array_equal(t.values.numpy(), ref.data)
+    np.testing.assert_array_equal(t.indptr.cpu().numpy(), ref.indptr)
+    np.testing.assert_array_equal(t.indices.cpu().numpy(), ref.indices)
+    np.testing.assert_array_equal(t.values.cpu().numpy(), ref.data)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("chunk", [1, 3, 512])
-def test_workplan_matches_numpy(chunk, monkeypatch):
+def test_workplan_matches_numpy(gpu, chunk, monkeypatch):
+    """WorkPlan runs the plan kernels (csrc/cf.cu k_plan_scan / k_plan_emit)."""
     from paper_2009_02251_b200.cf import WorkPlan
     rng = np.random.default_rng(chunk)
     gd = rng.zipf(1.5, size=400).astype(np.int64) - 1
     gs = np.r_[0, np.cumsum(rng.integers(1, 4, size=400))]  # samples per group
     rs = np.r_[0, np.cumsum(gd)][:-1] + 7  # CSR offset of each group's row
     monkeypatch.setattr(WorkPlan, "CHUNK", chunk)
-    p = WorkPlan(torch.from_numpy(gd), torch.device("cpu"), torch.from_numpy(gs), torch.from_numpy(rs))
+    p = WorkPlan(torch.from_numpy(gd).to(gpu), gpu, torch.from_numpy(gs).to(gpu), torch.from_numpy(rs).to(gpu))
     work, ginfo, ndone, nslots = _np_workplan(gd, chunk)
     wg, wc = work[0::2], work[1::2]
     nch, slot0, done = ginfo[0::3], ginfo[1::3], ginfo[2::3]
@@ -72,8 +77,8 @@ def test_workplan_matches_numpy(chunk, monkeypatch):
     length = np.where(split, np.minimum(gd[wg] - wc * chunk, chunk), gd[wg])
     meta = np.stack([length, gd[wg], gs[wg], gs[wg + 1], nch[wg], np.where(split, slot0[wg] + wc, -1), done[wg],
                      wc], 1)
-    np.testing.assert_array_equal(p.start.numpy(), start)
-    np.testing.assert_array_equal(p.meta.numpy(), meta.ravel().astype(np.int32))
+    np.testing.assert_array_equal(p.start[: p.nwork].cpu().numpy(), start)
+    np.testing.assert_array_equal(p.meta[: 8 * p.nwork].cpu().numpy(), meta.ravel().astype(np.int32))
     assert (p.ndone, p.nslots, p.nwork) == (ndone, nslots, wg.size)
     # every rating of every user is covered exactly once by the items
     cover = np.zeros(int(rs[-1] + gd[-1] + 8), dtype=np.int64)
