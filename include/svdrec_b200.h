@@ -107,6 +107,25 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
  * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
  * fall back to the plain kernel. */
 int svdrec_spmm_warps_per_sm(int32_t b);
+/* Hot-set variant of A @ X (even b <= 32) on the popularity-ranked CSR
+ * (svdrec_rank_rows): d_hidx[t] = -(rank + 1) for entries of the nhot
+ * most rated items (rank < nhot; their rows X[d_hot_items[rank]] are
+ * staged in every CTA's shared memory) and the item id otherwise, built by
+ * svdrec_spmm_hot_encode from the ranked indices and the rank -> item
+ * order; d_hval the ranked values.  Same segment plan / fix-up as
+ * svdrec_spmm (the ranked CSR has A's row structure), schedule of 16 warps
+ * per SM; nhot <= svdrec_spmm_hot_rows(b), which is 0 for the widths
+ * where the TMA-gather kernel is faster (the host then calls svdrec_spmm). */
+int svdrec_spmm_hot_rows(int32_t b);
+int svdrec_spmm_hot_encode(int64_t nnz, const int32_t* d_ranked, const int32_t* d_order, int32_t nhot,
+                           int32_t* d_out, void* stream);
+int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                    const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_hidx,
+                    const double* d_hval, const double* d_X, int64_t ldx, int64_t x_rows,
+                    const int32_t* d_hot_items,
+                    int32_t nhot, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
+                    const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1,
+                    int64_t nwarp, const int32_t* d_warp_seg, double* d_partial, void* stream);
 /* fp32 variant: X stored as float (half the gathered bytes), values,
  * accumulation and Y in double.  b in {4, 8, ..., 64}, 16-B aligned rows,
  * a schedule of svdrec_spmm_x32_warps_per_sm(b) warps per SM. */
@@ -348,6 +367,19 @@ int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double* d_Z, int6
 size_t svdrec_err_sum_workspace_bytes(int64_t nsamp);
 int svdrec_err_sum(int64_t nsamp, const double* d_pred, const double* d_truth,
                    double* d_out2, void* d_work, size_t work_bytes, void* stream);
+
+/* Popularity-ranked copy of a CSR (m rows, n <= 65536 columns), for
+ * svdrec_cf_predict: every entry's column replaced by d_rank[column] and
+ * every row reordered by rank (ranks distinct within a row).  One warp per
+ * row: a shared-memory bitset over the n ranks gives each entry's position
+ * (no sort; row-local writes).  Output has d_indptr's row structure. */
+int svdrec_rank_rows(int64_t m, int32_t n, const int64_t* d_indptr, const int32_t* d_indices,
+                     const double* d_values, const int32_t* d_rank, int32_t* d_out_indices,
+                     double* d_out_values, void* stream);
+
+/* Exclusive scan of n int64 values (d_in may equal d_out); the total goes
+ * to d_total (nullable). */
+int svdrec_scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, void* stream);
 
 /* Count samples whose (user, item) is stored in the CSR (ValidationMae's
  * disjointness check, cf.py:243-254); binary search per sample. */

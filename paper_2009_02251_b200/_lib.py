@@ -34,6 +34,10 @@ SIGNATURES = {
     "svdrec_normal_fill": (C.c_int, [_u64, _u64, _p, _i64, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_warps_per_sm": (C.c_int, [_i32]),
+    "svdrec_spmm_hot_rows": (C.c_int, [_i32]),
+    "svdrec_spmm_hot_encode": (C.c_int, [_i64, _p, _p, _i32, _p, _p]),
+    "svdrec_spmm_hot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i32, _p, _i64, _i32, _i64, _p, _p,
+                                  _p, _i64, _p, _p, _p]),
     "svdrec_spmm_x32_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_x32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_gemm_tn_workspace_bytes": (_sz, [_i64, _i64, _i64]),
@@ -69,6 +73,8 @@ SIGNATURES = {
     "svdrec_cf_plan_scan": (C.c_int, [_i64, _p, _p, _i32, _p, _p, _p, _p, _p]),
     "svdrec_cf_plan_emit": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "svdrec_csr_transpose_scratch": (_i64, [_i64]),
+    "svdrec_rank_rows": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _p, _p, _p]),
+    "svdrec_scan_i64": (C.c_int, [_i64, _p, _p, _p, _p]),
     "svdrec_csr_transpose": (C.c_int, [_i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _i64, _p]),
     "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
     "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),

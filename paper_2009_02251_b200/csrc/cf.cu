@@ -498,17 +498,23 @@ __global__ void __launch_bounds__(1024) k_plan_scan(int64_t ng, const int64_t* _
   const int T = blockDim.x, t = threadIdx.x;
   const int64_t per = (ng + T - 1) / T;
   const int64_t a = min64(ng, per * t), b = min64(ng, a + per);
-  auto nch_of = [&](int64_t d) -> int64_t { return d <= chunk ? 1 : (d + chunk - 1) / chunk; };
+  // 32-bit division (a 64-bit one is a long emulated sequence on the GPU)
+  auto nch_of = [&](int64_t d) -> int64_t {
+    return d <= chunk ? 1 : (int64_t)(((uint32_t)d + (uint32_t)chunk - 1u) / (uint32_t)chunk);
+  };
   int64_t sl = 0, dn = 0, it = 0, rated = 0;
+#pragma unroll 8
   for (int64_t g = a; g < b; ++g) {
-    const int64_t n = nch_of(gd[g]);
+    const int64_t d = gd[g];
+    const int64_t n = nch_of(d);
     if (n > 1) {
       sl += n;
       dn += 1;
     }
-    it += nch_of(gd[order[g]]);
-    rated += gd[g];
+    rated += d;
   }
+#pragma unroll 8
+  for (int64_t g = a; g < b; ++g) it += nch_of(gd[order[g]]);
   sh[0][t] = sl;
   sh[1][t] = dn;
   sh[2][t] = it;
@@ -528,6 +534,7 @@ __global__ void __launch_bounds__(1024) k_plan_scan(int64_t ng, const int64_t* _
   }
   int64_t s0 = sh[0][t] - sl, d0 = sh[1][t] - dn, i0 = sh[2][t] - it;
   const int64_t nslots = sh[0][T - 1];
+#pragma unroll 8
   for (int64_t g = a; g < b; ++g) {
     const int64_t n = nch_of(gd[g]);
     slot0[g] = n > 1 ? (int32_t)s0 : -1;
@@ -536,6 +543,9 @@ __global__ void __launch_bounds__(1024) k_plan_scan(int64_t ng, const int64_t* _
       s0 += n;
       d0 += 1;
     }
+  }
+#pragma unroll 8
+  for (int64_t g = a; g < b; ++g) {
     first[g] = i0;
     i0 += nch_of(gd[order[g]]);
   }
@@ -565,7 +575,7 @@ __global__ void k_plan_emit(int64_t ng, const int64_t* __restrict__ gd, const in
   if (j >= ng) return;
   const int64_t g = order[j];
   const int64_t deg = gd[g];
-  const int64_t nch = deg <= chunk ? 1 : (deg + chunk - 1) / chunk;
+  const int64_t nch = deg <= chunk ? 1 : (int64_t)(((uint32_t)deg + (uint32_t)chunk - 1u) / (uint32_t)chunk);
   const bool split = nch > 1;
   const int64_t w0 = first[j];
   for (int64_t c = 0; c < nch; ++c) {

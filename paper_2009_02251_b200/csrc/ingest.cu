@@ -98,34 +98,6 @@ __global__ void k_tr_totals(int32_t nb, int32_t g, const int32_t* __restrict__ h
   counts[c] = s;
 }
 
-// exclusive scan of counts[0, n) into indptr[0, n] (one CTA; n is a column
-// count, up to a few hundred thousand)
-__global__ void __launch_bounds__(1024) k_scan_counts(int64_t n, const int64_t* __restrict__ counts,
-                                                      int64_t* __restrict__ indptr) {
-  __shared__ int64_t part[1024];
-  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t a = min64(n, per * threadIdx.x), b = min64(n, a + per);
-  int64_t s = 0;
-#pragma unroll 8
-  for (int64_t i = a; i < b; ++i) s += counts[i];
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-    const int64_t v = threadIdx.x >= (unsigned)off ? part[threadIdx.x - off] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
-  }
-  int64_t run = part[threadIdx.x] - s;
-#pragma unroll 8
-  for (int64_t i = a; i < b; ++i) {
-    const int64_t c = counts[i];
-    indptr[i] = run;
-    run += c;
-  }
-  if (threadIdx.x == blockDim.x - 1) indptr[n] = part[threadIdx.x];
-}
-
 // relabel: output column id = the input row's processing position (rank)
 // instead of its index
 template <bool RELABEL>
@@ -199,10 +171,223 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_scatter(const int32_t* __rest
   }
 }
 
+// Ranked rows without a sort: every row's entries relabelled by the item
+// rank table and reordered by rank.  Ranks are distinct within a row, so
+// an entry's position in its row is the number of the row's ranks below
+// its own: one warp per row marks the row's ranks in a shared-memory
+// bitset over all n ranks, scans the words' popcounts, and reads each
+// position off the bitset (O(n / 32 + deg) per row, coalesced row-local
+// writes).  n <= kRankBits.
+constexpr int kRankWarps = 8;
+constexpr int kRankBits = 64 * 1024;
+constexpr int kRankWords = kRankBits / 32;
+
+__global__ void __launch_bounds__(kRankWarps * 32) k_rank_rows(int64_t m, int32_t n, const int64_t* __restrict__ indptr,
+                                                                const int32_t* __restrict__ indices,
+                                                                const double* __restrict__ values,
+                                                                const int32_t* __restrict__ rank,
+                                                                int32_t* __restrict__ out_idx,
+                                                                double* __restrict__ out_val) {
+  extern __shared__ uint32_t rs_mem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwords = (n + 31) >> 5;
+  uint32_t* bits = rs_mem + (size_t)wid * 2 * nwords;
+  uint32_t* pref = bits + nwords;  // exclusive prefix popcount per word
+  const int64_t gw = (int64_t)blockIdx.x * kRankWarps + wid;
+  const int64_t nw = (int64_t)gridDim.x * kRankWarps;
+  for (int i = lane; i < nwords; i += 32) bits[i] = 0u;
+  __syncwarp();
+  for (int64_t r = gw; r < m; r += nw) {
+    const int64_t a = indptr[r], b = indptr[r + 1];
+    // (the three passes over the row are unrolled so that a typical row's
+    // index and rank loads are all in flight at once)
+#pragma unroll 4
+    for (int64_t t = a + lane; t < b; t += 32) {
+      const int32_t k = rank[indices[t]];
+      atomicOr(&bits[k >> 5], 1u << (k & 31));
+    }
+    __syncwarp();
+    // prefix popcount over the words: each lane a contiguous stretch
+    const int per = (nwords + 31) >> 5;
+    const int w0 = lane * per, w1 = min(nwords, w0 + per);
+    int sum = 0;
+    for (int i = w0; i < w1; ++i) sum += __popc(bits[i]);
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+    for (int i = w0; i < w1; ++i) {
+      pref[i] = (uint32_t)run;
+      run += __popc(bits[i]);
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int64_t t = a + lane; t < b; t += 32) {
+      const int32_t k = rank[indices[t]];
+      const int pos = (int)pref[k >> 5] + __popc(bits[k >> 5] & ((1u << (k & 31)) - 1u));
+      out_idx[a + pos] = k;
+      out_val[a + pos] = values[t];
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int64_t t = a + lane; t < b; t += 32) bits[rank[indices[t]] >> 5] = 0u;  // clear only what was set
+    __syncwarp();
+  }
+}
+
+// Exclusive scan of int64 (n values) in three launches: per-tile sums,
+// one CTA scanning the tile sums, per-tile scan plus offset.  Optional
+// total written at out[n].
+constexpr int kScanT = 1024;
+constexpr int kScanPer = 8;  // values per thread per tile
+
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* sh, int64_t* total) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  int64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) sh[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int nwarp = blockDim.x >> 5;
+    int64_t x = lane < nwarp ? sh[lane] : 0;
+    int64_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += u;
+    }
+    if (lane < nwarp) sh[lane] = xi - x;
+    if (lane == nwarp - 1) sh[32] = xi;
+  }
+  __syncthreads();
+  const int64_t r = sh[wid] + incl - v;
+  if (total) *total = sh[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_tiles(int64_t n, const int64_t* __restrict__ in,
+                                                       int64_t* __restrict__ tile_sum) {
+  __shared__ int64_t sh[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanT * kScanPer + (int64_t)threadIdx.x * kScanPer;
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i)
+    if (base + i < n) s += in[base + i];
+  int64_t tot;
+  block_excl_scan(s, sh, &tot);
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_sums(int64_t ntiles, int64_t* __restrict__ tile_sum,
+                                                      int64_t* __restrict__ grand) {
+  __shared__ int64_t sh[33];
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < ntiles; b0 += kScanT) {
+    const int64_t i = b0 + threadIdx.x;
+    const int64_t v = i < ntiles ? tile_sum[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan(v, sh, &tot);
+    if (i < ntiles) tile_sum[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && grand) *grand = carry;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_apply(int64_t n, const int64_t* __restrict__ in,
+                                                       const int64_t* __restrict__ tile_off,
+                                                       int64_t* __restrict__ out) {
+  __shared__ int64_t sh[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanT * kScanPer + (int64_t)threadIdx.x * kScanPer;
+  int64_t v[kScanPer];
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0;
+    s += v[i];
+  }
+  int64_t run = tile_off[blockIdx.x] + block_excl_scan(s, sh, nullptr);
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+}
+
 }  // namespace
 }  // namespace svdrec
 
 using namespace svdrec;
+
+namespace svdrec {
+// exclusive scan of n int64 values (in may alias out); total -> *d_total
+// (nullable).  Scratch for the tile sums: a small cached device buffer.
+int scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, cudaStream_t s, int* launches) {
+  const int64_t per_tile = (int64_t)kScanT * kScanPer;
+  const int64_t ntiles = (n + per_tile - 1) / per_tile;
+  // tile sums: a grow-only buffer per device (stream-ordered allocations)
+  static int64_t* bufs[64] = {};
+  static int64_t caps[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return (int)cudaErrorInvalidDevice;
+  if (ntiles + 1 > caps[dev]) {
+    if (bufs[dev]) cudaFreeAsync(bufs[dev], s);
+    caps[dev] = ntiles + 1 > 4096 ? ntiles + 1 : 4096;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bufs[dev]), (size_t)caps[dev] * sizeof(int64_t), s);
+    if (e != cudaSuccess) {
+      bufs[dev] = nullptr;
+      caps[dev] = 0;
+      return (int)e;
+    }
+  }
+  int64_t* buf = bufs[dev];
+  if (n > 0) {
+    k_scan_tiles<<<(unsigned)ntiles, kScanT, 0, s>>>(n, d_in, buf);
+    k_scan_sums<<<1, kScanT, 0, s>>>(ntiles, buf, d_total);
+    k_scan_apply<<<(unsigned)ntiles, kScanT, 0, s>>>(n, d_in, buf, d_out);
+    *launches += 3;
+  } else if (d_total) {
+    cudaMemsetAsync(d_total, 0, sizeof(int64_t), s);
+  }
+  return (int)cudaGetLastError();
+}
+}  // namespace svdrec
+
+extern "C" int svdrec_rank_rows(int64_t m, int32_t n, const int64_t* d_indptr, const int32_t* d_indices,
+                                const double* d_values, const int32_t* d_rank, int32_t* d_out_indices,
+                                double* d_out_values, void* stream) {
+  SVDREC_ARG(m >= 0 && n >= 1 && n <= kRankBits, "rank_rows: needs 1 <= n <= %d (n=%d)", kRankBits, n);
+  if (m == 0) return 0;
+  const int nwords = (n + 31) / 32;
+  const size_t smem = (size_t)kRankWarps * 2 * nwords * sizeof(uint32_t);
+  SVDREC_CUDA(smem_attr_once(k_rank_rows, (int)((size_t)kRankWarps * 2 * kRankWords * sizeof(uint32_t))));
+  int per_sm = 0;
+  SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rank_rows, kRankWarps * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = min64((int64_t)sm_count() * per_sm, (m + kRankWarps - 1) / kRankWarps);
+  k_rank_rows<<<(unsigned)grid, kRankWarps * 32, smem, as_stream(stream)>>>(m, n, d_indptr, d_indices, d_values,
+                                                                             d_rank, d_out_indices, d_out_values);
+  return check_launch("rank_rows");
+}
+
+extern "C" int svdrec_scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, void* stream) {
+  SVDREC_ARG(n >= 0, "scan_i64: bad arguments");
+  int launches = 0;
+  const int rc = scan_i64(n, d_in, d_out, d_total, as_stream(stream), &launches);
+  if (rc) {
+    set_error("scan_i64: %s", cudaGetErrorString((cudaError_t)rc));
+    return rc;
+  }
+  return check_launch("scan_i64", launches);
+}
 
 extern "C" int64_t svdrec_csr_transpose_scratch(int64_t n_out) {
   // hist tables (int32, n_out x slices) + column totals (int64); the
@@ -246,8 +431,7 @@ extern "C" int svdrec_csr_transpose(int64_t nrows, int64_t n_out, int64_t total,
     k_tr_totals<<<(nb + 255) / 256, 256, 0, s>>>(nb, g, hist, counts + c0);
     launches += 2;
   }
-  k_scan_counts<<<1, 1024, 0, s>>>(n_out, counts, d_out_indptr);
-  launches += 1;
+  SVDREC_CUDA((cudaError_t)scan_i64(n_out, counts, d_out_indptr, d_out_indptr + n_out, s, &launches));
   // pass 2: per range, histogram (kept from pass 1 for a single range) ->
   // offsets -> stable scatter
   for (int64_t c0 = 0; c0 < n_out && total > 0; c0 += kBins) {

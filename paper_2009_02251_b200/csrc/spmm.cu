@@ -530,6 +530,215 @@ int tma_dispatch4_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_s
 #undef SVDREC_TMA4F
 }
 
+// ---------------------------------------------------------------------------
+// Hot-set variant for A @ X on the popularity-ranked CSR (b even, b <= 32).
+// Each row's entries are stored hottest item first; an entry's index is
+// -(rank + 1) for the nhot most rated items -- whose rows of X are staged
+// once per CTA in shared memory -- and the item id otherwise.  A 32-entry
+// batch therefore splits into a shared-memory prefix (LDS) and an
+// L2-gathered suffix (LDG, U steps in flight per lane), so only the cold
+// entries reach L2 (c3, b = 20: 1,280 hot rows hold ~66 % of the ratings).
+// One persistent CTA per SM; lanes as in k_spmm_tma (G = 32 / P groups of
+// P lanes x 2 doubles), nonzero-balanced warp ranges, fixed-order group
+// fold, two accumulator chains; loads are unconditional (masked entries
+// read a valid row and contribute 0 * x).
+struct __align__(16) TabEnt {
+  int32_t off;  // hot: rank * P (double2 units in shared memory); cold: item * ldx / 2
+  int32_t pad;
+  double v;
+};
+constexpr int kHotWarps = 16;
+constexpr int kTabSlots = 32 + 32;  // a batch + the padding of G * U <= 32 steps
+
+template <int P, int U>
+__global__ void __launch_bounds__(512, 1) k_spmm_hot(
+    int64_t nwarp, const int32_t* __restrict__ warp_seg, const int32_t* __restrict__ seg_row,
+    const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
+    const int32_t* __restrict__ hidx, const double* __restrict__ hval, const double* __restrict__ X, int64_t ldx,
+    const int32_t* __restrict__ hot_items, int nhot, double* __restrict__ Y, int64_t ldy,
+    double* __restrict__ partial) {
+  constexpr int B = 2 * P, G = 32 / P;
+  static_assert(G * U <= 32, "spmm_hot: padding exceeds the table");
+  __shared__ TabEnt tabs[kHotWarps * 2 * kTabSlots];
+  extern __shared__ __align__(16) double hs[];  // nhot rows of B doubles
+  for (int t = threadIdx.x; t < nhot * P; t += blockDim.x) {
+    const int r = t / P, c = t - (t / P) * P;
+    reinterpret_cast<double2*>(hs)[t] =
+        *reinterpret_cast<const double2*>(X + (int64_t)hot_items[r] * ldx + 2 * c);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nwarp) return;
+  const int g = lane / P, pc = lane - (lane / P) * P;
+  const bool active = g < G;
+  const double2* hrow = reinterpret_cast<const double2*>(hs) + pc;   // + rank * P
+  const double2* xrow = reinterpret_cast<const double2*>(X) + pc;    // + item * ldx / 2
+  const int64_t ldx2 = ldx / 2;
+  const int32_t s_lo = warp_seg[w], s_hi = warp_seg[w + 1];
+  // segment metadata, 32 segments at a time (as k_spmm_tma)
+  int32_t sb = s_lo;
+  int64_t mb = 0, me = 0;
+  int32_t mrow = 0, mslot = -1;
+  auto load_meta = [&]() {
+    const int32_t sg = sb + lane;
+    if (sg < s_hi) {
+      mb = seg_begin[sg];
+      me = seg_end[sg];
+      mrow = seg_row[sg];
+      mslot = seg_slot[sg];
+    }
+  };
+  load_meta();
+  int32_t cur = s_lo;
+  int64_t cb = 0, ce = 0;
+  int32_t crow = 0, cslot = -1;
+  auto enter = [&]() {
+    if (cur - sb >= 32) {
+      sb = cur;
+      load_meta();
+    }
+    const int i = cur - sb;
+    cb = __shfl_sync(0xffffffffu, mb, i);
+    ce = __shfl_sync(0xffffffffu, me, i);
+    crow = __shfl_sync(0xffffffffu, mrow, i);
+    cslot = __shfl_sync(0xffffffffu, mslot, i);
+  };
+  if (cur < s_hi) enter();
+  // the next 32-entry batch is loading while one is accumulated (two
+  // statically named buffers: no register move waits on a pending load)
+  struct Batch {
+    int32_t ci, row, slot;
+    double vi;
+    int nv, flags;  // flags bit 0: first batch of its segment, bit 1: last
+    bool ok;        // a batch (empty rows give batches with nv = 0)
+  };
+  bool cfirst = true;
+  auto load_batch = [&](Batch& k) {
+    k.ok = cur < s_hi;
+    if (!k.ok) return;
+    k.nv = (int)min64(32, ce - cb);
+    k.ci = 0;
+    k.vi = 0.0;
+    if (lane < k.nv) {
+      k.ci = __ldcs(hidx + cb + lane);
+      k.vi = __ldcs(hval + cb + lane);
+    }
+    const bool last = cb + 32 >= ce;
+    k.flags = (cfirst ? 1 : 0) | (last ? 2 : 0);
+    k.row = crow;
+    k.slot = cslot;
+    cfirst = false;
+    cb += 32;
+    if (last) {
+      ++cur;
+      cfirst = true;
+      if (cur < s_hi) enter();
+    }
+  };
+  // per-warp batch tables (offset, value): the hot prefix and the cold
+  // suffix of the current batch, each padded with G * U zero entries so
+  // the unrolled steps need no masks (a pad reads row 0 times 0.0)
+  TabEnt* ht = tabs + (size_t)(threadIdx.x >> 5) * 2 * kTabSlots;
+  TabEnt* ct = ht + kTabSlots;
+  double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+  auto process = [&](const Batch& k) {
+    const int32_t ci = k.ci;
+    const double vi = k.vi;
+    const int nv = k.nv;
+    if (k.flags & 1) {
+      a0 = make_double2(0.0, 0.0);
+      a1 = make_double2(0.0, 0.0);
+    }
+    const bool hot = lane < nv && ci < 0;
+    const int nh = __popc(__ballot_sync(0xffffffffu, hot));  // hot prefix
+    __syncwarp();  // the previous batch's tables are consumed
+    if (lane < nv) {
+      if (hot)
+        ht[lane] = TabEnt{(-ci - 1) * P, 0, vi};
+      else
+        ct[lane - nh] = TabEnt{ci * (int32_t)ldx2, 0, vi};
+    }
+    if (lane < G * U) {
+      ht[nh + lane] = TabEnt{0, 0, 0.0};
+      ct[nv - nh + lane] = TabEnt{0, 0, 0.0};
+    }
+    __syncwarp();
+    if (active) {
+      // hot entries: shared memory
+      for (int j = 0; j < nh; j += G * U) {
+        double2 x[U];
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const TabEnt e = ht[j + u * G + g];
+          v[u] = e.v;
+          x[u] = hrow[e.off];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          double2& acc = (u & 1) ? a1 : a0;
+          acc.x = fma(v[u], x[u].x, acc.x);
+          acc.y = fma(v[u], x[u].y, acc.y);
+        }
+      }
+      // cold entries: gathered from L2
+      for (int j = 0; j < nv - nh; j += G * U) {
+        double2 x[U];
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const TabEnt e = ct[j + u * G + g];
+          v[u] = e.v;
+          x[u] = __ldg(xrow + e.off);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          double2& acc = (u & 1) ? a1 : a0;
+          acc.x = fma(v[u], x[u].x, acc.x);
+          acc.y = fma(v[u], x[u].y, acc.y);
+        }
+      }
+    }
+    if (k.flags & 2) {
+      double2 t0 = make_double2(a0.x + a1.x, a0.y + a1.y);
+      double2 tot = t0;
+#pragma unroll
+      for (int h = 1; h < G; ++h) {
+        const double2 o = shfl_v(t0, (lane + h * P) & 31);
+        if (g == 0) {
+          tot.x += o.x;
+          tot.y += o.y;
+        }
+      }
+      if (g == 0) {
+        double* dst = k.slot < 0 ? (Y + (int64_t)k.row * ldy + 2 * pc) : (partial + (int64_t)k.slot * B + 2 * pc);
+        *reinterpret_cast<double2*>(dst) = tot;
+      }
+    }
+  };
+  Batch q0, q1;
+  load_batch(q0);
+  load_batch(q1);
+  while (q0.ok) {
+    process(q0);
+    load_batch(q0);
+    if (!q1.ok) break;
+    process(q1);
+    load_batch(q1);
+  }
+}
+
+// hot-encoded index of the ranked CSR: -(rank + 1) for rank < nhot, else
+// the item id (order[rank])
+__global__ void k_hot_encode(int64_t nnz, const int32_t* __restrict__ rk, const int32_t* __restrict__ order,
+                             int nhot, int32_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  const int32_t r = rk[t];
+  out[t] = r < nhot ? -(r + 1) : order[r];
+}
+
 __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, const int32_t* __restrict__ s0,
                         const int32_t* __restrict__ s1, const double* __restrict__ partial, double* __restrict__ Y,
                         int64_t ldy, int b) {
@@ -632,6 +841,83 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
                            const int32_t* d_warp_seg, double* d_partial, void* stream) {
   return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
                    ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, stream);
+}
+
+extern "C" int svdrec_spmm_hot_rows(int32_t b) {
+  if (b < 2 || b > 32 || b % 2) return 0;
+  // where the hot-set kernel beats k_spmm_tma (c3, A @ X, per call):
+  // b = 2 259 vs 339 us, 8 242 vs 320, 16 295 vs 338, 32 379 vs 592; not at
+  // b = 20 (397-414 vs 363: 160-B rows cost ~2 shared-memory wavefronts per
+  // hot entry through bank conflicts -- ncu: L1 data pipe 86 % busy)
+  if (b > 16 && b != 32) return 0;
+  // one 512-thread CTA per SM; the hot rows fill the 227 KB opt-in
+  return (int)((226 * 1024 - kHotWarps * 2 * kTabSlots * (int)sizeof(TabEnt)) / (8 * b));
+}
+
+extern "C" int svdrec_spmm_hot_encode(int64_t nnz, const int32_t* d_ranked, const int32_t* d_order, int32_t nhot,
+                                      int32_t* d_out, void* stream) {
+  SVDREC_ARG(nnz >= 0 && nhot >= 0, "spmm_hot_encode: bad arguments");
+  if (nnz == 0) return 0;
+  k_hot_encode<<<(unsigned)((nnz + 255) / 256), 256, 0, as_stream(stream)>>>(nnz, d_ranked, d_order, nhot, d_out);
+  return check_launch("spmm_hot_encode");
+}
+
+extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                               const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_hidx,
+                               const double* d_hval, const double* d_X, int64_t ldx, int64_t x_rows,
+                               const int32_t* d_hot_items,
+                               int32_t nhot, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
+                               const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1,
+                               int64_t nwarp, const int32_t* d_warp_seg, double* d_partial, void* stream) {
+  SVDREC_ARG(b >= 2 && b <= 32 && b % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0 && ldx >= b && ldy >= b,
+             "spmm_hot: needs even b <= 32 and 16-B aligned rows (b=%d)", b);
+  SVDREC_ARG(nhot >= 0 && nhot <= svdrec_spmm_hot_rows(b), "spmm_hot: %d hot rows exceed shared memory", nhot);
+  SVDREC_ARG(nwarp > 0 && d_warp_seg, "spmm_hot: needs a warp schedule (16 warps per SM)");
+  SVDREC_ARG(x_rows * (ldx / 2) < (1ll << 31), "spmm_hot: X too large for 32-bit row offsets");
+  SVDREC_ARG(((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
+               reinterpret_cast<uintptr_t>(d_partial)) % 16) == 0, "spmm_hot: operands must be 16-B aligned");
+  if (nseg == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  const size_t smem = (size_t)nhot * b * sizeof(double);
+  const int64_t grid = (nwarp + 15) / 16;
+#define SVDREC_HOT(PP)                                                                                     \
+  case PP:                                                                                                 \
+    SVDREC_CUDA(smem_attr_once(k_spmm_hot<PP, (PP < 8 ? PP : 8)>,                                         \
+                               226 * 1024 - kHotWarps * 2 * kTabSlots * (int)sizeof(TabEnt)));           \
+    k_spmm_hot<PP, (PP < 8 ? PP : 8)><<<(unsigned)grid, 512, smem, s>>>(                                   \
+        nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_hidx, d_hval, d_X, ldx,        \
+        d_hot_items, nhot, d_Y, ldy, d_partial);                                                           \
+    break;
+  switch (b / 2) {
+    SVDREC_HOT(1)
+    SVDREC_HOT(2)
+    SVDREC_HOT(3)
+    SVDREC_HOT(4)
+    SVDREC_HOT(5)
+    SVDREC_HOT(6)
+    SVDREC_HOT(7)
+    SVDREC_HOT(8)
+    SVDREC_HOT(9)
+    SVDREC_HOT(10)
+    SVDREC_HOT(11)
+    SVDREC_HOT(12)
+    SVDREC_HOT(13)
+    SVDREC_HOT(14)
+    SVDREC_HOT(15)
+    SVDREC_HOT(16)
+    default:
+      return SVDREC_E_ARG;
+  }
+#undef SVDREC_HOT
+  int rc = check_launch("spmm_hot");
+  if (rc) return rc;
+  if (nlong > 0) {
+    const int64_t tot = nlong * b;
+    k_fixup<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial,
+                                                          d_Y, ldy, b);
+    rc = check_launch("spmm_fixup");
+  }
+  return rc;
 }
 
 extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,

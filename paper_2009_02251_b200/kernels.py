@@ -8,6 +8,8 @@ copies.  Nothing here synchronises the device.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -154,9 +156,37 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
                  plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), *sched, ptr(part),
                  stream_handle())
         return Y
+    hot = _hot_rows(plan, b, ldx, ldy)
     with _span("spmm", nbytes, gathered):
-        _spmm_tma(plan, X, ldx, Y, ldy, b)
+        if hot:
+            _spmm_hot(plan, X, ldx, Y, ldy, b, hot)
+        else:
+            _spmm_tma(plan, X, ldx, Y, ldy, b)
     return Y
+
+
+# SVDREC_SPMM_HOT=0 keeps A @ X on the TMA-gather kernel (A/B measurements)
+SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "1") != "0"
+
+
+def _hot_rows(plan, b: int, ldx: int, ldy: int) -> int:
+    """Hot rows of X staged in shared memory by the hot-set kernel, or 0
+    when it does not apply (no popularity order on this CSR, odd b, b > 32)."""
+    if not SPMM_HOT or getattr(plan, "item_rank", None) is None or b % 2 or b > 32 or ldx % 2 or ldy % 2:
+        return 0
+    if plan.n * (ldx // 2) >= 1 << 31:
+        return 0
+    return min(int(query("svdrec_spmm_hot_rows", b)), plan.n)
+
+
+def _spmm_hot(plan, X, ldx, Y, ldy, b, nhot):
+    """The hot-set kernel (csrc/spmm.cu k_spmm_hot) on the ranked CSR."""
+    hidx, hval = plan.hot_encoded(nhot)
+    nwarp, wseg = plan.schedule(16)
+    call("svdrec_spmm_hot", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
+         ptr(hidx), ptr(hval), ptr(X), ldx, plan.n, ptr(plan.hot_items), nhot, ptr(Y), ldy, b, plan.nlong,
+         ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(plan.partial(b)),
+         stream_handle())
 
 
 def _spmm_tma(plan, X, ldx, Y, ldy, b):
@@ -428,6 +458,28 @@ def cf_plan_emit(gd, order, first, slot0, done_idx, group_start, row_start, chun
     """Scoring work plan, step 2 (csrc/cf.cu k_plan_emit): start / meta records."""
     call("svdrec_cf_plan_emit", gd.numel(), ptr(gd), ptr(order), ptr(first), ptr(slot0), ptr(done_idx),
          ptr(group_start), ptr(row_start), int(chunk), ptr(start), ptr(meta), stream_handle())
+
+
+def rank_rows(indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, n: int, rank: torch.Tensor):
+    """(ranked indices, values): columns relabelled by ``rank`` (int32, n
+    entries) and every row ordered by rank (csrc/ingest.cu k_rank_rows)."""
+    nnz = int(indices.numel())
+    out_idx = torch.empty(nnz, dtype=torch.int32, device=indices.device)
+    out_val = torch.empty(nnz, dtype=torch.float64, device=indices.device)
+    if nnz:
+        with _span("rank_rows", nnz * 24 + n * 4):
+            call("svdrec_rank_rows", indptr.numel() - 1, n, ptr(indptr), ptr(indices), ptr(values),
+                 ptr(rank.to(torch.int32).contiguous()), ptr(out_idx), ptr(out_val), stream_handle())
+    return out_idx, out_val
+
+
+def scan_i64(x: torch.Tensor, out: torch.Tensor | None = None, total: torch.Tensor | None = None) -> torch.Tensor:
+    """Exclusive scan of an int64 vector (csrc/ingest.cu)."""
+    x = x.to(torch.int64).contiguous()
+    if out is None:
+        out = torch.empty_like(x)
+    call("svdrec_scan_i64", x.numel(), ptr(x), ptr(out), ptr(total), stream_handle())
+    return out
 
 
 def csr_transpose(indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, n_out: int,

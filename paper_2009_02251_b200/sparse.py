@@ -237,6 +237,7 @@ class DeviceCSR:
         self._partial = {}
         self._ranked = None
         self._transpose = None
+        self._hot = {}
         self._sched = {}
         self.h2d_bytes = h2d_bytes
 
@@ -274,17 +275,35 @@ class DeviceCSR:
     def ranked(self):
         """(ranked indices, values, rank -> item order) for the CF scoring
         kernel: item ids replaced by popularity rank, each row ordered by
-        rank.  Built once on the device (cached) as the transpose of A.T
-        with A.T's rows taken in rank order (csrc/ingest.cu): every user's
-        row then lists its items hottest first, relabelled by rank."""
+        rank.  Built once on the device (cached), without a sort: per row
+        with a rank bitset (csrc/ingest.cu k_rank_rows) for up to 65536
+        items, else as the transpose of A.T taken in rank order."""
         if self._ranked is None:
             from . import kernels as K
 
-            AT = self._transpose_of_self()
-            _, rk, rv = K.csr_transpose(AT.indptr, AT.indices, AT.values, self.m, perm=self.hot_items,
-                                        relabel=True)
+            if self.n <= 65536:
+                rk, rv = K.rank_rows(self.indptr, self.indices, self.values, self.n, self.item_rank)
+            else:
+                AT = self._transpose_of_self()
+                _, rk, rv = K.csr_transpose(AT.indptr, AT.indices, AT.values, self.m, perm=self.hot_items,
+                                            relabel=True)
             self._ranked = (rk, rv, self.hot_items.to(torch.int64))
         return self._ranked
+
+    def hot_encoded(self, nhot: int):
+        """(index, values) of the ranked CSR for the hot-set SpMM: index =
+        -(rank + 1) for the nhot most rated items, else the item id (built
+        once per nhot on the device, cached)."""
+        hit = self._hot.get(nhot)
+        if hit is None:
+            from . import kernels as K
+
+            rk, rv, _ = self.ranked()
+            out = torch.empty_like(rk)
+            K.call("svdrec_spmm_hot_encode", rk.numel(), K.ptr(rk), K.ptr(self.hot_items), int(nhot), K.ptr(out),
+                   K.stream_handle())
+            hit = self._hot[nhot] = (out, rv)
+        return hit
 
     def _transpose_of_self(self) -> "DeviceCSR":
         return self._transpose if self._transpose is not None else self.transposed()

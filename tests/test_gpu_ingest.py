@@ -114,3 +114,32 @@ def test_work_plan_kernels_match_torch(gpu, ng, seed):
     assert (p.nwork, p.ndone, p.nslots, p.rated) == stats
     assert torch.equal(p.start[: p.nwork], start)
     assert torch.equal(p.meta[: 8 * p.nwork], meta)
+
+
+@pytest.mark.parametrize("m,n,seed", [(700, 300, 6), (3000, 40000, 7)])
+def test_rank_rows_matches_transpose(gpu, m, n, seed):
+    """The per-row bitset ranking (n <= 65536) and the transpose-of-A.T
+    construction give the same ranked CSR."""
+    import torch
+    from paper_2009_02251_b200 import kernels as K
+    M = _rand_csr(m, n, 0.03 if n < 1000 else 0.002, seed, empty_rows=(2,))
+    T = M.T.tocsr()
+    order = np.argsort(-np.diff(T.indptr), kind="stable")
+    rank = np.empty(n, dtype=np.int32)
+    rank[order] = np.arange(n)
+    ip, ix, dv = _dev(M, gpu)
+    rk, rv = K.rank_rows(ip, ix, dv, n, torch.as_tensor(rank, device=gpu))
+    tp, ti, tv = _dev(T, gpu)
+    _, rk2, rv2 = K.csr_transpose(tp, ti, tv, m, perm=torch.as_tensor(order, device=gpu), relabel=True)
+    assert torch.equal(rk, rk2) and torch.equal(rv, rv2)
+
+
+@pytest.mark.parametrize("n", [0, 1, 5000, 8192, 8193, 300001])
+def test_scan_i64(gpu, n):
+    import torch
+    from paper_2009_02251_b200 import kernels as K
+    x = torch.randint(0, 1000, (n,), dtype=torch.int64, device=gpu)
+    tot = torch.empty(1, dtype=torch.int64, device=gpu)
+    y = K.scan_i64(x, total=tot)
+    ref = torch.cumsum(x, 0) - x
+    assert torch.equal(y, ref) and int(tot) == int(x.sum())

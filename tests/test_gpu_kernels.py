@@ -224,3 +224,40 @@ def test_sharded_orth_single_rank(gpu):
     assert np.linalg.norm(Q.T @ Q - np.eye(20)) < 1e-13
     Qr = np.linalg.qr(Yh)[0]
     np.testing.assert_allclose(np.abs(np.sum(Q * Qr, 0)), 1.0, atol=1e-6)
+
+
+@pytest.mark.parametrize("b", [2, 6, 10, 16, 32])
+def test_spmm_hot_set_matches_tma(gpu, b):
+    """A @ X through the hot-set kernel (ranked CSR, hot rows of X in shared
+    memory) equals the TMA-gather kernel and scipy: Zipf items, empty rows,
+    rows long enough to be split into segments (partial slots + fix-up)."""
+    import torch
+    import paper_2009_02251_b200 as P
+    from paper_2009_02251_b200 import kernels as K
+    from scipy import sparse as sp
+    rng = np.random.default_rng(b)
+    m, n = 3000, 2500
+    deg = np.minimum(rng.lognormal(3.5, 1.3, m).astype(np.int64), n)
+    deg[:5] = 0
+    deg[5:8] = [2500, 2300, 2100]  # split rows
+    rows = np.repeat(np.arange(m), deg)
+    pz = 1.0 / np.arange(1, n + 1) ** 1.2
+    cols = np.concatenate([np.sort(rng.choice(n, d, replace=False, p=pz / pz.sum())) for d in deg if d])
+    vals = rng.integers(1, 11, cols.size) * 0.5
+    M = sp.csr_matrix((vals, (rows, cols)), shape=(m, n))
+    A = P.SparseRatings(M, 0.5, 5.0)
+    d = A.device(gpu)
+    X = torch.as_tensor(rng.standard_normal((n, b)), device=gpu)
+    assert K._hot_rows(d.A, b, b, b) > 0
+    Y1 = torch.empty(m, b, dtype=torch.float64, device=gpu)
+    K.spmm(d.A, X, Y1)
+    old, K.SPMM_HOT = K.SPMM_HOT, False
+    try:
+        Y2 = torch.empty(m, b, dtype=torch.float64, device=gpu)
+        K.spmm(d.A, X, Y2)
+    finally:
+        K.SPMM_HOT = old
+    ref = M @ X.cpu().numpy()
+    scale = np.abs(ref).max()
+    np.testing.assert_allclose(Y1.cpu().numpy(), ref, rtol=0, atol=1e-13 * scale)
+    np.testing.assert_allclose(Y1.cpu().numpy(), Y2.cpu().numpy(), rtol=0, atol=1e-13 * scale)

@@ -28,7 +28,9 @@ for it in range(3):
     order = torch.sort(-deg, stable=True).indices
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    _, rk, rv = K.csr_transpose(tp, ti, tv, m, perm=order, relabel=True)
+    rank = torch.empty(n, dtype=torch.int32, device=dev)
+    rank[order] = torch.arange(n, dtype=torch.int32, device=dev)
+    rk, rv = K.rank_rows(ip, ix, dv, n, rank)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     c = DeviceCSR(tp, ti, tv, (n, m))
