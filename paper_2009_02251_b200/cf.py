@@ -267,7 +267,7 @@ class _Samples:
             hit = self._plans[id(A)] = (A, WorkPlan(deg[gu], self.device, self.groups, d.A.indptr[gu]))
         return hit[1]
 
-    def check_bounds(self, A: SparseRatings) -> None:
+    def check_bounds(self, A: SparseRatings, exc: type = ValueError) -> None:
         if self.n == 0 or A.shape in self._checked:
             return
         u, i = self.users_np, self.items_np
@@ -277,7 +277,7 @@ class _Samples:
         bad = (u < 0) | (u >= A.m) | (i < 0) | (i >= A.n)
         if bad.any():
             j = int(np.flatnonzero(bad)[0])
-            raise ValueError(f"sample ({self.users_np[j]}, {self.items_np[j]}) outside matrix bounds")
+            raise exc(f"sample ({self.users_np[j]}, {self.items_np[j]}) outside matrix bounds")
         self._checked.add(A.shape)
 
 
@@ -335,6 +335,12 @@ def _errors(A, factors, s: _Samples, precision: str = "fp64"):
         return _sharded_errors(A, factors, s, precision)
     if s.n == 0:
         raise ValueError("cannot average zero errors")
+    # the reference's per-sample loop fails on an out-of-range user or item
+    # with IndexError (sparse.py row_slice, numpy indexing); checked here so
+    # no out-of-range index reaches the device
+    s.check_bounds(A, IndexError)
+    if factors.n_items != A.n:
+        raise ValueError("factor matrix does not cover this item set")
     val, _, _ = _predict_device(A, factors, s, A.device(factors.Xn.device).global_mean, precision)
     e = K.err_sum(val, s.truth).cpu().numpy()
     return float(e[0] / s.n), float(np.sqrt(e[1] / s.n))

@@ -214,7 +214,10 @@ def _load_csv_fast(path: Path, schema: CsvSchema) -> RatingsDataset | None:
         return None
     need = max(schema.user_col, schema.item_col, schema.rating_col) + 1
     try:
-        df = pd.read_csv(path, sep=schema.delimiter, header=None, skiprows=1 if schema.has_header else 0,
+        # round_trip: the C parser's default float converter is not always
+        # correctly rounded; the reference parses with float()
+        df = pd.read_csv(path, float_precision="round_trip", sep=schema.delimiter, header=None,
+                         skiprows=1 if schema.has_header else 0,
                          usecols=[schema.user_col, schema.item_col, schema.rating_col],
                          dtype={schema.user_col: str, schema.item_col: str, schema.rating_col: np.float64},
                          keep_default_na=False, na_filter=False, skip_blank_lines=True, engine="c",
@@ -388,7 +391,8 @@ def load_matrix_market(path: str | Path) -> SparseRatings:
         m, n, nnz = (int(x) for x in size)
         if min(m, n, nnz) < 0:
             raise ValueError
-        df = pd.read_csv(path, sep=r"\s+", header=None, skiprows=skip, comment="%", engine="c",
+        df = pd.read_csv(path, float_precision="round_trip", sep=r"\s+", header=None, skiprows=skip, comment="%",
+                         engine="c",
                          dtype={0: np.int64, 1: np.int64, 2: np.float64})
         if df.shape[1] != 3 or df.shape[0] != nnz:
             raise ValueError

@@ -13,6 +13,7 @@ sys.path.insert(0, str(HERE / "golden"))
 
 import inputs  # noqa: E402
 from paper_2009_02251_b200 import data as D  # noqa: E402
+from paper_2009_02251_b200 import SparseRatings  # noqa: E402
 
 G = np.load(HERE / "golden" / "data.npz")
 
@@ -171,3 +172,29 @@ def test_manifest_and_dataset_to_sparse(tmp_path):
     D.write_split_manifest(tmp_path / "man.txt", spec, (8, 1, 1))
     text = (tmp_path / "man.txt").read_text()
     assert "seed = 2" in text and "total = 10" in text
+
+
+def test_matrix_market_round_trip_random_doubles(tmp_path):
+    """Lossless round trip for arbitrary doubles (the fast parser must round
+    like float(); pandas' default converter changed ~15 % of such values)."""
+    from scipy import sparse as sp
+    rng = np.random.default_rng(11)
+    m, n, nnz = 120, 90, 6000
+    flat = rng.choice(m * n, nnz, replace=False)
+    vals = rng.uniform(0.5, 5.0, nnz)
+    M = sp.csr_matrix((vals, (flat // n, flat % n)), shape=(m, n))
+    A = SparseRatings(M, 0.5, 5.0)
+    p = tmp_path / "r.mtx"
+    D.save_matrix_market(p, A)
+    B = D.load_matrix_market(p)
+    assert np.array_equal(A.to_dense(), B.to_dense())
+
+
+def test_csv_ratings_parse_like_float(tmp_path):
+    rng = np.random.default_rng(12)
+    vals = rng.uniform(0.5, 5.0, 4000)
+    p = tmp_path / "r.csv"
+    p.write_text("u,i,r\n" + "".join(f"u{k},i{k % 97},{repr(float(v))}\n" for k, v in enumerate(vals)))
+    ds = D.load_ratings_csv(p)
+    got = np.array([s[2] for s in ds.samples])
+    assert np.array_equal(np.sort(got), np.sort(vals))

@@ -163,6 +163,24 @@ def test_evaluate_mae_matches_per_sample_loop(P):
     np.testing.assert_allclose(many[:, 0], [P.predict_rating(A, f, u, i).value for u, i, _ in samples], rtol=1e-12)
 
 
+def test_evaluate_rejects_out_of_range_samples(P):
+    """An out-of-range user or item raises IndexError (the reference's
+    per-sample loop fails there: sparse.py row_slice / numpy indexing)
+    before anything reaches the device; factors for another item set raise
+    ValueError.  The process's CUDA context stays usable."""
+    _, A = _ratings(P, 40, 30, 0.2, 9)
+    f = P.latent_from_qb(P.fixed_precision_qb(A, tol=0.7, block_size=5, seed=10))
+    for bad in ([(40, 3, 1.0)], [(3, 30, 1.0)], [(-1, 3, 1.0)]):
+        with pytest.raises(IndexError):
+            P.evaluate_mae(A, f, bad)
+        with pytest.raises(IndexError):
+            P.evaluate_errors(A, f, bad)
+    _, A2 = _ratings(P, 40, 31, 0.2, 9)
+    with pytest.raises(ValueError):
+        P.evaluate_mae(A2, f, [(1, 2, 3.0)])
+    assert np.isfinite(P.evaluate_mae(A, f, [(1, 2, 3.0)]))
+
+
 # ---------------------------------------------------------------------------
 # CF: the validation criterion and Alg. 5
 
