@@ -485,84 +485,36 @@ __global__ void k_overlap(int64_t ns, const int32_t* __restrict__ users, const i
   if (lo < indptr[users[t] + 1] && indices[lo] == it) atomicAdd(count, 1);
 }
 
-// Scoring work plan (the WorkPlan of cf.py) in two launches: k_plan_scan
-// (one CTA) turns the per-group degrees into chunk counts, partial-slot and
-// completion-counter bases (group order) and the first work item of each
-// group in heaviest-first order; k_plan_emit writes every item's start and
-// 8-int meta record.  Same arrays as the torch restatement it replaces.
-__global__ void __launch_bounds__(1024) k_plan_scan(int64_t ng, const int64_t* __restrict__ gd,
-                                                    const int64_t* __restrict__ order, int chunk,
-                                                    int64_t* __restrict__ first, int32_t* __restrict__ slot0,
-                                                    int32_t* __restrict__ done_idx, int64_t* __restrict__ stats) {
-  __shared__ int64_t sh[3][1024];
-  const int T = blockDim.x, t = threadIdx.x;
-  const int64_t per = (ng + T - 1) / T;
-  const int64_t a = min64(ng, per * t), b = min64(ng, a + per);
+// Scoring work plan (the WorkPlan of cf.py): k_plan_map writes, per group,
+// the values four exclusive scans turn into the plan's bases (partial
+// slots and completion counters of split groups, first work item of each
+// group in heaviest-first order, ratings streamed); k_plan_fin turns them
+// into the int32 bases and the plan's sizes; k_plan_emit writes every
+// item's start and 8-int meta record.  Same arrays as the torch
+// restatement it replaces (tests/test_gpu_ingest.py).
+__device__ __forceinline__ int64_t plan_nch(int64_t d, int chunk) {
   // 32-bit division (a 64-bit one is a long emulated sequence on the GPU)
-  auto nch_of = [&](int64_t d) -> int64_t {
-    return d <= chunk ? 1 : (int64_t)(((uint32_t)d + (uint32_t)chunk - 1u) / (uint32_t)chunk);
-  };
-  int64_t sl = 0, dn = 0, it = 0, rated = 0;
-#pragma unroll 8
-  for (int64_t g = a; g < b; ++g) {
-    const int64_t d = gd[g];
-    const int64_t n = nch_of(d);
-    if (n > 1) {
-      sl += n;
-      dn += 1;
-    }
-    rated += d;
-  }
-#pragma unroll 8
-  for (int64_t g = a; g < b; ++g) it += nch_of(gd[order[g]]);
-  sh[0][t] = sl;
-  sh[1][t] = dn;
-  sh[2][t] = it;
-  __syncthreads();
-  for (int off = 1; off < T; off <<= 1) {
-    int64_t v0 = 0, v1 = 0, v2 = 0;
-    if (t >= off) {
-      v0 = sh[0][t - off];
-      v1 = sh[1][t - off];
-      v2 = sh[2][t - off];
-    }
-    __syncthreads();
-    sh[0][t] += v0;
-    sh[1][t] += v1;
-    sh[2][t] += v2;
-    __syncthreads();
-  }
-  int64_t s0 = sh[0][t] - sl, d0 = sh[1][t] - dn, i0 = sh[2][t] - it;
-  const int64_t nslots = sh[0][T - 1];
-#pragma unroll 8
-  for (int64_t g = a; g < b; ++g) {
-    const int64_t n = nch_of(gd[g]);
-    slot0[g] = n > 1 ? (int32_t)s0 : -1;
-    done_idx[g] = n > 1 ? (int32_t)d0 : -1;
-    if (n > 1) {
-      s0 += n;
-      d0 += 1;
-    }
-  }
-#pragma unroll 8
-  for (int64_t g = a; g < b; ++g) {
-    first[g] = i0;
-    i0 += nch_of(gd[order[g]]);
-  }
-  // rated: a block reduction of the per-thread sums (reuse sh[0])
-  __syncthreads();
-  sh[0][t] = rated;
-  __syncthreads();
-  for (int off = T / 2; off > 0; off >>= 1) {
-    if (t < off) sh[0][t] += sh[0][t + off];
-    __syncthreads();
-  }
-  if (t == T - 1) {
-    stats[0] = sh[2][T - 1];  // work items (sh[1], sh[2] keep their scans)
-    stats[1] = sh[1][T - 1];  // split groups (completion counters)
-    stats[2] = nslots;        // partial slots
-  }
-  if (t == 0) stats[3] = sh[0][0];  // training ratings streamed per pass
+  return d <= chunk ? 1 : (int64_t)(((uint32_t)d + (uint32_t)chunk - 1u) / (uint32_t)chunk);
+}
+
+__global__ void k_plan_map(int64_t ng, const int64_t* __restrict__ gd, const int64_t* __restrict__ order, int chunk,
+                           int64_t* __restrict__ slots, int64_t* __restrict__ split, int64_t* __restrict__ items) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int64_t n = plan_nch(gd[g], chunk);
+  slots[g] = n > 1 ? n : 0;
+  split[g] = n > 1 ? 1 : 0;
+  items[g] = plan_nch(gd[order[g]], chunk);
+}
+
+__global__ void k_plan_fin(int64_t ng, const int64_t* __restrict__ gd, int chunk, const int64_t* __restrict__ slots,
+                           const int64_t* __restrict__ split, int32_t* __restrict__ slot0,
+                           int32_t* __restrict__ done_idx) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const bool sp = plan_nch(gd[g], chunk) > 1;
+  slot0[g] = sp ? (int32_t)slots[g] : -1;
+  done_idx[g] = sp ? (int32_t)split[g] : -1;
 }
 
 // j: position in heaviest-first order
@@ -575,7 +527,7 @@ __global__ void k_plan_emit(int64_t ng, const int64_t* __restrict__ gd, const in
   if (j >= ng) return;
   const int64_t g = order[j];
   const int64_t deg = gd[g];
-  const int64_t nch = deg <= chunk ? 1 : (int64_t)(((uint32_t)deg + (uint32_t)chunk - 1u) / (uint32_t)chunk);
+  const int64_t nch = plan_nch(deg, chunk);
   const bool split = nch > 1;
   const int64_t w0 = first[j];
   for (int64_t c = 0; c < nch; ++c) {
@@ -735,6 +687,10 @@ extern "C" int svdrec_count_overlap(int64_t nsamp, const int32_t* d_users, const
   return check_launch("count_overlap");
 }
 
+namespace svdrec {
+int scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, cudaStream_t s, int* launches);
+}
+
 extern "C" int svdrec_cf_plan_scan(int64_t ngroups, const int64_t* d_group_deg, const int64_t* d_order,
                                    int32_t chunk, int64_t* d_first, int32_t* d_slot0, int32_t* d_done_idx,
                                    int64_t* d_stats, void* stream) {
@@ -742,8 +698,27 @@ extern "C" int svdrec_cf_plan_scan(int64_t ngroups, const int64_t* d_group_deg, 
   cudaStream_t s = as_stream(stream);
   SVDREC_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(int64_t), s));
   if (ngroups == 0) return 0;
-  k_plan_scan<<<1, 1024, 0, s>>>(ngroups, d_group_deg, d_order, chunk, d_first, d_slot0, d_done_idx, d_stats);
-  return check_launch("cf_plan_scan");
+  int64_t* tmp = nullptr;  // slots, split flags, ratings (exclusive scans in place)
+  SVDREC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (size_t)ngroups * 3 * sizeof(int64_t), s));
+  int64_t *slots = tmp, *split = tmp + ngroups, *rated = tmp + 2 * ngroups;
+  const unsigned grid = (unsigned)((ngroups + 255) / 256);
+  int launches = 0;
+  k_plan_map<<<grid, 256, 0, s>>>(ngroups, d_group_deg, d_order, chunk, slots, split, d_first);
+  launches += 1;
+  int rc = scan_i64(ngroups, d_first, d_first, d_stats + 0, s, &launches);      // first item per ordered group
+  if (!rc) rc = scan_i64(ngroups, split, split, d_stats + 1, s, &launches);       // completion counters
+  if (!rc) rc = scan_i64(ngroups, slots, slots, d_stats + 2, s, &launches);       // partial slots
+  if (!rc) rc = scan_i64(ngroups, d_group_deg, rated, d_stats + 3, s, &launches); // ratings streamed
+  if (!rc) {
+    k_plan_fin<<<grid, 256, 0, s>>>(ngroups, d_group_deg, chunk, slots, split, d_slot0, d_done_idx);
+    launches += 1;
+  }
+  cudaFreeAsync(tmp, s);
+  if (rc) {
+    set_error("cf_plan_scan: %s", cudaGetErrorString((cudaError_t)rc));
+    return rc;
+  }
+  return check_launch("cf_plan_scan", launches);
 }
 
 extern "C" int svdrec_cf_plan_emit(int64_t ngroups, const int64_t* d_group_deg, const int64_t* d_order,
