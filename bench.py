@@ -261,6 +261,54 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def scaleout_variant(dev, peak) -> dict:
+    """BASELINE configs[4] on this GPU: 8,000,000 x 1,000,000, 2.0e9 ratings
+    generated on the device (rank 64, Zipf(1.2) items, half stars; int32
+    indices, fp64 values), adaptive QB with b = 64, p = 2 (passes 6), k
+    capped at 512 -- time to k = 512 (CUDA events, after one untimed block)
+    in fp64 and with float X in the SpMMs (the fp32 variant), and the
+    SpMM's compulsory-byte HBM rate."""
+    import torch
+    import paper_2009_02251_b200 as P
+    from paper_2009_02251_b200 import kernels as K, synth
+
+    b, passes, cap = 64, 6, 512
+    t = time.perf_counter()
+    A = synth.generate_device(synth.CONFIGS["c4_2b"], dev)
+    d = A.device()
+    torch.cuda.synchronize()
+    out = {"config": f"c4_2b: {d.m} users x {d.n} items, {d.nnz} ratings (device-generated), b={b}, "
+                     f"passes={passes} (p=2), k<={cap}", "generate_s": round(time.perf_counter() - t, 1)}
+    for prec in ("fp64", "fp32"):
+        g = P.qb_pass_blocks(A, b, passes, P.GaussianStream(1), max_rank=cap, precision=prec)
+        next(g).err  # warm-up block (first-call plans)
+        del g
+        torch.cuda.synchronize()
+        K.PROFILE = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ranks = []
+        for st in P.qb_pass_blocks(A, b, passes, P.GaussianStream(0), max_rank=cap, precision=prec):
+            ranks.append(st.rank)
+            if st.rank >= cap:
+                break
+        e1.record()
+        torch.cuda.synchronize()
+        prof = K.profile_summary(K.PROFILE)
+        K.PROFILE = None
+        c, ms, hbm_b, _ = prof.get("spmm", (0, 0.0, 0, 0))
+        ach = hbm_b / (ms / 1e3) / 1e9 if ms else None
+        out[prec] = {"time_to_k_s": round(e0.elapsed_time(e1) / 1e3, 4), "k": ranks[-1], "blocks": len(ranks),
+                     "spmm": {"calls": c, "ms_per_call": round(ms / max(c, 1), 2),
+                              "hbm_GBps": round(ach, 1) if ach else None,
+                              "hbm_frac": round(ach / peak, 4) if ach else None},
+                     "timing": "CUDA events around the whole run; per-call SpMM spans (events) recorded in it"}
+    out["peak_mem_GiB"] = round(torch.cuda.max_memory_allocated(dev) / 2**30, 1)
+    del A, d
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -499,6 +547,16 @@ def run_b200(args):
         "allocator_in_timed_region": alloc,
         "setup": {"generate_split_s": round(gen_s, 2)},
     }
+    if ws == 1 and not args.no_scaleout and not args.no_variants and CONFIG == "c3_20m":
+        # the c3 device state is released first (the 2e9-rating matrix peaks
+        # at ~134 GiB)
+        del A, d, vs, ts, f, trace
+        if variants:
+            del f32, tr32
+        gc.collect()
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(dev)
+        line["variants"]["c4_scaleout"] = scaleout_variant(dev, peak)
     if ws == 1 and not args.no_cpu_baseline:
         total, cores, info = cpu_port_run(tr, va, te, lo, hi)
         line["cpu_baseline"] = {"value": round(total, 3), "unit": "s", "cores": cores, "kind": "port",
@@ -531,6 +589,7 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the fp32-variant timing")
+    ap.add_argument("--no-scaleout", action="store_true", help="skip the config-4 (2e9 ratings) variant")
     args = ap.parse_args()
     CONFIG = args.config
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
