@@ -107,15 +107,17 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
  * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
  * fall back to the plain kernel. */
 int svdrec_spmm_warps_per_sm(int32_t b);
-/* Hot-set variant of A @ X (even b <= 32) on the popularity-ranked CSR
- * (svdrec_rank_rows): d_hidx[t] = -(rank + 1) for entries of the nhot
- * most rated items (rank < nhot; their rows X[d_hot_items[rank]] are
- * staged in every CTA's shared memory) and the item id otherwise, built by
- * svdrec_spmm_hot_encode from the ranked indices and the rank -> item
- * order; d_hval the ranked values.  Same segment plan / fix-up as
- * svdrec_spmm (the ranked CSR has A's row structure), schedule of 16 warps
- * per SM; nhot <= svdrec_spmm_hot_rows(b), which is 0 for the widths
- * where the TMA-gather kernel is faster (the host then calls svdrec_spmm). */
+/* Hot-set variant of A @ X (even b <= 32, or b % 4 == 0 up to 64) on the
+ * popularity-ranked CSR (svdrec_rank_rows: every row hottest item first):
+ * the rows X[d_hot_items[rank]] of the nhot most rated items (rank < nhot)
+ * are staged in every CTA's shared memory; d_hidx holds -(rank + 1) for
+ * their entries and the item id otherwise (svdrec_spmm_hot_encode from the
+ * ranked indices and the rank -> item order), d_hval the ranked values.
+ * Each 32-entry batch is split by a warp ballot into its hot entries
+ * (shared memory) and cold ones (L2 / HBM gathers).  Same segment plan /
+ * fix-up as svdrec_spmm (the ranked CSR has A's row structure), schedule of
+ * 16 warps per SM; nhot <= svdrec_spmm_hot_rows(b) (0: width not
+ * supported). */
 int svdrec_spmm_hot_rows(int32_t b);
 int svdrec_spmm_hot_encode(int64_t nnz, const int32_t* d_ranked, const int32_t* d_order, int32_t nhot,
                            int32_t* d_out, void* stream);

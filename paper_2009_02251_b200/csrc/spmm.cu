@@ -550,19 +550,24 @@ struct __align__(16) TabEnt {
 constexpr int kHotWarps = 16;
 constexpr int kTabSlots = 32 + 32;  // a batch + the padding of G * U <= 32 steps
 
-template <int P, int U>
+// V = 2: P = b / 2 lanes of one double2 per row; V = 4: P = b / 4 lanes
+// holding doubles {2pc, 2pc + 1} and {b/2 + 2pc, b/2 + 2pc + 1}, so each
+// LDS.128 / LDG.128 reads one contiguous half row per group (for b = 64: a
+// 128-B phase per 8 lanes, no bank conflicts).
+template <int P, int U, int V>
 __global__ void __launch_bounds__(512, 1) k_spmm_hot(
     int64_t nwarp, const int32_t* __restrict__ warp_seg, const int32_t* __restrict__ seg_row,
     const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ hidx, const double* __restrict__ hval, const double* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ hot_items, int nhot, double* __restrict__ Y, int64_t ldy,
     double* __restrict__ partial) {
-  constexpr int B = 2 * P, G = 32 / P;
+  constexpr int B = V * P, G = 32 / P, H = B / 4;  // H: double2 offset of the second half (V = 4)
+  constexpr int RB = B / 2;                        // double2 per row
   static_assert(G * U <= 32, "spmm_hot: padding exceeds the table");
   __shared__ TabEnt tabs[kHotWarps * 2 * kTabSlots];
   extern __shared__ __align__(16) double hs[];  // nhot rows of B doubles
-  for (int t = threadIdx.x; t < nhot * P; t += blockDim.x) {
-    const int r = t / P, c = t - (t / P) * P;
+  for (int t = threadIdx.x; t < nhot * RB; t += blockDim.x) {
+    const int r = t / RB, c = t - (t / RB) * RB;
     reinterpret_cast<double2*>(hs)[t] =
         *reinterpret_cast<const double2*>(X + (int64_t)hot_items[r] * ldx + 2 * c);
   }
@@ -572,7 +577,7 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
   if (w >= nwarp) return;
   const int g = lane / P, pc = lane - (lane / P) * P;
   const bool active = g < G;
-  const double2* hrow = reinterpret_cast<const double2*>(hs) + pc;   // + rank * P
+  const double2* hrow = reinterpret_cast<const double2*>(hs) + pc;   // + rank * RB
   const double2* xrow = reinterpret_cast<const double2*>(X) + pc;    // + item * ldx / 2
   const int64_t ldx2 = ldx / 2;
   const int32_t s_lo = warp_seg[w], s_hi = warp_seg[w + 1];
@@ -641,23 +646,28 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
   // the unrolled steps need no masks (a pad reads row 0 times 0.0)
   TabEnt* ht = tabs + (size_t)(threadIdx.x >> 5) * 2 * kTabSlots;
   TabEnt* ct = ht + kTabSlots;
+  // two accumulator chains (even / odd steps); V = 4 lanes hold two halves
   double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+  double2 c0 = make_double2(0.0, 0.0), c1 = make_double2(0.0, 0.0);
   auto process = [&](const Batch& k) {
     const int32_t ci = k.ci;
     const double vi = k.vi;
     const int nv = k.nv;
     if (k.flags & 1) {
-      a0 = make_double2(0.0, 0.0);
-      a1 = make_double2(0.0, 0.0);
+      a0 = a1 = c0 = c1 = make_double2(0.0, 0.0);
     }
+    // the batch's hot and cold entries, each in row order, go to their
+    // tables (a row's entries are in item order: hot and cold interleave)
     const bool hot = lane < nv && ci < 0;
-    const int nh = __popc(__ballot_sync(0xffffffffu, hot));  // hot prefix
+    const unsigned hm = __ballot_sync(0xffffffffu, hot);
+    const int nh = __popc(hm);
+    const int hpos = __popc(hm & ((1u << lane) - 1u));
     __syncwarp();  // the previous batch's tables are consumed
     if (lane < nv) {
       if (hot)
-        ht[lane] = TabEnt{(-ci - 1) * P, 0, vi};
+        ht[hpos] = TabEnt{(-ci - 1) * RB, 0, vi};
       else
-        ct[lane - nh] = TabEnt{ci * (int32_t)ldx2, 0, vi};
+        ct[lane - hpos] = TabEnt{ci * (int32_t)ldx2, 0, vi};
     }
     if (lane < G * U) {
       ht[nh + lane] = TabEnt{0, 0, 0.0};
@@ -667,53 +677,72 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
     if (active) {
       // hot entries: shared memory
       for (int j = 0; j < nh; j += G * U) {
-        double2 x[U];
+        double2 x[U], y[U];
         double v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const TabEnt e = ht[j + u * G + g];
           v[u] = e.v;
           x[u] = hrow[e.off];
+          if (V == 4) y[u] = hrow[e.off + H];
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           double2& acc = (u & 1) ? a1 : a0;
           acc.x = fma(v[u], x[u].x, acc.x);
           acc.y = fma(v[u], x[u].y, acc.y);
+          if (V == 4) {
+            double2& acd = (u & 1) ? c1 : c0;
+            acd.x = fma(v[u], y[u].x, acd.x);
+            acd.y = fma(v[u], y[u].y, acd.y);
+          }
         }
       }
-      // cold entries: gathered from L2
+      // cold entries: gathered from L2 / HBM
       for (int j = 0; j < nv - nh; j += G * U) {
-        double2 x[U];
+        double2 x[U], y[U];
         double v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const TabEnt e = ct[j + u * G + g];
           v[u] = e.v;
           x[u] = __ldg(xrow + e.off);
+          if (V == 4) y[u] = __ldg(xrow + e.off + H);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           double2& acc = (u & 1) ? a1 : a0;
           acc.x = fma(v[u], x[u].x, acc.x);
           acc.y = fma(v[u], x[u].y, acc.y);
+          if (V == 4) {
+            double2& acd = (u & 1) ? c1 : c0;
+            acd.x = fma(v[u], y[u].x, acd.x);
+            acd.y = fma(v[u], y[u].y, acd.y);
+          }
         }
       }
     }
     if (k.flags & 2) {
       double2 t0 = make_double2(a0.x + a1.x, a0.y + a1.y);
-      double2 tot = t0;
+      double2 t1 = make_double2(c0.x + c1.x, c0.y + c1.y);
+      double2 tot = t0, tot1 = t1;
 #pragma unroll
       for (int h = 1; h < G; ++h) {
         const double2 o = shfl_v(t0, (lane + h * P) & 31);
+        const double2 o1 = V == 4 ? shfl_v(t1, (lane + h * P) & 31) : o;
         if (g == 0) {
           tot.x += o.x;
           tot.y += o.y;
+          if (V == 4) {
+            tot1.x += o1.x;
+            tot1.y += o1.y;
+          }
         }
       }
       if (g == 0) {
-        double* dst = k.slot < 0 ? (Y + (int64_t)k.row * ldy + 2 * pc) : (partial + (int64_t)k.slot * B + 2 * pc);
-        *reinterpret_cast<double2*>(dst) = tot;
+        double* dst = k.slot < 0 ? (Y + (int64_t)k.row * ldy) : (partial + (int64_t)k.slot * B);
+        *reinterpret_cast<double2*>(dst + 2 * pc) = tot;
+        if (V == 4) *reinterpret_cast<double2*>(dst + 2 * H + 2 * pc) = tot1;
       }
     }
   };
@@ -729,13 +758,14 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
   }
 }
 
-// hot-encoded index of the ranked CSR: -(rank + 1) for rank < nhot, else
-// the item id (order[rank])
-__global__ void k_hot_encode(int64_t nnz, const int32_t* __restrict__ rk, const int32_t* __restrict__ order,
+// hot-encoded column index of the popularity-ranked CSR (rows in rank
+// order: hottest item first): -(rank + 1) for rank < nhot, else the item
+// id order[rank]
+__global__ void k_hot_encode(int64_t nnz, const int32_t* __restrict__ ranked, const int32_t* __restrict__ order,
                              int nhot, int32_t* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nnz) return;
-  const int32_t r = rk[t];
+  const int32_t r = ranked[t];
   out[t] = r < nhot ? -(r + 1) : order[r];
 }
 
@@ -844,12 +874,10 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
 }
 
 extern "C" int svdrec_spmm_hot_rows(int32_t b) {
-  if (b < 2 || b > 32 || b % 2) return 0;
-  // where the hot-set kernel beats k_spmm_tma (c3, A @ X, per call):
-  // b = 2 259 vs 339 us, 8 242 vs 320, 16 295 vs 338, 32 379 vs 592; not at
-  // b = 20 (397-414 vs 363: 160-B rows cost ~2 shared-memory wavefronts per
-  // hot entry through bank conflicts -- ncu: L1 data pipe 86 % busy)
-  if (b > 16 && b != 32) return 0;
+  // widths the hot-set kernel supports: even b <= 32 (2 doubles per lane),
+  // b % 4 == 0 up to 64 (4 per lane); which widths it is used for is the
+  // host's choice (kernels._hot_rows: where it measured faster)
+  if (b < 2 || b > 64 || b % 2 || (b > 32 && b % 4)) return 0;
   // one 512-thread CTA per SM; the hot rows fill the 227 KB opt-in
   return (int)((226 * 1024 - kHotWarps * 2 * kTabSlots * (int)sizeof(TabEnt)) / (8 * b));
 }
@@ -869,8 +897,8 @@ extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int
                                int32_t nhot, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
                                const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1,
                                int64_t nwarp, const int32_t* d_warp_seg, double* d_partial, void* stream) {
-  SVDREC_ARG(b >= 2 && b <= 32 && b % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0 && ldx >= b && ldy >= b,
-             "spmm_hot: needs even b <= 32 and 16-B aligned rows (b=%d)", b);
+  SVDREC_ARG(svdrec_spmm_hot_rows(b) > 0 && ldx % 2 == 0 && ldy % 2 == 0 && ldx >= b && ldy >= b,
+             "spmm_hot: needs even b <= 32 or b %% 4 == 0 <= 64, and 16-B aligned rows (b=%d)", b);
   SVDREC_ARG(nhot >= 0 && nhot <= svdrec_spmm_hot_rows(b), "spmm_hot: %d hot rows exceed shared memory", nhot);
   SVDREC_ARG(nwarp > 0 && d_warp_seg, "spmm_hot: needs a warp schedule (16 warps per SM)");
   SVDREC_ARG(x_rows * (ldx / 2) < (1ll << 31), "spmm_hot: X too large for 32-bit row offsets");
@@ -880,33 +908,48 @@ extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int
   cudaStream_t s = as_stream(stream);
   const size_t smem = (size_t)nhot * b * sizeof(double);
   const int64_t grid = (nwarp + 15) / 16;
-#define SVDREC_HOT(PP)                                                                                     \
+#define SVDREC_HOT(PP, VV)                                                                                 \
   case PP:                                                                                                 \
-    SVDREC_CUDA(smem_attr_once(k_spmm_hot<PP, (PP < 8 ? PP : 8)>,                                         \
+    SVDREC_CUDA(smem_attr_once(k_spmm_hot<PP, (PP < 8 ? PP : 8), VV>,                                     \
                                226 * 1024 - kHotWarps * 2 * kTabSlots * (int)sizeof(TabEnt)));           \
-    k_spmm_hot<PP, (PP < 8 ? PP : 8)><<<(unsigned)grid, 512, smem, s>>>(                                   \
+    k_spmm_hot<PP, (PP < 8 ? PP : 8), VV><<<(unsigned)grid, 512, smem, s>>>(                               \
         nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_hidx, d_hval, d_X, ldx,        \
         d_hot_items, nhot, d_Y, ldy, d_partial);                                                           \
     break;
-  switch (b / 2) {
-    SVDREC_HOT(1)
-    SVDREC_HOT(2)
-    SVDREC_HOT(3)
-    SVDREC_HOT(4)
-    SVDREC_HOT(5)
-    SVDREC_HOT(6)
-    SVDREC_HOT(7)
-    SVDREC_HOT(8)
-    SVDREC_HOT(9)
-    SVDREC_HOT(10)
-    SVDREC_HOT(11)
-    SVDREC_HOT(12)
-    SVDREC_HOT(13)
-    SVDREC_HOT(14)
-    SVDREC_HOT(15)
-    SVDREC_HOT(16)
-    default:
-      return SVDREC_E_ARG;
+  if (b <= 32) {
+    switch (b / 2) {
+      SVDREC_HOT(1, 2)
+      SVDREC_HOT(2, 2)
+      SVDREC_HOT(3, 2)
+      SVDREC_HOT(4, 2)
+      SVDREC_HOT(5, 2)
+      SVDREC_HOT(6, 2)
+      SVDREC_HOT(7, 2)
+      SVDREC_HOT(8, 2)
+      SVDREC_HOT(9, 2)
+      SVDREC_HOT(10, 2)
+      SVDREC_HOT(11, 2)
+      SVDREC_HOT(12, 2)
+      SVDREC_HOT(13, 2)
+      SVDREC_HOT(14, 2)
+      SVDREC_HOT(15, 2)
+      SVDREC_HOT(16, 2)
+      default:
+        return SVDREC_E_ARG;
+    }
+  } else {
+    switch (b / 4) {
+      SVDREC_HOT(9, 4)
+      SVDREC_HOT(10, 4)
+      SVDREC_HOT(11, 4)
+      SVDREC_HOT(12, 4)
+      SVDREC_HOT(13, 4)
+      SVDREC_HOT(14, 4)
+      SVDREC_HOT(15, 4)
+      SVDREC_HOT(16, 4)
+      default:
+        return SVDREC_E_ARG;
+    }
   }
 #undef SVDREC_HOT
   int rc = check_launch("spmm_hot");

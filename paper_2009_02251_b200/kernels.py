@@ -167,14 +167,25 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
 
 # SVDREC_SPMM_HOT=0 keeps A @ X on the TMA-gather kernel (A/B measurements)
 SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "1") != "0"
+# widths where the hot-set kernel measured faster than k_spmm_tma for A @ X
+# (config 3, us per call, hot vs TMA): b = 2 259 vs 339, 8 267 vs 321, 16
+# 298 vs 338, 32 386 vs 592, 64 554 vs 917; at b = 20 (414 vs 363: 160-B
+# rows straddle the 128-B shared-memory phases -- bank conflicts, ncu: L1
+# data pipe 86 % busy) and b = 40 (668 vs 650) it is slower.  Only where the
+# ranked CSR is cheap (n <= 65,536 items: svdrec_rank_rows); on config 4
+# (1e6 items) the L2 already serves the hot rows and the misses bound it.
+HOT_WIDTHS = frozenset(range(2, 17, 2)) | {32, 64}
 
 
-def _hot_rows(plan, b: int, ldx: int, ldy: int) -> int:
+def _hot_rows(plan, b: int, ldx: int, ldy: int, widths=None) -> int:
     """Hot rows of X staged in shared memory by the hot-set kernel, or 0
-    when it does not apply (no popularity order on this CSR, odd b, b > 32)."""
-    if not SPMM_HOT or getattr(plan, "item_rank", None) is None or b % 2 or b > 32 or ldx % 2 or ldy % 2:
+    when it is not used (no popularity order on this CSR, a width where the
+    TMA kernel is faster, unaligned rows)."""
+    if not SPMM_HOT or getattr(plan, "item_rank", None) is None or ldx % 2 or ldy % 2:
         return 0
-    if plan.n * (ldx // 2) >= 1 << 31:
+    if b not in (HOT_WIDTHS if widths is None else widths) or (b > 32 and (ldx % 4 or ldy % 4)):
+        return 0
+    if plan.n > 65536 or plan.n * (ldx // 2) >= 1 << 31:
         return 0
     return min(int(query("svdrec_spmm_hot_rows", b)), plan.n)
 

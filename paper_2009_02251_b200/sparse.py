@@ -293,7 +293,8 @@ class DeviceCSR:
     def hot_encoded(self, nhot: int):
         """(index, values) of the ranked CSR for the hot-set SpMM: index =
         -(rank + 1) for the nhot most rated items, else the item id (built
-        once per nhot on the device, cached)."""
+        once per nhot on the device, cached; one width at a time: 4 B per
+        rating)."""
         hit = self._hot.get(nhot)
         if hit is None:
             from . import kernels as K
@@ -302,7 +303,8 @@ class DeviceCSR:
             out = torch.empty_like(rk)
             K.call("svdrec_spmm_hot_encode", rk.numel(), K.ptr(rk), K.ptr(self.hot_items), int(nhot), K.ptr(out),
                    K.stream_handle())
-            hit = self._hot[nhot] = (out, rv)
+            hit = (out, rv)
+            self._hot = {nhot: hit}
         return hit
 
     def _transpose_of_self(self) -> "DeviceCSR":

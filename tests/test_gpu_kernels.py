@@ -226,7 +226,7 @@ def test_sharded_orth_single_rank(gpu):
     np.testing.assert_allclose(np.abs(np.sum(Q * Qr, 0)), 1.0, atol=1e-6)
 
 
-@pytest.mark.parametrize("b", [2, 6, 10, 16, 32])
+@pytest.mark.parametrize("b", [2, 6, 10, 16, 20, 32, 40, 64])
 def test_spmm_hot_set_matches_tma(gpu, b):
     """A @ X through the hot-set kernel (ranked CSR, hot rows of X in shared
     memory) equals the TMA-gather kernel and scipy: Zipf items, empty rows,
@@ -248,9 +248,13 @@ def test_spmm_hot_set_matches_tma(gpu, b):
     A = P.SparseRatings(M, 0.5, 5.0)
     d = A.device(gpu)
     X = torch.as_tensor(rng.standard_normal((n, b)), device=gpu)
-    assert K._hot_rows(d.A, b, b, b) > 0
+    assert K._hot_rows(d.A, b, b, b, widths={b}) > 0
+    old_w, K.HOT_WIDTHS = K.HOT_WIDTHS, frozenset({b})
     Y1 = torch.empty(m, b, dtype=torch.float64, device=gpu)
-    K.spmm(d.A, X, Y1)
+    try:
+        K.spmm(d.A, X, Y1)
+    finally:
+        K.HOT_WIDTHS = old_w
     old, K.SPMM_HOT = K.SPMM_HOT, False
     try:
         Y2 = torch.empty(m, b, dtype=torch.float64, device=gpu)
