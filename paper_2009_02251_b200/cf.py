@@ -227,10 +227,27 @@ class _Samples:
             r = np.array([float(s[2]) for s in arr], dtype=np.float64)
         self.n = int(u.size)
         self.users_np, self.items_np, self.truth_np = u, i, r
-        # grouped by user on the device: stable sort of the raw arrays
-        ud = to_device(u, np.int64, device)
-        idev = to_device(i, np.int64, device)
-        rd = to_device(r, np.float64, device)
+        # grouped by user on the device: stable sort of the raw arrays.  The
+        # uploads run on the copy stream, so they overlap whatever the
+        # current stream is computing (e.g. the first QB block)
+        from .sparse import _copy_stream
+
+        dv = torch.device(device)
+        if dv.type == "cuda":
+            if dv.index is None:
+                dv = torch.device("cuda", torch.cuda.current_device())
+            cur, side = torch.cuda.current_stream(dv), _copy_stream(dv)
+            with torch.cuda.stream(side):
+                ud = to_device(u, np.int64, device)
+                idev = to_device(i, np.int64, device)
+                rd = to_device(r, np.float64, device)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            for t in (ud, idev, rd):
+                t.record_stream(cur)
+            cur.wait_event(ev)
+        else:  # host-side planning tests
+            ud, idev, rd = (to_device(x, dt, device) for x, dt in ((u, np.int64), (i, np.int64), (r, np.float64)))
         self.h2d_bytes = self.n * 24
         order = torch.sort(ud, stable=True).indices if self.n else torch.zeros(0, dtype=torch.int64, device=device)
         us = ud[order]

@@ -210,6 +210,17 @@ def warp_plan_t(seg_begin: torch.Tensor, seg_end: torch.Tensor, nwarp: int, seg_
     return torch.cummax(out, 0).values.to(torch.int32)
 
 
+_COPY: dict = {}
+
+
+def _copy_stream(dev: torch.device) -> torch.cuda.Stream:
+    """One cached host-to-device copy stream per device."""
+    s = _COPY.get(dev.index)
+    if s is None:
+        s = _COPY[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
 class DeviceCSR:
     """One CSR in HBM plus its SpMM plan (built on the device)."""
 
@@ -243,11 +254,31 @@ class DeviceCSR:
 
     @classmethod
     def upload(cls, csr: sp.csr_matrix, device: torch.device) -> "DeviceCSR":
+        """Upload a host CSR.  The row pointers go first and the SpMM plans
+        (row pointers only) are built on the current stream while the
+        column indices and values are still copying on a side stream; the
+        current stream then waits for the copies."""
         from .hostio import to_device
 
-        t = lambda a, dt: to_device(a, dt, device)  # noqa: E731
-        return cls(t(csr.indptr, np.int64), t(csr.indices, np.int32), t(csr.data, np.float64), csr.shape,
-                   h2d_bytes=(csr.shape[0] + 1) * 8 + csr.nnz * 12)
+        dev = torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        cur = torch.cuda.current_stream(dev)
+        side = _copy_stream(dev)  # host sources: no device work to wait for
+        with torch.cuda.stream(side):
+            indptr = to_device(csr.indptr, np.int64, dev)
+            ev_ptr = torch.cuda.Event()
+            ev_ptr.record(side)
+            indices = to_device(csr.indices, np.int32, dev)
+            values = to_device(csr.data, np.float64, dev)
+            ev_all = torch.cuda.Event()
+            ev_all.record(side)
+        for t in (indptr, indices, values):
+            t.record_stream(cur)  # allocated on the side stream, used on this one
+        cur.wait_event(ev_ptr)
+        self = cls(indptr, indices, values, csr.shape, h2d_bytes=(csr.shape[0] + 1) * 8 + csr.nnz * 12)
+        cur.wait_event(ev_all)
+        return self
 
     def transposed(self) -> "DeviceCSR":
         """CSR of the transpose, built on the device: a stable counting-sort
