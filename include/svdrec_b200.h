@@ -112,20 +112,20 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
  * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
  * fall back to the plain kernel. */
 int svdrec_spmm_warps_per_sm(int32_t b);
-/* Hot-set variant of A @ X (even b <= 32, or b % 4 == 0 up to 64) on the
- * popularity-ranked CSR (svdrec_rank_rows: every row hottest item first):
- * the rows X[d_hot_items[rank]] of the nhot most rated items (rank < nhot)
- * are staged in every CTA's shared memory; d_hidx holds -(rank + 1) for
- * their entries and the item id otherwise (svdrec_spmm_hot_encode from the
- * ranked indices and the rank -> item order), d_hval the ranked values.
+/* Hot-set variant of A @ X (even b <= 32, or b % 4 == 0 up to 64): the
+ * rows X[d_hot_items[rank]] of the nhot most rated items (rank < nhot)
+ * are staged in every CTA's shared memory; the CSR is given as its
+ * hot-first copy (svdrec_spmm_hot_partition: every row stably partitioned
+ * into the hot items' entries, index -(rank + 1), then the others, index
+ * = item id; d_rank = item -> popularity rank), with A's row structure.
  * Each 32-entry batch is split by a warp ballot into its hot entries
  * (shared memory) and cold ones (L2 / HBM gathers).  Same segment plan /
- * fix-up as svdrec_spmm (the ranked CSR has A's row structure), schedule of
- * 16 warps per SM; nhot <= svdrec_spmm_hot_rows(b) (0: width not
- * supported). */
+ * fix-up as svdrec_spmm, schedule of 16 warps per SM;
+ * nhot <= svdrec_spmm_hot_rows(b) (0: width not supported). */
 int svdrec_spmm_hot_rows(int32_t b);
-int svdrec_spmm_hot_encode(int64_t nnz, const int32_t* d_ranked, const int32_t* d_order, int32_t nhot,
-                           int32_t* d_out, void* stream);
+int svdrec_spmm_hot_partition(int64_t m, const int64_t* d_indptr, const int32_t* d_indices,
+                              const double* d_values, const int32_t* d_rank, int32_t nhot,
+                              int32_t* d_out_indices, double* d_out_values, void* stream);
 int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
                     const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_hidx,
                     const double* d_hval, const double* d_X, int64_t ldx, int64_t x_rows,

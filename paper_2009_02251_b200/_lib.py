@@ -36,7 +36,7 @@ SIGNATURES = {
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_hot_rows": (C.c_int, [_i32]),
-    "svdrec_spmm_hot_encode": (C.c_int, [_i64, _p, _p, _i32, _p, _p]),
+    "svdrec_spmm_hot_partition": (C.c_int, [_i64, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "svdrec_spmm_hot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i32, _p, _i64, _i32, _i64, _p, _p,
                                   _p, _i64, _p, _p, _p]),
     "svdrec_spmm_x32_warps_per_sm": (C.c_int, [_i32]),

@@ -758,15 +758,49 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
   }
 }
 
-// hot-encoded column index of the popularity-ranked CSR (rows in rank
-// order: hottest item first): -(rank + 1) for rank < nhot, else the item
-// id order[rank]
-__global__ void k_hot_encode(int64_t nnz, const int32_t* __restrict__ ranked, const int32_t* __restrict__ order,
-                             int nhot, int32_t* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nnz) return;
-  const int32_t r = ranked[t];
-  out[t] = r < nhot ? -(r + 1) : order[r];
+// The hot-set kernel's copy of a CSR: every row stably partitioned into the
+// entries of the nhot most rated items (rank[item] < nhot) first and the
+// rest after, each part in the row's order; index -(rank + 1) for hot
+// entries, the item id otherwise.  One warp per row, two passes (count,
+// then place with ballot prefixes).  Batches are then (nearly) all hot or
+// all cold -- what the kernel needs; a full rank order is no faster.
+__global__ void k_hot_partition(int64_t m, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                const double* __restrict__ values, const int32_t* __restrict__ rank, int nhot,
+                                int32_t* __restrict__ out_idx, double* __restrict__ out_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t r = w0; r < m; r += nw) {
+    const int64_t a = indptr[r], b = indptr[r + 1];
+    int64_t nh = 0;
+    for (int64_t t0 = a; t0 < b; t0 += 32) {
+      const int64_t t = t0 + lane;
+      const bool hot = t < b && rank[indices[t]] < nhot;
+      nh += __popc(__ballot_sync(0xffffffffu, hot));
+    }
+    int64_t hrun = 0, crun = 0;
+    for (int64_t t0 = a; t0 < b; t0 += 32) {
+      const int64_t t = t0 + lane;
+      const bool valid = t < b;
+      int32_t c = 0, rk = 0;
+      double v = 0.0;
+      if (valid) {
+        c = indices[t];
+        rk = rank[c];
+        v = __ldcs(values + t);
+      }
+      const bool hot = valid && rk < nhot;
+      const unsigned hm = __ballot_sync(0xffffffffu, hot), vm = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const int64_t pos = hot ? a + hrun + __popc(hm & lt) : a + nh + crun + __popc(vm & ~hm & lt);
+        out_idx[pos] = hot ? -(rk + 1) : c;
+        out_val[pos] = v;
+      }
+      hrun += __popc(hm);
+      crun += __popc(vm & ~hm);
+    }
+  }
 }
 
 __global__ void k_fixup(int64_t nlong, const int32_t* __restrict__ long_row, const int32_t* __restrict__ s0,
@@ -882,12 +916,15 @@ extern "C" int svdrec_spmm_hot_rows(int32_t b) {
   return (int)((226 * 1024 - kHotWarps * 2 * kTabSlots * (int)sizeof(TabEnt)) / (8 * b));
 }
 
-extern "C" int svdrec_spmm_hot_encode(int64_t nnz, const int32_t* d_ranked, const int32_t* d_order, int32_t nhot,
-                                      int32_t* d_out, void* stream) {
-  SVDREC_ARG(nnz >= 0 && nhot >= 0, "spmm_hot_encode: bad arguments");
-  if (nnz == 0) return 0;
-  k_hot_encode<<<(unsigned)((nnz + 255) / 256), 256, 0, as_stream(stream)>>>(nnz, d_ranked, d_order, nhot, d_out);
-  return check_launch("spmm_hot_encode");
+extern "C" int svdrec_spmm_hot_partition(int64_t m, const int64_t* d_indptr, const int32_t* d_indices,
+                                         const double* d_values, const int32_t* d_rank, int32_t nhot,
+                                         int32_t* d_out_indices, double* d_out_values, void* stream) {
+  SVDREC_ARG(m >= 0 && nhot >= 0, "spmm_hot_partition: bad arguments");
+  if (m == 0) return 0;
+  const int64_t grid = min64((m + 7) / 8, (int64_t)sm_count() * 16);
+  k_hot_partition<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(m, d_indptr, d_indices, d_values, d_rank, nhot,
+                                                                  d_out_indices, d_out_values);
+  return check_launch("spmm_hot_partition");
 }
 
 extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,

@@ -171,9 +171,7 @@ SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "1") != "0"
 # (config 3, us per call, hot vs TMA): b = 2 259 vs 339, 8 267 vs 321, 16
 # 298 vs 338, 32 386 vs 592, 64 554 vs 917; at b = 20 (414 vs 363: 160-B
 # rows straddle the 128-B shared-memory phases -- bank conflicts, ncu: L1
-# data pipe 86 % busy) and b = 40 (668 vs 650) it is slower.  Only where the
-# ranked CSR is cheap (n <= 65,536 items: svdrec_rank_rows); on config 4
-# (1e6 items) the L2 already serves the hot rows and the misses bound it.
+# data pipe 86 % busy) and b = 40 (668 vs 650) it is slower.
 HOT_WIDTHS = frozenset(range(2, 17, 2)) | {32, 64}
 
 
@@ -185,13 +183,13 @@ def _hot_rows(plan, b: int, ldx: int, ldy: int, widths=None) -> int:
         return 0
     if b not in (HOT_WIDTHS if widths is None else widths) or (b > 32 and (ldx % 4 or ldy % 4)):
         return 0
-    if plan.n > 65536 or plan.n * (ldx // 2) >= 1 << 31:
+    if plan.n * (ldx // 2) >= 1 << 31:
         return 0
     return min(int(query("svdrec_spmm_hot_rows", b)), plan.n)
 
 
 def _spmm_hot(plan, X, ldx, Y, ldy, b, nhot):
-    """The hot-set kernel (csrc/spmm.cu k_spmm_hot) on the ranked CSR."""
+    """The hot-set kernel (csrc/spmm.cu k_spmm_hot) on the hot-first copy of this CSR."""
     hidx, hval = plan.hot_encoded(nhot)
     nwarp, wseg = plan.schedule(16)
     call("svdrec_spmm_hot", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),

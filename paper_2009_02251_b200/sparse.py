@@ -322,20 +322,20 @@ class DeviceCSR:
         return self._ranked
 
     def hot_encoded(self, nhot: int):
-        """(index, values) of the ranked CSR for the hot-set SpMM: index =
-        -(rank + 1) for the nhot most rated items, else the item id (built
-        once per nhot on the device, cached; one width at a time: 4 B per
-        rating)."""
+        """(index, values) of this CSR for the hot-set SpMM: every row
+        partitioned hot-first (the nhot most rated items' entries, index
+        -(rank + 1), then the others, index = item id), built once per nhot
+        on the device (cached; one width at a time: 12 B per rating)."""
         hit = self._hot.get(nhot)
         if hit is None:
             from . import kernels as K
 
-            rk, rv, _ = self.ranked()
-            out = torch.empty_like(rk)
-            K.call("svdrec_spmm_hot_encode", rk.numel(), K.ptr(rk), K.ptr(self.hot_items), int(nhot), K.ptr(out),
-                   K.stream_handle())
-            hit = (out, rv)
-            self._hot = {nhot: hit}
+            self._hot = {}  # release the previous width's copy first
+            idx = torch.empty_like(self.indices)
+            val = torch.empty_like(self.values)
+            K.call("svdrec_spmm_hot_partition", self.m, K.ptr(self.indptr), K.ptr(self.indices), K.ptr(self.values),
+                   K.ptr(self.item_rank), int(nhot), K.ptr(idx), K.ptr(val), K.stream_handle())
+            hit = self._hot[nhot] = (idx, val)
         return hit
 
     def _transpose_of_self(self) -> "DeviceCSR":

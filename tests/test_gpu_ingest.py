@@ -143,3 +143,25 @@ def test_scan_i64(gpu, n):
     y = K.scan_i64(x, total=tot)
     ref = torch.cumsum(x, 0) - x
     assert torch.equal(y, ref) and int(tot) == int(x.sum())
+
+
+@pytest.mark.parametrize("nhot", [0, 7, 50, 1000])
+def test_hot_partition_matches_numpy(gpu, nhot):
+    """The hot-set SpMM's copy of a CSR: each row stably partitioned into
+    the entries of the nhot most rated items (index -(rank + 1)) and the
+    rest (item id), values moved along."""
+    import paper_2009_02251_b200 as P
+    M = _rand_csr(400, 300, 0.05, 11 + nhot, empty_rows=(0, 5))
+    A = P.SparseRatings(M, 0.5, 5.0)
+    c = A.device(gpu).A
+    idx, val = c.hot_encoded(nhot)
+    rank = c.item_rank.cpu().numpy()
+    want_i, want_v = [], []
+    for r in range(M.shape[0]):
+        cols = M.indices[M.indptr[r]:M.indptr[r + 1]]
+        vals = M.data[M.indptr[r]:M.indptr[r + 1]]
+        hot = rank[cols] < nhot
+        want_i += list(-(rank[cols[hot]] + 1)) + list(cols[~hot])
+        want_v += list(vals[hot]) + list(vals[~hot])
+    assert np.array_equal(idx.cpu().numpy(), np.array(want_i, dtype=np.int32))
+    assert np.array_equal(val.cpu().numpy(), np.array(want_v))
