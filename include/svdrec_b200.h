@@ -50,11 +50,6 @@ const char* svdrec_last_error(void);
 int svdrec_device_sm_count(void);
 /* Number of kernels this library has launched in the process so far. */
 long long svdrec_launch_count(void);
-/* Persisting L2 access-policy window on a stream: kernels launched on it
- * afterwards keep [d_base, d_base + bytes) in the set-aside part of L2
- * (hit ratio scaled to the set-aside size).  bytes = 0 removes the window.
- * Returns the window size applied (0: unsupported / removed). */
-int64_t svdrec_l2_window(void* stream, const void* d_base, int64_t bytes);
 
 /* ---------------------------------------------------------------------
  * Gaussian stream.  Replaces GaussianStream.normal / gaussian_matrix

@@ -30,7 +30,6 @@ SIGNATURES = {
     "svdrec_last_error": (C.c_char_p, []),
     "svdrec_device_sm_count": (C.c_int, []),
     "svdrec_launch_count": (C.c_longlong, []),
-    "svdrec_l2_window": (_i64, [_p, _p, _i64]),
     "svdrec_normal_workspace_bytes": (_sz, [_i64]),
     "svdrec_normal_fill": (C.c_int, [_u64, _u64, _p, _i64, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p]),
