@@ -466,6 +466,10 @@ int tma_dispatch4(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, 
 #undef SVDREC_TMA4
 }
 
+#ifndef SVDREC_SPMM_S2
+#define SVDREC_SPMM_S2 2  // ring stages per warp
+#endif
+constexpr int kS2 = SVDREC_SPMM_S2;
 #ifndef SVDREC_SPMM_W2
 #define SVDREC_SPMM_W2 8
 #endif
@@ -855,7 +859,7 @@ int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin
   // SVDREC_SPMM_KIND=0 forces the plain kernel (A/B measurements)
   static const int kind = getenv("SVDREC_SPMM_KIND") ? atoi(getenv("SVDREC_SPMM_KIND")) : 1;
   if (vec2 && b <= 32 && nwarp > 0 && d_warp_seg && kind != 0 && xrows < (1ll << 31)) {
-    rc = tma_dispatch<2, kW2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+    rc = tma_dispatch<kS2, kW2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
                               d_values, d_X, ldx, d_Y, ldy, d_partial, s);
     if (rc) return rc;
     goto fixup;
