@@ -379,6 +379,23 @@ int svdrec_rank_rows(int64_t m, int32_t n, const int64_t* d_indptr, const int32_
                      const double* d_values, const int32_t* d_rank, int32_t* d_out_indices,
                      double* d_out_values, void* stream);
 
+/* The SpMM row-segment plan on the device (what the Python host's
+ * segment_plan / warp_plan define, sparse.py).  seg_plan_count: per row
+ * the exclusive scans d_first (first segment), d_sbase (first partial
+ * slot of a split row), d_lidx (fix-up record of a split row), all m
+ * int64, and d_totals = (segments, partial slots, split rows);
+ * seg_plan_emit writes the arrays of svdrec_spmm's plan.  warp_plan: the
+ * nwarp + 1 contiguous, cost-balanced range starts (cost = entries +
+ * seg_cost per segment); d_scratch holds nseg + 1 int64. */
+int svdrec_seg_plan_count(int64_t m, const int64_t* d_indptr, int32_t seg_max, int64_t* d_first,
+                          int64_t* d_sbase, int64_t* d_lidx, int64_t* d_totals, void* stream);
+int svdrec_seg_plan_emit(int64_t m, const int64_t* d_indptr, int32_t seg_max, const int64_t* d_first,
+                         const int64_t* d_sbase, const int64_t* d_lidx, int32_t* d_seg_row,
+                         int64_t* d_seg_begin, int64_t* d_seg_end, int32_t* d_seg_slot,
+                         int32_t* d_long_row, int32_t* d_long_s0, int32_t* d_long_s1, void* stream);
+int svdrec_warp_plan(int64_t nseg, const int64_t* d_seg_begin, const int64_t* d_seg_end, int64_t nwarp,
+                     int32_t seg_cost, int64_t* d_scratch, int32_t* d_out, void* stream);
+
 /* Exclusive scan of n int64 values (d_in may equal d_out); the total goes
  * to d_total (nullable). */
 int svdrec_scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, void* stream);

@@ -75,6 +75,9 @@ SIGNATURES = {
     "svdrec_csr_transpose_scratch": (_i64, [_i64]),
     "svdrec_rank_rows": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "svdrec_scan_i64": (C.c_int, [_i64, _p, _p, _p, _p]),
+    "svdrec_seg_plan_count": (C.c_int, [_i64, _p, _i32, _p, _p, _p, _p, _p]),
+    "svdrec_seg_plan_emit": (C.c_int, [_i64, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "svdrec_warp_plan": (C.c_int, [_i64, _p, _p, _i64, _i32, _p, _p, _p]),
     "svdrec_csr_transpose": (C.c_int, [_i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _i64, _p]),
     "svdrec_inv_sqrt_workspace_bytes": (_sz, [_i32]),
     "svdrec_inv_sqrt": (C.c_int, [_i32, _p, _i64, _p, _i64, _p, _sz, _p, _p, _p]),

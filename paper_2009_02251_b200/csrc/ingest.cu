@@ -321,6 +321,80 @@ __global__ void __launch_bounds__(kScanT) k_scan_apply(int64_t n, const int64_t*
   }
 }
 
+// SpMM row-segment plan (sparse.py segment_plan / warp_plan): rows cut
+// into segments of <= seg_max entries; split rows own consecutive partial
+// slots (numbered in row order) and a fix-up record; the warp schedule
+// cuts the segments into nwarp contiguous ranges of about equal cost
+// (entries + 16 per segment).
+__global__ void k_seg_count(int64_t m, const int64_t* __restrict__ indptr, int seg_max, int64_t* __restrict__ nps,
+                            int64_t* __restrict__ split_nps, int64_t* __restrict__ is_split) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const int64_t d = indptr[r + 1] - indptr[r];
+  const int64_t n = d <= seg_max ? 1 : (d + seg_max - 1) / seg_max;
+  nps[r] = n;
+  split_nps[r] = n > 1 ? n : 0;
+  is_split[r] = n > 1 ? 1 : 0;
+}
+
+__global__ void k_seg_emit(int64_t m, const int64_t* __restrict__ indptr, int seg_max,
+                           const int64_t* __restrict__ first, const int64_t* __restrict__ sbase,
+                           const int64_t* __restrict__ lidx, int32_t* __restrict__ seg_row,
+                           int64_t* __restrict__ seg_begin, int64_t* __restrict__ seg_end,
+                           int32_t* __restrict__ seg_slot, int32_t* __restrict__ long_row,
+                           int32_t* __restrict__ long_s0, int32_t* __restrict__ long_s1) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const int64_t a = indptr[r], e = indptr[r + 1];
+  const int64_t d = e - a;
+  const int64_t n = d <= seg_max ? 1 : (d + seg_max - 1) / seg_max;
+  const int64_t f = first[r];
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t b = a + j * seg_max;
+    seg_row[f + j] = (int32_t)r;
+    seg_begin[f + j] = b;
+    seg_end[f + j] = min64(b + seg_max, e);
+    seg_slot[f + j] = n > 1 ? (int32_t)(sbase[r] + j) : -1;
+  }
+  if (n > 1) {
+    const int64_t l = lidx[r];
+    long_row[l] = (int32_t)r;
+    long_s0[l] = (int32_t)sbase[r];
+    long_s1[l] = (int32_t)(sbase[r] + n);
+  }
+}
+
+__global__ void k_seg_cost(int64_t nseg, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
+                           int seg_cost, int64_t* __restrict__ cost) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nseg) cost[j] = seg_end[j] - seg_begin[j] + seg_cost;
+}
+
+// excl: exclusive scan of the segment costs, total = their sum; cut i (1 <=
+// i < nwarp) = 1 + the first j whose inclusive cost >= i * (total / nwarp)
+// (float64, numpy searchsorted 'left'), capped at nseg
+__global__ void k_warp_cuts(int64_t nseg, int64_t nwarp, const int64_t* __restrict__ excl,
+                            const int64_t* __restrict__ d_total, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > nwarp) return;
+  if (i == 0 || i == nwarp || nseg == 0) {
+    out[i] = i == 0 ? 0 : (int32_t)nseg;
+    return;
+  }
+  const int64_t total = *d_total;
+  const double target = (double)i * ((double)total / (double)nwarp);
+  int64_t lo = 0, hi = nseg;  // first j in [0, nseg) with incl[j] >= target, else nseg
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int64_t incl = mid + 1 < nseg ? excl[mid + 1] : total;
+    if ((double)incl >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  out[i] = (int32_t)min64(lo + 1, nseg);
+}
+
 }  // namespace
 }  // namespace svdrec
 
@@ -376,6 +450,60 @@ extern "C" int svdrec_rank_rows(int64_t m, int32_t n, const int64_t* d_indptr, c
   k_rank_rows<<<(unsigned)grid, kRankWarps * 32, smem, as_stream(stream)>>>(m, n, d_indptr, d_indices, d_values,
                                                                              d_rank, d_out_indices, d_out_values);
   return check_launch("rank_rows");
+}
+
+extern "C" int svdrec_seg_plan_count(int64_t m, const int64_t* d_indptr, int32_t seg_max, int64_t* d_first,
+                                     int64_t* d_sbase, int64_t* d_lidx, int64_t* d_totals, void* stream) {
+  SVDREC_ARG(m >= 0 && seg_max >= 1, "seg_plan_count: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  if (m == 0) {
+    SVDREC_CUDA(cudaMemsetAsync(d_totals, 0, 3 * sizeof(int64_t), s));
+    return 0;
+  }
+  const unsigned grid = (unsigned)((m + 255) / 256);
+  k_seg_count<<<grid, 256, 0, s>>>(m, d_indptr, seg_max, d_first, d_sbase, d_lidx);
+  int launches = 1;
+  int rc = scan_i64(m, d_first, d_first, d_totals + 0, s, &launches);
+  if (!rc) rc = scan_i64(m, d_sbase, d_sbase, d_totals + 1, s, &launches);
+  if (!rc) rc = scan_i64(m, d_lidx, d_lidx, d_totals + 2, s, &launches);
+  if (rc) {
+    set_error("seg_plan_count: %s", cudaGetErrorString((cudaError_t)rc));
+    return rc;
+  }
+  return check_launch("seg_plan_count", launches);
+}
+
+extern "C" int svdrec_seg_plan_emit(int64_t m, const int64_t* d_indptr, int32_t seg_max, const int64_t* d_first,
+                                    const int64_t* d_sbase, const int64_t* d_lidx, int32_t* d_seg_row,
+                                    int64_t* d_seg_begin, int64_t* d_seg_end, int32_t* d_seg_slot,
+                                    int32_t* d_long_row, int32_t* d_long_s0, int32_t* d_long_s1, void* stream) {
+  SVDREC_ARG(m >= 0 && seg_max >= 1, "seg_plan_emit: bad arguments");
+  if (m == 0) return 0;
+  k_seg_emit<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      m, d_indptr, seg_max, d_first, d_sbase, d_lidx, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_long_row,
+      d_long_s0, d_long_s1);
+  return check_launch("seg_plan_emit");
+}
+
+extern "C" int svdrec_warp_plan(int64_t nseg, const int64_t* d_seg_begin, const int64_t* d_seg_end, int64_t nwarp,
+                                int32_t seg_cost, int64_t* d_scratch, int32_t* d_out, void* stream) {
+  SVDREC_ARG(nseg >= 0 && nwarp >= 1, "warp_plan: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  int launches = 0;
+  int64_t* cost = d_scratch;          // nseg
+  int64_t* total = d_scratch + nseg;  // 1
+  if (nseg > 0) {
+    k_seg_cost<<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(nseg, d_seg_begin, d_seg_end, seg_cost, cost);
+    launches += 1;
+    const int rc = scan_i64(nseg, cost, cost, total, s, &launches);
+    if (rc) {
+      set_error("warp_plan: %s", cudaGetErrorString((cudaError_t)rc));
+      return rc;
+    }
+  }
+  k_warp_cuts<<<(unsigned)((nwarp + 1 + 255) / 256), 256, 0, s>>>(nseg, nwarp, cost, total, d_out);
+  launches += 1;
+  return check_launch("warp_plan", launches);
 }
 
 extern "C" int svdrec_scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, void* stream) {

@@ -195,6 +195,45 @@ def segment_plan_t(indptr: torch.Tensor, seg_max: int = SEG_MAX):
     return seg_row, seg_begin, seg_end, slot, long_row, s0, s1, nslots
 
 
+def segment_plan_dev(indptr: torch.Tensor, seg_max: int = SEG_MAX):
+    """segment_plan by the plan kernels (csrc/ingest.cu) on a CUDA tensor:
+    the same arrays, one small read for the sizes."""
+    from . import kernels as K
+
+    dev = indptr.device
+    m = indptr.numel() - 1
+    first = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    sbase = torch.empty_like(first)
+    lidx = torch.empty_like(first)
+    tot = torch.empty(3, dtype=torch.int64, device=dev)
+    K.call("svdrec_seg_plan_count", m, K.ptr(indptr), int(seg_max), K.ptr(first), K.ptr(sbase), K.ptr(lidx),
+           K.ptr(tot), K.stream_handle())
+    nseg, nslots, nlong = (int(x) for x in tot.cpu().numpy())
+    seg_row = torch.empty(nseg, dtype=torch.int32, device=dev)
+    seg_begin = torch.empty(nseg, dtype=torch.int64, device=dev)
+    seg_end = torch.empty(nseg, dtype=torch.int64, device=dev)
+    seg_slot = torch.empty(nseg, dtype=torch.int32, device=dev)
+    long_row = torch.empty(nlong, dtype=torch.int32, device=dev)
+    s0 = torch.empty(nlong, dtype=torch.int32, device=dev)
+    s1 = torch.empty(nlong, dtype=torch.int32, device=dev)
+    K.call("svdrec_seg_plan_emit", m, K.ptr(indptr), int(seg_max), K.ptr(first), K.ptr(sbase), K.ptr(lidx),
+           K.ptr(seg_row), K.ptr(seg_begin), K.ptr(seg_end), K.ptr(seg_slot), K.ptr(long_row), K.ptr(s0), K.ptr(s1),
+           K.stream_handle())
+    return seg_row, seg_begin, seg_end, seg_slot, long_row, s0, s1, nslots
+
+
+def warp_plan_dev(seg_begin: torch.Tensor, seg_end: torch.Tensor, nwarp: int, seg_cost: int = 16) -> torch.Tensor:
+    """warp_plan by a kernel (csrc/ingest.cu) on CUDA tensors (same result)."""
+    from . import kernels as K
+
+    nseg = seg_begin.numel()
+    scratch = torch.empty(nseg + 1, dtype=torch.int64, device=seg_begin.device)
+    out = torch.empty(nwarp + 1, dtype=torch.int32, device=seg_begin.device)
+    K.call("svdrec_warp_plan", nseg, K.ptr(seg_begin), K.ptr(seg_end), int(nwarp), int(seg_cost), K.ptr(scratch),
+           K.ptr(out), K.stream_handle())
+    return out
+
+
 def warp_plan_t(seg_begin: torch.Tensor, seg_end: torch.Tensor, nwarp: int, seg_cost: int = 16) -> torch.Tensor:
     """warp_plan on torch tensors (same result as the numpy version)."""
     dev = seg_begin.device
@@ -231,7 +270,8 @@ class DeviceCSR:
         self.indices = indices.to(torch.int32)
         self.values = values.to(torch.float64)
         self.nnz = int(self.indices.numel())
-        sr, sb, se, sl, lr, s0, s1, nslots = segment_plan_t(self.indptr)
+        cuda = self.device.type == "cuda"
+        sr, sb, se, sl, lr, s0, s1, nslots = (segment_plan_dev if cuda else segment_plan_t)(self.indptr)
         self.nseg = int(sr.numel())
         self.seg_row = sr.to(torch.int32)
         self.seg_begin = sb
@@ -244,7 +284,7 @@ class DeviceCSR:
         self.nslots = nslots
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count if self.device.type == "cuda" else 148
         self.nwarp = int(max(1, min(self.nseg, sms * WARPS_PER_SM)))
-        self.warp_seg = warp_plan_t(sb, se, self.nwarp)
+        self.warp_seg = (warp_plan_dev if cuda else warp_plan_t)(sb, se, self.nwarp)
         self._partial = {}
         self._ranked = None
         self._transpose = None
@@ -300,7 +340,8 @@ class DeviceCSR:
             sms = torch.cuda.get_device_properties(self.device).multi_processor_count \
                 if self.device.type == "cuda" else 148
             nw = int(max(1, min(self.nseg, sms * warps_per_sm)))
-            hit = self._sched[warps_per_sm] = (nw, warp_plan_t(self.seg_begin, self.seg_end, nw))
+            plan = warp_plan_dev if self.device.type == "cuda" else warp_plan_t
+            hit = self._sched[warps_per_sm] = (nw, plan(self.seg_begin, self.seg_end, nw))
         return hit
 
     def ranked(self):

@@ -165,3 +165,24 @@ def test_hot_partition_matches_numpy(gpu, nhot):
         want_v += list(vals[hot]) + list(vals[~hot])
     assert np.array_equal(idx.cpu().numpy(), np.array(want_i, dtype=np.int32))
     assert np.array_equal(val.cpu().numpy(), np.array(want_v))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_segment_and_warp_plan_kernels_match_numpy(gpu, seed):
+    """The SpMM plan built by the kernels equals sparse.segment_plan /
+    warp_plan (the numpy definitions) -- empty rows, rows split into
+    several segments."""
+    import torch
+    from paper_2009_02251_b200 import sparse as S
+    rng = np.random.default_rng(seed)
+    deg = rng.zipf(1.3, size=5000).clip(0, 9000)
+    deg[rng.random(5000) < 0.1] = 0
+    indptr = np.r_[0, np.cumsum(deg)].astype(np.int64)
+    ref = S.segment_plan(indptr, seg_max=256)
+    got = S.segment_plan_dev(torch.as_tensor(indptr, device=gpu), seg_max=256)
+    for a, b in zip(ref[:7], got[:7]):
+        np.testing.assert_array_equal(np.asarray(a, dtype=np.int64), b.cpu().numpy().astype(np.int64))
+    assert ref[7] == got[7]
+    for nw in (1, 7, 64, 5000, 100000):
+        np.testing.assert_array_equal(S.warp_plan(ref[1], ref[2], nw),
+                                      S.warp_plan_dev(got[1], got[2], nw).cpu().numpy())
