@@ -50,6 +50,13 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 int sm_count();
 
+// occupancy (resident CTAs per SM) cached per (kernel, device, block, smem)
+cudaError_t blocks_per_sm(const void* kernel, int threads, size_t smem, int* out);
+template <class K>
+cudaError_t blocks_per_sm(K* kernel, int threads, size_t smem, int* out) {
+  return blocks_per_sm(reinterpret_cast<const void*>(kernel), threads, smem, out);
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the attribute is per device, so a process driving several GPUs sets it on
 // each of them (lib.cu keeps the set of (kernel, device) pairs done).

@@ -27,6 +27,10 @@
 //                while a tile is scattered (two-deep register pipeline).
 // Traffic: the entries are read twice and written once (scattered); the
 // per-(column, slice) tables are n x slices int32 (transient).
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 
 namespace svdrec {
@@ -406,23 +410,29 @@ namespace svdrec {
 int scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, cudaStream_t s, int* launches) {
   const int64_t per_tile = (int64_t)kScanT * kScanPer;
   const int64_t ntiles = (n + per_tile - 1) / per_tile;
-  // tile sums: a grow-only buffer per device (stream-ordered allocations)
-  static int64_t* bufs[64] = {};
-  static int64_t caps[64] = {};
+  // tile sums: a grow-only buffer per (device, stream), allocated and freed
+  // stream-ordered on that stream, so scans issued concurrently on two
+  // streams (e.g. SpMM plans beside the scoring plan) never share scratch
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<int64_t*, int64_t>> bufs;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return (int)cudaErrorInvalidDevice;
-  if (ntiles + 1 > caps[dev]) {
-    if (bufs[dev]) cudaFreeAsync(bufs[dev], s);
-    caps[dev] = ntiles + 1 > 4096 ? ntiles + 1 : 4096;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bufs[dev]), (size_t)caps[dev] * sizeof(int64_t), s);
-    if (e != cudaSuccess) {
-      bufs[dev] = nullptr;
-      caps[dev] = 0;
-      return (int)e;
+  int64_t* buf = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = bufs[{dev, s}];
+    if (ntiles + 1 > slot.second) {
+      if (slot.first) cudaFreeAsync(slot.first, s);
+      const int64_t cap = ntiles + 1 > 4096 ? ntiles + 1 : 4096;
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&slot.first), (size_t)cap * sizeof(int64_t), s);
+      if (e != cudaSuccess) {
+        slot = {nullptr, 0};
+        return (int)e;
+      }
+      slot.second = cap;
     }
+    buf = slot.first;
   }
-  int64_t* buf = bufs[dev];
   if (n > 0) {
     k_scan_tiles<<<(unsigned)ntiles, kScanT, 0, s>>>(n, d_in, buf);
     k_scan_sums<<<1, kScanT, 0, s>>>(ntiles, buf, d_total);
@@ -444,7 +454,7 @@ extern "C" int svdrec_rank_rows(int64_t m, int32_t n, const int64_t* d_indptr, c
   const size_t smem = (size_t)kRankWarps * 2 * nwords * sizeof(uint32_t);
   SVDREC_CUDA(smem_attr_once(k_rank_rows, (int)((size_t)kRankWarps * 2 * kRankWords * sizeof(uint32_t))));
   int per_sm = 0;
-  SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rank_rows, kRankWarps * 32, smem));
+  SVDREC_CUDA(blocks_per_sm(k_rank_rows, kRankWarps * 32, smem, &per_sm));
   if (per_sm < 1) per_sm = 1;
   const int64_t grid = min64((int64_t)sm_count() * per_sm, (m + kRankWarps - 1) / kRankWarps);
   k_rank_rows<<<(unsigned)grid, kRankWarps * 32, smem, as_stream(stream)>>>(m, n, d_indptr, d_indices, d_values,

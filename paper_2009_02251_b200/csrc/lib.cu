@@ -2,7 +2,9 @@
 #include <cstdarg>
 #include <atomic>
 #include <mutex>
+#include <map>
 #include <set>
+#include <tuple>
 #include <utility>
 
 #include "common.cuh"
@@ -22,15 +24,45 @@ static std::atomic<long long> g_launches{0};
 
 void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// SM count of the CURRENT device (a process may drive several GPUs)
 int sm_count() {
-  static int n = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-  });
+  static std::mutex mu;
+  static std::map<int, int> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it != per_dev.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  per_dev[dev] = n;
   return n;
+}
+
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor cached per (kernel, device,
+// block size, dynamic shared memory)
+cudaError_t blocks_per_sm(const void* kernel, int threads, size_t smem, int* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(kernel, dev, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return cudaSuccess;
+    }
+  }
+  int n = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = n;
+  *out = n;
+  return cudaSuccess;
 }
 
 static std::mutex g_attr_mu;

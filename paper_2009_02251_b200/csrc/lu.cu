@@ -323,7 +323,7 @@ int try_lu_smem(int64_t r, int32_t b, double* d_A, int64_t lda, double* d_udiag,
   if (smem > kLuSmemMax) return 0;
   SVDREC_CUDA(smem_attr_once(k_lu_smem, (int)kLuSmemMax));
   int per_sm = 0;
-  SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu_smem, kLuThreads, smem));
+  SVDREC_CUDA(blocks_per_sm(k_lu_smem, kLuThreads, smem, &per_sm));
   if (per_sm < 2) return 0;
   double* cand = reinterpret_cast<double*>(w + align_up((size_t)r * 4) + align_up(2 * sizeof(Cand) * (size_t)sm_count() * 8));
   int32_t bb = b;
@@ -353,15 +353,12 @@ extern "C" int svdrec_lu_lower(int64_t r, int32_t b, double* d_A, int64_t lda, d
   bool used = false;
   int rc = try_lu_smem(r, b, d_A, lda, d_udiag, static_cast<char*>(d_work), d_status, as_stream(stream), &used);
   if (rc || used) return rc;
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int per_sm = 0;
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, 0));
-    max_blocks = per_sm * sm_count();
-    // grid barrier cost grows with the block count: 2 CTAs per SM is plenty
-    if (max_blocks > sm_count() * 2) max_blocks = sm_count() * 2;
-    if (max_blocks < 1) max_blocks = 1;
-  }
+  int per_sm = 0;
+  SVDREC_CUDA(blocks_per_sm(k_lu, kLuThreads, 0, &per_sm));
+  int max_blocks = per_sm * sm_count();
+  // grid barrier cost grows with the block count: 2 CTAs per SM is plenty
+  if (max_blocks > sm_count() * 2) max_blocks = sm_count() * 2;
+  if (max_blocks < 1) max_blocks = 1;
   int64_t want = (r + kLuThreads - 1) / kLuThreads;
   int nblk = (int)(want < max_blocks ? want : max_blocks);
   if (nblk < 1) nblk = 1;

@@ -321,17 +321,13 @@ extern "C" int svdrec_inv_sqrt(int32_t k, const double* d_G, int64_t ldg, double
   }
   const int use_tma = (k % 2 == 0) && k >= 2;
   const size_t smem = use_tma ? kNsSmemT : kNsSmem;
-  static int max_blocks_t[2] = {0, 0};
-  int& max_blocks = max_blocks_t[use_tma];
   SVDREC_CUDA(smem_attr_once(k_ns, (int)kNsSmemT));
-  if (!max_blocks) {
-    int per_sm = 0;
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ns, kNsThreads, smem));
-    max_blocks = per_sm * sm_count();
-    if (max_blocks > 4 * sm_count()) max_blocks = 4 * sm_count();
-    if (max_blocks > 4096) max_blocks = 4096;
-    if (max_blocks < 1) max_blocks = 1;
-  }
+  int per_sm = 0;
+  SVDREC_CUDA(blocks_per_sm(k_ns, kNsThreads, smem, &per_sm));
+  int max_blocks = per_sm * sm_count();
+  if (max_blocks > 4 * sm_count()) max_blocks = 4 * sm_count();
+  if (max_blocks > 4096) max_blocks = 4096;
+  if (max_blocks < 1) max_blocks = 1;
   const int nt = (k + NT - 1) / NT;
   int nblk = 2 * nt * nt;
   if (nblk > max_blocks) nblk = max_blocks;

@@ -408,11 +408,8 @@ int nn_tma_launch(int64_t r, int64_t p, int64_t q, double alpha, const double* X
   SVDREC_CUDA(smem_attr_once(k_nn_tma<NT>, 100 * 1024));
   const int64_t ntiles = (r + kNnRT - 1) / kNnRT;
   const int64_t gy = (q + 31) / 32;
-  static int per_sm = 0, per_qb = -1;  // smem depends on qb: re-query when it changes
-  if (per_qb != qb) {
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<NT>, kNnW * 32, smem));
-    per_qb = qb;
-  }
+  int per_sm = 0;  // smem depends on qb
+  SVDREC_CUDA(blocks_per_sm(k_nn_tma<NT>, kNnW * 32, smem, &per_sm));
   const int64_t slots = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
   const int64_t per_col = (slots + gy - 1) / gy;  // CTAs per column block
   const int tpc = (int)((ntiles + per_col - 1) / per_col);
@@ -444,11 +441,9 @@ template <int MT, int NT>
 int nn_launch(int64_t r, int64_t p, int q, double alpha, const double* X, int64_t ldx, const double* C, int64_t ldc,
               double beta, double* Y, int64_t ldy, cudaStream_t s) {
   const int64_t ntiles = (r + 8 * MT - 1) / (8 * MT);
-  static int per_sm = 0;  // resident 4-warp CTAs per SM (register bound)
-  if (!per_sm) {
-    SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_mma<MT, NT, 4>, 128, 0));
-    if (per_sm < 1) per_sm = 1;
-  }
+  int per_sm = 0;  // resident 4-warp CTAs per SM (register bound)
+  SVDREC_CUDA(blocks_per_sm(k_nn_mma<MT, NT, 4>, 128, 0, &per_sm));
+  if (per_sm < 1) per_sm = 1;
   const int64_t max_warps = (int64_t)sm_count() * per_sm * 4;
   const int tpw = (int)((ntiles + max_warps - 1) / max_warps);
   const int64_t warps = (ntiles + tpw - 1) / tpw;

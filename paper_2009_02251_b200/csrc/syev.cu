@@ -322,15 +322,12 @@ int run_jacobi(int64_t rows, int k, const double* A, int64_t lda, double* W, dou
   }
   const double tol_b = fmin(1e-10, 2.220446049250313e-16 * (double)(rows > 4 ? rows : 4));
   if (k > 1 && rows <= kBRowsMax) {
-    static int max_blocks_b = 0;
     const size_t smem = (size_t)2 * kBW * (kBRowsMax | 1) * 8;
     SVDREC_CUDA(smem_attr_once(k_bjacobi, (int)smem));
-    if (!max_blocks_b) {
-      int per_sm = 0;
-      SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, kBT, smem));
-      max_blocks_b = per_sm * sm_count();
-      if (max_blocks_b < 1) max_blocks_b = 1;
-    }
+    int per_sm = 0;
+    SVDREC_CUDA(blocks_per_sm(k_bjacobi, kBT, smem, &per_sm));
+    int max_blocks_b = per_sm * sm_count();
+    if (max_blocks_b < 1) max_blocks_b = 1;
     const int nb = (k + kBW - 1) / kBW;
     const int npairs = nb > 1 ? ((nb + 1) & ~1) / 2 : 1;
     int nblk = npairs < max_blocks_b ? npairs : max_blocks_b;
@@ -341,13 +338,10 @@ int run_jacobi(int64_t rows, int k, const double* A, int64_t lda, double* W, dou
     SVDREC_CUDA(cudaLaunchCooperativeKernel((void*)k_bjacobi, dim3(nblk), dim3(kBT), args, smem, s));
     note_launches(1);
   } else if (k > 1) {
-    static int max_blocks = 0;
-    if (!max_blocks) {
-      int per_sm = 0;
-      SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, kJThreads, 0));
-      max_blocks = per_sm * sm_count();
-      if (max_blocks < 1) max_blocks = 1;
-    }
+    int per_sm = 0;
+    SVDREC_CUDA(blocks_per_sm(k_jacobi, kJThreads, 0, &per_sm));
+    int max_blocks = per_sm * sm_count();
+    if (max_blocks < 1) max_blocks = 1;
     const int npairs = ((k + 1) & ~1) / 2;
     int nblk = (npairs * 32 + kJThreads - 1) / kJThreads;
     if (nblk > max_blocks) nblk = max_blocks;

@@ -347,7 +347,7 @@ int run_tsqr_gated(const Plan& p, int64_t r, int32_t b, const double* d_A, int64
     if (v.nc > maxnc) maxnc = v.nc;
   }
   int per_sm = 0;
-  SVDREC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr_coop, kThreads, smem_q));
+  SVDREC_CUDA(blocks_per_sm(k_tsqr_coop, kThreads, smem_q, &per_sm));
   int64_t grid = (int64_t)(per_sm > 0 ? per_sm : 1) * sm_count();
   if (grid > maxnc) grid = maxnc;
   int32_t bb = b;
