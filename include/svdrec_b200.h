@@ -90,8 +90,16 @@ int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_pos,
  *   nwarp/warp_seg            : optional balanced schedule (nwarp = 0:
  *                               none): warp w owns segments
  *                               [warp_seg[w], warp_seg[w+1]) -- contiguous,
- *                               ~equal nonzeros (sparse.py: warp_plan),
- *                               nwarp = SMs x svdrec_spmm_warps_per_sm(b)
+ *                               ~equal nonzeros (svdrec_warp_plan), nwarp =
+ *                               SMs x svdrec_spmm_warps_per_sm(b)
+ *   warp_chunk/chunks         : the same schedule in chunk records, which
+ *                               the pipelined kernel for even b <= 32 reads
+ *                               (svdrec_chunk_plan: 16-B records of <= 32
+ *                               entries; svdrec_warp_chunks: warp w owns
+ *                               records [warp_chunk[w], warp_chunk[w+1])).
+ *                               32 < b <= 64 (b % 4 == 0) runs the wide
+ *                               kernel on warp_seg; without the matching
+ *                               plan the plain row-per-warp kernel runs
  *   d_partial                 : (nslots x b) scratch
  * ------------------------------------------------------------------- */
 int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
@@ -100,12 +108,12 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
                 const double* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
                 int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                 const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
-                double* d_partial, void* stream);
-/* Warps per SM of the schedule (nwarp = SMs x this, warp_seg as above)
- * that the fast path for width b expects: 16 for even
- * b <= 32 (two 8-warp CTAs, 2 doubles per lane), fewer for 32 < b <= 64 with
- * b % 4 == 0 (4 doubles per lane, wider gather rings).  Other schedules
- * fall back to the plain kernel. */
+                const int32_t* d_warp_chunk, const void* d_chunks, double* d_partial, void* stream);
+/* Warps per SM of the schedule (nwarp = SMs x this) that the pipelined
+ * kernel for width b runs: 16 for even b <= 32 (two 8-warp CTAs, 2 doubles
+ * per lane), fewer for 32 < b <= 64 with b % 4 == 0 (4 doubles per lane,
+ * wider gather rings).  Without a schedule (or for odd b / unaligned rows)
+ * the plain row-per-warp kernel runs. */
 int svdrec_spmm_warps_per_sm(int32_t b);
 /* Hot-set variant of A @ X (even b <= 32, or b % 4 == 0 up to 64): the
  * rows X[d_hot_items[rank]] of the nhot most rated items (rank < nhot)
@@ -138,7 +146,7 @@ int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg
                     const float* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
                     int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                     const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
-                    double* d_partial, void* stream);
+                    const int32_t* d_warp_chunk, const void* d_chunks, double* d_partial, void* stream);
 /* ---------------------------------------------------------------------
  * Dense tall-skinny contractions (the deflation products of
  * rsvd.py:135-142, 179-194: Q @ (B @ X), Q @ (Q.T @ X), B.T @ (Q.T @ X)
@@ -395,6 +403,20 @@ int svdrec_seg_plan_emit(int64_t m, const int64_t* d_indptr, int32_t seg_max, co
                          int32_t* d_long_row, int32_t* d_long_s0, int32_t* d_long_s1, void* stream);
 int svdrec_warp_plan(int64_t nseg, const int64_t* d_seg_begin, const int64_t* d_seg_end, int64_t nwarp,
                      int32_t seg_cost, int64_t* d_scratch, int32_t* d_out, void* stream);
+/* The pipelined SpMM's chunk plan (linalg.py:141-158 has no counterpart:
+ * scipy walks the CSR row by row).  chunk_plan: every segment cut into
+ * chunks of <= 32 entries, one 16-B record each (int32 x 4: low word of the
+ * first entry's offset; output row, or ~slot for a split row's partial;
+ * entries | first-of-segment << 8 | last-of-segment << 9; high word of the
+ * offset).  d_cbase: nseg + 1 int64 (per segment its first record; [nseg] =
+ * the record count); d_recs: room for nnz / 32 + nseg records.
+ * warp_chunks: warp_chunk[w] = first record of segment warp_seg[w]
+ * (nwarp + 1 int32). */
+int svdrec_chunk_plan(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                      const int64_t* d_seg_end, const int32_t* d_seg_slot, int64_t* d_cbase,
+                      void* d_recs, void* stream);
+int svdrec_warp_chunks(int64_t nwarp, const int32_t* d_warp_seg, int64_t nseg, const int64_t* d_cbase,
+                       int32_t* d_warp_chunk, void* stream);
 
 /* Exclusive scan of n int64 values (d_in may equal d_out); the total goes
  * to d_total (nullable). */

@@ -399,6 +399,48 @@ __global__ void k_warp_cuts(int64_t nseg, int64_t nwarp, const int64_t* __restri
   out[i] = (int32_t)min64(lo + 1, nseg);
 }
 
+// Chunk records of the pipelined SpMM (csrc/spmm.cu k_spmm_pipe): every
+// segment cut into chunks of <= 32 nonzeros (an empty row is one chunk with
+// no entries), one 16-B record each: x / w = low / high word of the first
+// entry's offset, y = the output row (>= 0) or ~slot of a split row's
+// partial sum, z = entries | first chunk of its segment << 8 | last << 9.
+__global__ void k_chunk_count(int64_t nseg, const int64_t* __restrict__ seg_begin,
+                              const int64_t* __restrict__ seg_end, int64_t* __restrict__ cnt) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nseg) return;
+  const int64_t d = seg_end[j] - seg_begin[j];
+  cnt[j] = d <= 32 ? 1 : (d + 31) >> 5;
+}
+
+__global__ void k_chunk_emit(int64_t nseg, const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin,
+                             const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
+                             const int64_t* __restrict__ cbase, int4* __restrict__ recs) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nseg) return;
+  const int64_t a = seg_begin[j], e = seg_end[j];
+  const int64_t n = e - a <= 32 ? 1 : (e - a + 31) >> 5;
+  const int32_t slot = seg_slot[j];
+  const int32_t dst = slot < 0 ? seg_row[j] : ~slot;
+  int4* out = recs + cbase[j];
+  for (int64_t c = 0; c < n; ++c) {
+    const int64_t o = a + 32 * c;
+    const int nv = (int)min64(32, e - o);
+    const int64_t off = nv > 0 ? o : 0;  // an empty chunk reads nothing: keep its address inside the arrays
+    out[c] = make_int4((int)(uint32_t)(off & 0xffffffffll), dst, nv | (c == 0 ? 256 : 0) | (c == n - 1 ? 512 : 0),
+                       (int)(uint32_t)(off >> 32));
+  }
+}
+
+// warp_chunk[w] = first chunk of warp w's segment range (w = nwarp: the total)
+__global__ void k_warp_chunks(int64_t nwarp, const int32_t* __restrict__ warp_seg, int64_t nseg,
+                              const int64_t* __restrict__ cbase, const int64_t* __restrict__ total,
+                              int32_t* __restrict__ warp_chunk) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > nwarp) return;
+  const int64_t sgm = warp_seg[w];
+  warp_chunk[w] = (int32_t)(sgm < nseg ? cbase[sgm] : *total);
+}
+
 }  // namespace
 }  // namespace svdrec
 
@@ -514,6 +556,39 @@ extern "C" int svdrec_warp_plan(int64_t nseg, const int64_t* d_seg_begin, const 
   k_warp_cuts<<<(unsigned)((nwarp + 1 + 255) / 256), 256, 0, s>>>(nseg, nwarp, cost, total, d_out);
   launches += 1;
   return check_launch("warp_plan", launches);
+}
+
+// Chunk plan of the pipelined SpMM.  d_cbase: nseg + 1 int64 (exclusive scan
+// of the chunk counts; [nseg] = their total); d_recs: room for
+// nnz / 32 + nseg records (an upper bound known without a read-back).
+extern "C" int svdrec_chunk_plan(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
+                                 const int64_t* d_seg_end, const int32_t* d_seg_slot, int64_t* d_cbase,
+                                 void* d_recs, void* stream) {
+  SVDREC_ARG(nseg >= 0, "chunk_plan: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  if (nseg == 0) {
+    SVDREC_CUDA(cudaMemsetAsync(d_cbase, 0, sizeof(int64_t), s));
+    return 0;
+  }
+  const unsigned grid = (unsigned)((nseg + 255) / 256);
+  k_chunk_count<<<grid, 256, 0, s>>>(nseg, d_seg_begin, d_seg_end, d_cbase);
+  int launches = 1;
+  const int rc = scan_i64(nseg, d_cbase, d_cbase, d_cbase + nseg, s, &launches);
+  if (rc) {
+    set_error("chunk_plan: %s", cudaGetErrorString((cudaError_t)rc));
+    return rc;
+  }
+  k_chunk_emit<<<grid, 256, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_cbase,
+                                    reinterpret_cast<int4*>(d_recs));
+  return check_launch("chunk_plan", launches + 1);
+}
+
+extern "C" int svdrec_warp_chunks(int64_t nwarp, const int32_t* d_warp_seg, int64_t nseg, const int64_t* d_cbase,
+                                  int32_t* d_warp_chunk, void* stream) {
+  SVDREC_ARG(nwarp >= 1 && nseg >= 0, "warp_chunks: bad arguments");
+  k_warp_chunks<<<(unsigned)((nwarp + 1 + 255) / 256), 256, 0, as_stream(stream)>>>(nwarp, d_warp_seg, nseg, d_cbase,
+                                                                                    d_cbase + nseg, d_warp_chunk);
+  return check_launch("warp_chunks");
 }
 
 extern "C" int svdrec_scan_i64(int64_t n, const int64_t* d_in, int64_t* d_out, int64_t* d_total, void* stream) {

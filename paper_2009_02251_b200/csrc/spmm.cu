@@ -146,7 +146,7 @@ struct TmaGeom {
   static constexpr int G4 = (4 * B * ES + 127) / 128 * 128 / ES;  // elements per gather4 block (128-B aligned)
   static constexpr int ROWS = 8 * G4;                              // 32 rows
   static constexpr int ROWSD = ROWS * ES / 8;
-  static constexpr int STG = ROWSD + 64;  // + 32 values + 16 (meta, pad) + 16 (32 column ids)
+  static constexpr int STG = ROWSD + 64;  // k_spmm_tma stage: + 32 values + 16 (meta, pad) + 16 (32 column ids)
 };
 
 // V doubles per lane (V = 2: b <= 32; V = 4: 32 < b <= 64, b % 4 == 0),
@@ -401,38 +401,6 @@ int tma_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int3
   return check_launch("spmm_tma");
 }
 
-template <int S, int W>
-int tma_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
-                 const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot, const int32_t* indices,
-                 const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
-                 cudaStream_t s) {
-#define SVDREC_TMA(PP)                                                                                          \
-  case PP:                                                                                                      \
-    return tma_launch<PP, S, W>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot, indices, values, \
-                                X, ldx, Y, ldy, partial, s);
-  switch (b / 2) {
-    SVDREC_TMA(1)
-    SVDREC_TMA(2)
-    SVDREC_TMA(3)
-    SVDREC_TMA(4)
-    SVDREC_TMA(5)
-    SVDREC_TMA(6)
-    SVDREC_TMA(7)
-    SVDREC_TMA(8)
-    SVDREC_TMA(9)
-    SVDREC_TMA(10)
-    SVDREC_TMA(11)
-    SVDREC_TMA(12)
-    SVDREC_TMA(13)
-    SVDREC_TMA(14)
-    SVDREC_TMA(15)
-    SVDREC_TMA(16)
-    default:
-      return SVDREC_E_ARG;
-  }
-#undef SVDREC_TMA
-}
-
 // Wide blocks (32 < b <= 64, b % 4 == 0): four doubles per lane, P = b / 4
 // lanes per row, one CTA of w4_warps(P) warps per SM (the rings of 4-row
 // gathers of b-wide rows are twice as large).
@@ -466,42 +434,6 @@ int tma_dispatch4(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, 
 #undef SVDREC_TMA4
 }
 
-#ifndef SVDREC_SPMM_S2
-#define SVDREC_SPMM_S2 2  // ring stages per warp
-#endif
-constexpr int kS2 = SVDREC_SPMM_S2;
-#ifndef SVDREC_SPMM_W2
-#define SVDREC_SPMM_W2 8
-#endif
-// warps per CTA of the 2-CTA-per-SM variant (rings: 2 stages x ~5.6 KB per
-// warp at b = 20)
-constexpr int kW2 = SVDREC_SPMM_W2;
-
-// fp32 X (the fp32 variant): same kernels with float rows (half the gathered
-// bytes); b % 4 == 0 so every TMA row is a multiple of 16 B.
-int tma_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_seg, const int32_t* seg_row,
-                     const int64_t* seg_begin, const int64_t* seg_end, const int32_t* seg_slot,
-                     const int32_t* indices, const double* values, const float* X, int64_t ldx, double* Y,
-                     int64_t ldy, double* partial, cudaStream_t s) {
-#define SVDREC_TMAF(PP)                                                                                             \
-  case PP:                                                                                                          \
-    return tma_launch<PP, 2, 8, 2, float>(xrows, nwarp, warp_seg, seg_row, seg_begin, seg_end, seg_slot,     \
-                                                 indices, values, X, ldx, Y, ldy, partial, s);
-  switch (b / 2) {
-    SVDREC_TMAF(2)
-    SVDREC_TMAF(4)
-    SVDREC_TMAF(6)
-    SVDREC_TMAF(8)
-    SVDREC_TMAF(10)
-    SVDREC_TMAF(12)
-    SVDREC_TMAF(14)
-    SVDREC_TMAF(16)
-    default:
-      return SVDREC_E_ARG;
-  }
-#undef SVDREC_TMAF
-}
-
 // fp32 X, 32 < b <= 64 (b % 4 == 0): four floats per lane; the rings are
 // half as wide as the double ones, so twice the warps fit (<= 12 per SM).
 constexpr int w4f_warps(int P) {
@@ -532,6 +464,292 @@ int tma_dispatch4_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_s
       return SVDREC_E_ARG;
   }
 #undef SVDREC_TMA4F
+}
+
+// ---------------------------------------------------------------------------
+// Chunk-record pipeline (round 2): the same gather4 rings, driven by the
+// precomputed 16-B chunk records of csrc/ingest.cu (svdrec_chunk_plan)
+// instead of per-segment metadata, shuffles and 64-bit bounds arithmetic --
+// k_spmm_tma above runs ~390 warp instructions per 32-entry chunk and is
+// bound by that serial stream (16 warps per SM, ~2,250 cycles per chunk per
+// warp whatever the ring depth).  Here a chunk costs ~120:
+//   fetch   the chunk's 32 column ids and values go global -> shared memory
+//           by cp.async (LDGSTS, zero-filled past the
+//           chunk's end), D chunks deep, so no register waits on the CSR
+//           stream's HBM latency;
+//   gather  lanes 0..7 read four ids each with one LDS.128 and issue the
+//           gather4 of those X rows into the S-deep row ring (mbarrier tx);
+//   consume as k_spmm_tma: NS unrolled LDS.128 + LDS.64 + DFMA steps on two
+//           accumulator chains, fixed-order group fold at a segment's end.
+// Summation order per output element is the one of k_spmm / k_spmm_tma.
+// (an L2 evict-first cache hint on these 4- / 8-byte copies raises "illegal
+// instruction" on sm_100a: plain .ca copies)
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kRecRing = 16;   // per-warp ring of chunk records in shared memory
+constexpr int kRecAhead = 8;   // records are copied in this many chunks ahead of their fetch
+
+template <int P, int S, int D, int V, typename TX>
+struct PipeGeom {
+  using Gm = TmaGeom<P, V, TX>;
+  static constexpr int CSRB = 384;  // bytes per CSR slot: 32 values, 32 ids
+  static constexpr int WARPB = S * Gm::ROWSD * 8 + (D * CSRB + kRecRing * 16 + 127) / 128 * 128;  // bytes per warp
+};
+
+template <int P, int S, int D, int W, int V, typename TX = double>
+__global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
+    const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_chunk,
+    const int4* __restrict__ chunks, const int32_t* __restrict__ indices, const double* __restrict__ values,
+    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial) {
+  static_assert(D >= S, "spmm: the CSR ring must be at least as deep as the row ring");
+  static_assert(kRecAhead >= 2 * (D - S + 1) && kRecAhead + D <= kRecRing, "spmm: record ring too small");
+  using Gm = TmaGeom<P, V, TX>;
+  using Pg = PipeGeom<P, S, D, V, TX>;
+  constexpr int B = Gm::B, G = 32 / P, G4 = Gm::G4, ROWS = Gm::ROWSD;
+  extern __shared__ __align__(128) unsigned char smb[];
+  __shared__ __align__(8) uint64_t bars[W * S];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  unsigned char* base = smb + (size_t)wib * Pg::WARPB;
+  double* rows = reinterpret_cast<double*>(base);                   // S stages of ROWS doubles
+  unsigned char* csr = base + (size_t)S * ROWS * 8;                 // D slots of CSRB bytes
+  int4* rring = reinterpret_cast<int4*>(csr + D * Pg::CSRB);        // kRecRing chunk records
+  uint64_t* bar = bars + wib * S;
+  if (lane < S) mbar_init(bar + lane, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  if (w >= nwarp) return;
+  const int g = lane / P, pc = lane - (lane / P) * P;
+  const bool active = g < G;
+
+  const int32_t c_lo = warp_chunk[w], c_hi = warp_chunk[w + 1];
+  const int n = c_hi - c_lo;
+  if (n <= 0) return;
+  // the chunk records travel through their own small ring: the first
+  // kRecAhead are read here, record j + kRecAhead is copied in (cp.async,
+  // lane 0) at step j, so no step waits on a record's global load
+  if (lane < kRecAhead && lane < n) rring[lane] = __ldg(chunks + c_lo + lane);
+  __syncwarp();
+  int fj = 0, fs = 0;  // next chunk to fetch (relative), its CSR slot
+  int step = 0;        // fetch() calls so far minus the prologue's: record step + kRecAhead is requested
+  auto fetch = [&](bool ahead) {
+    if (fj < n) {
+      const int4 rec = rring[fj & (kRecRing - 1)];
+      const int64_t off = (int64_t)(((uint64_t)(uint32_t)rec.w << 32) | (uint32_t)rec.x);
+      const bool in = lane < (rec.z & 63);
+      const int64_t o = off + (in ? lane : 0);
+      unsigned char* sl = csr + fs * Pg::CSRB;
+      cp_async8(sl + 8 * lane, values + o, in ? 8u : 0u);
+      cp_async4(sl + 256 + 4 * lane, indices + o, in ? 4u : 0u);
+      ++fj;
+    }
+    if (ahead) {
+      const int rj = step + kRecAhead;
+      if (lane == 0 && rj < n) cp_async16(rring + (rj & (kRecRing - 1)), chunks + c_lo + rj);
+      ++step;
+    }
+    cp_async_commit();
+    if (++fs == D) fs = 0;
+  };
+  int gs = 0, gr = 0, gj = 0;  // CSR slot / row stage / chunk of the next gather
+  auto gather = [&]() {
+    cp_async_wait<D - S>();
+    __syncwarp();
+    const unsigned char* sl = csr + gs * Pg::CSRB;
+    const int nvf = rring[gj & (kRecRing - 1)].z;
+    const int ng = ((nvf & 63) + 3) >> 2;
+    if (lane == 0) mbar_expect_tx(bar + gr, (unsigned)(ng * 4 * B * sizeof(TX)));
+    if (lane < ng) {
+      const int4 r = *reinterpret_cast<const int4*>(sl + 256 + 16 * lane);
+      tma_gather4(reinterpret_cast<TX*>(rows + gr * ROWS) + lane * G4, &tmX, 0, r.x, r.y, r.z, r.w, bar + gr);
+    }
+    ++gj;
+    if (++gs == D) gs = 0;
+    if (++gr == S) gr = 0;
+  };
+  Acc<V> acc, acc1;
+  acc.zero();
+  acc1.zero();
+  int cs = 0, cr = 0, cj = 0;
+  unsigned cph = 0;  // phase parity of row stage cr
+  auto consume = [&]() {
+    const unsigned char* sl = csr + cs * Pg::CSRB;
+    const int4 m = rring[cj & (kRecRing - 1)];  // y: destination, z: entries | flags
+    const int nv = m.z & 63;
+    mbar_wait(bar + cr, cph);
+    if (m.z & 256) {
+      acc.zero();
+      acc1.zero();
+    }
+    if (active) {
+      constexpr int NS = (32 + G - 1) / G;
+      const TX* sx = reinterpret_cast<const TX*>(rows + cr * ROWS);
+      const TX* xr = sx + ((g >> 2) * G4 + (g & 3) * B) + V * pc;
+      const double* vr = reinterpret_cast<const double*>(sl) + g;
+      Acc<V> xs[NS];
+      double vs[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        const int j = q * G + g;
+        const int jo = q * G;
+        const int jc = j < 32 ? j : 31;
+        const TX* src = G4 == 4 * B ? xr + jo * B : sx + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
+        xs[q].load(src);
+        vs[q] = vr[jc - g];
+      }
+      if (nv == 32) {
+        // a full chunk (most of them): no per-step bounds
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if ((q + 1) * G <= 32 || q * G + g < 32) {
+            if (q & 1)
+              acc1.fma(vs[q], xs[q]);
+            else
+              acc.fma(vs[q], xs[q]);
+          }
+        }
+      } else {
+        const int left = nv - g;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if (q * G < left) {
+            if (q & 1)
+              acc1.fma(vs[q], xs[q]);
+            else
+              acc.fma(vs[q], xs[q]);
+          }
+        }
+      }
+    }
+    if (m.z & 512) {
+      acc.add(acc1);
+      Acc<V> tot = acc;
+#pragma unroll
+      for (int h = 1; h < G; ++h) {
+        const Acc<V> o = acc.shfl((lane + h * P) & 31);
+        if (g == 0) tot.add(o);
+      }
+      if (g == 0) {
+        double* dst = m.y >= 0 ? (Y + (int64_t)m.y * ldy + V * pc) : (partial + (int64_t)(~m.y) * B + V * pc);
+        tot.store(dst);
+      }
+    }
+    __syncwarp();  // every lane is done with the stage and the CSR slot
+    ++cj;
+    if (++cs == D) cs = 0;
+    if (++cr == S) {
+      cr = 0;
+      cph ^= 1u;
+    }
+  };
+
+#pragma unroll
+  for (int t = 0; t <= D - S; ++t) fetch(false);
+  for (int i = 0; i < n + S - 1; ++i) {
+    if (i < n) gather();
+    if (i >= S - 1) consume();
+    fetch(true);
+  }
+  cp_async_wait<0>();
+}
+
+template <int P, int S, int D, int W, int V = 2, typename TX = double>
+int pipe_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const void* chunks, const int32_t* indices,
+                const double* values, const TX* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
+                cudaStream_t s) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) {
+    set_error("spmm: cuTensorMapEncodeTiled unavailable");
+    return SVDREC_E_UNSUPPORTED;
+  }
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)(V * P), (cuuint64_t)xrows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(TX)};
+  const cuuint32_t box[2] = {(cuuint32_t)(V * P), 1};
+  const cuuint32_t es[2] = {1, 1};
+  const CUtensorMapDataType dt = sizeof(TX) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUresult r = enc(&tm, dt, 2, const_cast<TX*>(X), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("spmm: tensor map encode failed (%d)", (int)r);
+    return SVDREC_E_UNSUPPORTED;
+  }
+  constexpr size_t ring = (size_t)W * PipeGeom<P, S, D, V, TX>::WARPB;
+  constexpr size_t kMaxSmem = 226 * 1024;
+  if constexpr (ring > kMaxSmem) {
+    set_error("spmm: the gather rings of this build exceed shared memory (b=%d)", V * P);
+    return SVDREC_E_UNSUPPORTED;
+  } else {
+    SVDREC_CUDA(smem_attr_once(k_spmm_pipe<P, S, D, W, V, TX>, (int)kMaxSmem));
+    const int64_t grid = (nwarp + W - 1) / W;
+    k_spmm_pipe<P, S, D, W, V, TX><<<(unsigned)grid, W * 32, ring, s>>>(
+        tm, nwarp, warp_chunk, reinterpret_cast<const int4*>(chunks), indices, values, Y, ldy, partial);
+    return check_launch("spmm_pipe");
+  }
+}
+
+#ifndef SVDREC_SPMM_S2
+#define SVDREC_SPMM_S2 2  // row-ring stages per warp
+#endif
+#ifndef SVDREC_SPMM_D2
+#define SVDREC_SPMM_D2 4  // CSR-ring slots per warp
+#endif
+#ifndef SVDREC_SPMM_W2
+#define SVDREC_SPMM_W2 8  // warps per CTA of the 2-CTA-per-SM variant (b <= 32)
+#endif
+constexpr int kS2 = SVDREC_SPMM_S2, kD2 = SVDREC_SPMM_D2, kW2 = SVDREC_SPMM_W2;
+
+#define SVDREC_PIPE_ARGS xrows, nwarp, warp_chunk, chunks, indices, values, X, ldx, Y, ldy, partial, s
+
+// even b <= 32: the chunk-record pipeline, two CTAs of kW2 warps per SM
+int pipe_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const void* chunks,
+                  const int32_t* indices, const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                  double* partial, cudaStream_t s) {
+#define SVDREC_PIPE(PP) \
+  case PP:              \
+    return pipe_launch<PP, kS2, kD2, kW2, 2, double>(SVDREC_PIPE_ARGS);
+  switch (b / 2) {
+    SVDREC_PIPE(1) SVDREC_PIPE(2) SVDREC_PIPE(3) SVDREC_PIPE(4) SVDREC_PIPE(5) SVDREC_PIPE(6) SVDREC_PIPE(7)
+    SVDREC_PIPE(8) SVDREC_PIPE(9) SVDREC_PIPE(10) SVDREC_PIPE(11) SVDREC_PIPE(12) SVDREC_PIPE(13)
+    SVDREC_PIPE(14) SVDREC_PIPE(15) SVDREC_PIPE(16)
+    default: return SVDREC_E_ARG;
+  }
+#undef SVDREC_PIPE
+}
+
+// fp32 X (the fp32 variant), b % 4 == 0 <= 32: the same kernel with float
+// rows (half the gathered bytes; every TMA row a multiple of 16 B)
+int pipe_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const void* chunks,
+                      const int32_t* indices, const double* values, const float* X, int64_t ldx, double* Y,
+                      int64_t ldy, double* partial, cudaStream_t s) {
+#define SVDREC_PIPEF(PP) \
+  case PP:               \
+    return pipe_launch<PP, kS2, kD2, 8, 2, float>(SVDREC_PIPE_ARGS);
+  switch (b / 2) {
+    SVDREC_PIPEF(2) SVDREC_PIPEF(4) SVDREC_PIPEF(6) SVDREC_PIPEF(8) SVDREC_PIPEF(10) SVDREC_PIPEF(12)
+    SVDREC_PIPEF(14) SVDREC_PIPEF(16)
+    default: return SVDREC_E_ARG;
+  }
+#undef SVDREC_PIPEF
 }
 
 // ---------------------------------------------------------------------------
@@ -842,62 +1060,13 @@ extern "C" int svdrec_spmm_warps_per_sm(int32_t b) {
 }
 
 namespace {
-int spmm_impl(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin, const int64_t* d_seg_end,
-              const int32_t* d_seg_slot, const int32_t* d_indices, const double* d_values, const double* d_X,
-              int64_t ldx, int64_t xrows, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
-              const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
-              const int32_t* d_warp_seg, double* d_partial, void* stream) {
-  SVDREC_ARG(b >= 1 && ldx >= b && ldy >= b && nseg >= 0 && nlong >= 0, "spmm: bad arguments b=%d", b);
-  if (nseg == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  const bool vec2 = (b % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
-                    ((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
-                      reinterpret_cast<uintptr_t>(d_partial)) %
-                         16 ==
-                     0);
-  int rc = 0;
-  // SVDREC_SPMM_KIND=0 forces the plain kernel (A/B measurements)
-  static const int kind = getenv("SVDREC_SPMM_KIND") ? atoi(getenv("SVDREC_SPMM_KIND")) : 1;
-  if (vec2 && b <= 32 && nwarp > 0 && d_warp_seg && kind != 0 && xrows < (1ll << 31)) {
-    rc = tma_dispatch<kS2, kW2>(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
-                              d_values, d_X, ldx, d_Y, ldy, d_partial, s);
-    if (rc) return rc;
-    goto fixup;
-  }
-  if (vec2 && b > 32 && b <= 64 && b % 4 == 0 && ldx % 4 == 0 && nwarp > 0 && d_warp_seg && kind != 0 &&
-      xrows < (1ll << 31)) {
-    rc = tma_dispatch4(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
-                       d_values, d_X, ldx, d_Y, ldy, d_partial, s);
-    if (rc) return rc;
-    goto fixup;
-  }
-  {
-  const int vec = vec2 ? 2 : 1;
-  const int lanes_needed = (b + vec - 1) / vec;
-  const int lpn = lanes_needed >= 32 ? 32 : lanes_needed;
-  const int npw = 32 / lpn;
-  const int tb = 256;
-  const int64_t warps = nseg;
-  int64_t grid = (warps * 32 + tb - 1) / tb;
-  const int64_t cap = (int64_t)sm_count() * 8 * 64;
-  if (grid > cap) grid = cap;
-  if (vec2)
-    k_spmm<2><<<(unsigned)grid, tb, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
-                                             d_values, d_X, ldx, d_Y, ldy, b, d_partial, lpn, npw);
-  else
-    k_spmm<1><<<(unsigned)grid, tb, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
-                                             d_values, d_X, ldx, d_Y, ldy, b, d_partial, lpn, npw);
-  rc = check_launch("spmm");
-  if (rc) return rc;
-  }
-fixup:
-  if (nlong > 0) {
-    const int64_t tot = nlong * b;
-    k_fixup<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nlong, d_long_row, d_long_slot0, d_long_slot1,
-                                                          d_partial, d_Y, ldy, b);
-    rc = check_launch("spmm_fixup");
-  }
-  return rc;
+int run_fixup(int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1,
+              const double* d_partial, double* d_Y, int64_t ldy, int32_t b, cudaStream_t s) {
+  if (nlong <= 0) return 0;
+  const int64_t tot = nlong * b;
+  k_fixup<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial, d_Y,
+                                                        ldy, b);
+  return check_launch("spmm_fixup");
 }
 }  // namespace
 
@@ -906,9 +1075,45 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
                            const double* d_values, const double* d_X, int64_t ldx, int64_t xrows, double* d_Y,
                            int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
                            const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
-                           const int32_t* d_warp_seg, double* d_partial, void* stream) {
-  return spmm_impl(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices, d_values, d_X, ldx, xrows, d_Y,
-                   ldy, b, nlong, d_long_row, d_long_slot0, d_long_slot1, nwarp, d_warp_seg, d_partial, stream);
+                           const int32_t* d_warp_seg, const int32_t* d_warp_chunk, const void* d_chunks,
+                           double* d_partial, void* stream) {
+  SVDREC_ARG(b >= 1 && ldx >= b && ldy >= b && nseg >= 0 && nlong >= 0, "spmm: bad arguments b=%d", b);
+  if (nseg == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  const bool vec2 = (b % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
+                      reinterpret_cast<uintptr_t>(d_partial)) %
+                         16 ==
+                     0);
+  // SVDREC_SPMM_KIND=0 forces the plain kernel (A/B measurements)
+  static const int kind = getenv("SVDREC_SPMM_KIND") ? atoi(getenv("SVDREC_SPMM_KIND")) : 1;
+  const bool sched = vec2 && nwarp > 0 && kind != 0 && xrows < (1ll << 31);
+  int rc = 0;
+  if (sched && b <= 32 && d_warp_chunk && d_chunks) {
+    rc = pipe_dispatch(b, xrows, nwarp, d_warp_chunk, d_chunks, d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial,
+                       s);
+  } else if (sched && b > 32 && b <= 64 && b % 4 == 0 && ldx % 4 == 0 && d_warp_seg) {
+    rc = tma_dispatch4(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                       d_values, d_X, ldx, d_Y, ldy, d_partial, s);
+  } else {
+    const int vec = vec2 ? 2 : 1;
+    const int lanes_needed = (b + vec - 1) / vec;
+    const int lpn = lanes_needed >= 32 ? 32 : lanes_needed;
+    const int npw = 32 / lpn;
+    const int tb = 256;
+    int64_t grid = (nseg * 32 + tb - 1) / tb;
+    const int64_t cap = (int64_t)sm_count() * 8 * 64;
+    if (grid > cap) grid = cap;
+    if (vec2)
+      k_spmm<2><<<(unsigned)grid, tb, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                                               d_values, d_X, ldx, d_Y, ldy, b, d_partial, lpn, npw);
+    else
+      k_spmm<1><<<(unsigned)grid, tb, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
+                                               d_values, d_X, ldx, d_Y, ldy, b, d_partial, lpn, npw);
+    rc = check_launch("spmm");
+  }
+  if (rc) return rc;
+  return run_fixup(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial, d_Y, ldy, b, s);
 }
 
 extern "C" int svdrec_spmm_hot_rows(int32_t b) {
@@ -1009,28 +1214,24 @@ extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int
                                const double* d_values, const float* d_X, int64_t ldx, int64_t xrows, double* d_Y,
                                int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
                                const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
-                               const int32_t* d_warp_seg, double* d_partial, void* stream) {
+                               const int32_t* d_warp_seg, const int32_t* d_warp_chunk, const void* d_chunks,
+                               double* d_partial, void* stream) {
   SVDREC_ARG(b >= 4 && b <= 64 && b % 4 == 0 && ldx >= b && ldx % 4 == 0 && ldy >= b && ldy % 2 == 0 && nseg >= 0 &&
                  nlong >= 0 && (b <= 32 || ldy % 4 == 0),
              "spmm_x32: needs b in {4, 8, ..., 64} and 16-B aligned rows (b=%d)", b);
-  SVDREC_ARG(nwarp > 0 && d_warp_seg, "spmm_x32: needs a warp schedule");
+  SVDREC_ARG(nwarp > 0 && (b <= 32 ? (d_warp_chunk && d_chunks) : d_warp_seg != nullptr),
+             "spmm_x32: needs a schedule (chunk plan for b <= 32, warp ranges above)");
   SVDREC_ARG(((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
                reinterpret_cast<uintptr_t>(d_partial)) % 16) == 0,
              "spmm_x32: operands must be 16-B aligned");
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
-  int rc = b <= 32 ? tma_dispatch_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
-                                     d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, s)
-                   : tma_dispatch4_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot,
-                                       d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, s);
+  const int rc = b <= 32 ? pipe_dispatch_f32(b, xrows, nwarp, d_warp_chunk, d_chunks, d_indices, d_values, d_X, ldx,
+                                             d_Y, ldy, d_partial, s)
+                         : tma_dispatch4_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end,
+                                             d_seg_slot, d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, s);
   if (rc) return rc;
-  if (nlong > 0) {
-    const int64_t tot = nlong * b;
-    k_fixup<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial,
-                                                          d_Y, ldy, b);
-    rc = check_launch("spmm_fixup");
-  }
-  return rc;
+  return run_fixup(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial, d_Y, ldy, b, s);
 }
 
 extern "C" int svdrec_spmm_x32_warps_per_sm(int32_t b) {

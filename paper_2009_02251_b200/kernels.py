@@ -148,13 +148,12 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
         # fp32 variant: X stored as float (a rounded copy), fp64 values / accumulation / Y
         X32 = torch.empty(X.shape[0], b, dtype=torch.float32, device=X.device)
         X32.copy_(X)
-        nw, ws = plan.schedule(query("svdrec_spmm_x32_warps_per_sm", b))
-        sched = (nw, ptr(ws))
+        nw, wseg, wc, recs = _schedules(plan, query("svdrec_spmm_x32_warps_per_sm", b), b)
         with _span("spmm", plan.nnz * 12 + (plan.m + 1) * 8 + plan.n * b * 4 + plan.m * b * 8, plan.nnz * 4 * b):
             call("svdrec_spmm_x32", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end),
                  ptr(plan.seg_slot), ptr(plan.indices), ptr(plan.values), ptr(X32), b, plan.n, ptr(Y), ldy, b,
-                 plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), *sched, ptr(part),
-                 stream_handle())
+                 plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), nw, ptr(wseg), ptr(wc),
+                 ptr(recs), ptr(part), stream_handle())
         return Y
     hot = _hot_rows(plan, b, ldx, ldy)
     with _span("spmm", nbytes, gathered):
@@ -165,20 +164,20 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
     return Y
 
 
-# SVDREC_SPMM_HOT=0 keeps A @ X on the TMA-gather kernel (A/B measurements)
+# SVDREC_SPMM_HOT=0 keeps A @ X on the TMA-gather kernels (A/B measurements)
 SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "1") != "0"
-# widths where the hot-set kernel measured faster than k_spmm_tma for A @ X
-# (config 3, us per call, hot vs TMA): b = 2 259 vs 339, 8 267 vs 321, 16
-# 298 vs 338, 32 386 vs 592, 64 554 vs 917; at b = 20 (414 vs 363: 160-B
-# rows straddle the 128-B shared-memory phases -- bank conflicts, ncu: L1
-# data pipe 86 % busy) and b = 40 (668 vs 650) it is slower.
-HOT_WIDTHS = frozenset(range(2, 17, 2)) | {32, 64}
+# widths where the hot-set kernel measured faster than the TMA-gather kernels
+# for A @ X (config 3, us per call, hot vs TMA): b = 2 259 vs 286, 8 267 vs
+# 272, 32 386 vs 560, 64 554 vs 917; at b = 16 (298 vs 295), 20 (414 vs 331:
+# 160-B rows straddle the 128-B shared-memory phases -- bank conflicts, ncu:
+# L1 data pipe 86 % busy) and 40 (668 vs 650) it is not.
+HOT_WIDTHS = frozenset({2, 4, 6, 8, 32, 64})
 
 
 def _hot_rows(plan, b: int, ldx: int, ldy: int, widths=None) -> int:
     """Hot rows of X staged in shared memory by the hot-set kernel, or 0
     when it is not used (no popularity order on this CSR, a width where the
-    TMA kernel is faster, unaligned rows)."""
+    TMA kernels are faster, unaligned rows)."""
     if not SPMM_HOT or getattr(plan, "item_rank", None) is None or ldx % 2 or ldy % 2:
         return 0
     if b not in (HOT_WIDTHS if widths is None else widths) or (b > 32 and (ldx % 4 or ldy % 4)):
@@ -198,12 +197,24 @@ def _spmm_hot(plan, X, ldx, Y, ldy, b, nhot):
          stream_handle())
 
 
+def _schedules(plan, warps_per_sm: int, b: int):
+    """(nwarp, warp_seg, warp_chunk, records) for width b: the chunk plan
+    for the pipelined kernel (b <= 32), the segment ranges for the wide one."""
+    if b <= 32:
+        nwarp, wchunk, recs = plan.chunk_schedule(warps_per_sm)
+        return nwarp, None, wchunk, recs
+    nwarp, wseg = plan.schedule(warps_per_sm)
+    return nwarp, wseg, None, None
+
+
 def _spmm_tma(plan, X, ldx, Y, ldy, b):
-    """The TMA-gather kernel (csrc/spmm.cu) on one CSR."""
-    nwarp, wseg = plan.schedule(query("svdrec_spmm_warps_per_sm", b))
+    """The TMA-gather kernels (csrc/spmm.cu: k_spmm_pipe for even b <= 32,
+    k_spmm_tma for the wide blocks) on one CSR."""
+    nwarp, wseg, wchunk, recs = _schedules(plan, query("svdrec_spmm_warps_per_sm", b), b)
     call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
          ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
-         ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(plan.partial(b)), stream_handle())
+         ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(wchunk), ptr(recs), ptr(plan.partial(b)),
+         stream_handle())
 
 
 def gemm_tn(X: torch.Tensor, Y: torch.Tensor, C: torch.Tensor | None = None, alpha: float = 1.0,

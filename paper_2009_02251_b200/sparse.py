@@ -290,6 +290,8 @@ class DeviceCSR:
         self._transpose = None
         self._hot = {}
         self._sched = {}
+        self._chunks = None
+        self._wchunk = {}
         self.h2d_bytes = h2d_bytes
 
     @classmethod
@@ -343,6 +345,28 @@ class DeviceCSR:
             plan = warp_plan_dev if self.device.type == "cuda" else warp_plan_t
             hit = self._sched[warps_per_sm] = (nw, plan(self.seg_begin, self.seg_end, nw))
         return hit
+
+    def chunk_schedule(self, warps_per_sm: int):
+        """(nwarp, warp_chunk, records): the pipelined SpMM's chunk plan
+        (csrc/ingest.cu svdrec_chunk_plan: <= 32-entry chunks of the
+        segments, one 16-B record each; built once, on the device, without a
+        read-back) and this schedule's per-warp record ranges."""
+        from . import kernels as K
+
+        if self._chunks is None:
+            cbase = torch.empty(self.nseg + 1, dtype=torch.int64, device=self.device)
+            recs = torch.empty((self.nnz // 32 + self.nseg, 4), dtype=torch.int32, device=self.device)
+            K.call("svdrec_chunk_plan", self.nseg, K.ptr(self.seg_row), K.ptr(self.seg_begin), K.ptr(self.seg_end),
+                   K.ptr(self.seg_slot), K.ptr(cbase), K.ptr(recs), K.stream_handle())
+            self._chunks = (cbase, recs)
+        cbase, recs = self._chunks
+        hit = self._wchunk.get(warps_per_sm)
+        if hit is None:
+            nw, wseg = self.schedule(warps_per_sm)
+            wc = torch.empty(nw + 1, dtype=torch.int32, device=self.device)
+            K.call("svdrec_warp_chunks", nw, K.ptr(wseg), self.nseg, K.ptr(cbase), K.ptr(wc), K.stream_handle())
+            hit = self._wchunk[warps_per_sm] = (nw, wc)
+        return hit[0], hit[1], recs
 
     def ranked(self):
         """(ranked indices, values, rank -> item order) for the CF scoring

@@ -1,8 +1,10 @@
 /* A plain-C consumer of libsvdrec_b200.so (no Python, no torch): the
  * binding a C / cgo / JNI host would write.  Builds a random CSR, runs
  * svdrec_spmm with (a) the trivial plan -- one segment per row, no warp
- * schedule -- and (b) a contiguous warp schedule (the TMA fast path), and
- * checks both against a host loop; then checks the error contract.
+ * schedule -- and (b) a contiguous warp schedule with the chunk plan the
+ * library builds from it (svdrec_chunk_plan / svdrec_warp_chunks: the
+ * pipelined TMA path), and checks both against a host loop; then checks
+ * the error contract.
  * Exit code 0 = pass.  Build: see tests/test_gpu_c_abi.py. */
 #include <cuda_runtime.h>
 #include <math.h>
@@ -78,7 +80,9 @@ int main(void) {
   int fails = 0;
   for (int pass = 0; pass < 2; ++pass) {
     int64_t nwarp = 0;
-    int32_t* d_ws = NULL;
+    int32_t *d_ws = NULL, *d_wc = NULL;
+    int64_t* d_cbase = NULL;
+    void* d_recs = NULL;
     if (pass == 1) { /* contiguous warp ranges of about equal nonzeros */
       nwarp = (int64_t)svdrec_device_sm_count() * svdrec_spmm_warps_per_sm(b);
       if (nwarp > m) nwarp = m;
@@ -92,10 +96,19 @@ int main(void) {
       }
       d_ws = dev_copy(ws, (nwarp + 1) * 4);
       free(ws);
+      CK(cudaMalloc((void**)&d_cbase, (m + 1) * 8));
+      CK(cudaMalloc(&d_recs, (nnz / 32 + m) * 16));
+      CK(cudaMalloc((void**)&d_wc, (nwarp + 1) * 4));
+      int prc = svdrec_chunk_plan(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_cbase, d_recs, NULL);
+      if (!prc) prc = svdrec_warp_chunks(nwarp, d_ws, m, d_cbase, d_wc, NULL);
+      if (prc) {
+        fprintf(stderr, "chunk plan: %s\n", svdrec_last_error());
+        return 4;
+      }
     }
     CK(cudaMemset(d_Y, 0, m * b * 8));
     int rc = svdrec_spmm(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_ind, d_val, d_X, b, n, d_Y, b, b, 0,
-                         NULL, NULL, NULL, nwarp, d_ws, d_part, NULL);
+                         NULL, NULL, NULL, nwarp, d_ws, d_wc, d_recs, d_part, NULL);
     if (rc) {
       fprintf(stderr, "svdrec_spmm: %s\n", svdrec_last_error());
       return 4;
@@ -110,10 +123,13 @@ int main(void) {
     printf("pass %d (nwarp %lld): max rel err %.3e\n", pass, (long long)nwarp, worst);
     if (!(worst <= 1e-12)) ++fails;
     if (d_ws) cudaFree(d_ws);
+    if (d_wc) cudaFree(d_wc);
+    if (d_cbase) cudaFree(d_cbase);
+    if (d_recs) cudaFree(d_recs);
   }
   /* error contract: bad arguments -> nonzero status and a message */
   int rc = svdrec_spmm(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_ind, d_val, d_X, 1, n, d_Y, b, b, 0, NULL,
-                       NULL, NULL, 0, NULL, d_part, NULL);
+                       NULL, NULL, 0, NULL, NULL, NULL, d_part, NULL);
   if (rc == 0 || svdrec_last_error()[0] == 0) ++fails;
   printf("bad ldx -> rc %d: %s\n", rc, svdrec_last_error());
   printf("%s\n", fails ? "FAIL" : "PASS");

@@ -167,6 +167,39 @@ def test_hot_partition_matches_numpy(gpu, nhot):
     assert np.array_equal(val.cpu().numpy(), np.array(want_v))
 
 
+def test_chunk_plan_matches_numpy(gpu):
+    """The pipelined SpMM's chunk records (svdrec_chunk_plan): every segment
+    in chunks of <= 32 entries with first / last flags, an empty row as one
+    empty chunk, split rows pointing at their partial slots; per-warp record
+    ranges (svdrec_warp_chunks)."""
+    import paper_2009_02251_b200 as P
+    rng = np.random.default_rng(3)
+    m, n = 700, 3000
+    deg = np.minimum(rng.lognormal(3.0, 1.5, m).astype(np.int64), n)
+    deg[:4] = 0
+    deg[4] = n  # split into segments
+    rows = np.repeat(np.arange(m), deg)
+    cols = np.concatenate([np.sort(rng.choice(n, d, replace=False)) for d in deg if d])
+    M = sp.csr_matrix((rng.integers(1, 11, cols.size) * 0.5, (rows, cols)), shape=(m, n))
+    c = P.SparseRatings(M, 0.5, 5.0).device(gpu).A
+    nw, wc, recs = c.chunk_schedule(16)
+    sr, sb, se, sl = (t.cpu().numpy() for t in (c.seg_row, c.seg_begin, c.seg_end, c.seg_slot))
+    assert (sl >= 0).any()
+    want, first = [], []
+    for j in range(sr.size):
+        a, e = int(sb[j]), int(se[j])
+        dst = int(sr[j]) if sl[j] < 0 else ~int(sl[j])
+        starts = list(range(a, e, 32)) or [None]
+        first.append(len(want))
+        for t, o in enumerate(starts):
+            nv = 0 if o is None else min(32, e - o)
+            want.append((o or 0, dst, nv | (256 if t == 0 else 0) | (512 if t == len(starts) - 1 else 0), 0))
+    first.append(len(want))
+    assert np.array_equal(recs.cpu().numpy()[: len(want)], np.array(want, dtype=np.int32))
+    wseg = c.schedule(16)[1].cpu().numpy()
+    assert nw == wseg.size - 1 and np.array_equal(wc.cpu().numpy(), np.array(first, dtype=np.int32)[wseg])
+
+
 @pytest.mark.parametrize("seed", [0, 1])
 def test_segment_and_warp_plan_kernels_match_numpy(gpu, seed):
     """The SpMM plan built by the kernels equals sparse.segment_plan /

@@ -228,8 +228,8 @@ def test_sharded_orth_single_rank(gpu):
 
 @pytest.mark.parametrize("b", [2, 6, 10, 16, 20, 32, 40, 64])
 def test_spmm_hot_set_matches_tma(gpu, b):
-    """A @ X through the hot-set kernel (ranked CSR, hot rows of X in shared
-    memory) equals the TMA-gather kernel and scipy: Zipf items, empty rows,
+    """A @ X through the hot-set kernel (hot-first CSR, hot rows of X in shared
+    memory) equals the TMA-gather kernels and scipy: Zipf items, empty rows,
     rows long enough to be split into segments (partial slots + fix-up)."""
     import torch
     import paper_2009_02251_b200 as P
