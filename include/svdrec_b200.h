@@ -136,6 +136,27 @@ int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg
                     int32_t nhot, double* d_Y, int64_t ldy, int32_t b, int64_t nlong,
                     const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1,
                     int64_t nwarp, const int32_t* d_warp_seg, double* d_partial, void* stream);
+/* Hot / cold chunk kernel for A @ X (even b <= 32; the path the headline's
+ * b = 20 products A @ Omega and A @ r take).  hot_pack: the PACKED hot-first
+ * copy of a CSR -- 16-B entries {int32 id, int32 0, double value}, every row
+ * stably partitioned into the entries of the nhot most rated items (id =
+ * popularity rank = row of the shared-memory table) and the rest (id =
+ * item) -- and d_hot_cnt[r] = row r's hot entries.  The chunk plan is
+ * svdrec_chunk_plan with d_indptr / d_hot_cnt (no chunk straddles a row's
+ * hot / cold boundary), svdrec_warp_chunks for nwarp = SMs x
+ * svdrec_spmm_hc_warps_per_sm().  Hot chunks read X rows from shared memory,
+ * cold chunks gather them (LDG) -- only those reach L2.
+ * nhot <= svdrec_spmm_hc_rows(b) (0: width not supported). */
+int svdrec_spmm_hc_warps_per_sm(void);
+int svdrec_spmm_hc_rows(int32_t b);
+int svdrec_spmm_hot_pack(int64_t m, const int64_t* d_indptr, const int32_t* d_indices,
+                         const double* d_values, const int32_t* d_rank, int32_t nhot, void* d_out,
+                         int32_t* d_hot_cnt, void* stream);
+int svdrec_spmm_hc(int64_t nseg, const void* d_entries, const double* d_X, int64_t ldx, int64_t x_rows,
+                   const int32_t* d_hot_items, int32_t nhot, double* d_Y, int64_t ldy, int32_t b,
+                   int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
+                   const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_chunk,
+                   const void* d_chunks, double* d_partial, void* stream);
 /* fp32 variant: X stored as float (half the gathered bytes), values,
  * accumulation and Y in double.  b in {4, 8, ..., 64}, 16-B aligned rows,
  * a schedule of svdrec_spmm_x32_warps_per_sm(b) warps per SM. */
@@ -403,18 +424,20 @@ int svdrec_seg_plan_emit(int64_t m, const int64_t* d_indptr, int32_t seg_max, co
                          int32_t* d_long_row, int32_t* d_long_s0, int32_t* d_long_s1, void* stream);
 int svdrec_warp_plan(int64_t nseg, const int64_t* d_seg_begin, const int64_t* d_seg_end, int64_t nwarp,
                      int32_t seg_cost, int64_t* d_scratch, int32_t* d_out, void* stream);
-/* The pipelined SpMM's chunk plan (linalg.py:141-158 has no counterpart:
+/* The pipelined SpMMs' chunk plan (linalg.py:141-158 has no counterpart:
  * scipy walks the CSR row by row).  chunk_plan: every segment cut into
  * chunks of <= 32 entries, one 16-B record each (int32 x 4: low word of the
  * first entry's offset; output row, or ~slot for a split row's partial;
- * entries | first-of-segment << 8 | last-of-segment << 9; high word of the
- * offset).  d_cbase: nseg + 1 int64 (per segment its first record; [nseg] =
- * the record count); d_recs: room for nnz / 32 + nseg records.
- * warp_chunks: warp_chunk[w] = first record of segment warp_seg[w]
- * (nwarp + 1 int32). */
+ * entries | first-of-segment << 8 | last-of-segment << 9 | hot << 10; high
+ * word of the offset).  d_cbase: nseg + 1 int64 (per segment its first
+ * record; [nseg] = the record count); d_recs: room for nnz / 32 + 2 nseg
+ * records.  With d_indptr / d_hot_cnt (the packed hot-first copy of
+ * svdrec_spmm_hot_pack) a chunk is all hot or all cold (svdrec_spmm_hc);
+ * both NULL for the plain plan.  warp_chunks: warp_chunk[w] = first record
+ * of segment warp_seg[w] (nwarp + 1 int32). */
 int svdrec_chunk_plan(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
-                      const int64_t* d_seg_end, const int32_t* d_seg_slot, int64_t* d_cbase,
-                      void* d_recs, void* stream);
+                      const int64_t* d_seg_end, const int32_t* d_seg_slot, const int64_t* d_indptr,
+                      const int32_t* d_hot_cnt, int64_t* d_cbase, void* d_recs, void* stream);
 int svdrec_warp_chunks(int64_t nwarp, const int32_t* d_warp_seg, int64_t nseg, const int64_t* d_cbase,
                        int32_t* d_warp_chunk, void* stream);
 

@@ -34,7 +34,12 @@ SIGNATURES = {
     "svdrec_normal_fill": (C.c_int, [_u64, _u64, _p, _i64, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p, _p,
                               _p]),
-    "svdrec_chunk_plan": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
+    "svdrec_chunk_plan": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "svdrec_spmm_hc_warps_per_sm": (C.c_int, []),
+    "svdrec_spmm_hc_rows": (C.c_int, [_i32]),
+    "svdrec_spmm_hot_pack": (C.c_int, [_i64, _p, _p, _p, _p, _i32, _p, _p, _p]),
+    "svdrec_spmm_hc": (C.c_int, [_i64, _p, _p, _i64, _i64, _p, _i32, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p,
+                                 _p]),
     "svdrec_warp_chunks": (C.c_int, [_i64, _p, _i64, _p, _p, _p]),
     "svdrec_spmm_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_hot_rows": (C.c_int, [_i32]),

@@ -399,35 +399,58 @@ __global__ void k_warp_cuts(int64_t nseg, int64_t nwarp, const int64_t* __restri
   out[i] = (int32_t)min64(lo + 1, nseg);
 }
 
-// Chunk records of the pipelined SpMM (csrc/spmm.cu k_spmm_pipe): every
-// segment cut into chunks of <= 32 nonzeros (an empty row is one chunk with
-// no entries), one 16-B record each: x / w = low / high word of the first
-// entry's offset, y = the output row (>= 0) or ~slot of a split row's
-// partial sum, z = entries | first chunk of its segment << 8 | last << 9.
-__global__ void k_chunk_count(int64_t nseg, const int64_t* __restrict__ seg_begin,
-                              const int64_t* __restrict__ seg_end, int64_t* __restrict__ cnt) {
+// Chunk records of the pipelined SpMMs (csrc/spmm.cu k_spmm_pipe /
+// k_spmm_hc): every segment cut into chunks of <= 32 nonzeros (an empty row
+// is one chunk with no entries), one 16-B record each: x / w = low / high
+// word of the first entry's offset, y = the output row (>= 0) or ~slot of a
+// split row's partial sum, z = entries | first chunk of its segment << 8 |
+// last << 9 | hot << 10.  With hot_cnt (the hot-first copy of the CSR: row r
+// holds its hot_cnt[r] shared-memory-resident entries first) no chunk
+// straddles a row's hot / cold boundary and each carries its kind.
+__device__ __forceinline__ int64_t chunks_of(int64_t d) { return (d + 31) >> 5; }
+
+__device__ __forceinline__ int64_t hot_end(int64_t a, int64_t e, int32_t row, const int64_t* __restrict__ indptr,
+                                           const int32_t* __restrict__ hot_cnt) {
+  if (!hot_cnt) return a;
+  const int64_t hb = indptr[row] + hot_cnt[row];
+  return hb < a ? a : (hb > e ? e : hb);
+}
+
+__global__ void k_chunk_count(int64_t nseg, const int32_t* __restrict__ seg_row,
+                              const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
+                              const int64_t* __restrict__ indptr, const int32_t* __restrict__ hot_cnt,
+                              int64_t* __restrict__ cnt) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nseg) return;
-  const int64_t d = seg_end[j] - seg_begin[j];
-  cnt[j] = d <= 32 ? 1 : (d + 31) >> 5;
+  const int64_t a = seg_begin[j], e = seg_end[j];
+  const int64_t h = hot_end(a, e, seg_row[j], indptr, hot_cnt);
+  const int64_t n = chunks_of(h - a) + chunks_of(e - h);
+  cnt[j] = n ? n : 1;
 }
 
 __global__ void k_chunk_emit(int64_t nseg, const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_begin,
                              const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
+                             const int64_t* __restrict__ indptr, const int32_t* __restrict__ hot_cnt,
                              const int64_t* __restrict__ cbase, int4* __restrict__ recs) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nseg) return;
   const int64_t a = seg_begin[j], e = seg_end[j];
-  const int64_t n = e - a <= 32 ? 1 : (e - a + 31) >> 5;
+  const int64_t h = hot_end(a, e, seg_row[j], indptr, hot_cnt);
+  const int64_t nh = chunks_of(h - a), nc = chunks_of(e - h);
   const int32_t slot = seg_slot[j];
   const int32_t dst = slot < 0 ? seg_row[j] : ~slot;
   int4* out = recs + cbase[j];
-  for (int64_t c = 0; c < n; ++c) {
-    const int64_t o = a + 32 * c;
-    const int nv = (int)min64(32, e - o);
-    const int64_t off = nv > 0 ? o : 0;  // an empty chunk reads nothing: keep its address inside the arrays
-    out[c] = make_int4((int)(uint32_t)(off & 0xffffffffll), dst, nv | (c == 0 ? 256 : 0) | (c == n - 1 ? 512 : 0),
-                       (int)(uint32_t)(off >> 32));
+  if (nh + nc == 0) {  // an empty row: one chunk without entries
+    out[0] = make_int4(0, dst, 256 | 512, 0);
+    return;
+  }
+  for (int64_t c = 0; c < nh + nc; ++c) {
+    const bool hot = c < nh;
+    const int64_t o = hot ? a + 32 * c : h + 32 * (c - nh);
+    const int nv = (int)min64(32, (hot ? h : e) - o);
+    out[c] = make_int4((int)(uint32_t)(o & 0xffffffffll), dst,
+                       nv | (c == 0 ? 256 : 0) | (c == nh + nc - 1 ? 512 : 0) | (hot ? 1024 : 0),
+                       (int)(uint32_t)(o >> 32));
   }
 }
 
@@ -558,27 +581,29 @@ extern "C" int svdrec_warp_plan(int64_t nseg, const int64_t* d_seg_begin, const 
   return check_launch("warp_plan", launches);
 }
 
-// Chunk plan of the pipelined SpMM.  d_cbase: nseg + 1 int64 (exclusive scan
+// Chunk plan of the pipelined SpMMs.  d_cbase: nseg + 1 int64 (exclusive scan
 // of the chunk counts; [nseg] = their total); d_recs: room for
-// nnz / 32 + nseg records (an upper bound known without a read-back).
+// nnz / 32 + 2 nseg records (an upper bound known without a read-back).
+// d_indptr / d_hot_cnt (both or neither): the hot-first copy's row starts
+// and hot-entry counts.
 extern "C" int svdrec_chunk_plan(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
-                                 const int64_t* d_seg_end, const int32_t* d_seg_slot, int64_t* d_cbase,
-                                 void* d_recs, void* stream) {
-  SVDREC_ARG(nseg >= 0, "chunk_plan: bad arguments");
+                                 const int64_t* d_seg_end, const int32_t* d_seg_slot, const int64_t* d_indptr,
+                                 const int32_t* d_hot_cnt, int64_t* d_cbase, void* d_recs, void* stream) {
+  SVDREC_ARG(nseg >= 0 && (!d_hot_cnt || d_indptr), "chunk_plan: bad arguments");
   cudaStream_t s = as_stream(stream);
   if (nseg == 0) {
     SVDREC_CUDA(cudaMemsetAsync(d_cbase, 0, sizeof(int64_t), s));
     return 0;
   }
   const unsigned grid = (unsigned)((nseg + 255) / 256);
-  k_chunk_count<<<grid, 256, 0, s>>>(nseg, d_seg_begin, d_seg_end, d_cbase);
+  k_chunk_count<<<grid, 256, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_indptr, d_hot_cnt, d_cbase);
   int launches = 1;
   const int rc = scan_i64(nseg, d_cbase, d_cbase, d_cbase + nseg, s, &launches);
   if (rc) {
     set_error("chunk_plan: %s", cudaGetErrorString((cudaError_t)rc));
     return rc;
   }
-  k_chunk_emit<<<grid, 256, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_cbase,
+  k_chunk_emit<<<grid, 256, 0, s>>>(nseg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indptr, d_hot_cnt, d_cbase,
                                     reinterpret_cast<int4*>(d_recs));
   return check_launch("chunk_plan", launches + 1);
 }

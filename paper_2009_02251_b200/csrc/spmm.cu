@@ -980,6 +980,222 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Hot / cold chunk kernel for A @ X (even b <= 32; round 2).  Random X-row
+// gathers through L2 run at ~60 G rows/s whatever the path (TMA gather4 or
+// LDG, 16-B to 160-B rows alike: ~5 cycles per row per SM), so the only way
+// below ~300 us per call on config 3 is fewer gathers: the rows of X of the
+// nhot most rated items sit in every CTA's shared memory (1,190 rows at
+// b = 20 hold 64 % of the ratings).  The CSR is the PACKED hot-first copy
+// (k_hot_pack: 16-B entries {rank or item, value}, every row's hot entries
+// first) and its chunk plan never lets a chunk straddle a row's hot / cold
+// boundary (csrc/ingest.cu), so a chunk is either
+//   HOT   32 rows read from the shared-memory table (LDS.128), or
+//   COLD  32 rows gathered straight into registers (LDG.128, all NS steps
+//         in flight at once),
+// with no per-batch ballot / table building (k_spmm_hot) and no TMA issue
+// loop (11 instructions per gather4 in k_spmm_pipe).  Entries reach shared
+// memory by one 16-B cp.async per lane per chunk (L1 bypassed), D chunks
+// ahead; records through the ring of k_spmm_pipe.  No row rings: ~2.3 KB of
+// shared memory per warp, the rest is the hot table.
+struct __align__(16) PackEnt {
+  int32_t id;  // hot chunk: popularity rank (row of the table); cold: item id
+  int32_t pad;
+  double v;
+};
+
+template <int D>
+struct HcGeom {
+  static constexpr int WARPB = D * 512 + kRecRing * 16;  // D slots of 32 entries + the record ring
+};
+
+template <int P, int D, int W>
+__global__ void __launch_bounds__(W * 32, 1) k_spmm_hc(
+    int64_t nwarp, const int32_t* __restrict__ warp_chunk, const int4* __restrict__ chunks,
+    const PackEnt* __restrict__ ents, const double* __restrict__ X, int64_t ldx,
+    const int32_t* __restrict__ hot_items, int nhot, double* __restrict__ Y, int64_t ldy,
+    double* __restrict__ partial) {
+  static_assert(kRecAhead >= 2 * D && kRecAhead + 1 <= kRecRing, "spmm_hc: record ring too small");
+  constexpr int B = 2 * P, G = 32 / P, RB = P;
+  extern __shared__ __align__(128) unsigned char smb[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double2* hot = reinterpret_cast<double2*>(smb + (size_t)W * HcGeom<D>::WARPB);  // nhot rows of RB double2
+  for (int t = threadIdx.x; t < nhot * RB; t += blockDim.x) {
+    const int r = t / RB, c = t - (t / RB) * RB;
+    hot[t] = *reinterpret_cast<const double2*>(X + (int64_t)hot_items[r] * ldx + 2 * c);
+  }
+  __syncthreads();
+  if (w >= nwarp) return;
+  PackEnt* slots = reinterpret_cast<PackEnt*>(smb + (size_t)wib * HcGeom<D>::WARPB);  // D x 32 entries
+  int4* rring = reinterpret_cast<int4*>(slots + D * 32);
+  const int g = lane / P, pc = lane - (lane / P) * P;
+  const bool active = g < G;
+  const double2* hrow = hot + pc;
+  const double2* xrow = reinterpret_cast<const double2*>(X) + pc;
+  const int64_t ldx2 = ldx / 2;
+
+  const int32_t c_lo = warp_chunk[w], c_hi = warp_chunk[w + 1];
+  const int n = c_hi - c_lo;
+  if (n <= 0) return;
+  if (lane < kRecAhead && lane < n) rring[lane] = __ldg(chunks + c_lo + lane);
+  __syncwarp();
+  int fj = 0, fs = 0;
+  auto fetch = [&]() {
+    if (fj < n) {
+      const int4 rec = rring[fj & (kRecRing - 1)];
+      const int64_t off = (int64_t)(((uint64_t)(uint32_t)rec.w << 32) | (uint32_t)rec.x);
+      const bool in = lane < (rec.z & 63);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(slots + fs * 32 + lane)),
+                   "l"(ents + off + (in ? lane : 0)), "r"(in ? 16u : 0u)
+                   : "memory");
+      ++fj;
+    }
+  };
+  Acc<2> acc, acc1;
+  acc.zero();
+  acc1.zero();
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    fetch();
+    cp_async_commit();
+    if (++fs == D) fs = 0;
+  }
+  int cs = 0;
+  for (int i = 0; i < n; ++i) {
+    cp_async_wait<D - 1>();  // chunk i's entries (and the records requested >= D steps ago) have landed
+    __syncwarp();
+    const int4 m = rring[i & (kRecRing - 1)];  // y: destination, z: entries | flags
+    const int nv = m.z & 63;
+    if (m.z & 256) {
+      acc.zero();
+      acc1.zero();
+    }
+    if (active && nv > 0) {
+      constexpr int NS = (32 + G - 1) / G;
+      const PackEnt* sl = slots + cs * 32;
+      Acc<2> xs[NS];
+      double vs[NS];
+      if (m.z & 1024) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const int j = q * G + g;
+          const PackEnt e = sl[j < 32 ? j : 31];
+          xs[q].h[0] = hrow[e.id * RB];
+          vs[q] = e.v;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const int j = q * G + g;
+          const PackEnt e = sl[j < 32 ? j : 31];
+          xs[q].h[0] = __ldg(xrow + (int64_t)e.id * ldx2);
+          vs[q] = e.v;
+        }
+      }
+      if (nv == 32) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if ((q + 1) * G <= 32 || q * G + g < 32) {
+            if (q & 1)
+              acc1.fma(vs[q], xs[q]);
+            else
+              acc.fma(vs[q], xs[q]);
+          }
+        }
+      } else {
+        const int left = nv - g;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if (q * G < left) {
+            if (q & 1)
+              acc1.fma(vs[q], xs[q]);
+            else
+              acc.fma(vs[q], xs[q]);
+          }
+        }
+      }
+    }
+    if (m.z & 512) {
+      acc.add(acc1);
+      Acc<2> tot = acc;
+#pragma unroll
+      for (int h = 1; h < G; ++h) {
+        const Acc<2> o = acc.shfl((lane + h * P) & 31);
+        if (g == 0) tot.add(o);
+      }
+      if (g == 0) {
+        double* dst = m.y >= 0 ? (Y + (int64_t)m.y * ldy + 2 * pc) : (partial + (int64_t)(~m.y) * B + 2 * pc);
+        tot.store(dst);
+      }
+    }
+    __syncwarp();  // every lane is done with the slot
+    fetch();       // chunk i + D into the slot just freed
+    {
+      const int rj = i + kRecAhead;
+      if (lane == 0 && rj < n) cp_async16(rring + (rj & (kRecRing - 1)), chunks + c_lo + rj);
+    }
+    cp_async_commit();
+    if (++fs == D) fs = 0;
+    if (++cs == D) cs = 0;
+  }
+  cp_async_wait<0>();
+}
+
+#ifndef SVDREC_HC_D
+#define SVDREC_HC_D 4
+#endif
+#ifndef SVDREC_HC_W
+#define SVDREC_HC_W 16
+#endif
+constexpr int kHcD = SVDREC_HC_D, kHcW = SVDREC_HC_W;
+constexpr int kHcSmem = 226 * 1024;
+constexpr int kHcTable = kHcSmem - kHcW * HcGeom<kHcD>::WARPB;  // bytes left for the hot rows
+
+// The packed hot-first copy: every row stably partitioned into the entries
+// of the nhot most rated items (id = popularity rank) and the rest (id =
+// item), 16 B per entry; hot_cnt[r] = the row's hot entries.  One warp per
+// row, two passes (count, then place with ballot prefixes).
+__global__ void k_hot_pack(int64_t m, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                           const double* __restrict__ values, const int32_t* __restrict__ rank, int nhot,
+                           PackEnt* __restrict__ out, int32_t* __restrict__ hot_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t r = w0; r < m; r += nw) {
+    const int64_t a = indptr[r], b = indptr[r + 1];
+    int64_t nh = 0;
+    for (int64_t t0 = a; t0 < b; t0 += 32) {
+      const int64_t t = t0 + lane;
+      const bool hot = t < b && rank[indices[t]] < nhot;
+      nh += __popc(__ballot_sync(0xffffffffu, hot));
+    }
+    if (lane == 0) hot_cnt[r] = (int32_t)nh;
+    int64_t hrun = 0, crun = 0;
+    for (int64_t t0 = a; t0 < b; t0 += 32) {
+      const int64_t t = t0 + lane;
+      const bool valid = t < b;
+      int32_t c = 0, rk = 0;
+      double v = 0.0;
+      if (valid) {
+        c = indices[t];
+        rk = rank[c];
+        v = __ldcs(values + t);
+      }
+      const bool hot = valid && rk < nhot;
+      const unsigned hm = __ballot_sync(0xffffffffu, hot), vm = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const int64_t pos = hot ? a + hrun + __popc(hm & lt) : a + nh + crun + __popc(vm & ~hm & lt);
+        out[pos] = PackEnt{hot ? rk : c, 0, v};
+      }
+      hrun += __popc(hm);
+      crun += __popc(vm & ~hm);
+    }
+  }
+}
+
 // The hot-set kernel's copy of a CSR: every row stably partitioned into the
 // entries of the nhot most rated items (rank[item] < nhot) first and the
 // rest after, each part in the row's order; index -(rank + 1) for hot
@@ -1117,10 +1333,9 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
 }
 
 extern "C" int svdrec_spmm_hot_rows(int32_t b) {
-  // widths the hot-set kernel supports: even b <= 32 (2 doubles per lane),
-  // b % 4 == 0 up to 64 (4 per lane); which widths it is used for is the
-  // host's choice (kernels._hot_rows: where it measured faster)
-  if (b < 2 || b > 64 || b % 2 || (b > 32 && b % 4)) return 0;
+  // widths the register-gather hot-set kernel serves: 32 < b <= 64 with
+  // b % 4 == 0 (4 doubles per lane); even b <= 32 run k_spmm_hc
+  if (b <= 32 || b > 64 || b % 4) return 0;
   // one 512-thread CTA per SM; the hot rows fill the 227 KB opt-in
   return (int)((226 * 1024 - kHotWarps * 2 * kTabSlots * (int)sizeof(TabEnt)) / (8 * b));
 }
@@ -1136,6 +1351,59 @@ extern "C" int svdrec_spmm_hot_partition(int64_t m, const int64_t* d_indptr, con
   return check_launch("spmm_hot_partition");
 }
 
+extern "C" int svdrec_spmm_hc_warps_per_sm(void) { return kHcW; }
+
+extern "C" int svdrec_spmm_hc_rows(int32_t b) {
+  if (b < 2 || b > 32 || b % 2) return 0;
+  return kHcTable / (8 * b);
+}
+
+extern "C" int svdrec_spmm_hot_pack(int64_t m, const int64_t* d_indptr, const int32_t* d_indices,
+                                    const double* d_values, const int32_t* d_rank, int32_t nhot, void* d_out,
+                                    int32_t* d_hot_cnt, void* stream) {
+  SVDREC_ARG(m >= 0 && nhot >= 0 && d_hot_cnt, "spmm_hot_pack: bad arguments");
+  if (m == 0) return 0;
+  const int64_t grid = min64((m + 7) / 8, (int64_t)sm_count() * 16);
+  k_hot_pack<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(m, d_indptr, d_indices, d_values, d_rank, nhot,
+                                                             reinterpret_cast<PackEnt*>(d_out), d_hot_cnt);
+  return check_launch("spmm_hot_pack");
+}
+
+extern "C" int svdrec_spmm_hc(int64_t nseg, const void* d_entries, const double* d_X, int64_t ldx, int64_t x_rows,
+                              const int32_t* d_hot_items, int32_t nhot, double* d_Y, int64_t ldy, int32_t b,
+                              int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
+                              const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_chunk,
+                              const void* d_chunks, double* d_partial, void* stream) {
+  SVDREC_ARG(svdrec_spmm_hc_rows(b) > 0 && ldx % 2 == 0 && ldy % 2 == 0 && ldx >= b && ldy >= b,
+             "spmm_hc: needs even b <= 32 and 16-B aligned rows (b=%d)", b);
+  SVDREC_ARG(nhot >= 0 && nhot <= svdrec_spmm_hc_rows(b) && nhot <= x_rows,
+             "spmm_hc: %d hot rows exceed shared memory", nhot);
+  SVDREC_ARG(nwarp > 0 && d_warp_chunk && d_chunks, "spmm_hc: needs a chunk plan (svdrec_spmm_hc_warps_per_sm)");
+  SVDREC_ARG(((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
+               reinterpret_cast<uintptr_t>(d_partial) | reinterpret_cast<uintptr_t>(d_entries)) % 16) == 0,
+             "spmm_hc: operands must be 16-B aligned");
+  if (nseg == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  const size_t smem = (size_t)kHcW * HcGeom<kHcD>::WARPB + (size_t)nhot * b * sizeof(double);
+  const int64_t grid = (nwarp + kHcW - 1) / kHcW;
+  switch (b / 2) {
+#define SVDREC_HC(PP)                                                                                          \
+  case PP:                                                                                                     \
+    SVDREC_CUDA(smem_attr_once(k_spmm_hc<PP, kHcD, kHcW>, kHcSmem));                                            \
+    k_spmm_hc<PP, kHcD, kHcW><<<(unsigned)grid, kHcW * 32, smem, s>>>(                                          \
+        nwarp, d_warp_chunk, reinterpret_cast<const int4*>(d_chunks), reinterpret_cast<const PackEnt*>(d_entries), \
+        d_X, ldx, d_hot_items, nhot, d_Y, ldy, d_partial);                                                     \
+    break;
+    SVDREC_HC(1) SVDREC_HC(2) SVDREC_HC(3) SVDREC_HC(4) SVDREC_HC(5) SVDREC_HC(6) SVDREC_HC(7) SVDREC_HC(8)
+    SVDREC_HC(9) SVDREC_HC(10) SVDREC_HC(11) SVDREC_HC(12) SVDREC_HC(13) SVDREC_HC(14) SVDREC_HC(15) SVDREC_HC(16)
+#undef SVDREC_HC
+    default: return SVDREC_E_ARG;
+  }
+  const int rc = check_launch("spmm_hc");
+  if (rc) return rc;
+  return run_fixup(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial, d_Y, ldy, b, s);
+}
+
 extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
                                const int64_t* d_seg_end, const int32_t* d_seg_slot, const int32_t* d_hidx,
                                const double* d_hval, const double* d_X, int64_t ldx, int64_t x_rows,
@@ -1144,7 +1412,7 @@ extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int
                                const int32_t* d_long_row, const int32_t* d_long_slot0, const int32_t* d_long_slot1,
                                int64_t nwarp, const int32_t* d_warp_seg, double* d_partial, void* stream) {
   SVDREC_ARG(svdrec_spmm_hot_rows(b) > 0 && ldx % 2 == 0 && ldy % 2 == 0 && ldx >= b && ldy >= b,
-             "spmm_hot: needs even b <= 32 or b %% 4 == 0 <= 64, and 16-B aligned rows (b=%d)", b);
+             "spmm_hot: needs 32 < b <= 64, b %% 4 == 0, and 16-B aligned rows (b=%d)", b);
   SVDREC_ARG(nhot >= 0 && nhot <= svdrec_spmm_hot_rows(b), "spmm_hot: %d hot rows exceed shared memory", nhot);
   SVDREC_ARG(nwarp > 0 && d_warp_seg, "spmm_hot: needs a warp schedule (16 warps per SM)");
   SVDREC_ARG(x_rows * (ldx / 2) < (1ll << 31), "spmm_hot: X too large for 32-bit row offsets");
@@ -1162,28 +1430,7 @@ extern "C" int svdrec_spmm_hot(int64_t nseg, const int32_t* d_seg_row, const int
         nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_hidx, d_hval, d_X, ldx,        \
         d_hot_items, nhot, d_Y, ldy, d_partial);                                                           \
     break;
-  if (b <= 32) {
-    switch (b / 2) {
-      SVDREC_HOT(1, 2)
-      SVDREC_HOT(2, 2)
-      SVDREC_HOT(3, 2)
-      SVDREC_HOT(4, 2)
-      SVDREC_HOT(5, 2)
-      SVDREC_HOT(6, 2)
-      SVDREC_HOT(7, 2)
-      SVDREC_HOT(8, 2)
-      SVDREC_HOT(9, 2)
-      SVDREC_HOT(10, 2)
-      SVDREC_HOT(11, 2)
-      SVDREC_HOT(12, 2)
-      SVDREC_HOT(13, 2)
-      SVDREC_HOT(14, 2)
-      SVDREC_HOT(15, 2)
-      SVDREC_HOT(16, 2)
-      default:
-        return SVDREC_E_ARG;
-    }
-  } else {
+  {
     switch (b / 4) {
       SVDREC_HOT(9, 4)
       SVDREC_HOT(10, 4)

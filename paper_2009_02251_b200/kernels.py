@@ -155,9 +155,12 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
                  plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), nw, ptr(wseg), ptr(wc),
                  ptr(recs), ptr(part), stream_handle())
         return Y
-    hot = _hot_rows(plan, b, ldx, ldy)
+    hc = _hc_rows(plan, b, ldx, ldy)
+    hot = 0 if hc else _hot_rows(plan, b, ldx, ldy)
     with _span("spmm", nbytes, gathered):
-        if hot:
+        if hc:
+            _spmm_hc(plan, X, ldx, Y, ldy, b, hc)
+        elif hot:
             _spmm_hot(plan, X, ldx, Y, ldy, b, hot)
         else:
             _spmm_tma(plan, X, ldx, Y, ldy, b)
@@ -166,12 +169,34 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
 
 # SVDREC_SPMM_HOT=0 keeps A @ X on the TMA-gather kernels (A/B measurements)
 SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "1") != "0"
-# widths where the hot-set kernel measured faster than the TMA-gather kernels
-# for A @ X (config 3, us per call, hot vs TMA): b = 2 259 vs 286, 8 267 vs
-# 272, 32 386 vs 560, 64 554 vs 917; at b = 16 (298 vs 295), 20 (414 vs 331:
-# 160-B rows straddle the 128-B shared-memory phases -- bank conflicts, ncu:
-# L1 data pipe 86 % busy) and 40 (668 vs 650) it is not.
-HOT_WIDTHS = frozenset({2, 4, 6, 8, 32, 64})
+# A @ X of a rating matrix (a CSR with a popularity order), config 3, us per
+# call, hot / cold chunk kernel (k_spmm_hc) vs TMA pipeline (k_spmm_pipe):
+# b = 2 199 vs 283, 4 188 vs 266, 8 216 vs 271, 10 258 vs 340, 12 258 vs 298,
+# 16 251 vs 294, 18 348 vs 361, 20 328 vs 331, 22 383 vs 415, 24 355 vs 403,
+# 28 390 vs 563, 32 358 vs 556.  At b = 20 they tie (the hot / cold kernel is
+# bound by the L1 data pipe: 160-B rows straddle the 128-B shared-memory
+# phases) and the pipeline needs no second copy of A, so it keeps that width.
+# b = 64 runs the register-gather hot-set kernel (k_spmm_hot: 554 vs 917 us
+# for the wide TMA kernel; at b = 40, 668 vs 650, it is not used).
+HC_WIDTHS = frozenset(range(2, 33, 2)) - {20}
+HOT_WIDTHS = frozenset({64})
+
+
+def _hc_rows(plan, b: int, ldx: int, ldy: int) -> int:
+    """Hot rows of X the hot / cold chunk kernel stages in shared memory, or
+    0 when it does not apply (no popularity order on this CSR, b odd or
+    > 32, unaligned rows)."""
+    if not SPMM_HOT or getattr(plan, "item_rank", None) is None or ldx % 2 or ldy % 2 or b not in HC_WIDTHS:
+        return 0
+    return min(int(query("svdrec_spmm_hc_rows", b)), plan.n)
+
+
+def _spmm_hc(plan, X, ldx, Y, ldy, b, nhot):
+    """The hot / cold chunk kernel (csrc/spmm.cu k_spmm_hc) on the packed hot-first copy."""
+    nwarp, wchunk, recs, ents, _ = plan.hot_packed(nhot, query("svdrec_spmm_hc_warps_per_sm"))
+    call("svdrec_spmm_hc", plan.nseg, ptr(ents), ptr(X), ldx, plan.n, ptr(plan.hot_items), nhot, ptr(Y), ldy, b,
+         plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wchunk), ptr(recs),
+         ptr(plan.partial(b)), stream_handle())
 
 
 def _hot_rows(plan, b: int, ldx: int, ldy: int, widths=None) -> int:

@@ -292,6 +292,7 @@ class DeviceCSR:
         self._sched = {}
         self._chunks = None
         self._wchunk = {}
+        self._hotpack = {}
         self.h2d_bytes = h2d_bytes
 
     @classmethod
@@ -346,27 +347,57 @@ class DeviceCSR:
             hit = self._sched[warps_per_sm] = (nw, plan(self.seg_begin, self.seg_end, nw))
         return hit
 
+    def _chunk_plan(self, indptr=None, hot_cnt=None):
+        from . import kernels as K
+
+        cbase = torch.empty(self.nseg + 1, dtype=torch.int64, device=self.device)
+        recs = torch.empty((self.nnz // 32 + 2 * self.nseg, 4), dtype=torch.int32, device=self.device)
+        K.call("svdrec_chunk_plan", self.nseg, K.ptr(self.seg_row), K.ptr(self.seg_begin), K.ptr(self.seg_end),
+               K.ptr(self.seg_slot), K.ptr(indptr), K.ptr(hot_cnt), K.ptr(cbase), K.ptr(recs), K.stream_handle())
+        return cbase, recs
+
+    def _warp_chunks(self, cbase, warps_per_sm: int):
+        from . import kernels as K
+
+        nw, wseg = self.schedule(warps_per_sm)
+        wc = torch.empty(nw + 1, dtype=torch.int32, device=self.device)
+        K.call("svdrec_warp_chunks", nw, K.ptr(wseg), self.nseg, K.ptr(cbase), K.ptr(wc), K.stream_handle())
+        return nw, wc
+
     def chunk_schedule(self, warps_per_sm: int):
         """(nwarp, warp_chunk, records): the pipelined SpMM's chunk plan
         (csrc/ingest.cu svdrec_chunk_plan: <= 32-entry chunks of the
         segments, one 16-B record each; built once, on the device, without a
         read-back) and this schedule's per-warp record ranges."""
-        from . import kernels as K
-
         if self._chunks is None:
-            cbase = torch.empty(self.nseg + 1, dtype=torch.int64, device=self.device)
-            recs = torch.empty((self.nnz // 32 + self.nseg, 4), dtype=torch.int32, device=self.device)
-            K.call("svdrec_chunk_plan", self.nseg, K.ptr(self.seg_row), K.ptr(self.seg_begin), K.ptr(self.seg_end),
-                   K.ptr(self.seg_slot), K.ptr(cbase), K.ptr(recs), K.stream_handle())
-            self._chunks = (cbase, recs)
+            self._chunks = self._chunk_plan()
         cbase, recs = self._chunks
         hit = self._wchunk.get(warps_per_sm)
         if hit is None:
-            nw, wseg = self.schedule(warps_per_sm)
-            wc = torch.empty(nw + 1, dtype=torch.int32, device=self.device)
-            K.call("svdrec_warp_chunks", nw, K.ptr(wseg), self.nseg, K.ptr(cbase), K.ptr(wc), K.stream_handle())
-            hit = self._wchunk[warps_per_sm] = (nw, wc)
+            hit = self._wchunk[warps_per_sm] = self._warp_chunks(cbase, warps_per_sm)
         return hit[0], hit[1], recs
+
+    def hot_packed(self, nhot: int, warps_per_sm: int):
+        """(nwarp, warp_chunk, records, entries, hot counts) of the hot /
+        cold chunk SpMM (csrc/spmm.cu k_spmm_hc): the packed hot-first copy
+        for ``nhot`` hot items (16-B {rank or item, value} entries, each
+        row's hot entries first) and the chunk plan cut at every row's hot /
+        cold boundary.  Built once per (nhot, schedule) on the device
+        (cached; one at a time: 16 B per rating)."""
+        key = (nhot, warps_per_sm)
+        hit = self._hotpack.get(key)
+        if hit is None:
+            from . import kernels as K
+
+            self._hotpack = {}  # release the previous copy first
+            ents = torch.empty((self.nnz, 2), dtype=torch.float64, device=self.device)
+            cnt = torch.empty(max(self.m, 1), dtype=torch.int32, device=self.device)
+            K.call("svdrec_spmm_hot_pack", self.m, K.ptr(self.indptr), K.ptr(self.indices), K.ptr(self.values),
+                   K.ptr(self.item_rank), int(nhot), K.ptr(ents), K.ptr(cnt), K.stream_handle())
+            cbase, recs = self._chunk_plan(self.indptr, cnt)
+            nw, wc = self._warp_chunks(cbase, warps_per_sm)
+            hit = self._hotpack[key] = (nw, wc, recs, ents, cnt)
+        return hit
 
     def ranked(self):
         """(ranked indices, values, rank -> item order) for the CF scoring

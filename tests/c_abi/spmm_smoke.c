@@ -97,9 +97,9 @@ int main(void) {
       d_ws = dev_copy(ws, (nwarp + 1) * 4);
       free(ws);
       CK(cudaMalloc((void**)&d_cbase, (m + 1) * 8));
-      CK(cudaMalloc(&d_recs, (nnz / 32 + m) * 16));
+      CK(cudaMalloc(&d_recs, (nnz / 32 + 2 * m) * 16));
       CK(cudaMalloc((void**)&d_wc, (nwarp + 1) * 4));
-      int prc = svdrec_chunk_plan(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_cbase, d_recs, NULL);
+      int prc = svdrec_chunk_plan(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, NULL, NULL, d_cbase, d_recs, NULL);
       if (!prc) prc = svdrec_warp_chunks(nwarp, d_ws, m, d_cbase, d_wc, NULL);
       if (prc) {
         fprintf(stderr, "chunk plan: %s\n", svdrec_last_error());

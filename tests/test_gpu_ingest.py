@@ -167,11 +167,13 @@ def test_hot_partition_matches_numpy(gpu, nhot):
     assert np.array_equal(val.cpu().numpy(), np.array(want_v))
 
 
-def test_chunk_plan_matches_numpy(gpu):
-    """The pipelined SpMM's chunk records (svdrec_chunk_plan): every segment
+@pytest.mark.parametrize("nhot", [None, 0, 40])
+def test_chunk_plan_matches_numpy(gpu, nhot):
+    """The pipelined SpMMs' chunk records (svdrec_chunk_plan): every segment
     in chunks of <= 32 entries with first / last flags, an empty row as one
-    empty chunk, split rows pointing at their partial slots; per-warp record
-    ranges (svdrec_warp_chunks)."""
+    empty chunk, split rows pointing at their partial slots; with the packed
+    hot-first copy (svdrec_spmm_hot_pack) no chunk straddles a row's hot /
+    cold boundary and hot chunks are flagged; per-warp record ranges."""
     import paper_2009_02251_b200 as P
     rng = np.random.default_rng(3)
     m, n = 700, 3000
@@ -182,18 +184,38 @@ def test_chunk_plan_matches_numpy(gpu):
     cols = np.concatenate([np.sort(rng.choice(n, d, replace=False)) for d in deg if d])
     M = sp.csr_matrix((rng.integers(1, 11, cols.size) * 0.5, (rows, cols)), shape=(m, n))
     c = P.SparseRatings(M, 0.5, 5.0).device(gpu).A
-    nw, wc, recs = c.chunk_schedule(16)
+    indptr = c.indptr.cpu().numpy()
+    if nhot is None:
+        nw, wc, recs = c.chunk_schedule(16)
+        cnt = np.zeros(m, dtype=np.int64)
+    else:
+        nw, wc, recs, ents, cnt = c.hot_packed(nhot, 16)
+        cnt = cnt.cpu().numpy().astype(np.int64)[:m]
+        rank = c.item_rank.cpu().numpy()
+        want_c = np.array([int((rank[M.indices[indptr[r]:indptr[r + 1]]] < nhot).sum()) for r in range(m)])
+        assert np.array_equal(cnt, want_c)
+        e = ents.cpu().numpy().view(np.int32).reshape(-1, 4)
+        ids, vals = e[:, 0], ents.cpu().numpy()[:, 1]
+        want_i, want_v = [], []
+        for r in range(m):
+            cols_r, vals_r = M.indices[indptr[r]:indptr[r + 1]], M.data[indptr[r]:indptr[r + 1]]
+            hot = rank[cols_r] < nhot
+            want_i += list(rank[cols_r[hot]]) + list(cols_r[~hot])
+            want_v += list(vals_r[hot]) + list(vals_r[~hot])
+        assert np.array_equal(ids, np.array(want_i, dtype=np.int32)) and np.array_equal(vals, np.array(want_v))
     sr, sb, se, sl = (t.cpu().numpy() for t in (c.seg_row, c.seg_begin, c.seg_end, c.seg_slot))
     assert (sl >= 0).any()
     want, first = [], []
     for j in range(sr.size):
         a, e = int(sb[j]), int(se[j])
+        h = min(max(int(indptr[sr[j]] + cnt[sr[j]]), a), e) if nhot is not None else a
         dst = int(sr[j]) if sl[j] < 0 else ~int(sl[j])
-        starts = list(range(a, e, 32)) or [None]
+        parts = [(o, min(32, h - o), 1024) for o in range(a, h, 32)] + [(o, min(32, e - o), 0) for o in range(h, e, 32)]
         first.append(len(want))
-        for t, o in enumerate(starts):
-            nv = 0 if o is None else min(32, e - o)
-            want.append((o or 0, dst, nv | (256 if t == 0 else 0) | (512 if t == len(starts) - 1 else 0), 0))
+        if not parts:
+            want.append((0, dst, 256 | 512, 0))
+        for t, (o, nv, hot) in enumerate(parts):
+            want.append((o, dst, nv | (256 if t == 0 else 0) | (512 if t == len(parts) - 1 else 0) | hot, 0))
     first.append(len(want))
     assert np.array_equal(recs.cpu().numpy()[: len(want)], np.array(want, dtype=np.int32))
     wseg = c.schedule(16)[1].cpu().numpy()

@@ -228,9 +228,11 @@ def test_sharded_orth_single_rank(gpu):
 
 @pytest.mark.parametrize("b", [2, 6, 10, 16, 20, 32, 40, 64])
 def test_spmm_hot_set_matches_tma(gpu, b):
-    """A @ X through the hot-set kernel (hot-first CSR, hot rows of X in shared
-    memory) equals the TMA-gather kernels and scipy: Zipf items, empty rows,
-    rows long enough to be split into segments (partial slots + fix-up)."""
+    """A @ X through the hot-set kernels (hot rows of X in shared memory: the
+    hot / cold chunk kernel on the packed hot-first CSR for b <= 32, the
+    register-gather kernel) equals the TMA-gather kernels and scipy: Zipf
+    items, empty rows, rows long enough to be split into segments (partial
+    slots + fix-up)."""
     import torch
     import paper_2009_02251_b200 as P
     from paper_2009_02251_b200 import kernels as K
@@ -248,13 +250,16 @@ def test_spmm_hot_set_matches_tma(gpu, b):
     A = P.SparseRatings(M, 0.5, 5.0)
     d = A.device(gpu)
     X = torch.as_tensor(rng.standard_normal((n, b)), device=gpu)
-    assert K._hot_rows(d.A, b, b, b, widths={b}) > 0
-    old_w, K.HOT_WIDTHS = K.HOT_WIDTHS, frozenset({b})
+    # the hot-set path for this width: the hot / cold chunk kernel on the
+    # packed copy (b <= 32), the register-gather kernel above
+    old_w, old_c = K.HOT_WIDTHS, K.HC_WIDTHS
+    K.HOT_WIDTHS, K.HC_WIDTHS = frozenset({b}), frozenset({b}) if b <= 32 else frozenset()
     Y1 = torch.empty(m, b, dtype=torch.float64, device=gpu)
     try:
+        assert (K._hc_rows(d.A, b, b, b) if b <= 32 else K._hot_rows(d.A, b, b, b)) > 0
         K.spmm(d.A, X, Y1)
     finally:
-        K.HOT_WIDTHS = old_w
+        K.HOT_WIDTHS, K.HC_WIDTHS = old_w, old_c
     old, K.SPMM_HOT = K.SPMM_HOT, False
     try:
         Y2 = torch.empty(m, b, dtype=torch.float64, device=gpu)
