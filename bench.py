@@ -516,7 +516,7 @@ def run_b200(args):
     roof_cf = roof("cf_predict", "svdrec_cf_predict (k_predict<R>)", 18904.6,
                    "CSR stream + every gathered item row; ceiling: random 1920-B row gathers from L2, 32 warps/SM "
                    "(tools/probe_l2bw.cu on B200)")
-    roof_spmm = roof("spmm", "svdrec_spmm (k_spmm_tma: TMA gather4 pipeline)", 7799.0,
+    roof_spmm = roof("spmm", "svdrec_spmm (k_spmm_pipe: chunk-record TMA gather4 pipeline)", 7799.0,
                      "CSR stream + every gathered row of X; ceiling: random 160-B row gathers from L2, 64 warps/SM "
                      "(tools/probe_l2bw.cu on B200)")
     # the line's roofline is the kernel with the larger share of the step

@@ -415,7 +415,9 @@ int svdrec_rank_rows(int64_t m, int32_t n, const int64_t* d_indptr, const int32_
  * int64, and d_totals = (segments, partial slots, split rows);
  * seg_plan_emit writes the arrays of svdrec_spmm's plan.  warp_plan: the
  * nwarp + 1 contiguous, cost-balanced range starts (cost = entries +
- * seg_cost per segment); d_scratch holds nseg + 1 int64. */
+ * seg_cost per segment; seg_cost < 0: entries rounded up to whole 32-entry
+ * chunks, at least one, plus -seg_cost -- what the chunk kernels execute);
+ * d_scratch holds nseg + 1 int64. */
 int svdrec_seg_plan_count(int64_t m, const int64_t* d_indptr, int32_t seg_max, int64_t* d_first,
                           int64_t* d_sbase, int64_t* d_lidx, int64_t* d_totals, void* stream);
 int svdrec_seg_plan_emit(int64_t m, const int64_t* d_indptr, int32_t seg_max, const int64_t* d_first,

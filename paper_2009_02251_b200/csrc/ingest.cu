@@ -371,7 +371,11 @@ __global__ void k_seg_emit(int64_t m, const int64_t* __restrict__ indptr, int se
 __global__ void k_seg_cost(int64_t nseg, const int64_t* __restrict__ seg_begin, const int64_t* __restrict__ seg_end,
                            int seg_cost, int64_t* __restrict__ cost) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < nseg) cost[j] = seg_end[j] - seg_begin[j] + seg_cost;
+  if (j >= nseg) return;
+  const int64_t d = seg_end[j] - seg_begin[j];
+  // seg_cost < 0: the chunk kernels' cost -- whole 32-entry chunks (at least
+  // one) plus -seg_cost per segment (its fold and store)
+  cost[j] = seg_cost >= 0 ? d + seg_cost : (d <= 32 ? 32 : ((d + 31) >> 5) << 5) - seg_cost;
 }
 
 // excl: exclusive scan of the segment costs, total = their sum; cut i (1 <=

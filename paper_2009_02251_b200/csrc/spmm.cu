@@ -1029,8 +1029,29 @@ __global__ void __launch_bounds__(W * 32, 1) k_spmm_hc(
   if (w >= nwarp) return;
   PackEnt* slots = reinterpret_cast<PackEnt*>(smb + (size_t)wib * HcGeom<D>::WARPB);  // D x 32 entries
   int4* rring = reinterpret_cast<int4*>(slots + D * 32);
-  const int g = lane / P, pc = lane - (lane / P) * P;
+  // lane -> (row group g, 16-B piece pc of the row).  For 8 < P < 16 (rows of
+  // 144..240 B) the first eight pieces of each group's row take one whole
+  // quarter-warp -- a 128-B contiguous, conflict-free shared-memory phase --
+  // and the rows' tails share the last phase; otherwise groups are
+  // contiguous runs of P lanes.
+  constexpr bool kPhased = P > 8 && P < 16;
+  constexpr int T = kPhased ? P - 8 : 0;  // tail pieces per row
+  int g, pc;
+  if (kPhased) {
+    if (lane < 8 * G) {
+      g = lane >> 3;
+      pc = lane & 7;
+    } else {
+      const int t = lane - 8 * G;
+      g = t / (T ? T : 1);
+      pc = 8 + t - g * T;
+    }
+  } else {
+    g = lane / P;
+    pc = lane - g * P;
+  }
   const bool active = g < G;
+  auto lane_of = [&](int gg, int p) { return kPhased ? (p < 8 ? 8 * gg + p : 8 * G + gg * T + (p - 8)) : gg * P + p; };
   const double2* hrow = hot + pc;
   const double2* xrow = reinterpret_cast<const double2*>(X) + pc;
   const int64_t ldx2 = ldx / 2;
@@ -1122,7 +1143,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_spmm_hc(
       Acc<2> tot = acc;
 #pragma unroll
       for (int h = 1; h < G; ++h) {
-        const Acc<2> o = acc.shfl((lane + h * P) & 31);
+        const Acc<2> o = acc.shfl(lane_of(h, pc < P ? pc : 0) & 31);
         if (g == 0) tot.add(o);
       }
       if (g == 0) {

@@ -153,6 +153,19 @@ def segment_plan(indptr: np.ndarray, seg_max: int = SEG_MAX):
 
 
 WARPS_PER_SM = 16  # pipelined SpMM: resident warps per SM (2 CTAs x 8 warps)
+# segment cost of the chunk kernels' schedules (svdrec_warp_plan, seg_cost < 0):
+# whole 32-entry chunks plus 5 entries' worth for the segment's fold and store
+CHUNK_COST = -5
+
+
+def _seg_cost(d, seg_cost: int):
+    """Cost of segments of ``d`` entries: d + seg_cost, or for seg_cost < 0 the
+    chunk kernels' cost (whole 32-entry chunks, at least one) - seg_cost."""
+    if seg_cost >= 0:
+        return d + seg_cost
+    chunks = (d + 31) // 32
+    chunks = np.maximum(chunks, 1) if isinstance(d, np.ndarray) else torch.clamp(chunks, min=1)
+    return chunks * 32 - seg_cost
 
 
 def warp_plan(seg_begin: np.ndarray, seg_end: np.ndarray, nwarp: int, seg_cost: int = 16) -> np.ndarray:
@@ -160,7 +173,7 @@ def warp_plan(seg_begin: np.ndarray, seg_end: np.ndarray, nwarp: int, seg_cost: 
     about equal cost (nonzeros + ``seg_cost`` per segment); returns the
     ``nwarp + 1`` range starts (int32) the pipelined SpMM kernel reads."""
     nseg = seg_begin.size
-    cost = np.cumsum((seg_end - seg_begin) + seg_cost, dtype=np.int64)
+    cost = np.cumsum(_seg_cost(seg_end - seg_begin, seg_cost), dtype=np.int64)
     total = int(cost[-1]) if nseg else 0
     targets = (np.arange(1, nwarp, dtype=np.float64) * (total / max(nwarp, 1)))
     cuts = np.searchsorted(cost, targets, side="left") + 1 if nseg else np.zeros(nwarp - 1, np.int64)
@@ -241,7 +254,7 @@ def warp_plan_t(seg_begin: torch.Tensor, seg_end: torch.Tensor, nwarp: int, seg_
     out = torch.zeros(nwarp + 1, dtype=torch.int64, device=dev)
     out[-1] = nseg
     if nseg and nwarp > 1:
-        cost = torch.cumsum((seg_end - seg_begin) + seg_cost, 0)
+        cost = torch.cumsum(_seg_cost(seg_end - seg_begin, seg_cost), 0)
         total = cost[-1].to(torch.float64)
         targets = torch.arange(1, nwarp, dtype=torch.float64, device=dev) * (total / nwarp)
         cuts = torch.searchsorted(cost.to(torch.float64), targets, side="left") + 1
@@ -334,17 +347,19 @@ class DeviceCSR:
         self._transpose = t
         return t
 
-    def schedule(self, warps_per_sm: int) -> tuple[int, torch.Tensor]:
-        """(nwarp, warp_seg) for a kernel running ``warps_per_sm`` warps per SM."""
-        if warps_per_sm == WARPS_PER_SM:
+    def schedule(self, warps_per_sm: int, seg_cost: int = 16) -> tuple[int, torch.Tensor]:
+        """(nwarp, warp_seg) for a kernel running ``warps_per_sm`` warps per
+        SM: contiguous segment ranges of about equal cost (entries +
+        ``seg_cost`` per segment; CHUNK_COST: whole 32-entry chunks)."""
+        if warps_per_sm == WARPS_PER_SM and seg_cost == 16:
             return self.nwarp, self.warp_seg
-        hit = self._sched.get(warps_per_sm)
+        hit = self._sched.get((warps_per_sm, seg_cost))
         if hit is None:
             sms = torch.cuda.get_device_properties(self.device).multi_processor_count \
                 if self.device.type == "cuda" else 148
             nw = int(max(1, min(self.nseg, sms * warps_per_sm)))
             plan = warp_plan_dev if self.device.type == "cuda" else warp_plan_t
-            hit = self._sched[warps_per_sm] = (nw, plan(self.seg_begin, self.seg_end, nw))
+            hit = self._sched[(warps_per_sm, seg_cost)] = (nw, plan(self.seg_begin, self.seg_end, nw, seg_cost))
         return hit
 
     def _chunk_plan(self, indptr=None, hot_cnt=None):
@@ -359,7 +374,7 @@ class DeviceCSR:
     def _warp_chunks(self, cbase, warps_per_sm: int):
         from . import kernels as K
 
-        nw, wseg = self.schedule(warps_per_sm)
+        nw, wseg = self.schedule(warps_per_sm, CHUNK_COST)
         wc = torch.empty(nw + 1, dtype=torch.int32, device=self.device)
         K.call("svdrec_warp_chunks", nw, K.ptr(wseg), self.nseg, K.ptr(cbase), K.ptr(wc), K.stream_handle())
         return nw, wc

@@ -175,6 +175,7 @@ def test_chunk_plan_matches_numpy(gpu, nhot):
     hot-first copy (svdrec_spmm_hot_pack) no chunk straddles a row's hot /
     cold boundary and hot chunks are flagged; per-warp record ranges."""
     import paper_2009_02251_b200 as P
+    from paper_2009_02251_b200 import sparse as S
     rng = np.random.default_rng(3)
     m, n = 700, 3000
     deg = np.minimum(rng.lognormal(3.0, 1.5, m).astype(np.int64), n)
@@ -218,7 +219,7 @@ def test_chunk_plan_matches_numpy(gpu, nhot):
             want.append((o, dst, nv | (256 if t == 0 else 0) | (512 if t == len(parts) - 1 else 0) | hot, 0))
     first.append(len(want))
     assert np.array_equal(recs.cpu().numpy()[: len(want)], np.array(want, dtype=np.int32))
-    wseg = c.schedule(16)[1].cpu().numpy()
+    wseg = c.schedule(16, S.CHUNK_COST)[1].cpu().numpy()
     assert nw == wseg.size - 1 and np.array_equal(wc.cpu().numpy(), np.array(first, dtype=np.int32)[wseg])
 
 
@@ -239,5 +240,6 @@ def test_segment_and_warp_plan_kernels_match_numpy(gpu, seed):
         np.testing.assert_array_equal(np.asarray(a, dtype=np.int64), b.cpu().numpy().astype(np.int64))
     assert ref[7] == got[7]
     for nw in (1, 7, 64, 5000, 100000):
-        np.testing.assert_array_equal(S.warp_plan(ref[1], ref[2], nw),
-                                      S.warp_plan_dev(got[1], got[2], nw).cpu().numpy())
+        for cost in (16, S.CHUNK_COST):
+            np.testing.assert_array_equal(S.warp_plan(ref[1], ref[2], nw, cost),
+                                          S.warp_plan_dev(got[1], got[2], nw, cost).cpu().numpy())

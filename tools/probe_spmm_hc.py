@@ -29,6 +29,7 @@ def t(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
+K.HC_WIDTHS = frozenset(range(2, 33, 2))  # measure every supported width
 print("hc warps/SM", K.query("svdrec_spmm_hc_warps_per_sm"))
 for b in [int(x) for x in sys.argv[1:]] or [2, 8, 16, 20, 32]:
     X = torch.randn(A.n, b, dtype=torch.float64, device=dev)

@@ -6,7 +6,7 @@ captures, into profiles/traffic.json (read by bench.py for the roofline's
 
 Each capture holds consecutive launches of one kernel from one bench step
 (`-k regex:k_predict -c 13`: every CF scoring launch of a step, k = 20..260;
-`-k regex:k_spmm_tma -c 8`); the per-launch figure is the mean of
+`-k regex:k_spmm_pipe -c 8`); the per-launch figure is the mean of
 dram__bytes_read.sum + dram__bytes_write.sum over the captured launches.
 """
 from __future__ import annotations
@@ -19,7 +19,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-KEYS = {"k_predict": "cf_predict", "k_spmm_tma": "spmm"}
+KEYS = {"k_predict": "cf_predict", "k_spmm_pipe": "spmm"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
