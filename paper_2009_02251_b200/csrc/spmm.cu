@@ -548,51 +548,42 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
   // lane 0) at step j, so no step waits on a record's global load
   if (lane < kRecAhead && lane < n) rring[lane] = __ldg(chunks + c_lo + lane);
   __syncwarp();
-  int fj = 0, fs = 0;  // next chunk to fetch (relative), its CSR slot
-  int step = 0;        // fetch() calls so far minus the prologue's: record step + kRecAhead is requested
-  auto fetch = [&](bool ahead) {
-    if (fj < n) {
-      const int4 rec = rring[fj & (kRecRing - 1)];
+  // The main loop is unrolled by D, so every ring index below is a
+  // compile-time constant of the unrolled step u (i = i0 + u, i0 % D == 0):
+  // CSR slot i % D = u, row stage i % S = u % S, and -- D / S being even --
+  // the stage's phase parity too.
+  static_assert(D % S == 0 && (D / S) % 2 == 0 && kRecRing % D == 0, "spmm: ring sizes must nest");
+  auto fetch = [&](int f, int fs, int rj) {  // CSR of chunk f into slot fs; request record rj
+    if (f < n) {
+      const int4 rec = rring[f & (kRecRing - 1)];
       const int64_t off = (int64_t)(((uint64_t)(uint32_t)rec.w << 32) | (uint32_t)rec.x);
       const bool in = lane < (rec.z & 63);
       const int64_t o = off + (in ? lane : 0);
       unsigned char* sl = csr + fs * Pg::CSRB;
       cp_async8(sl + 8 * lane, values + o, in ? 8u : 0u);
       cp_async4(sl + 256 + 4 * lane, indices + o, in ? 4u : 0u);
-      ++fj;
     }
-    if (ahead) {
-      const int rj = step + kRecAhead;
-      if (lane == 0 && rj < n) cp_async16(rring + (rj & (kRecRing - 1)), chunks + c_lo + rj);
-      ++step;
-    }
+    if (rj >= 0 && rj < n && lane == 0) cp_async16(rring + (rj & (kRecRing - 1)), chunks + c_lo + rj);
     cp_async_commit();
-    if (++fs == D) fs = 0;
   };
-  int gs = 0, gr = 0, gj = 0;  // CSR slot / row stage / chunk of the next gather
-  auto gather = [&]() {
+  auto gather = [&](int j, int gs, int gr) {  // chunk j: CSR slot gs -> row stage gr
     cp_async_wait<D - S>();
     __syncwarp();
     const unsigned char* sl = csr + gs * Pg::CSRB;
-    const int nvf = rring[gj & (kRecRing - 1)].z;
+    const int nvf = rring[j & (kRecRing - 1)].z;
     const int ng = ((nvf & 63) + 3) >> 2;
     if (lane == 0) mbar_expect_tx(bar + gr, (unsigned)(ng * 4 * B * sizeof(TX)));
     if (lane < ng) {
       const int4 r = *reinterpret_cast<const int4*>(sl + 256 + 16 * lane);
       tma_gather4(reinterpret_cast<TX*>(rows + gr * ROWS) + lane * G4, &tmX, 0, r.x, r.y, r.z, r.w, bar + gr);
     }
-    ++gj;
-    if (++gs == D) gs = 0;
-    if (++gr == S) gr = 0;
   };
   Acc<V> acc, acc1;
   acc.zero();
   acc1.zero();
-  int cs = 0, cr = 0, cj = 0;
-  unsigned cph = 0;  // phase parity of row stage cr
-  auto consume = [&]() {
+  auto consume = [&](int j, int cs, int cr, unsigned cph) {  // chunk j from CSR slot cs / row stage cr (parity cph)
     const unsigned char* sl = csr + cs * Pg::CSRB;
-    const int4 m = rring[cj & (kRecRing - 1)];  // y: destination, z: entries | flags
+    const int4 m = rring[j & (kRecRing - 1)];  // y: destination, z: entries | flags
     const int nv = m.z & 63;
     mbar_wait(bar + cr, cph);
     if (m.z & 256) {
@@ -608,9 +599,9 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
       double vs[NS];
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
-        const int j = q * G + g;
+        const int jj = q * G + g;
         const int jo = q * G;
-        const int jc = j < 32 ? j : 31;
+        const int jc = jj < 32 ? jj : 31;
         const TX* src = G4 == 4 * B ? xr + jo * B : sx + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
         xs[q].load(src);
         vs[q] = vr[jc - g];
@@ -653,20 +644,27 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
       }
     }
     __syncwarp();  // every lane is done with the stage and the CSR slot
-    ++cj;
-    if (++cs == D) cs = 0;
-    if (++cr == S) {
-      cr = 0;
-      cph ^= 1u;
-    }
   };
 
+  constexpr int F = D - S + 1;  // chunks fetched ahead of the gather
 #pragma unroll
-  for (int t = 0; t <= D - S; ++t) fetch(false);
-  for (int i = 0; i < n + S - 1; ++i) {
-    if (i < n) gather();
-    if (i >= S - 1) consume();
-    fetch(true);
+  for (int t = 0; t < F; ++t) fetch(t, t, -1);
+  const int total = n + S - 1;
+  for (int i0 = 0; i0 < total; i0 += D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const int i = i0 + u;
+      if (i < total) {
+        if (i < n) gather(i, u, u % S);
+        // chunk j = i - (S - 1) = i0 + e, e = u - S + 1: slot (u + F) % D, stage (u + 1) % S, phase
+        // parity (j / S) & 1 = (e / S) & 1 for e >= 0, else 1 (i0 / S is even)
+        if (i >= S - 1) {
+          const int e = u - S + 1;
+          consume(i - (S - 1), (u + F) % D, (u + 1) % S, e >= 0 ? (unsigned)((e / S) & 1) : 1u);
+        }
+        fetch(i + F, (u + F) % D, i + kRecAhead);
+      }
+    }
   }
   cp_async_wait<0>();
 }
