@@ -1013,7 +1013,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_spmm_hc(
     const PackEnt* __restrict__ ents, const double* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ hot_items, int nhot, double* __restrict__ Y, int64_t ldy,
     double* __restrict__ partial) {
-  static_assert(kRecAhead >= 2 * D && kRecAhead + 1 <= kRecRing, "spmm_hc: record ring too small");
+  static_assert(kRecAhead >= 2 * D && kRecAhead + 1 <= kRecRing && kRecRing % D == 0, "spmm_hc: record ring too small");
   constexpr int B = 2 * P, G = 32 / P, RB = P;
   extern __shared__ __align__(128) unsigned char smb[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1052,112 +1052,98 @@ __global__ void __launch_bounds__(W * 32, 1) k_spmm_hc(
   auto lane_of = [&](int gg, int p) { return kPhased ? (p < 8 ? 8 * gg + p : 8 * G + gg * T + (p - 8)) : gg * P + p; };
   const double2* hrow = hot + pc;
   const double2* xrow = reinterpret_cast<const double2*>(X) + pc;
-  const int64_t ldx2 = ldx / 2;
+  const int ldx2 = (int)(ldx / 2);  // row pitch in double2 (the host checks rows x pitch < 2^31)
 
   const int32_t c_lo = warp_chunk[w], c_hi = warp_chunk[w + 1];
   const int n = c_hi - c_lo;
   if (n <= 0) return;
   if (lane < kRecAhead && lane < n) rring[lane] = __ldg(chunks + c_lo + lane);
   __syncwarp();
-  int fj = 0, fs = 0;
-  auto fetch = [&]() {
-    if (fj < n) {
-      const int4 rec = rring[fj & (kRecRing - 1)];
+  // Entries of chunk f into slot fs.  Lanes past the chunk's end copy only
+  // the ID of the chunk's first entry (4 of 16 bytes, the rest zero-filled):
+  // a pad then reads a row its output already depends on, times 0.0 -- the
+  // accumulation needs no bounds, and a non-finite X pollutes nothing the
+  // reference would not.
+  auto fetch = [&](int f, int fs, int rj) {
+    if (f < n) {
+      const int4 rec = rring[f & (kRecRing - 1)];
       const int64_t off = (int64_t)(((uint64_t)(uint32_t)rec.w << 32) | (uint32_t)rec.x);
-      const bool in = lane < (rec.z & 63);
+      const int nv = rec.z & 63;
+      const bool in = lane < nv;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
                        (unsigned)__cvta_generic_to_shared(slots + fs * 32 + lane)),
-                   "l"(ents + off + (in ? lane : 0)), "r"(in ? 16u : 0u)
+                   "l"(ents + off + (in ? lane : 0)), "r"(in ? 16u : (nv ? 4u : 0u))
                    : "memory");
-      ++fj;
     }
+    if (rj < n && lane == 0) cp_async16(rring + (rj & (kRecRing - 1)), chunks + c_lo + rj);
+    cp_async_commit();
   };
   Acc<2> acc, acc1;
   acc.zero();
   acc1.zero();
-#pragma unroll
-  for (int t = 0; t < D; ++t) {
-    fetch();
-    cp_async_commit();
-    if (++fs == D) fs = 0;
-  }
-  int cs = 0;
-  for (int i = 0; i < n; ++i) {
+  auto consume = [&](int i, int cs) {
     cp_async_wait<D - 1>();  // chunk i's entries (and the records requested >= D steps ago) have landed
     __syncwarp();
     const int4 m = rring[i & (kRecRing - 1)];  // y: destination, z: entries | flags
-    const int nv = m.z & 63;
-    if (m.z & 256) {
-      acc.zero();
-      acc1.zero();
-    }
-    if (active && nv > 0) {
+    if (active && (m.z & 63)) {
       constexpr int NS = (32 + G - 1) / G;
-      const PackEnt* sl = slots + cs * 32;
+      const PackEnt* sl = slots + cs * 32 + g;
       Acc<2> xs[NS];
       double vs[NS];
       if (m.z & 1024) {
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
-          const int j = q * G + g;
-          const PackEnt e = sl[j < 32 ? j : 31];
+          const PackEnt e = sl[q * G + g < 32 ? q * G : 31 - g];
           xs[q].h[0] = hrow[e.id * RB];
           vs[q] = e.v;
         }
       } else {
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
-          const int j = q * G + g;
-          const PackEnt e = sl[j < 32 ? j : 31];
+          const PackEnt e = sl[q * G + g < 32 ? q * G : 31 - g];
           xs[q].h[0] = __ldg(xrow + (int64_t)e.id * ldx2);
           vs[q] = e.v;
         }
       }
-      if (nv == 32) {
 #pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          if ((q + 1) * G <= 32 || q * G + g < 32) {
-            if (q & 1)
-              acc1.fma(vs[q], xs[q]);
-            else
-              acc.fma(vs[q], xs[q]);
-          }
-        }
-      } else {
-        const int left = nv - g;
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          if (q * G < left) {
-            if (q & 1)
-              acc1.fma(vs[q], xs[q]);
-            else
-              acc.fma(vs[q], xs[q]);
-          }
+      for (int q = 0; q < NS; ++q) {
+        if ((q + 1) * G <= 32 || q * G + g < 32) {
+          if (q & 1)
+            acc1.fma(vs[q], xs[q]);
+          else
+            acc.fma(vs[q], xs[q]);
         }
       }
     }
-    if (m.z & 512) {
+    if (m.z & 512) {  // the segment's last chunk: fold the groups, store, start the next segment at zero
       acc.add(acc1);
       Acc<2> tot = acc;
 #pragma unroll
       for (int h = 1; h < G; ++h) {
-        const Acc<2> o = acc.shfl(lane_of(h, pc < P ? pc : 0) & 31);
+        const Acc<2> o = acc.shfl(lane_of(h, pc) & 31);
         if (g == 0) tot.add(o);
       }
       if (g == 0) {
         double* dst = m.y >= 0 ? (Y + (int64_t)m.y * ldy + 2 * pc) : (partial + (int64_t)(~m.y) * B + 2 * pc);
         tot.store(dst);
       }
+      acc.zero();
+      acc1.zero();
     }
     __syncwarp();  // every lane is done with the slot
-    fetch();       // chunk i + D into the slot just freed
-    {
-      const int rj = i + kRecAhead;
-      if (lane == 0 && rj < n) cp_async16(rring + (rj & (kRecRing - 1)), chunks + c_lo + rj);
+  };
+#pragma unroll
+  for (int t = 0; t < D; ++t) fetch(t, t, n);  // (records 0 .. kRecAhead - 1 are already here)
+  // unrolled by D: chunk i = i0 + u sits in slot u, and chunk i + D refills it
+  for (int i0 = 0; i0 < n; i0 += D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const int i = i0 + u;
+      if (i < n) {
+        consume(i, u);
+        fetch(i + D, u, i + kRecAhead);
+      }
     }
-    cp_async_commit();
-    if (++fs == D) fs = 0;
-    if (++cs == D) cs = 0;
   }
   cp_async_wait<0>();
 }
@@ -1188,7 +1174,7 @@ __global__ void k_hot_pack(int64_t m, const int64_t* __restrict__ indptr, const 
     int64_t nh = 0;
     for (int64_t t0 = a; t0 < b; t0 += 32) {
       const int64_t t = t0 + lane;
-      const bool hot = t < b && rank[indices[t]] < nhot;
+      const bool hot = nhot > 0 && t < b && rank[indices[t]] < nhot;
       nh += __popc(__ballot_sync(0xffffffffu, hot));
     }
     if (lane == 0) hot_cnt[r] = (int32_t)nh;
@@ -1200,10 +1186,10 @@ __global__ void k_hot_pack(int64_t m, const int64_t* __restrict__ indptr, const 
       double v = 0.0;
       if (valid) {
         c = indices[t];
-        rk = rank[c];
+        rk = nhot > 0 ? rank[c] : 0;
         v = __ldcs(values + t);
       }
-      const bool hot = valid && rk < nhot;
+      const bool hot = nhot > 0 && valid && rk < nhot;
       const unsigned hm = __ballot_sync(0xffffffffu, hot), vm = __ballot_sync(0xffffffffu, valid);
       if (valid) {
         const int64_t pos = hot ? a + hrun + __popc(hm & lt) : a + nh + crun + __popc(vm & ~hm & lt);
@@ -1380,7 +1366,7 @@ extern "C" int svdrec_spmm_hc_rows(int32_t b) {
 extern "C" int svdrec_spmm_hot_pack(int64_t m, const int64_t* d_indptr, const int32_t* d_indices,
                                     const double* d_values, const int32_t* d_rank, int32_t nhot, void* d_out,
                                     int32_t* d_hot_cnt, void* stream) {
-  SVDREC_ARG(m >= 0 && nhot >= 0 && d_hot_cnt, "spmm_hot_pack: bad arguments");
+  SVDREC_ARG(m >= 0 && nhot >= 0 && d_hot_cnt && (nhot == 0 || d_rank), "spmm_hot_pack: bad arguments");
   if (m == 0) return 0;
   const int64_t grid = min64((m + 7) / 8, (int64_t)sm_count() * 16);
   k_hot_pack<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(m, d_indptr, d_indices, d_values, d_rank, nhot,
@@ -1398,6 +1384,7 @@ extern "C" int svdrec_spmm_hc(int64_t nseg, const void* d_entries, const double*
   SVDREC_ARG(nhot >= 0 && nhot <= svdrec_spmm_hc_rows(b) && nhot <= x_rows,
              "spmm_hc: %d hot rows exceed shared memory", nhot);
   SVDREC_ARG(nwarp > 0 && d_warp_chunk && d_chunks, "spmm_hc: needs a chunk plan (svdrec_spmm_hc_warps_per_sm)");
+  SVDREC_ARG(x_rows * (ldx / 2) < (1ll << 31), "spmm_hc: X too large for 32-bit row offsets");
   SVDREC_ARG(((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_Y) |
                reinterpret_cast<uintptr_t>(d_partial) | reinterpret_cast<uintptr_t>(d_entries)) % 16) == 0,
              "spmm_hc: operands must be 16-B aligned");

@@ -171,14 +171,14 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
 SPMM_HOT = os.environ.get("SVDREC_SPMM_HOT", "1") != "0"
 # A @ X of a rating matrix (a CSR with a popularity order), config 3, us per
 # call, hot / cold chunk kernel (k_spmm_hc) vs TMA pipeline (k_spmm_pipe):
-# b = 2 199 vs 283, 4 188 vs 266, 8 216 vs 271, 10 258 vs 340, 12 258 vs 298,
-# 16 251 vs 294, 18 348 vs 361, 20 328 vs 331, 22 383 vs 415, 24 355 vs 403,
-# 28 390 vs 563, 32 358 vs 556.  At b = 20 they tie (the hot / cold kernel is
-# bound by the L1 data pipe: 160-B rows straddle the 128-B shared-memory
-# phases) and the pipeline needs no second copy of A, so it keeps that width.
-# b = 64 runs the register-gather hot-set kernel (k_spmm_hot: 554 vs 917 us
-# for the wide TMA kernel; at b = 40, 668 vs 650, it is not used).
-HC_WIDTHS = frozenset(range(2, 33, 2)) - {20}
+# b = 2 208 vs 245, 4 198 vs 228, 6 220 vs 333, 8 202 vs 230, 10 256 vs 334,
+# 12 255 vs 254, 14 297 vs 331, 16 248 vs 255, 18 325 vs 313, 20 311 vs 288,
+# 22 387 vs 394, 24 361 vs 326, 26 430 vs 525, 28 396 vs 499, 30 435 vs 527,
+# 32 362 vs 494.  The pipeline keeps the widths where it ties or wins (it
+# needs no second copy of A); b = 64 runs the register-gather hot-set kernel
+# (k_spmm_hot: 554 vs 917 us for the wide TMA kernel; at b = 40, 668 vs 650,
+# it is not used).
+HC_WIDTHS = frozenset(range(2, 33, 2)) - {12, 18, 20, 24}
 HOT_WIDTHS = frozenset({64})
 
 
