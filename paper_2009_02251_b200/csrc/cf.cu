@@ -165,6 +165,9 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
               double* __restrict__ out_val, double* __restrict__ out_raw, uint8_t* __restrict__ out_fb) {
   constexpr int NA = NT * VE;
   const int kp = (k + VE - 1) / VE * VE;
+  // row pitches as 32-bit values: row * pitch is then one IMAD.WIDE instead
+  // of a 64 x 64-bit multiply per gathered row (the host checks they fit)
+  const int ldy32 = (int)ldy, ldn32 = (int)ldn;
   extern __shared__ __align__(16) unsigned char hs_raw[];
   TY* hs = reinterpret_cast<TY*>(hs_raw);  // nhot rows + a zero row (padding target), stride kp
   for (int64_t t = threadIdx.x; t < (int64_t)(nhot + 1) * kp; t += blockDim.x) {
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
         double vv[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
-          rows[q] = Yr + (int64_t)s_cold[wid][j + q] * ldy;
+          rows[q] = Yr + (int64_t)s_cold[wid][j + q] * ldy32;
           vv[q] = s_val[wid][j + q];
         }
         accum<NT, U, false, TY, VE>(P, S, rows, vv, lane, kp);
@@ -344,8 +347,8 @@ __global__ void __launch_bounds__(PredictShape<NT * VE>::kThreads, 1)
         const double n0 = __shfl_sync(0xffffffffu, nl, q);
         const double n1 = q + 1 < ns ? __shfl_sync(0xffffffffu, nl, (q + 1) & 31) : 0.0;
         const bool ok0 = n0 != 0.0 && deg > 0, ok1 = n1 != 0.0 && deg > 0;
-        const double* row0 = Xn + (int64_t)j0 * ldn;
-        const double* row1 = Xn + (int64_t)j1 * ldn;
+        const double* row0 = Xn + (int64_t)j0 * ldn32;
+        const double* row1 = Xn + (int64_t)j1 * ldn32;
         double num0 = 0.0, den0 = 0.0, num1 = 0.0, den1 = 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t)
@@ -589,6 +592,7 @@ int cf_predict_impl(int64_t nwork, const int64_t* d_work_start, const int32_t* d
   const int ve = k <= 32 ? 1 : (k <= 64 || VMAX == 2 ? 2 : 4);
   SVDREC_ARG(ldy % VMAX == 0 && reinterpret_cast<uintptr_t>(d_Yr) % 16 == 0,
              "cf_predict: Yr rows must be 16-B aligned (ldy %% %d == 0)", VMAX);
+  SVDREC_ARG(ldy < (1ll << 31) && ldn < (1ll << 31), "cf_predict: row pitches must fit 32 bits");
   const int kp = (k + ve - 1) / ve * ve;
   const int nt = (kp / ve + 31) / 32;  // vector steps per lane
   // one persistent CTA per SM holding the hottest items' unit rows in

@@ -586,10 +586,6 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
     const int4 m = rring[j & (kRecRing - 1)];  // y: destination, z: entries | flags
     const int nv = m.z & 63;
     mbar_wait(bar + cr, cph);
-    if (m.z & 256) {
-      acc.zero();
-      acc1.zero();
-    }
     if (active) {
       constexpr int NS = (32 + G - 1) / G;
       const TX* sx = reinterpret_cast<const TX*>(rows + cr * ROWS);
@@ -642,6 +638,8 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
         double* dst = m.y >= 0 ? (Y + (int64_t)m.y * ldy + V * pc) : (partial + (int64_t)(~m.y) * B + V * pc);
         tot.store(dst);
       }
+      acc.zero();  // the next segment starts at zero (segments never span warps)
+      acc1.zero();
     }
     __syncwarp();  // every lane is done with the stage and the CSR slot
   };
