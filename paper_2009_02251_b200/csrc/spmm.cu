@@ -539,6 +539,23 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
   if (w >= nwarp) return;
   const int g = lane / P, pc = lane - (lane / P) * P;
   const bool active = g < G;
+  // where this lane's piece of row j = q G + g sits in a stage (elements of
+  // TX).  When four rows fill a whole number of 128-B units the rows are
+  // contiguous and the offset is a constant per step; otherwise (gather4
+  // blocks padded to 128 B: 3-, 5-, 7-lane rows, float rows) the NS offsets
+  // are computed once here instead of per chunk.
+  constexpr int NS = (32 + G - 1) / G;
+  constexpr bool kContig = G4 == 4 * B;
+  int offs[kContig ? 1 : NS];
+  if constexpr (!kContig) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const int jc = q * G + g < 32 ? q * G + g : 31;
+      offs[q] = (jc >> 2) * G4 + (jc & 3) * B + V * pc;
+    }
+  } else {
+    offs[0] = 0;
+  }
 
   const int32_t c_lo = warp_chunk[w], c_hi = warp_chunk[w + 1];
   const int n = c_hi - c_lo;
@@ -587,7 +604,6 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
     const int nv = m.z & 63;
     mbar_wait(bar + cr, cph);
     if (active) {
-      constexpr int NS = (32 + G - 1) / G;
       const TX* sx = reinterpret_cast<const TX*>(rows + cr * ROWS);
       const TX* xr = sx + ((g >> 2) * G4 + (g & 3) * B) + V * pc;
       const double* vr = reinterpret_cast<const double*>(sl) + g;
@@ -598,7 +614,7 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
         const int jj = q * G + g;
         const int jo = q * G;
         const int jc = jj < 32 ? jj : 31;
-        const TX* src = G4 == 4 * B ? xr + jo * B : sx + (jc >> 2) * G4 + (jc & 3) * B + V * pc;
+        const TX* src = kContig ? xr + jo * B : sx + offs[kContig ? 0 : q];
         xs[q].load(src);
         vs[q] = vr[jc - g];
       }
