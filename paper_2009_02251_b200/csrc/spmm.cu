@@ -5,16 +5,21 @@
 // sketch / power / projection pass of Algs. 1-3 (rsvd.py:135-143,
 // 179-194) is one call.  A.T @ X is the same kernel on the CSR of A.T.
 //
-// HBM design: the CSR stream (int32 column + float64 value = 12 B per
-// nonzero) is read once with coalesced 32-wide loads; the dense rows of X
-// (b doubles, 16-B vector loads) are gathered through L1/L2 (X is small
-// next to A: n*b*8 bytes).  One warp owns one row segment; its 32 lanes are
-// split into NPW groups of LPN = ceil(b/VEC) lanes, so NPW nonzeros are in
-// flight per step (b = 20: 3 nonzeros x 10 lanes x double2).  Column/value
-// pairs are fetched 32 at a time and broadcast with shuffles.  Rows longer
-// than the plan's segment cap (power-law items) are split; their partial
-// sums land in a scratch slot and a fix-up kernel adds them in slot order,
-// so the result is bitwise deterministic.
+// Kernels (which one runs is decided in svdrec_spmm / by the host,
+// kernels.py):
+//   k_spmm_pipe  even b <= 32 (the headline's b = 20): chunk-record pipeline,
+//                CSR chunks and records through cp.async rings, X rows by
+//                TMA gather4 into per-warp row rings;
+//   k_spmm_tma   32 < b <= 64 (b % 4 == 0): the segment-metadata TMA pipeline;
+//   k_spmm_hc    A @ X of a rating matrix at even b <= 32 where it measured
+//                faster: packed hot-first CSR, the most rated items' rows of
+//                X in shared memory, cold rows gathered into registers;
+//   k_spmm_hot   A @ X at b = 64: the register-gather hot-set kernel;
+//   k_spmm       any b / unaligned operands: one warp per row segment, 32
+//                (column, value) pairs at a time broadcast by shuffles.
+// Rows longer than the plan's segment cap (power-law items) are split; their
+// partial sums land in a scratch slot and a fix-up kernel adds them in slot
+// order, so every result is bitwise deterministic.
 #include <cstdlib>
 
 #include "tma.cuh"
@@ -120,7 +125,8 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t nseg, const int32_t* __res
 }
 
 // ---------------------------------------------------------------------------
-// TMA-pipelined variant (b even, b <= 32, 16-B aligned operands).  Each warp
+// TMA-pipelined variant on segment metadata (round 1; now the wide blocks'
+// kernel: 32 < b <= 64, V = 4 doubles per lane).  Each warp
 // owns a contiguous, nonzero-balanced range of segments (host plan
 // ``warp_seg``; segment metadata read 32 at a time) and streams it in chunks
 // of 32 nonzeros through a ring of S = 2 shared-memory stages: while chunk c
@@ -993,12 +999,9 @@ __global__ void __launch_bounds__(512, 1) k_spmm_hot(
 }
 
 // ---------------------------------------------------------------------------
-// Hot / cold chunk kernel for A @ X (even b <= 32; round 2).  Random X-row
-// gathers through L2 run at ~60 G rows/s whatever the path (TMA gather4 or
-// LDG, 16-B to 160-B rows alike: ~5 cycles per row per SM), so the only way
-// below ~300 us per call on config 3 is fewer gathers: the rows of X of the
-// nhot most rated items sit in every CTA's shared memory (1,190 rows at
-// b = 20 hold 64 % of the ratings).  The CSR is the PACKED hot-first copy
+// Hot / cold chunk kernel for A @ X (even b <= 32; round 2): the rows of X
+// of the nhot most rated items sit in every CTA's shared memory (1,216 rows
+// at b = 20 hold 64 % of the ratings).  The CSR is the PACKED hot-first copy
 // (k_hot_pack: 16-B entries {rank or item, value}, every row's hot entries
 // first) and its chunk plan never lets a chunk straddle a row's hot / cold
 // boundary (csrc/ingest.cu), so a chunk is either
