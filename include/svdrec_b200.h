@@ -100,6 +100,16 @@ int svdrec_normal_fill(uint64_t key_lo, uint64_t key_hi, int64_t* d_pos,
  *                               32 < b <= 64 (b % 4 == 0) runs the wide
  *                               kernel on warp_seg; without the matching
  *                               plan the plain row-per-warp kernel runs
+ *   slot_long/long_done       : optional, for the pipelined kernel: the
+ *                               split rows' partial sums are added inside
+ *                               the kernel (by the warp that finishes a
+ *                               row's last outstanding segment, in slot
+ *                               order: the fix-up kernel's sum bit for bit)
+ *                               instead of by a second launch.  slot_long[s]
+ *                               = index of slot s's split row; long_done =
+ *                               nlong int32 tickets, zero before the first
+ *                               call (the kernel leaves them zero).  NULL:
+ *                               the fix-up kernel runs
  *   d_partial                 : (nslots x b) scratch
  * ------------------------------------------------------------------- */
 int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_begin,
@@ -108,7 +118,8 @@ int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg_beg
                 const double* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
                 int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                 const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
-                const int32_t* d_warp_chunk, const void* d_chunks, double* d_partial, void* stream);
+                const int32_t* d_warp_chunk, const void* d_chunks, const int32_t* d_slot_long,
+                int32_t* d_long_done, double* d_partial, void* stream);
 /* Warps per SM of the schedule (nwarp = SMs x this) that the pipelined
  * kernel for width b runs: 16 for even b <= 32 (two 8-warp CTAs, 2 doubles
  * per lane), fewer for 32 < b <= 64 with b % 4 == 0 (4 doubles per lane,
@@ -167,7 +178,8 @@ int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int64_t* d_seg
                     const float* d_X, int64_t ldx, int64_t x_rows, double* d_Y, int64_t ldy,
                     int32_t b, int64_t nlong, const int32_t* d_long_row, const int32_t* d_long_slot0,
                     const int32_t* d_long_slot1, int64_t nwarp, const int32_t* d_warp_seg,
-                    const int32_t* d_warp_chunk, const void* d_chunks, double* d_partial, void* stream);
+                    const int32_t* d_warp_chunk, const void* d_chunks, const int32_t* d_slot_long,
+                    int32_t* d_long_done, double* d_partial, void* stream);
 /* ---------------------------------------------------------------------
  * Dense tall-skinny contractions (the deflation products of
  * rsvd.py:135-142, 179-194: Q @ (B @ X), Q @ (Q.T @ X), B.T @ (Q.T @ X)

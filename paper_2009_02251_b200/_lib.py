@@ -33,7 +33,7 @@ SIGNATURES = {
     "svdrec_normal_workspace_bytes": (_sz, [_i64]),
     "svdrec_normal_fill": (C.c_int, [_u64, _u64, _p, _i64, _i64, _p, _p, _i64, _p, _sz, _p, _p]),
     "svdrec_spmm": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p, _p, _p,
-                              _p]),
+                              _p, _p, _p]),
     "svdrec_chunk_plan": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "svdrec_spmm_hc_warps_per_sm": (C.c_int, []),
     "svdrec_spmm_hc_rows": (C.c_int, [_i32]),
@@ -48,7 +48,7 @@ SIGNATURES = {
                                   _p, _i64, _p, _p, _p]),
     "svdrec_spmm_x32_warps_per_sm": (C.c_int, [_i32]),
     "svdrec_spmm_x32": (C.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p, _p, _i64, _p, _p,
-                                  _p, _p, _p]),
+                                  _p, _p, _p, _p, _p]),
     "svdrec_gemm_tn_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "svdrec_gemm_tn": (C.c_int, [_i64, _i64, _i64, _f64, _p, _i64, _p, _i64, _f64, _p, _i64, _p, _sz, _p]),
     "svdrec_gemm_nn": (C.c_int, [_i64, _i64, _i64, _f64, _p, _i64, _p, _i64, _f64, _p, _i64, _p]),

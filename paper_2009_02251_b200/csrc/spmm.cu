@@ -520,11 +520,22 @@ struct PipeGeom {
   static constexpr int WARPB = S * Gm::ROWSD * 8 + (D * CSRB + kRecRing * 16 + 127) / 128 * 128;  // bytes per warp
 };
 
+// Split rows folded into the SpMM kernel: slot -> split-row index, the rows'
+// slot ranges and destinations, and one zero-initialised ticket per split row
+// (done == nullptr: the separate fix-up kernel adds the partials instead).
+struct FixArgs {
+  const int32_t* slot_long;
+  const int32_t* row;
+  const int32_t* s0;
+  const int32_t* s1;
+  int* done;
+};
+
 template <int P, int S, int D, int W, int V, typename TX = double>
 __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
     const __grid_constant__ CUtensorMap tmX, int64_t nwarp, const int32_t* __restrict__ warp_chunk,
     const int4* __restrict__ chunks, const int32_t* __restrict__ indices, const double* __restrict__ values,
-    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial) {
+    double* __restrict__ Y, int64_t ldy, double* __restrict__ partial, FixArgs fix) {
   static_assert(D >= S, "spmm: the CSR ring must be at least as deep as the row ring");
   static_assert(kRecAhead >= 2 * (D - S + 1) && kRecAhead + D <= kRecRing, "spmm: record ring too small");
   using Gm = TmaGeom<P, V, TX>;
@@ -660,6 +671,34 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
         double* dst = m.y >= 0 ? (Y + (int64_t)m.y * ldy + V * pc) : (partial + (int64_t)(~m.y) * B + V * pc);
         tot.store(dst);
       }
+      if (m.y < 0 && fix.done != nullptr) {
+        // a split row's segment: the warp that completes the row's last
+        // outstanding segment adds the row's partial sums in slot order (the
+        // fix-up kernel's sum, bit for bit) -- no separate launch
+        __threadfence();  // this segment's partial is visible before its ticket
+        __syncwarp();
+        const int L = __ldg(fix.slot_long + (~m.y));
+        const int s0 = __ldg(fix.s0 + L), s1 = __ldg(fix.s1 + L);
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(fix.done + L, 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == s1 - s0 - 1) {
+          __threadfence();
+          if (g == 0) {
+            Acc<V> sum;
+            sum.zero();
+            for (int sl2 = s0; sl2 < s1; ++sl2) {
+              Acc<V> p;
+#pragma unroll
+              for (int h = 0; h < V / 2; ++h)
+                p.h[h] = __ldcg(reinterpret_cast<const double2*>(partial + (int64_t)sl2 * B + V * pc) + h);
+              sum.add(p);
+            }
+            sum.store(Y + (int64_t)__ldg(fix.row + L) * ldy + V * pc);
+          }
+          if (lane == 0) fix.done[L] = 0;  // ready for the next launch
+        }
+      }
       acc.zero();  // the next segment starts at zero (segments never span warps)
       acc1.zero();
     }
@@ -691,7 +730,7 @@ __global__ void __launch_bounds__(W * 32, (V == 2 ? 2 : 1)) k_spmm_pipe(
 
 template <int P, int S, int D, int W, int V = 2, typename TX = double>
 int pipe_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const void* chunks, const int32_t* indices,
-                const double* values, const TX* X, int64_t ldx, double* Y, int64_t ldy, double* partial,
+                const double* values, const TX* X, int64_t ldx, double* Y, int64_t ldy, double* partial, FixArgs fix,
                 cudaStream_t s) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
@@ -720,7 +759,7 @@ int pipe_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const v
     SVDREC_CUDA(smem_attr_once(k_spmm_pipe<P, S, D, W, V, TX>, (int)kMaxSmem));
     const int64_t grid = (nwarp + W - 1) / W;
     k_spmm_pipe<P, S, D, W, V, TX><<<(unsigned)grid, W * 32, ring, s>>>(
-        tm, nwarp, warp_chunk, reinterpret_cast<const int4*>(chunks), indices, values, Y, ldy, partial);
+        tm, nwarp, warp_chunk, reinterpret_cast<const int4*>(chunks), indices, values, Y, ldy, partial, fix);
     return check_launch("spmm_pipe");
   }
 }
@@ -736,12 +775,12 @@ int pipe_launch(int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const v
 #endif
 constexpr int kS2 = SVDREC_SPMM_S2, kD2 = SVDREC_SPMM_D2, kW2 = SVDREC_SPMM_W2;
 
-#define SVDREC_PIPE_ARGS xrows, nwarp, warp_chunk, chunks, indices, values, X, ldx, Y, ldy, partial, s
+#define SVDREC_PIPE_ARGS xrows, nwarp, warp_chunk, chunks, indices, values, X, ldx, Y, ldy, partial, fix, s
 
 // even b <= 32: the chunk-record pipeline, two CTAs of kW2 warps per SM
 int pipe_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const void* chunks,
                   const int32_t* indices, const double* values, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                  double* partial, cudaStream_t s) {
+                  double* partial, FixArgs fix, cudaStream_t s) {
 #define SVDREC_PIPE(PP) \
   case PP:              \
     return pipe_launch<PP, kS2, kD2, kW2, 2, double>(SVDREC_PIPE_ARGS);
@@ -758,7 +797,7 @@ int pipe_dispatch(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_chunk
 // rows (half the gathered bytes; every TMA row a multiple of 16 B)
 int pipe_dispatch_f32(int b, int64_t xrows, int64_t nwarp, const int32_t* warp_chunk, const void* chunks,
                       const int32_t* indices, const double* values, const float* X, int64_t ldx, double* Y,
-                      int64_t ldy, double* partial, cudaStream_t s) {
+                      int64_t ldy, double* partial, FixArgs fix, cudaStream_t s) {
 #define SVDREC_PIPEF(PP) \
   case PP:               \
     return pipe_launch<PP, kS2, kD2, 8, 2, float>(SVDREC_PIPE_ARGS);
@@ -1314,8 +1353,9 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
                            int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
                            const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
                            const int32_t* d_warp_seg, const int32_t* d_warp_chunk, const void* d_chunks,
-                           double* d_partial, void* stream) {
+                           const int32_t* d_slot_long, int32_t* d_long_done, double* d_partial, void* stream) {
   SVDREC_ARG(b >= 1 && ldx >= b && ldy >= b && nseg >= 0 && nlong >= 0, "spmm: bad arguments b=%d", b);
+  SVDREC_ARG(!d_long_done || d_slot_long, "spmm: the in-kernel fix-up needs the slot -> split-row map");
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
   const bool vec2 = (b % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
@@ -1328,8 +1368,10 @@ extern "C" int svdrec_spmm(int64_t nseg, const int32_t* d_seg_row, const int64_t
   const bool sched = vec2 && nwarp > 0 && kind != 0 && xrows < (1ll << 31);
   int rc = 0;
   if (sched && b <= 32 && d_warp_chunk && d_chunks) {
+    const FixArgs fix{d_slot_long, d_long_row, d_long_slot0, d_long_slot1, nlong > 0 ? d_long_done : nullptr};
     rc = pipe_dispatch(b, xrows, nwarp, d_warp_chunk, d_chunks, d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial,
-                       s);
+                       fix, s);
+    if (rc || fix.done) return rc;  // the split rows were added inside the kernel
   } else if (sched && b > 32 && b <= 64 && b % 4 == 0 && ldx % 4 == 0 && d_warp_seg) {
     rc = tma_dispatch4(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_indices,
                        d_values, d_X, ldx, d_Y, ldy, d_partial, s);
@@ -1485,7 +1527,7 @@ extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int
                                int64_t ldy, int32_t b, int64_t nlong, const int32_t* d_long_row,
                                const int32_t* d_long_slot0, const int32_t* d_long_slot1, int64_t nwarp,
                                const int32_t* d_warp_seg, const int32_t* d_warp_chunk, const void* d_chunks,
-                               double* d_partial, void* stream) {
+                               const int32_t* d_slot_long, int32_t* d_long_done, double* d_partial, void* stream) {
   SVDREC_ARG(b >= 4 && b <= 64 && b % 4 == 0 && ldx >= b && ldx % 4 == 0 && ldy >= b && ldy % 2 == 0 && nseg >= 0 &&
                  nlong >= 0 && (b <= 32 || ldy % 4 == 0),
              "spmm_x32: needs b in {4, 8, ..., 64} and 16-B aligned rows (b=%d)", b);
@@ -1496,11 +1538,13 @@ extern "C" int svdrec_spmm_x32(int64_t nseg, const int32_t* d_seg_row, const int
              "spmm_x32: operands must be 16-B aligned");
   if (nseg == 0) return 0;
   cudaStream_t s = as_stream(stream);
+  const bool infix = b <= 32 && nlong > 0 && d_long_done && d_slot_long;
+  const FixArgs fix{d_slot_long, d_long_row, d_long_slot0, d_long_slot1, infix ? d_long_done : nullptr};
   const int rc = b <= 32 ? pipe_dispatch_f32(b, xrows, nwarp, d_warp_chunk, d_chunks, d_indices, d_values, d_X, ldx,
-                                             d_Y, ldy, d_partial, s)
+                                             d_Y, ldy, d_partial, fix, s)
                          : tma_dispatch4_f32(b, xrows, nwarp, d_warp_seg, d_seg_row, d_seg_begin, d_seg_end,
                                              d_seg_slot, d_indices, d_values, d_X, ldx, d_Y, ldy, d_partial, s);
-  if (rc) return rc;
+  if (rc || infix) return rc;
   return run_fixup(nlong, d_long_row, d_long_slot0, d_long_slot1, d_partial, d_Y, ldy, b, s);
 }
 

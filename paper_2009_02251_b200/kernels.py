@@ -153,7 +153,7 @@ def spmm(plan, X: torch.Tensor, Y: torch.Tensor, precision: str = "fp64") -> tor
             call("svdrec_spmm_x32", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end),
                  ptr(plan.seg_slot), ptr(plan.indices), ptr(plan.values), ptr(X32), b, plan.n, ptr(Y), ldy, b,
                  plan.nlong, ptr(plan.long_row), ptr(plan.long_s0), ptr(plan.long_s1), nw, ptr(wseg), ptr(wc),
-                 ptr(recs), ptr(part), stream_handle())
+                 ptr(recs), ptr(plan.slot_long), ptr(plan.long_done), ptr(part), stream_handle())
         return Y
     hc = _hc_rows(plan, b, ldx, ldy)
     hot = 0 if hc else _hot_rows(plan, b, ldx, ldy)
@@ -238,8 +238,8 @@ def _spmm_tma(plan, X, ldx, Y, ldy, b):
     nwarp, wseg, wchunk, recs = _schedules(plan, query("svdrec_spmm_warps_per_sm", b), b)
     call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
          ptr(plan.indices), ptr(plan.values), ptr(X), ldx, plan.n, ptr(Y), ldy, b, plan.nlong, ptr(plan.long_row),
-         ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(wchunk), ptr(recs), ptr(plan.partial(b)),
-         stream_handle())
+         ptr(plan.long_s0), ptr(plan.long_s1), nwarp, ptr(wseg), ptr(wchunk), ptr(recs), ptr(plan.slot_long),
+         ptr(plan.long_done), ptr(plan.partial(b)), stream_handle())
 
 
 def gemm_tn(X: torch.Tensor, Y: torch.Tensor, C: torch.Tensor | None = None, alpha: float = 1.0,

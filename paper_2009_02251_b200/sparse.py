@@ -295,6 +295,15 @@ class DeviceCSR:
         self.long_s0 = s0.to(torch.int32)
         self.long_s1 = s1.to(torch.int32)
         self.nslots = nslots
+        # in-kernel fix-up of the split rows (pipelined SpMM): slot -> split-row
+        # index and one ticket per split row (the kernel leaves them at zero)
+        if self.nlong:
+            self.slot_long = torch.repeat_interleave(
+                torch.arange(self.nlong, dtype=torch.int32, device=self.device),
+                (self.long_s1 - self.long_s0).to(torch.int64), output_size=int(nslots))
+            self.long_done = torch.zeros(self.nlong, dtype=torch.int32, device=self.device)
+        else:
+            self.slot_long = self.long_done = None
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count if self.device.type == "cuda" else 148
         self.nwarp = int(max(1, min(self.nseg, sms * WARPS_PER_SM)))
         self.warp_seg = (warp_plan_dev if cuda else warp_plan_t)(sb, se, self.nwarp)

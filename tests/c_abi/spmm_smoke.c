@@ -108,7 +108,7 @@ int main(void) {
     }
     CK(cudaMemset(d_Y, 0, m * b * 8));
     int rc = svdrec_spmm(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_ind, d_val, d_X, b, n, d_Y, b, b, 0,
-                         NULL, NULL, NULL, nwarp, d_ws, d_wc, d_recs, d_part, NULL);
+                         NULL, NULL, NULL, nwarp, d_ws, d_wc, d_recs, NULL, NULL, d_part, NULL);
     if (rc) {
       fprintf(stderr, "svdrec_spmm: %s\n", svdrec_last_error());
       return 4;
@@ -129,7 +129,7 @@ int main(void) {
   }
   /* error contract: bad arguments -> nonzero status and a message */
   int rc = svdrec_spmm(m, d_seg_row, d_seg_begin, d_seg_end, d_seg_slot, d_ind, d_val, d_X, 1, n, d_Y, b, b, 0, NULL,
-                       NULL, NULL, 0, NULL, NULL, NULL, d_part, NULL);
+                       NULL, NULL, 0, NULL, NULL, NULL, NULL, NULL, d_part, NULL);
   if (rc == 0 || svdrec_last_error()[0] == 0) ++fails;
   printf("bad ldx -> rc %d: %s\n", rc, svdrec_last_error());
   printf("%s\n", fails ? "FAIL" : "PASS");

@@ -35,7 +35,7 @@ def plain(plan, X, Y):
     b = X.shape[1]
     call("svdrec_spmm", plan.nseg, ptr(plan.seg_row), ptr(plan.seg_begin), ptr(plan.seg_end), ptr(plan.seg_slot),
          ptr(plan.indices), ptr(plan.values), ptr(X), b, plan.n, ptr(Y), b, b, plan.nlong, ptr(plan.long_row),
-         ptr(plan.long_s0), ptr(plan.long_s1), 0, None, None, None, ptr(plan.partial(b)), stream_handle())
+         ptr(plan.long_s0), ptr(plan.long_s1), 0, None, None, None, None, None, ptr(plan.partial(b)), stream_handle())
     return Y
 
 
