@@ -39,6 +39,8 @@ F64 = torch.float64
 # final Q is the same up to column signs (bench: 42.8 vs 43.8 ms per step,
 # same k, MAE trace and test RMSE to every printed digit)
 LU_BASIS = os.environ.get("SVDREC_LU_BASIS", "cqr")
+# SVDREC_LOOKAHEAD=0: every sketch matrix is drawn in place on the QB stream (A/B measurements)
+LOOKAHEAD = os.environ.get("SVDREC_LOOKAHEAD", "1") != "0"
 
 class QbState:
     """Snapshot of a growing QB factorization after a completed block.
@@ -138,6 +140,17 @@ class FrobTolerance:
 
 
 TerminationCriterion = Callable[[QbState], bool]
+
+
+_LOOKAHEAD: dict = {}
+
+
+def _lookahead_stream(dev: torch.device) -> torch.cuda.Stream:
+    """One cached stream per device for the sketch look-ahead draws."""
+    s = _LOOKAHEAD.get(dev.index)
+    if s is None:
+        s = _LOOKAHEAD[dev.index] = torch.cuda.Stream(device=dev)
+    return s
 
 
 class _QbEngine:
@@ -294,6 +307,63 @@ class _QbEngine:
     def normal(self, rows: int, cols: int, out):
         return self.stream.normal_device(rows, cols, out=out, status=self.status)
 
+    # -- sketch look-ahead ----------------------------------------------------
+    # The sketch matrix Omega of block l + 1 (rsvd.py:178: one
+    # standard_normal((n, b)) per block) does not depend on the factorization,
+    # and its draw is a chain of small latency-bound kernels (csrc/gaussian.cu:
+    # ~77 us at 26,744 x 20).  It is drawn one block ahead on a side stream,
+    # into the other of two Omega buffers, with its status flags going to the
+    # mailbox the next block will use.  The stream position lives on the
+    # device and all draws stay in order; a drawn-ahead Omega that is never
+    # used (the consumer stopped) is rolled back, so the stream ends exactly
+    # where the reference's would.
+    LOOKAHEAD_BYTES = 64 << 20  # larger sketches are throughput-bound: drawn in place
+
+    def next_omega(self, n: int):
+        """Omega of the block being started (n x b; ``n`` is the global
+        column count: a sharded sketch side draws the full matrix and keeps
+        its rows, and is not drawn ahead)."""
+        la, self._la = getattr(self, "_la", None), None
+        if la is not None:
+            ev, buf, _, mb = la
+            torch.cuda.current_stream(self.dev).wait_event(ev)
+            self.mb, self.status = mb, mb["status"]  # the flags of this block's draw are in this mailbox
+            return buf
+        if not hasattr(self, "_om"):
+            self._om = [torch.empty(self.n, self.b, dtype=F64, device=self.dev) for _ in range(2)]
+            self._om_i = 0
+        self._om_i ^= 1
+        return self.normal(n, self.b, self._om[self._om_i])
+
+    def prefetch_omega(self, n: int) -> None:
+        """Queue the draw of the next block's Omega on the look-ahead stream
+        (after everything queued so far on this stream: the buffer's last
+        reader is behind us)."""
+        if n != self.n or n * self.b * 8 > self.LOOKAHEAD_BYTES or not hasattr(self, "_om"):
+            return
+        cur = torch.cuda.current_stream(self.dev)
+        side = _lookahead_stream(self.dev)
+        ev0 = torch.cuda.Event()
+        ev0.record(cur)
+        side.wait_event(ev0)
+        mb = K.Mailbox(self.dev, colsq=("f8", self.b), total=("f8", 1), status=("u4", 1))
+        self._om_i ^= 1
+        buf = self._om[self._om_i]
+        with torch.cuda.stream(side):
+            saved = self.stream.pos.clone()
+            self.stream.normal_device(self.n, self.b, out=buf, status=mb["status"])
+            ev = torch.cuda.Event()
+            ev.record(side)
+        self._la = (ev, buf, saved, mb)
+
+    def release_lookahead(self) -> None:
+        """Undo a drawn-ahead Omega nobody used: the reference never drew it."""
+        la, self._la = getattr(self, "_la", None), None
+        if la is not None:
+            ev, _, saved, _ = la
+            torch.cuda.current_stream(self.dev).wait_event(ev)
+            self.stream.pos.copy_(saved)
+
     def state(self) -> QbState:
         return QbState(self.Q[:, : self.K], self.Bt[:, : self.K], None, self.blocks, self.b, self.frob,
                        None, engine=self)
@@ -427,25 +497,30 @@ def qb_pass_blocks(A: SparseRatings, block_size: int, passes: int, stream: Gauss
     cap = min(m, n) if max_rank is None else min(min(m, n), max_rank + b)
     E = _QbEngine.create(A, b, stream, cap, precision)
     nsteps = (passes - 1) // 2
-    while (E.blocks + 1) * b <= min(m, n) - b:
-        if passes % 2 == 0:
-            om = E.normal(n, b, E.yn)
-            ql = E.A_mul(om, E.ym)
-            E.minus_QBX(ql, om)
-            E.lu(ql)
-        else:
-            ql = E.normal(m, b, E.ym)
-        for t in range(1, nsteps + 1):
-            r = E.AT_mul(ql, E.yn)
-            y = E.A_mul(r, E.ym2 if ql is E.ym else E.ym)
-            if t == nsteps:
-                E.minus_QBX(y, r)
-                E.orth_into(y, y)
+    try:
+        while (E.blocks + 1) * b <= min(m, n) - b:
+            if passes % 2 == 0:
+                om = E.next_omega(n)
+                ql = E.A_mul(om, E.ym)
+                E.minus_QBX(ql, om)
+                if LOOKAHEAD and (E.blocks + 2) * b <= min(m, n) - b:
+                    E.prefetch_omega(n)  # block l + 1's sketch matrix, drawn beside this block
+                E.lu(ql)
             else:
-                E.lu(y)
-            ql = y
-        E.append(ql)
-        yield E.state()
+                ql = E.normal(m, b, E.ym)
+            for t in range(1, nsteps + 1):
+                r = E.AT_mul(ql, E.yn)
+                y = E.A_mul(r, E.ym2 if ql is E.ym else E.ym)
+                if t == nsteps:
+                    E.minus_QBX(y, r)
+                    E.orth_into(y, y)
+                else:
+                    E.lu(y)
+                ql = y
+            E.append(ql)
+            yield E.state()
+    finally:
+        E.release_lookahead()
 
 
 def _refined_rank(row_energy: np.ndarray, frob_sq: float, eps: float) -> tuple[int, float]:

@@ -50,6 +50,38 @@ def test_pass_engine_golden(gpu, passes):
             break
 
 
+@pytest.mark.parametrize("passes", [4, 6])
+def test_sketch_lookahead_leaves_the_stream_where_the_reference_would(gpu, passes):
+    """Alg. 3's sketch matrix of block l + 1 is drawn one block ahead on a side
+    stream (rsvd._QbEngine.prefetch_omega).  A consumer that stops after l
+    blocks must find the Gaussian stream exactly where the reference leaves
+    it -- l draws of (n, b) (reference rsvd.py:178) -- and the blocks must
+    equal the ones computed without the look-ahead."""
+    import paper_2009_02251_b200 as P
+    from paper_2009_02251_b200 import rsvd
+    import inputs
+    _, A = inputs.rand_sparse(120, 150, 0.08, seed=1)
+    R = _R(A)
+    n, b = 150, 15
+    st = P.GaussianStream(4)
+    gen = P.qb_pass_blocks(R, b, passes, st)
+    got = [next(gen) for _ in range(2)]
+    Bs = [s.B.copy() for s in got]
+    gen.close()
+    after = st.normal(4, 3)
+    ref = P.GaussianStream(4)
+    for _ in range(2):
+        ref.normal_device(n, b)
+    np.testing.assert_array_equal(after, ref.normal(4, 3))
+    old, rsvd.LOOKAHEAD = rsvd.LOOKAHEAD, False
+    try:
+        plain = [s.B.copy() for s, _ in zip(P.qb_pass_blocks(R, b, passes, P.GaussianStream(4)), range(2))]
+    finally:
+        rsvd.LOOKAHEAD = old
+    for x, y in zip(Bs, plain):
+        np.testing.assert_array_equal(x, y)
+
+
 def test_drivers_golden(gpu):
     import paper_2009_02251_b200 as P
     import inputs
