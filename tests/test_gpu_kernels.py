@@ -226,6 +226,44 @@ def test_sharded_orth_single_rank(gpu):
     np.testing.assert_allclose(np.abs(np.sum(Q * Qr, 0)), 1.0, atol=1e-6)
 
 
+@pytest.mark.parametrize("b", [8, 20])
+def test_spmm_in_kernel_fixup_equals_fixup_kernel(gpu, b):
+    """Split rows (longer than the segment cap): the pipelined kernel adds
+    their partial sums itself -- the warp finishing a row's last outstanding
+    segment, in slot order -- and must give the fix-up kernel's result bit for
+    bit, leave its tickets at zero, and do so again on the next call."""
+    import torch
+    import paper_2009_02251_b200 as P
+    from paper_2009_02251_b200 import kernels as K
+    from scipy import sparse as sp
+    rng = np.random.default_rng(7 + b)
+    m, n = 6000, 900
+    deg = np.minimum(rng.lognormal(3.0, 1.2, m).astype(np.int64), n)
+    rows = np.repeat(np.arange(m), deg)
+    pz = 1.0 / np.arange(1, n + 1) ** 1.1
+    cols = np.concatenate([np.sort(rng.choice(n, d, replace=False, p=pz / pz.sum())) for d in deg if d])
+    M = sp.csr_matrix((rng.integers(1, 11, cols.size) * 0.5, (rows, cols)), shape=(m, n))
+    d = P.SparseRatings(M, 0.5, 5.0).device(gpu)
+    plan = d.AT  # item rows: the popular items are rated by thousands of users
+    assert plan.nlong > 0 and plan.long_done is not None
+    X = torch.as_tensor(rng.standard_normal((m, b)), device=gpu)
+    outs = []
+    for tickets in (True, False, True):
+        saved = plan.long_done
+        if not tickets:
+            plan.long_done = None
+        try:
+            Y = torch.empty(n, b, dtype=torch.float64, device=gpu)
+            K._spmm_tma(plan, X, b, Y, b, b)
+        finally:
+            plan.long_done = saved
+        outs.append(Y)
+        assert int(plan.long_done.abs().sum()) == 0
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = M.T @ X.cpu().numpy()
+    np.testing.assert_allclose(outs[0].cpu().numpy(), ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+
+
 @pytest.mark.parametrize("b", [2, 6, 10, 16, 20, 32, 40, 64])
 def test_spmm_hot_set_matches_tma(gpu, b):
     """A @ X through the hot-set kernels (hot rows of X in shared memory: the
