@@ -55,10 +55,15 @@ def full(path, out):
             per[d["ID"]][d["Metric Name"]] = f'{d["Metric Value"]} {d["Metric Unit"]}'.strip()
     rr = list(csv.reader(io.StringIO(raw)))
     traffic = {}
+    pipes = {}
     if rr:
         h = rr[0]
+        # FP64 tensor-core (DMMA) and FP64 pipe activity, where the report has them
+        pk = [c for c in h if ("pipe_tensor" in c or "pipe_fp64" in c or "pipe_fmaheavy" in c)
+              and "pct_of_peak_sustained_active" in c]
         for r in rr[2:]:
             d = dict(zip(h, r))
+            pipes[d["ID"]] = [(c, d[c]) for c in pk if d.get(c) not in (None, "", "n/a")]
             try:
                 rd = float(d.get("dram__bytes_read.sum", "0").replace(",", ""))
                 wr = float(d.get("dram__bytes_write.sum", "0").replace(",", ""))
@@ -74,6 +79,8 @@ def full(path, out):
         if i in traffic:
             rd, wr, unit = traffic[i]
             lines.append(f"- dram__bytes_read.sum + dram__bytes_write.sum: {rd:.4g} + {wr:.4g} {unit}")
+        for c, v in pipes.get(i, []):
+            lines.append(f"- {c}: {v} %")
         lines.append("")
     open(out, "w").write("\n".join(lines))
     print("\n".join(lines))
